@@ -1,0 +1,124 @@
+"""Regenerate the frozen fixtures under tests/golden/ (run in the build container).
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+* `lod_reference.npz` — pyramids computed by the REFERENCE itself:
+  `chunkcast.ops.build_lod(source_from_array(x, chunk))` resolved through
+  `chunkcast.Engine` (`pkg/src/chunkcast/ops.py:714-727`, `engine.py:423-448`).
+  These pin `oracle.lod` (bit-exact) and the CUDA LOD kernel.
+* `rw_*.npz` — random-walker outputs of the float64 oracle (`oracle.rw`,
+  tol 1e-10) on the synthetic configs.  The reference has no random walker,
+  so these are oracle outputs, not reference outputs (parity unpinned).
+
+`/root/reference` is not available on the GPU box; only the frozen files
+travel.  `MANIFEST.json` holds SHA-256 digests of inputs and outputs.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+from oracle import rw  # noqa: E402
+from paper_2509_26213_b200 import synthetic as syn  # noqa: E402
+
+LOD_CASES = {
+    # name: (shape, chunk, dtype seed)
+    "r3d": ((21, 18, 13), (8, 8, 8)),
+    "r2d": ((37, 29), (8, 8)),
+    "r1d": ((11,), (3,)),
+    "phantom3d": ((64, 64, 64), (16, 16, 16)),
+    "phantom2d": ((96, 80), (16, 16)),
+}
+
+RW_CASES = {
+    # name: (shape, seedset, brick, levels)
+    "c1_s1": ((64, 64, 64), "S1", (32, 32, 32), 1),
+    "c1_s2": ((64, 64, 64), "S2", (32, 32, 32), 1),
+    "h3d_s1": ((48, 48, 48), "S1", (16, 16, 16), 2),
+    "h3d_ragged_s2": ((40, 36, 28), "S2", (16, 16, 16), 2),
+    "h2d_s1": ((128, 128), "S1", (32, 32), 3),
+    "h2d_s2": ((96, 112), "S2", (32, 32), 2),
+}
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def lod_input(name, shape):
+    if name.startswith("phantom"):
+        return syn.phantom(shape)
+    rng = np.random.default_rng(0xC0FFEE + len(shape))
+    return rng.random(shape, dtype=np.float32)
+
+
+def make_lod(manifest):
+    from chunkcast import ops
+    from chunkcast.engine import Engine, EngineConfig
+    from chunkcast.store import StoreConfig
+
+    arrays = {}
+    with Engine(EngineConfig(stores=StoreConfig(ram_capacity=1 << 28))) as eng:
+        for name, (shape, chunk) in LOD_CASES.items():
+            x = lod_input(name, shape)
+            pyr = ops.build_lod(ops.source_from_array(x, chunk))
+            if not name.startswith("phantom"):  # phantoms are regenerated from synthetic.py
+                arrays[f"{name}/input"] = x
+            levels_sha = [sha(x)]
+            for k in range(1, pyr.num_levels):
+                node = pyr.node(k)
+                chunks = eng.resolve(node)
+                full = np.zeros(node.md.size, dtype=np.float32)
+                for pos, arr in zip(node.md.chunk_positions(), chunks):
+                    begin, end = node.md.chunk_logical_region(pos)
+                    dst = tuple(slice(b, e) for b, e in zip(begin, end))
+                    full[dst] = arr[tuple(slice(0, e - b) for b, e in zip(begin, end))]
+                arrays[f"{name}/level{k}"] = full
+                levels_sha.append(sha(full))
+            manifest["lod"][name] = {
+                "shape": list(shape), "chunk": list(chunk), "levels": pyr.num_levels,
+                "input_sha256": sha(x),
+                "levels_sha256": levels_sha,
+            }
+    np.savez_compressed(os.path.join(HERE, "lod_reference.npz"), **arrays)
+
+
+def make_rw(manifest):
+    params = rw.RWParams(beta=100.0, min_weight=1e-6, tol=1e-10, max_iter=20000)
+    for name, (shape, which, brick, levels) in RW_CASES.items():
+        vol = syn.phantom(shape)
+        seeds = syn.seeds(shape, which)
+        res = rw.hierarchical_random_walker(vol, seeds, brick, levels, params)
+        out = {"labels": res.labels}
+        for k, p in enumerate(res.prob):
+            out[f"prob{k}"] = p.astype(np.float32)
+        np.savez_compressed(os.path.join(HERE, f"rw_{name}.npz"), **out)
+        manifest["rw"][name] = {
+            "shape": list(shape), "seeds": which, "brick": list(brick), "levels": levels,
+            "beta": params.beta, "min_weight": params.min_weight, "tol": params.tol,
+            "input_sha256": sha(vol), "seeds_sha256": sha(seeds),
+            "prob0_sha256": sha(out["prob0"]), "labels_sha256": sha(res.labels),
+            "iterations_max": [int(i.max()) if len(i) else 0 for i in res.iterations],
+        }
+        print(name, manifest["rw"][name]["iterations_max"], flush=True)
+
+
+def main():
+    manifest = {"lod": {}, "rw": {}}
+    make_lod(manifest)
+    make_rw(manifest)
+    with open(os.path.join(HERE, "MANIFEST.json"), "w") as f:
+        json.dump(manifest, f, indent=1, sort_keys=True)
+
+
+if __name__ == "__main__":
+    main()
