@@ -1,0 +1,331 @@
+"""Benchmark of the hierarchical random-walker hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c4|c2|c3|c1]
+
+One step = one full hierarchical random-walker segmentation of a synthetic
+volume already resident in HBM: LOD pyramid, seed projection, coarsest-level
+solve, upsample + brick-wise Jacobi-PCG solve of every finer level,
+probabilities and labels of level 0 written to HBM.  `value` = level-0
+voxels / second over all ranks (max-over-ranks device time).
+
+Default workload = BASELINE.json config 4 (1024^3, 4 levels, 32^3 bricks),
+the configuration the metric's 1/2/4/8-GPU scaling is quoted on; it fits one
+B200.  Under torchrun (N > 1) the bricks of every level are sharded across
+ranks (sharding.py) with an NCCL halo exchange between levels.
+
+`--impl reference` times the CPU reference of the path (the float64 numpy
+oracle, brick-parallel on all host cores; the reference package has no
+random walker of its own) on a bounded sample of the same
+workload and prints the same JSON line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "c4": dict(shape=(1024, 1024, 1024), brick=(32, 32, 32), levels=4,
+               desc="config 4: 1024^3 f32 two-blob phantom + noise, 4-level hierarchy (1024/512/256/128), "
+                    "32^3 bricks, seeds S1",
+               sample=dict(shape=(128, 128, 128), levels=4)),
+    "c2": dict(shape=(256, 256, 256), brick=(32, 32, 32), levels=2,
+               desc="config 2: 256^3 f32 two-blob phantom + noise, 2-level hierarchy, 32^3 bricks, seeds S1",
+               sample=dict(shape=(128, 128, 128), levels=2)),
+    "c3": dict(shape=(16384, 16384), brick=(64, 64), levels=9,
+               desc="config 3: 16384^2 f32 two-blob image + noise, 9-level hierarchy, 64^2 bricks, seeds S1",
+               sample=dict(shape=(1024, 1024), levels=5)),
+    "c1": dict(shape=(64, 64, 64), brick=(32, 32, 32), levels=1,
+               desc="config 1: 64^3 f32 two-blob phantom + noise, single level, seeds S1",
+               sample=dict(shape=(64, 64, 64), levels=1)),
+}
+METRIC = "random-walker voxels/sec"
+UNIT = "voxel/s"
+BETA, WMIN, TOL = 100.0, 1e-6, 1e-6
+
+
+def load_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.thread.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle) on a bounded sample
+
+
+def cpu_reference_sample(wl, steps=1, warmup=0):
+    import numpy as np
+
+    from oracle import rw as orw
+    from paper_2509_26213_b200 import synthetic
+
+    s = wl["sample"]
+    # bricks are split into slabs of brick rows along dim 0, one thread each
+    cores = min(len(os.sched_getaffinity(0)), -(-s["shape"][0] // wl["brick"][0]))
+    vol = synthetic.phantom(s["shape"])
+    seeds = synthetic.seeds(s["shape"], "S1")
+    params = orw.RWParams(beta=BETA, min_weight=WMIN, tol=TOL, max_iter=10_000)
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        orw.hierarchical_random_walker(vol, seeds, wl["brick"], s["levels"], params, threads=cores)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+    n = int(np.prod(s["shape"]))
+    sample = (f"full hierarchical RW of the same generator/seeds/beta/tol/bricks at {'x'.join(map(str, s['shape']))} "
+              f"with {s['levels']} levels ({n} voxels) instead of {'x'.join(map(str, wl['shape']))}; "
+              f"float64 numpy oracle, bricks split over {cores} threads")
+    return n, times, cores, sample
+
+
+def run_reference(args, wl, rank):
+    if rank != 0:
+        return 0
+    n, times, cores, sample = cpu_reference_sample(wl, args.steps, args.warmup)
+    total = sum(times)
+    value = n * len(times) / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl["desc"], "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our path
+
+
+def run_ours(args, wl, rank, world):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import __graft_entry__ as entry
+
+    entry.build()
+    from paper_2509_26213_b200 import _native, api, device, sharding, synthetic
+    from paper_2509_26213_b200.config import RWConfig
+
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = _native.lib()
+    cfg = RWConfig(beta=BETA, min_weight=WMIN, tol=TOL, max_iter=10_000, check_every=args.check_every)
+    shape, brick, levels = wl["shape"], wl["brick"], wl["levels"]
+    nvox = math.prod(shape)
+    vol = synthetic.phantom_device(shape, device=dev)
+    seeds = synthetic.seeds_device(shape, "S1", device=dev)
+    ws = device.Workspace(dev)
+    plan = sharding.ShardPlan.build(shape, brick, levels, rank, world, device=dev) if world > 1 else None
+
+    def step():
+        if plan is None:
+            return device.hierarchical_random_walker(vol, seeds, brick, levels, cfg, workspace=ws)
+        return sharding.hierarchical_random_walker_sharded(vol, seeds, plan, cfg, workspace=ws)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+    barrier()
+
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = lib.rwb_kernel_launches()
+    cg_ms, cg_bytes, per_level = 0.0, 0.0, None
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            res = step()
+            for k, st in enumerate(res.stats):
+                if st is None:
+                    continue
+                bvol = math.prod(res.volumes[k].shape) if k == len(res.stats) - 1 else math.prod(brick)
+                cg_ms += st["cg_ms"]
+                cg_bytes += sharding.cg_bytes_per_voxel_iter(len(shape)) * bvol * st["iterations_sum"]
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    launches = lib.rwb_kernel_launches() - launches0
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    per_level = [dict(st, level=k, shape=list(res.volumes[k].shape)) for k, st in enumerate(res.stats)]
+
+    # end to end through the public API with pinned host buffers (N = 1 only:
+    # the sharded path keeps level-0 results distributed)
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        vol_h = vol.cpu().pin_memory()
+        seeds_h = seeds.cpu().pin_memory()
+        out_p = torch.empty(shape, dtype=torch.float32, pin_memory=True)
+        out_l = torch.empty(shape, dtype=torch.uint8, pin_memory=True)
+        api.segment(vol_h, seeds_h, brick, levels, cfg, out_prob=out_p, out_labels=out_l, workspace=ws)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            api.segment(vol_h, seeds_h, brick, levels, cfg, out_prob=out_p, out_labels=out_l, workspace=ws)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1) / args.steps
+        e2e = {"value": nvox / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": vol_h.numel() * 4 + seeds_h.numel(),
+               "d2h_bytes_per_step": out_p.numel() * 4 + out_l.numel(),
+               "api": "paper_2509_26213_b200.api.segment (pinned host in/out)"}
+        del vol_h, seeds_h, out_p, out_l
+
+    peak, peak_src = load_peak()
+    achieved = cg_bytes / (cg_ms / 1e3) / 1e9 if cg_ms > 0 else 0.0
+    roofline = {"bound": "hbm", "kernel": "CG iteration (cg_pass1 + cg_pass2), all levels",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                "peak_source": peak_src,
+                "bytes_per_voxel_iter": sharding.cg_bytes_per_voxel_iter(len(shape)),
+                "cg_ms_per_step": cg_ms / args.steps,
+                "note": "achieved = algorithmic CG bytes (bytes_per_voxel_iter x brick voxels x per-brick "
+                        "iterations, summed over levels) / device time of the CG launches (CUDA events)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        n, times, cores, sample = cpu_reference_sample(wl, steps=1)
+        cpu = {"value": n / times[0], "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": nvox * args.steps / (ms_max / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (device-generated phantom, torch RNG noise)",
+            "config": {"workload": wl["desc"], "size": list(shape), "brick": list(brick), "levels": levels,
+                       "beta": BETA, "min_weight": WMIN, "tol": TOL, "parallelism": f"bricks sharded x{world}"
+                       if world > 1 else "1 GPU",
+                       "l2": f"inputs {nvox * 5 / 2**30:.1f} GiB (f32 volume + u8 seeds) > 126 MB L2; no flush"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks.summary(),
+            "gpu_launches": int(launches),
+            "levels": per_level,
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(WORKLOADS), default="c4")
+    ap.add_argument("--check-every", type=int, default=16)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    rank = int(os.environ.get("RANK", 0))
+    wl = WORKLOADS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, wl, rank)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl")
+    try:
+        return run_ours(args, wl, rank, world)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,149 @@
+/*
+ * rwb.h — C ABI of the B200 hierarchical random-walker library (librwb.so).
+ *
+ * This is the drop-in boundary under the reference's compute-graph operator
+ * API (`OperatorNode.kernel(h, input_arrays, out)`,
+ * pkg/src/chunkcast/graph.py:18-51, driven by `_generic_compute_body`,
+ * pkg/src/chunkcast/engine.py:999-1076).  Every entry point below replaces
+ * one operator kernel of the reference (or, for the random walker, the
+ * operator the reference's paper describes but the package leaves out,
+ * SPEC.md:8).  The Python binding is `paper_2509_26213_b200/_native.py`
+ * (ctypes); INTEGRATION.md shows the binding a reference maintainer adds.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only.  All array pointers are DEVICE pointers
+ *    (cudaMalloc / torch CUDA storage) unless stated otherwise; the caller
+ *    owns all memory, including the solver workspace.
+ *  - Arrays are dense row-major with the LAST dimension fastest, like the
+ *    reference's chunk payloads (model.py:3-6).  `size[0]` is the slowest
+ *    dimension (TensorMetaData.size order, model.py:98-117).  ndim is 2 or 3
+ *    (the LOD kernel also takes 1).
+ *  - Every call is stream-ordered on `stream` (a cudaStream_t, NULL = legacy
+ *    default stream) and reentrant: distinct host threads may call with
+ *    distinct streams.  The only blocking call is rwb_solve_level, which
+ *    polls convergence on its own stream.
+ *  - Return value: RWB_OK (0) on success, a negative RWB_ERR_* code on
+ *    failure; rwb_last_error() then returns a thread-local message.
+ */
+#ifndef RWB_H
+#define RWB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RWB_ABI_VERSION 1
+
+enum {
+  RWB_OK = 0,
+  RWB_ERR_INVALID = -1,     /* bad argument (shape, pointer, parameter) */
+  RWB_ERR_CUDA = -2,        /* CUDA runtime error (message has the cause) */
+  RWB_ERR_WORKSPACE = -3,   /* workspace too small */
+  RWB_ERR_UNSUPPORTED = -4, /* no sm_100 device / unsupported configuration */
+};
+
+/* Geometry of one pyramid level and its brick (chunk) grid.
+ * Bricks cover [origin + h*brick, origin + (h+1)*brick) ∩ [0, size) per
+ * dimension; origin = 0 gives the reference's chunk grid
+ * (TensorMetaData.chunk_grid_dims / chunk_logical_region, model.py:125-170).
+ * brick == size makes the whole level one brick (the coarsest-level solve). */
+typedef struct {
+  int32_t ndim;
+  int32_t reserved;
+  int64_t size[3];
+  int64_t brick[3];
+  int64_t origin[3]; /* each in (-brick, 0] */
+} rwb_geometry_t;
+
+typedef struct {
+  float beta;          /* edge weight exp(-beta * dI^2) */
+  float min_weight;    /* lower clamp of every edge weight */
+  float tol;           /* per-brick stop: ||r|| <= tol * ||b|| (Jacobi-scaled system) */
+  int32_t max_iter;    /* per-brick iteration cap */
+  int32_t check_every; /* iterations per convergence poll (0 = library default) */
+  int32_t flags;       /* RWB_SOLVE_* */
+} rwb_solve_params_t;
+
+#define RWB_SOLVE_NO_GRAPH 1 /* launch iterations directly instead of via a CUDA graph */
+
+typedef struct {
+  int64_t bricks;          /* bricks solved by this call */
+  int64_t converged;       /* reached tol */
+  int64_t not_converged;   /* hit max_iter */
+  int64_t zero_rhs;        /* ||b|| == 0: exact solution 0, no iterations */
+  int64_t iterations_max;  /* max over bricks */
+  int64_t iterations_sum;  /* sum over bricks (for algorithmic-byte accounting) */
+  int64_t unknowns;        /* unseeded voxels solved for */
+  int32_t sweeps;          /* PCG iterations launched (= iterations_max rounded up to a poll) */
+  float cg_ms;             /* device time of the CG iteration launches (CUDA events on `stream`) */
+} rwb_solve_stats_t;
+
+int rwb_abi_version(void);
+const char* rwb_last_error(void);
+/* Process-wide count of librwb kernels launched so far (graph replays count
+ * every kernel node).  Lets callers report how many of the library's kernels
+ * ran inside a timed region. */
+int64_t rwb_kernel_launches(void);
+/* sm count and compute capability of the current device; RWB_ERR_UNSUPPORTED if not sm_100. */
+int rwb_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor);
+
+/* One LOD pyramid step, level k -> k+1:
+ * f32(downsample_mean(f32(separable_conv(src, [.25,.5,.25]^d, clamp)))).
+ * Replaces the separable_conv + downsample_mean pair that build_lod chains
+ * per level (ops.py:714-727, kernels ops.py:503-530 and ops.py:642-661);
+ * bit-identical to them (same float64 operation order).
+ * dst has size ceil(size/2) per dimension. */
+int rwb_lod_down_f32(int32_t ndim, const int64_t* size, const float* src, float* dst, void* stream);
+
+/* Seed labels (0 none, 1 fg, 2 bg) of the next coarser level: a coarse voxel
+ * is 1 (2) if one of its downsample_mean block children (ops.py:629-636) is
+ * 1 (2) and none is 2 (1), else 0.  coarse has size ceil(size/2). */
+int rwb_project_seeds_u8(int32_t ndim, const int64_t* size, const uint8_t* fine, uint8_t* coarse,
+                         void* stream);
+
+/* Coarse-to-fine prolongation: cell-centred multilinear, fine index g reads
+ * parent coordinate g/2 - 1/4, clamped.  fine_size must satisfy
+ * ceil(fine_size/2) == parent_size. */
+int rwb_upsample_f32(int32_t ndim, const int64_t* parent_size, const float* parent,
+                     const int64_t* fine_size, float* fine, void* stream);
+
+/* Forward edge weights, lanes-last (the ElementType(F32, ndim) payload layout,
+ * model.py:66-80): weights[i*ndim + k] = max(exp(-beta*(I_i - I_{i+e_k})^2), min_weight),
+ * 0 where i+e_k is outside the volume. */
+int rwb_edge_weights_f32(int32_t ndim, const int64_t* size, const float* volume, float beta,
+                         float min_weight, float* weights, void* stream);
+
+/* labels[i] = prob[i] > 0.5 (cast_array semantics of a boolean, ops.py:44-52). */
+int rwb_labels_u8(int64_t n, const float* prob, uint8_t* labels, void* stream);
+
+/* Bytes of solver workspace for n_bricks bricks of `geom` (n_bricks < 0: all). */
+size_t rwb_solve_workspace_bytes(const rwb_geometry_t* geom, int64_t n_bricks);
+
+/* Random-walker solve of the listed bricks of one level.
+ *  intensity : f32 level (size)         seeds : u8 level, 0/1/2
+ *  bound     : f32 level or NULL.  Values of the Dirichlet nodes outside a
+ *              brick and the initial guess inside it (the upsampled parent
+ *              level).  NULL only when the geometry has a single brick
+ *              (coarsest level), initial guess 0.
+ *  brick_list: device int32 row-major brick indices, or NULL for all bricks
+ *              (n_bricks then ignored).  Listed bricks must be distinct.
+ *  prob      : f32 level output; written only inside the listed bricks.  May
+ *              alias `bound` (all reads of bound happen before any write).
+ *  labels    : u8 level output (prob > 0.5) or NULL.
+ *  stats     : host pointer or NULL.
+ * Blocking on the host: returns when the listed bricks have converged (or hit
+ * max_iter); all work is stream-ordered on `stream`. */
+int rwb_solve_level(const rwb_geometry_t* geom, const float* intensity, const uint8_t* seeds,
+                    const float* bound, const int32_t* brick_list, int64_t n_bricks,
+                    const rwb_solve_params_t* params, float* prob, uint8_t* labels,
+                    void* workspace, size_t workspace_bytes, rwb_solve_stats_t* stats,
+                    void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RWB_H */

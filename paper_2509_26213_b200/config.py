@@ -1,0 +1,26 @@
+"""Random-walker parameters (canonically encodable, so they can feed operator ids).
+
+The reference's operator params must be encodable by `canon.encode`
+(dict/list/float/int/str only, `pkg/src/chunkcast/canon.py:19-50`); `params()`
+returns that form.
+"""
+
+from __future__ import annotations
+
+from dataclasses import asdict, dataclass
+
+
+@dataclass(frozen=True)
+class RWConfig:
+    beta: float = 100.0        # edge weight exp(-beta * dI^2), intensities in [0, 1]
+    min_weight: float = 1e-6   # lower clamp of every edge weight
+    tol: float = 1e-6          # per-brick ||r|| <= tol * ||b|| on the Jacobi-scaled system
+    max_iter: int = 10_000     # per-brick iteration cap
+    check_every: int = 16      # CG iterations per convergence poll (one CUDA graph)
+    use_graph: bool = True     # run each poll interval as one CUDA graph launch
+
+    def params(self) -> dict:
+        d = asdict(self)
+        d.pop("check_every")
+        d.pop("use_graph")
+        return {k: (float(v) if isinstance(v, float) else int(v)) for k, v in d.items()}

@@ -1,0 +1,52 @@
+// Shared helpers for librwb (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "rwb.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "librwb is written for Blackwell (sm_100a); compile with -gencode arch=compute_100a,code=sm_100a"
+#endif
+
+namespace rwb {
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+int cuda_fail(cudaError_t err, const char* what);
+
+#define RWB_CUDA(call)                                   \
+  do {                                                   \
+    cudaError_t err__ = (call);                          \
+    if (err__ != cudaSuccess) return ::rwb::cuda_fail(err__, #call); \
+  } while (0)
+
+#define RWB_LAUNCH_CHECK(what)                           \
+  do {                                                   \
+    cudaError_t err__ = cudaGetLastError();              \
+    if (err__ != cudaSuccess) return ::rwb::cuda_fail(err__, what); \
+  } while (0)
+
+// Dense level shape, padded to 3 dims (leading dims of size 1).
+struct Shape3 {
+  int nz, ny, nx;
+  __host__ __device__ long long count() const { return (long long)nz * ny * nx; }
+};
+
+int shape_from(int32_t ndim, const int64_t* size, Shape3* out);
+
+// process-wide kernel launch counter (rwb_kernel_launches)
+void count_launches(long long n);
+
+inline unsigned ceil_div_u(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
+
+// Edge weight of the Grady random walker: max(exp(-beta*(a-b)^2), w_min).
+__device__ __forceinline__ float edge_weight(float a, float b, float beta, float wmin) {
+  float d = a - b;
+  return fmaxf(expf(-beta * d * d), wmin);
+}
+
+}  // namespace rwb

@@ -1,0 +1,334 @@
+// Per-voxel operators of the hierarchical random walker: LOD step, seed
+// projection, coarse-to-fine upsampling, edge weights, labels.
+//
+// All of them are HBM-bound streaming kernels (a few bytes per voxel).  One
+// thread per OUTPUT voxel, x fastest so warps read/write contiguous rows;
+// neighbourhood re-reads are served by L1 (x/y neighbours are in the same or
+// adjacent warps).
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <string>
+
+#include "rwb_common.cuh"
+
+namespace rwb {
+
+static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+
+void count_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t err, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorName(err) + " (" + cudaGetErrorString(err) + ")";
+  return RWB_ERR_CUDA;
+}
+
+int shape_from(int32_t ndim, const int64_t* size, Shape3* out) {
+  if (ndim < 1 || ndim > 3 || size == nullptr) return fail(RWB_ERR_INVALID, "ndim must be 1..3");
+  int64_t s[3] = {1, 1, 1};
+  for (int i = 0; i < ndim; ++i) {
+    if (size[i] < 1 || size[i] > (1ll << 30)) return fail(RWB_ERR_INVALID, "dimension size out of range");
+    s[3 - ndim + i] = size[i];
+  }
+  if (s[0] * s[1] * s[2] > (1ll << 40)) return fail(RWB_ERR_INVALID, "level too large");
+  out->nz = (int)s[0];
+  out->ny = (int)s[1];
+  out->nx = (int)s[2];
+  return RWB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// LOD step: f32(mean2(f32(conv3_clamp(x)))) with the reference's float64
+// operation order (ops.py:533-548 then ops.py:664-676): every 1-D pass is
+// acc = 0; acc += k0*a; acc += k1*b; acc += k2*c (products by powers of two
+// are exact, so fma == mul+add here), dims in order z, y, x; the conv result
+// is rounded to f32 before the pairwise means.
+
+__device__ __forceinline__ double conv3(double a, double b, double c) {
+  double acc = 0.0;
+  acc += 0.25 * a;
+  acc += 0.5 * b;
+  acc += 0.25 * c;
+  return acc;
+}
+
+__device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+template <bool HAS_Z, bool HAS_Y>
+__global__ void __launch_bounds__(256) lod_down_kernel(const float* __restrict__ src, Shape3 fs,
+                                                       float* __restrict__ dst, Shape3 cs) {
+  long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= cs.count()) return;
+  int jx = (int)(o % cs.nx);
+  long long t = o / cs.nx;
+  int jy = (int)(t % cs.ny);
+  int jz = (int)(t / cs.ny);
+  // fine index windows 2j-1 .. 2j+2, clamped
+  int zi[4], yi[4], xi[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    zi[k] = clampi(2 * jz - 1 + k, 0, fs.nz - 1);
+    yi[k] = clampi(2 * jy - 1 + k, 0, fs.ny - 1);
+    xi[k] = clampi(2 * jx - 1 + k, 0, fs.nx - 1);
+  }
+  const int ncz = HAS_Z ? ((2 * jz + 1 < fs.nz) ? 2 : 1) : 1;
+  const int ncy = HAS_Y ? ((2 * jy + 1 < fs.ny) ? 2 : 1) : 1;
+  const int ncx = (2 * jx + 1 < fs.nx) ? 2 : 1;
+  const long long sxy = (long long)fs.ny * fs.nx;
+
+  // conv along z for the 2 child planes at every (y, x) of the 4x4 window
+  double A[2][4][4];
+#pragma unroll
+  for (int cz = 0; cz < 2; ++cz)
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        if (!HAS_Y && a != 1) { A[cz][a][b] = 0.0; continue; }
+        if (HAS_Z) {
+          const float* col = src + (long long)yi[a] * fs.nx + xi[b];
+          double v0 = __ldg(col + zi[cz] * sxy);
+          double v1 = __ldg(col + zi[cz + 1] * sxy);
+          double v2 = __ldg(col + zi[cz + 2] * sxy);
+          A[cz][a][b] = conv3(v0, v1, v2);
+        } else {
+          A[cz][a][b] = (double)__ldg(src + (long long)yi[a] * fs.nx + xi[b]);
+        }
+      }
+  float C[2][2][2];
+#pragma unroll
+  for (int cz = 0; cz < 2; ++cz)
+#pragma unroll
+    for (int cy = 0; cy < 2; ++cy) {
+      double B[4];
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        B[b] = HAS_Y ? conv3(A[cz][cy][b], A[cz][cy + 1][b], A[cz][cy + 2][b]) : A[cz][1][b];
+#pragma unroll
+      for (int cx = 0; cx < 2; ++cx) C[cz][cy][cx] = (float)conv3(B[cx], B[cx + 1], B[cx + 2]);
+    }
+  // pairwise means, dims z, y, x
+  double m0[2][2];
+#pragma unroll
+  for (int cy = 0; cy < 2; ++cy)
+#pragma unroll
+    for (int cx = 0; cx < 2; ++cx)
+      m0[cy][cx] = ncz == 2 ? ((double)C[0][cy][cx] + (double)C[1][cy][cx]) * 0.5 : (double)C[0][cy][cx];
+  double m1[2];
+#pragma unroll
+  for (int cx = 0; cx < 2; ++cx) m1[cx] = ncy == 2 ? (m0[0][cx] + m0[1][cx]) * 0.5 : m0[0][cx];
+  double m2 = ncx == 2 ? (m1[0] + m1[1]) * 0.5 : m1[0];
+  dst[o] = (float)m2;
+}
+
+// ---------------------------------------------------------------------------
+// seed projection: fg if any child fg and none bg; bg symmetric; else 0
+
+__global__ void __launch_bounds__(256) project_seeds_kernel(const uint8_t* __restrict__ fine, Shape3 fs,
+                                                            uint8_t* __restrict__ coarse, Shape3 cs) {
+  long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= cs.count()) return;
+  int jx = (int)(o % cs.nx);
+  long long t = o / cs.nx;
+  int jy = (int)(t % cs.ny);
+  int jz = (int)(t / cs.ny);
+  bool fg = false, bg = false;
+  for (int z = 2 * jz; z < min(2 * jz + 2, fs.nz); ++z)
+    for (int y = 2 * jy; y < min(2 * jy + 2, fs.ny); ++y)
+      for (int x = 2 * jx; x < min(2 * jx + 2, fs.nx); ++x) {
+        uint8_t s = fine[((long long)z * fs.ny + y) * fs.nx + x];
+        fg |= (s == 1);
+        bg |= (s == 2);
+      }
+  coarse[o] = (fg && !bg) ? 1 : ((bg && !fg) ? 2 : 0);
+}
+
+// ---------------------------------------------------------------------------
+// cell-centred multilinear prolongation (parent coordinate g/2 - 1/4, clamped)
+
+struct Taps {
+  int i0, i1;
+  float w0, w1;
+};
+
+__device__ __forceinline__ Taps up_taps(int g, int m) {
+  Taps t;
+  int j = g >> 1;
+  if (g & 1) {
+    t.i0 = j;
+    t.i1 = min(j + 1, m - 1);
+    t.w0 = 0.75f;
+    t.w1 = 0.25f;
+  } else {
+    t.i0 = max(j - 1, 0);
+    t.i1 = j;
+    t.w0 = 0.25f;
+    t.w1 = 0.75f;
+  }
+  return t;
+}
+
+__global__ void __launch_bounds__(256) upsample_kernel(const float* __restrict__ parent, Shape3 ps,
+                                                       float* __restrict__ fine, Shape3 fs) {
+  long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= fs.count()) return;
+  int gx = (int)(o % fs.nx);
+  long long t = o / fs.nx;
+  int gy = (int)(t % fs.ny);
+  int gz = (int)(t / fs.ny);
+  Taps tz = fs.nz > 1 ? up_taps(gz, ps.nz) : Taps{0, 0, 1.0f, 0.0f};
+  Taps ty = fs.ny > 1 ? up_taps(gy, ps.ny) : Taps{0, 0, 1.0f, 0.0f};
+  Taps tx = up_taps(gx, ps.nx);
+  const long long sxy = (long long)ps.ny * ps.nx;
+  auto row = [&](int z, int y) {
+    const float* p = parent + z * sxy + (long long)y * ps.nx;
+    return tx.w0 * __ldg(p + tx.i0) + tx.w1 * __ldg(p + tx.i1);
+  };
+  float r0 = ty.w0 * row(tz.i0, ty.i0) + ty.w1 * row(tz.i0, ty.i1);
+  float r1 = ty.w0 * row(tz.i1, ty.i0) + ty.w1 * row(tz.i1, ty.i1);
+  fine[o] = tz.w0 * r0 + tz.w1 * r1;
+}
+
+// ---------------------------------------------------------------------------
+// forward edge weights, lanes-last
+
+__global__ void __launch_bounds__(256) edge_weights_kernel(const float* __restrict__ vol, Shape3 s, int ndim,
+                                                           float beta, float wmin, float* __restrict__ w) {
+  long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= s.count()) return;
+  int x = (int)(o % s.nx);
+  long long t = o / s.nx;
+  int y = (int)(t % s.ny);
+  int z = (int)(t / s.ny);
+  float c = vol[o];
+  const long long sxy = (long long)s.ny * s.nx;
+  float* out = w + o * ndim;
+  int lane = 0;
+  if (ndim == 3) out[lane++] = (z + 1 < s.nz) ? edge_weight(c, __ldg(vol + o + sxy), beta, wmin) : 0.0f;
+  if (ndim >= 2) out[lane++] = (y + 1 < s.ny) ? edge_weight(c, __ldg(vol + o + s.nx), beta, wmin) : 0.0f;
+  out[lane] = (x + 1 < s.nx) ? edge_weight(c, __ldg(vol + o + 1), beta, wmin) : 0.0f;
+}
+
+__global__ void __launch_bounds__(256) labels_kernel(const float* __restrict__ prob, long long n,
+                                                     uint8_t* __restrict__ labels) {
+  long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o < n) labels[o] = prob[o] > 0.5f ? 1 : 0;
+}
+
+}  // namespace rwb
+
+using namespace rwb;
+
+static int coarse_of(const Shape3& f, Shape3* c) {
+  c->nz = (f.nz + 1) / 2;
+  c->ny = (f.ny + 1) / 2;
+  c->nx = (f.nx + 1) / 2;
+  return RWB_OK;
+}
+
+extern "C" int rwb_abi_version(void) { return RWB_ABI_VERSION; }
+
+extern "C" const char* rwb_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" int64_t rwb_kernel_launches(void) { return (int64_t)g_launches.load(); }
+
+extern "C" int rwb_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc_minor) {
+  int dev = 0;
+  RWB_CUDA(cudaGetDevice(&dev));
+  cudaDeviceProp prop;
+  RWB_CUDA(cudaGetDeviceProperties(&prop, dev));
+  if (sm_count) *sm_count = prop.multiProcessorCount;
+  if (cc_major) *cc_major = prop.major;
+  if (cc_minor) *cc_minor = prop.minor;
+  if (prop.major != 10) return fail(RWB_ERR_UNSUPPORTED, "librwb is built for sm_100a (B200); found sm_" +
+                                                             std::to_string(prop.major) + std::to_string(prop.minor));
+  return RWB_OK;
+}
+
+extern "C" int rwb_lod_down_f32(int32_t ndim, const int64_t* size, const float* src, float* dst, void* stream) {
+  Shape3 fs, cs;
+  int rc = shape_from(ndim, size, &fs);
+  if (rc) return rc;
+  if (!src || !dst) return fail(RWB_ERR_INVALID, "null pointer");
+  coarse_of(fs, &cs);
+  if (ndim == 1) cs.ny = fs.ny, cs.nz = fs.nz;
+  if (ndim == 2) cs.nz = fs.nz;
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned grid = ceil_div_u(cs.count(), 256);
+  if (ndim == 3)
+    lod_down_kernel<true, true><<<grid, 256, 0, st>>>(src, fs, dst, cs);
+  else if (ndim == 2)
+    lod_down_kernel<false, true><<<grid, 256, 0, st>>>(src, fs, dst, cs);
+  else
+    lod_down_kernel<false, false><<<grid, 256, 0, st>>>(src, fs, dst, cs);
+  RWB_LAUNCH_CHECK("lod_down_kernel");
+  count_launches(1);
+  return RWB_OK;
+}
+
+extern "C" int rwb_project_seeds_u8(int32_t ndim, const int64_t* size, const uint8_t* fine, uint8_t* coarse,
+                                    void* stream) {
+  Shape3 fs, cs;
+  int rc = shape_from(ndim, size, &fs);
+  if (rc) return rc;
+  if (!fine || !coarse) return fail(RWB_ERR_INVALID, "null pointer");
+  coarse_of(fs, &cs);
+  if (ndim < 3) cs.nz = fs.nz;
+  if (ndim < 2) cs.ny = fs.ny;
+  project_seeds_kernel<<<ceil_div_u(cs.count(), 256), 256, 0, (cudaStream_t)stream>>>(fine, fs, coarse, cs);
+  RWB_LAUNCH_CHECK("project_seeds_kernel");
+  count_launches(1);
+  return RWB_OK;
+}
+
+extern "C" int rwb_upsample_f32(int32_t ndim, const int64_t* parent_size, const float* parent,
+                                const int64_t* fine_size, float* fine, void* stream) {
+  Shape3 ps, fs, chk;
+  int rc = shape_from(ndim, parent_size, &ps);
+  if (rc) return rc;
+  rc = shape_from(ndim, fine_size, &fs);
+  if (rc) return rc;
+  if (!parent || !fine) return fail(RWB_ERR_INVALID, "null pointer");
+  coarse_of(fs, &chk);
+  if (ndim < 3) chk.nz = fs.nz;
+  if (ndim < 2) chk.ny = fs.ny;
+  if (chk.nz != ps.nz || chk.ny != ps.ny || chk.nx != ps.nx)
+    return fail(RWB_ERR_INVALID, "fine size is not a 2x refinement of the parent size");
+  upsample_kernel<<<ceil_div_u(fs.count(), 256), 256, 0, (cudaStream_t)stream>>>(parent, ps, fine, fs);
+  RWB_LAUNCH_CHECK("upsample_kernel");
+  count_launches(1);
+  return RWB_OK;
+}
+
+extern "C" int rwb_edge_weights_f32(int32_t ndim, const int64_t* size, const float* volume, float beta,
+                                    float min_weight, float* weights, void* stream) {
+  Shape3 s;
+  int rc = shape_from(ndim, size, &s);
+  if (rc) return rc;
+  if (!volume || !weights) return fail(RWB_ERR_INVALID, "null pointer");
+  if (!(beta >= 0.0f) || !(min_weight >= 0.0f)) return fail(RWB_ERR_INVALID, "beta and min_weight must be >= 0");
+  edge_weights_kernel<<<ceil_div_u(s.count(), 256), 256, 0, (cudaStream_t)stream>>>(volume, s, ndim, beta,
+                                                                                     min_weight, weights);
+  RWB_LAUNCH_CHECK("edge_weights_kernel");
+  count_launches(1);
+  return RWB_OK;
+}
+
+extern "C" int rwb_labels_u8(int64_t n, const float* prob, uint8_t* labels, void* stream) {
+  if (n < 0) return fail(RWB_ERR_INVALID, "negative length");
+  if (n == 0) return RWB_OK;
+  if (!prob || !labels) return fail(RWB_ERR_INVALID, "null pointer");
+  labels_kernel<<<ceil_div_u(n, 256), 256, 0, (cudaStream_t)stream>>>(prob, n, labels);
+  RWB_LAUNCH_CHECK("labels_kernel");
+  count_launches(1);
+  return RWB_OK;
+}

@@ -1,0 +1,781 @@
+// Brick-batched Jacobi-PCG random-walker solve of one pyramid level.
+//
+// Every brick of a level is an independent Dirichlet problem (oracle/rw.py,
+// DESIGN.md §3).  All listed bricks are solved together, in lockstep, with
+// per-brick CG scalars: one launch per CG pass covers every unconverged
+// brick, so the GPU stays full while bricks converge at different
+// iteration counts.
+//
+// The system is solved in Jacobi-scaled form: with s_i = diag_i^-1/2,
+// A' = S L_UU S has unit diagonal, off-diagonals -w'_ij = -w_ij s_i s_j, and
+// CG on A' y = S b is Jacobi-PCG on L_UU x = b with x = S y.  The scaled
+// forward weights w' are zero on every edge that leaves the brick or touches
+// a Dirichlet node, so the block-diagonal operator needs no brick masks in
+// the iteration and no preconditioner array.
+//
+// Workspace (brick-local, each brick padded to the full brick box, brick
+// `slot` at offset slot*bvol, x fastest):
+//   y, r, p[2], q, w'x, w'y, w'z, s   (f32)   -> 36 B/voxel (3D), 32 B (2D)
+// Per CG iteration and unknown, HBM traffic is
+//   pass 1: read r, p_in, w'x, w'y, w'z; write p_out, q   (28 B; 2D: 24 B)
+//   pass 2: read y, r, p_out, q;        write y, r        (24 B)
+// = 52 B (3D) / 48 B (2D) of algorithmic bytes.
+//
+// Per-brick reductions are deterministic: each CTA writes one partial, the
+// last CTA of a brick to finish (atomic ticket) sums the partials in a fixed
+// order in float64.  Results are therefore independent of which other bricks
+// share the launch (multi-GPU sharding gives bit-identical bytes).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "rwb_common.cuh"
+
+namespace rwb {
+
+constexpr int TX = 32;  // threads along x (one warp per row segment)
+constexpr int TY = 8;   // threads along y
+constexpr int TZ = 8;   // z extent marched by each thread
+constexpr int NTHREADS = TX * TY;
+
+enum BrickState : int { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_ZERO = 3 };
+
+struct Geo {
+  int nz, ny, nx;  // level
+  int bz, by, bx;  // brick box
+  int oz, oy, ox;  // brick grid origin
+  int gz, gy, gx;  // brick grid
+  int tz, ty, tx;  // tiles per brick
+  int tiles;
+  long long bvol;  // bz*by*bx
+  long long sxy;   // ny*nx
+  int is3d;
+};
+
+struct Work {
+  float *y, *r, *p0, *p1, *q, *wx, *wy, *wz, *sc;
+  double* rr;  // [2][nb]
+  double* pq;  // [nb]
+  double* bb;  // [nb]
+  int* state;  // [nb]
+  int* iters;  // [nb]
+  unsigned* ticket;  // [nb]
+  float2* part;      // [nb*tiles]
+  int* alist;        // [nb] compacted active slots
+  int* base_it;      // [1]  iteration count at the start of the current graph chunk
+  int* n_active;     // [1]
+  unsigned long long* unknowns;  // [1]
+  int* stat_i;       // [8] device stats scratch
+};
+
+// ---------------------------------------------------------------------------
+// brick/tile addressing
+
+struct TileCtx {
+  int slot, brick, tile;
+  int hz, hy, hx;       // brick coords
+  int gz0, gy0, gx0;    // global coords of brick-local (0,0,0)
+  int lz0, lz1, ly, lx; // this thread's column and z range (local)
+  bool col;             // column inside the brick box
+};
+
+__device__ __forceinline__ TileCtx tile_ctx(const Geo& g, const int* __restrict__ list, int slot, int tile) {
+  TileCtx c;
+  c.slot = slot;
+  c.tile = tile;
+  c.brick = list ? list[slot] : slot;
+  c.hx = c.brick % g.gx;
+  int t = c.brick / g.gx;
+  c.hy = t % g.gy;
+  c.hz = t / g.gy;
+  c.gz0 = g.oz + c.hz * g.bz;
+  c.gy0 = g.oy + c.hy * g.by;
+  c.gx0 = g.ox + c.hx * g.bx;
+  int ttx = tile % g.tx;
+  int tt = tile / g.tx;
+  int tty = tt % g.ty;
+  int ttz = tt / g.ty;
+  c.lx = ttx * TX + threadIdx.x;
+  c.ly = tty * TY + threadIdx.y;
+  c.lz0 = ttz * TZ;
+  c.lz1 = min(c.lz0 + TZ, g.bz);
+  c.col = c.lx < g.bx && c.ly < g.by;
+  return c;
+}
+
+// one CTA per (slot, tile) for the non-iterative kernels
+__device__ __forceinline__ TileCtx tile_ctx(const Geo& g, const int* __restrict__ list) {
+  int slot = blockIdx.x / g.tiles;
+  return tile_ctx(g, list, slot, blockIdx.x - slot * g.tiles);
+}
+
+// block-wide sum of two floats -> thread 0
+__device__ __forceinline__ float2 block_sum2(float a, float b) {
+  __shared__ float2 warp_part[NTHREADS / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  if ((tid & 31) == 0) warp_part[tid >> 5] = make_float2(a, b);
+  __syncthreads();
+  float2 s = make_float2(0.f, 0.f);
+  if (tid == 0) {
+#pragma unroll
+    for (int w = 0; w < NTHREADS / 32; ++w) {
+      s.x += warp_part[w].x;
+      s.y += warp_part[w].y;
+    }
+  }
+  return s;
+}
+
+// Publish this CTA's partial; the last CTA of the brick reduces all partials
+// (fixed order, float64).  Must be called by all threads of the CTA.  Returns
+// true in exactly one thread (thread 0 of the brick's last CTA), which then
+// holds the brick totals in *sum0 / *sum1.  Ends with a CTA barrier so the
+// shared scratch can be reused by the next work item.
+__device__ __forceinline__ bool brick_reduce(const Geo& g, const Work& w, int slot, int tile, float a, float b,
+                                             double* sum0, double* sum1) {
+  __shared__ bool last;
+  float2 s = block_sum2(a, b);
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  bool mine = false;
+  if (g.tiles == 1) {
+    if (tid == 0) {
+      *sum0 = (double)s.x;
+      *sum1 = (double)s.y;
+      mine = true;
+    }
+    __syncthreads();
+    return mine;
+  }
+  if (tid == 0) {
+    w.part[(long long)slot * g.tiles + tile] = s;
+    __threadfence();
+    unsigned t = atomicAdd(&w.ticket[slot], 1u);
+    last = (t == (unsigned)g.tiles - 1);
+  }
+  __syncthreads();
+  if (last && tid < 32) {
+    __threadfence();
+    double sa = 0.0, sb = 0.0;
+    const float2* p = w.part + (long long)slot * g.tiles;
+    for (int i = tid; i < g.tiles; i += 32) {
+      float2 v = __ldcg(p + i);
+      sa += (double)v.x;
+      sb += (double)v.y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sa += __shfl_xor_sync(0xffffffffu, sa, o);
+      sb += __shfl_xor_sync(0xffffffffu, sb, o);
+    }
+    if (tid == 0) {
+      *sum0 = sa;
+      *sum1 = sb;
+      w.ticket[slot] = 0;
+      mine = true;
+    }
+  }
+  __syncthreads();
+  return mine;
+}
+
+// ---------------------------------------------------------------------------
+// setup
+
+// Sum of the weights of all edges of voxel (z,y,x) inside the level, fixed
+// order -z,+z,-y,+y,-x,+x (K1 and K2 must produce bit-identical diagonals).
+__device__ __forceinline__ float level_diag(const Geo& g, const float* __restrict__ I, long long gi, int z, int y,
+                                            int x, float c, float beta, float wmin) {
+  float d = 0.f;
+  if (g.is3d) {
+    if (z > 0) d += edge_weight(c, __ldg(I + gi - g.sxy), beta, wmin);
+    if (z + 1 < g.nz) d += edge_weight(c, __ldg(I + gi + g.sxy), beta, wmin);
+  }
+  if (y > 0) d += edge_weight(c, __ldg(I + gi - g.nx), beta, wmin);
+  if (y + 1 < g.ny) d += edge_weight(c, __ldg(I + gi + g.nx), beta, wmin);
+  if (x > 0) d += edge_weight(c, __ldg(I + gi - 1), beta, wmin);
+  if (x + 1 < g.nx) d += edge_weight(c, __ldg(I + gi + 1), beta, wmin);
+  return d;
+}
+
+// K1: scale s = diag^-1/2 for unknowns, 0 for seeds / padding / isolated voxels.
+__global__ void __launch_bounds__(NTHREADS) setup_scale_kernel(Geo g, Work w, const int* __restrict__ list,
+                                                               const float* __restrict__ I,
+                                                               const uint8_t* __restrict__ S, float beta,
+                                                               float wmin) {
+  TileCtx c = tile_ctx(g, list);
+  if (!c.col) return;
+  const int gy = c.gy0 + c.ly, gx = c.gx0 + c.lx;
+  const bool colin = gy >= 0 && gy < g.ny && gx >= 0 && gx < g.nx;
+  long long lbase = (long long)c.slot * g.bvol + (long long)c.ly * g.bx + c.lx;
+  for (int lz = c.lz0; lz < c.lz1; ++lz) {
+    long long li = lbase + (long long)lz * g.by * g.bx;
+    const int gz = c.gz0 + lz;
+    float s = 0.f;
+    if (colin && gz >= 0 && gz < g.nz) {
+      long long gi = (long long)gz * g.sxy + (long long)gy * g.nx + gx;
+      if (S[gi] == 0) {
+        float d = level_diag(g, I, gi, gz, gy, gx, __ldg(I + gi), beta, wmin);
+        s = d > 0.f ? 1.0f / sqrtf(d) : 0.f;
+      }
+    }
+    w.sc[li] = s;
+  }
+}
+
+__device__ __forceinline__ float seed_value(uint8_t s) { return s == 1 ? 1.0f : 0.0f; }
+
+// K2: scaled forward weights, r0 = S(b - L x0), y0 = x0 / s, p = 0; per-brick
+// ||S b||^2 and ||r0||^2.
+__global__ void __launch_bounds__(NTHREADS) setup_system_kernel(Geo g, Work w, const int* __restrict__ list,
+                                                                const float* __restrict__ I,
+                                                                const uint8_t* __restrict__ S,
+                                                                const float* __restrict__ bound, float beta,
+                                                                float wmin, float tol2, int max_iter) {
+  TileCtx c = tile_ctx(g, list);
+  float acc_bb = 0.f, acc_rr = 0.f;
+  unsigned n_unknown = 0;
+  if (c.col) {
+    const int gy = c.gy0 + c.ly, gx = c.gx0 + c.lx;
+    const bool colin = gy >= 0 && gy < g.ny && gx >= 0 && gx < g.nx;
+    const long long sbz = (long long)g.by * g.bx;
+    long long lbase = (long long)c.slot * g.bvol + (long long)c.ly * g.bx + c.lx;
+    for (int lz = c.lz0; lz < c.lz1; ++lz) {
+      long long li = lbase + (long long)lz * sbz;
+      const int gz = c.gz0 + lz;
+      float si = w.sc[li];
+      float wfx = 0.f, wfy = 0.f, wfz = 0.f, r = 0.f, y = 0.f;
+      if (si > 0.f && colin && gz >= 0 && gz < g.nz) {
+        ++n_unknown;
+        long long gi = (long long)gz * g.sxy + (long long)gy * g.nx + gx;
+        const float ci = __ldg(I + gi);
+        const float x0 = bound ? bound[gi] : 0.f;
+        float diag = 0.f, b = 0.f, acc = 0.f;
+        // neighbour visit in the same order as level_diag
+        auto visit = [&](bool inlevel, bool inbrick, long long gn, long long ln, float* fwd) {
+          if (!inlevel) return;
+          float wt = edge_weight(ci, __ldg(I + gn), beta, wmin);
+          diag += wt;
+          float sn = inbrick ? w.sc[ln] : 0.f;
+          if (sn > 0.f) {
+            acc += wt * (bound ? bound[gn] : 0.f);
+            if (fwd) *fwd = wt * si * sn;
+          } else {
+            uint8_t sv = S[gn];
+            float val = sv ? seed_value(sv) : (bound ? bound[gn] : 0.f);
+            b += wt * val;
+          }
+        };
+        if (g.is3d) {
+          visit(gz > 0, lz > 0, gi - g.sxy, li - sbz, nullptr);
+          visit(gz + 1 < g.nz, lz + 1 < g.bz, gi + g.sxy, li + sbz, &wfz);
+        }
+        visit(gy > 0, c.ly > 0, gi - g.nx, li - g.bx, nullptr);
+        visit(gy + 1 < g.ny, c.ly + 1 < g.by, gi + g.nx, li + g.bx, &wfy);
+        visit(gx > 0, c.lx > 0, gi - 1, li - 1, nullptr);
+        visit(gx + 1 < g.nx, c.lx + 1 < g.bx, gi + 1, li + 1, &wfx);
+        r = si * (b + acc - diag * x0);
+        y = x0 / si;
+        float sb = si * b;
+        acc_bb += sb * sb;
+        acc_rr += r * r;
+      }
+      w.wx[li] = wfx;
+      w.wy[li] = wfy;
+      if (g.is3d) w.wz[li] = wfz;
+      w.r[li] = r;
+      w.y[li] = y;
+      w.p0[li] = 0.f;
+    }
+  }
+  {
+    __shared__ unsigned cta_unknown;
+    if (threadIdx.x == 0 && threadIdx.y == 0) cta_unknown = 0;
+    __syncthreads();
+    if (n_unknown) atomicAdd(&cta_unknown, n_unknown);
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0 && cta_unknown)
+      atomicAdd(w.unknowns, (unsigned long long)cta_unknown);
+  }
+  double bb, rr;
+  if (brick_reduce(g, w, c.slot, c.tile, acc_bb, acc_rr, &bb, &rr)) {
+    w.bb[c.slot] = bb;
+    w.rr[c.slot] = rr;  // parity 0
+    int st = ST_ACTIVE;
+    if (bb <= 0.0)
+      st = ST_ZERO;  // no Dirichlet coupling: the exact solution is 0
+    else if (rr <= (double)tol2 * bb)
+      st = ST_CONVERGED;
+    else if (max_iter <= 0)
+      st = ST_MAXITER;
+    w.state[c.slot] = st;
+    w.iters[c.slot] = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CG passes.  Persistent grid: CTAs stride over the work items
+// (active brick, tile) of the compacted active list; the list is rebuilt
+// between graph chunks, so converged bricks stop costing launches.
+
+__global__ void __launch_bounds__(NTHREADS) cg_pass1_kernel(Geo g, Work w, int nb, const int* __restrict__ list,
+                                                            int j) {
+  const int n_items = *w.n_active * g.tiles;
+  const int par = j & 1;
+  const int it = *w.base_it + j;
+  const float* __restrict__ pin = par ? w.p1 : w.p0;
+  float* __restrict__ pout = par ? w.p0 : w.p1;
+  const float* __restrict__ R = w.r;
+  const long long sbz = (long long)g.by * g.bx;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int slot = w.alist[item / g.tiles];
+    if (w.state[slot] != ST_ACTIVE) continue;  // uniform per CTA
+    TileCtx c = tile_ctx(g, list, slot, item % g.tiles);
+    const double rr = w.rr[(long long)par * nb + slot];
+    const double rr_prev = w.rr[(long long)(par ^ 1) * nb + slot];
+    const float beta = (it == 0 || rr_prev <= 0.0) ? 0.f : (float)(rr / rr_prev);
+    float acc = 0.f;
+    if (c.col) {
+      const long long lbase = (long long)slot * g.bvol + (long long)c.ly * g.bx + c.lx;
+      const bool hx0 = c.lx > 0, hx1 = c.lx + 1 < g.bx, hy0 = c.ly > 0, hy1 = c.ly + 1 < g.by;
+      auto pn_at = [&](long long i) { return __ldg(R + i) + beta * __ldg(pin + i); };
+      long long li = lbase + (long long)c.lz0 * sbz;
+      float pm = (g.is3d && c.lz0 > 0) ? pn_at(li - sbz) : 0.f;
+      float wzm = (g.is3d && c.lz0 > 0) ? __ldg(w.wz + li - sbz) : 0.f;
+      float pc = pn_at(li);
+      for (int lz = c.lz0; lz < c.lz1; ++lz, li += sbz) {
+        const bool up = g.is3d && lz + 1 < g.bz;
+        float pp = up ? pn_at(li + sbz) : 0.f;
+        float wzc = up ? __ldg(w.wz + li) : 0.f;
+        float s = wzc * pp + wzm * pm;
+        if (hx1) s += __ldg(w.wx + li) * pn_at(li + 1);
+        if (hx0) s += __ldg(w.wx + li - 1) * pn_at(li - 1);
+        if (hy1) s += __ldg(w.wy + li) * pn_at(li + g.bx);
+        if (hy0) s += __ldg(w.wy + li - g.bx) * pn_at(li - g.bx);
+        float q = pc - s;
+        pout[li] = pc;
+        w.q[li] = q;
+        acc += pc * q;
+        pm = pc;
+        pc = pp;
+        wzm = wzc;
+      }
+    }
+    double pq, unused;
+    if (brick_reduce(g, w, slot, c.tile, acc, 0.f, &pq, &unused)) w.pq[slot] = pq;
+  }
+}
+
+__global__ void __launch_bounds__(NTHREADS) cg_pass2_kernel(Geo g, Work w, int nb, const int* __restrict__ list,
+                                                            int j, float tol2, int max_iter) {
+  const int n_items = *w.n_active * g.tiles;
+  const int par = j & 1;
+  const int it = *w.base_it + j;
+  const float* __restrict__ P = par ? w.p0 : w.p1;  // pass-1 output
+  const long long sbz = (long long)g.by * g.bx;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int slot = w.alist[item / g.tiles];
+    if (w.state[slot] != ST_ACTIVE) continue;
+    TileCtx c = tile_ctx(g, list, slot, item % g.tiles);
+    const double rr = w.rr[(long long)par * nb + slot];
+    const double pq = w.pq[slot];
+    const float alpha = pq != 0.0 ? (float)(rr / pq) : 0.f;
+    float acc = 0.f;
+    if (c.col) {
+      long long li = (long long)slot * g.bvol + (long long)c.ly * g.bx + c.lx + (long long)c.lz0 * sbz;
+      for (int lz = c.lz0; lz < c.lz1; ++lz, li += sbz) {
+        float y = w.y[li] + alpha * __ldg(P + li);
+        float r = w.r[li] - alpha * __ldg(w.q + li);
+        w.y[li] = y;
+        w.r[li] = r;
+        acc += r * r;
+      }
+    }
+    double rr_new, unused;
+    if (brick_reduce(g, w, slot, c.tile, acc, 0.f, &rr_new, &unused)) {
+      w.rr[(long long)(par ^ 1) * nb + slot] = rr_new;
+      // decide here so the next pass-1 launch already skips finished bricks
+      if (rr_new <= (double)tol2 * w.bb[slot]) {
+        w.iters[slot] = it + 1;
+        w.state[slot] = ST_CONVERGED;
+      } else if (it + 1 >= max_iter) {
+        w.iters[slot] = it + 1;
+        w.state[slot] = ST_MAXITER;
+      }
+    }
+  }
+}
+
+// Single CTA: advance the iteration base by k and rebuild the compacted list
+// of active slots (stable order).
+__global__ void __launch_bounds__(1024) advance_kernel(Work w, int nb, int k) {
+  __shared__ int warp_tot[32];
+  __shared__ int base;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int start = 0; start < nb; start += 1024) {
+    int s = start + threadIdx.x;
+    int a = (s < nb && w.state[s] == ST_ACTIVE) ? 1 : 0;
+    unsigned m = __ballot_sync(0xffffffffu, a);
+    int pre = __popc(m & ((1u << lane) - 1u));
+    if (lane == 0) warp_tot[wid] = __popc(m);
+    __syncthreads();
+    int off = 0;
+    for (int i = 0; i < wid; ++i) off += warp_tot[i];
+    if (a) w.alist[base + off + pre] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int i = 0; i < 32; ++i) t += warp_tot[i];
+      base += t;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    *w.n_active = base;
+    *w.base_it += k;
+  }
+}
+
+__global__ void finalize_kernel(Work w, int nb) {
+  int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < nb && w.state[s] == ST_ACTIVE) {
+    w.state[s] = ST_MAXITER;
+    w.iters[s] = *w.base_it;
+  }
+}
+
+// prob = seed value | s*y | 0 (zero-rhs brick) | bound (isolated voxel)
+__global__ void __launch_bounds__(NTHREADS) epilogue_kernel(Geo g, Work w, const int* __restrict__ list,
+                                                            const uint8_t* __restrict__ S,
+                                                            const float* __restrict__ bound,
+                                                            float* __restrict__ prob, uint8_t* __restrict__ labels) {
+  TileCtx c = tile_ctx(g, list);
+  if (!c.col) return;
+  const int gy = c.gy0 + c.ly, gx = c.gx0 + c.lx;
+  if (gy < 0 || gy >= g.ny || gx < 0 || gx >= g.nx) return;
+  const int st = w.state[c.slot];
+  const long long sbz = (long long)g.by * g.bx;
+  long long li = (long long)c.slot * g.bvol + (long long)c.ly * g.bx + c.lx + (long long)c.lz0 * sbz;
+  for (int lz = c.lz0; lz < c.lz1; ++lz, li += sbz) {
+    const int gz = c.gz0 + lz;
+    if (gz < 0 || gz >= g.nz) continue;
+    long long gi = (long long)gz * g.sxy + (long long)gy * g.nx + gx;
+    uint8_t sv = S[gi];
+    float s = w.sc[li];
+    float p;
+    if (sv)
+      p = seed_value(sv);
+    else if (s > 0.f)
+      p = st == ST_ZERO ? 0.f : s * w.y[li];
+    else
+      p = bound ? bound[gi] : 0.f;
+    prob[gi] = p;
+    if (labels) labels[gi] = p > 0.5f ? 1 : 0;
+  }
+}
+
+// stat_i: [0] converged [1] maxiter [2] zero-rhs [3] max iterations [4..5] u64 sum of iterations
+__global__ void __launch_bounds__(1024) stats_kernel(Work w, int nb) {
+  __shared__ int sh[4];
+  __shared__ unsigned long long sum;
+  if (threadIdx.x < 4) sh[threadIdx.x] = 0;
+  if (threadIdx.x == 0) sum = 0;
+  __syncthreads();
+  int c1 = 0, c2 = 0, c3 = 0, mx = 0;
+  unsigned long long sm = 0;
+  for (int s = threadIdx.x; s < nb; s += blockDim.x) {
+    int st = w.state[s];
+    c1 += st == ST_CONVERGED;
+    c2 += st == ST_MAXITER;
+    c3 += st == ST_ZERO;
+    int it = st == ST_ZERO ? 0 : w.iters[s];
+    mx = max(mx, it);
+    sm += (unsigned long long)it;
+  }
+  atomicAdd(&sh[0], c1);
+  atomicAdd(&sh[1], c2);
+  atomicAdd(&sh[2], c3);
+  atomicMax(&sh[3], mx);
+  atomicAdd(&sum, sm);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 4; ++i) w.stat_i[i] = sh[i];
+    *reinterpret_cast<unsigned long long*>(w.stat_i + 4) = sum;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+static int make_geo(const rwb_geometry_t* geom, Geo* g) {
+  if (!geom) return fail(RWB_ERR_INVALID, "null geometry");
+  if (geom->ndim != 2 && geom->ndim != 3) return fail(RWB_ERR_INVALID, "solver supports ndim 2 or 3");
+  Shape3 s;
+  int rc = shape_from(geom->ndim, geom->size, &s);
+  if (rc) return rc;
+  int64_t b[3] = {1, 1, 1}, o[3] = {0, 0, 0};
+  for (int i = 0; i < geom->ndim; ++i) {
+    b[3 - geom->ndim + i] = geom->brick[i];
+    o[3 - geom->ndim + i] = geom->origin[i];
+  }
+  for (int i = 0; i < 3; ++i) {
+    if (b[i] < 1 || b[i] > (1 << 20)) return fail(RWB_ERR_INVALID, "brick size out of range");
+    if (o[i] > 0 || o[i] <= -b[i]) return fail(RWB_ERR_INVALID, "origin must lie in (-brick, 0]");
+  }
+  g->nz = s.nz, g->ny = s.ny, g->nx = s.nx;
+  g->bz = (int)b[0], g->by = (int)b[1], g->bx = (int)b[2];
+  g->oz = (int)o[0], g->oy = (int)o[1], g->ox = (int)o[2];
+  g->gz = (int)((s.nz - o[0] + b[0] - 1) / b[0]);
+  g->gy = (int)((s.ny - o[1] + b[1] - 1) / b[1]);
+  g->gx = (int)((s.nx - o[2] + b[2] - 1) / b[2]);
+  g->tz = (g->bz + TZ - 1) / TZ;
+  g->ty = (g->by + TY - 1) / TY;
+  g->tx = (g->bx + TX - 1) / TX;
+  g->tiles = g->tz * g->ty * g->tx;
+  g->bvol = (long long)g->bz * g->by * g->bx;
+  g->sxy = (long long)g->ny * g->nx;
+  g->is3d = geom->ndim == 3;
+  return RWB_OK;
+}
+
+enum { L_Y, L_R, L_P0, L_P1, L_Q, L_WX, L_WY, L_WZ, L_SC, L_RR, L_PQ, L_BB, L_STATE, L_ITERS, L_TICKET,
+       L_ALIST, L_PART, L_MISC, L_N };
+
+struct Layout {
+  size_t off[L_N];
+  size_t total;
+};
+
+static Layout layout(const Geo& g, long long nb) {
+  Layout L;
+  const size_t vox = (size_t)nb * (size_t)g.bvol * sizeof(float);
+  const size_t sizes[L_N] = {vox, vox, vox, vox, vox, vox, vox, g.is3d ? vox : 0, vox,
+                             2 * nb * sizeof(double), nb * sizeof(double), nb * sizeof(double),
+                             nb * sizeof(int), nb * sizeof(int), nb * sizeof(unsigned), nb * sizeof(int),
+                             (size_t)nb * g.tiles * sizeof(float2), 64};
+  size_t o = 0;
+  for (int i = 0; i < L_N; ++i) {
+    L.off[i] = o;
+    o = align_up(o + sizes[i], 256);
+  }
+  L.total = o;
+  return L;
+}
+
+static Work carve(const Layout& L, char* base, const Geo& g) {
+  Work w;
+  float** f[9] = {&w.y, &w.r, &w.p0, &w.p1, &w.q, &w.wx, &w.wy, &w.wz, &w.sc};
+  for (int i = 0; i < 9; ++i) *f[i] = reinterpret_cast<float*>(base + L.off[L_Y + i]);
+  if (!g.is3d) w.wz = nullptr;
+  w.rr = reinterpret_cast<double*>(base + L.off[L_RR]);
+  w.pq = reinterpret_cast<double*>(base + L.off[L_PQ]);
+  w.bb = reinterpret_cast<double*>(base + L.off[L_BB]);
+  w.state = reinterpret_cast<int*>(base + L.off[L_STATE]);
+  w.iters = reinterpret_cast<int*>(base + L.off[L_ITERS]);
+  w.ticket = reinterpret_cast<unsigned*>(base + L.off[L_TICKET]);
+  w.alist = reinterpret_cast<int*>(base + L.off[L_ALIST]);
+  w.part = reinterpret_cast<float2*>(base + L.off[L_PART]);
+  char* misc = base + L.off[L_MISC];
+  w.base_it = reinterpret_cast<int*>(misc);
+  w.n_active = reinterpret_cast<int*>(misc + 4);
+  w.unknowns = reinterpret_cast<unsigned long long*>(misc + 8);
+  w.stat_i = reinterpret_cast<int*>(misc + 16);
+  return w;
+}
+
+struct PinnedScratch {
+  int* host = nullptr;
+  ~PinnedScratch() {
+    if (host) cudaFreeHost(host);
+  }
+};
+static thread_local PinnedScratch t_pinned;
+
+static int pinned(int** out) {
+  if (!t_pinned.host) RWB_CUDA(cudaHostAlloc(&t_pinned.host, 64, cudaHostAllocDefault));
+  *out = t_pinned.host;
+  return RWB_OK;
+}
+
+static int persistent_grid(int* grid) {
+  static thread_local int cached = 0;
+  if (!cached) {
+    int dev = 0, sms = 0, per1 = 0, per2 = 0;
+    RWB_CUDA(cudaGetDevice(&dev));
+    RWB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, cg_pass1_kernel, NTHREADS, 0));
+    RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, cg_pass2_kernel, NTHREADS, 0));
+    cached = sms * std::max(1, std::min(per1, per2));
+  }
+  *grid = cached;
+  return RWB_OK;
+}
+
+static int launch_chunk(const Geo& g, const Work& w, int nb, const int* list, int k, float tol2, int max_iter,
+                        int grid, cudaStream_t st) {
+  // counted by the caller (graph replays count 2k+1 kernels each)
+  dim3 block(TX, TY);
+  for (int j = 0; j < k; ++j) {
+    cg_pass1_kernel<<<grid, block, 0, st>>>(g, w, nb, list, j);
+    cg_pass2_kernel<<<grid, block, 0, st>>>(g, w, nb, list, j, tol2, max_iter);
+  }
+  advance_kernel<<<1, 1024, 0, st>>>(w, nb, k);
+  RWB_LAUNCH_CHECK("cg iteration kernels");
+  return RWB_OK;
+}
+
+}  // namespace rwb
+
+using namespace rwb;
+
+extern "C" size_t rwb_solve_workspace_bytes(const rwb_geometry_t* geom, int64_t n_bricks) {
+  Geo g;
+  if (make_geo(geom, &g)) return 0;
+  long long total = (long long)g.gz * g.gy * g.gx;
+  long long nb = n_bricks < 0 ? total : n_bricks;
+  return layout(g, nb).total;
+}
+
+extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensity, const uint8_t* seeds,
+                               const float* bound, const int32_t* brick_list, int64_t n_bricks,
+                               const rwb_solve_params_t* params, float* prob, uint8_t* labels, void* workspace,
+                               size_t workspace_bytes, rwb_solve_stats_t* stats, void* stream) {
+  Geo g;
+  int rc = make_geo(geom, &g);
+  if (rc) return rc;
+  if (!intensity || !seeds || !prob || !params || !workspace) return fail(RWB_ERR_INVALID, "null pointer");
+  const long long total = (long long)g.gz * g.gy * g.gx;
+  const long long nbl = brick_list ? n_bricks : total;
+  if (nbl < 0 || nbl > total) return fail(RWB_ERR_INVALID, "n_bricks out of range");
+  if (!bound && total > 1) return fail(RWB_ERR_INVALID, "bound may be NULL only for a single-brick level");
+  if (!(params->tol >= 0.f) || !(params->beta >= 0.f) || !(params->min_weight >= 0.f) || params->max_iter < 0)
+    return fail(RWB_ERR_INVALID, "invalid solve parameters");
+  if (nbl * (long long)g.tiles >= (1ll << 31)) return fail(RWB_ERR_INVALID, "too many bricks for one launch");
+  const Layout L = layout(g, nbl);
+  if (workspace_bytes < L.total)
+    return fail(RWB_ERR_WORKSPACE, "workspace too small: need " + std::to_string(L.total) + " bytes");
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  if (nbl == 0) return RWB_OK;
+  const int nb = (int)nbl;
+  cudaStream_t st = (cudaStream_t)stream;
+  Work w = carve(L, (char*)workspace, g);
+  const int* list = brick_list;
+  const float tol2 = params->tol * params->tol;
+  const int max_iter = params->max_iter;
+  int k = params->check_every > 0 ? params->check_every : 16;
+  k += k & 1;  // parity of the global iteration must match the captured j
+  int grid = 0;
+  rc = persistent_grid(&grid);
+  if (rc) return rc;
+
+  // zero the scalar region (rr .. misc) in one memset
+  RWB_CUDA(cudaMemsetAsync((char*)workspace + L.off[L_RR], 0, L.total - L.off[L_RR], st));
+  const unsigned sgrid = (unsigned)((long long)nb * g.tiles);
+  dim3 block(TX, TY);
+  setup_scale_kernel<<<sgrid, block, 0, st>>>(g, w, list, intensity, seeds, params->beta, params->min_weight);
+  setup_system_kernel<<<sgrid, block, 0, st>>>(g, w, list, intensity, seeds, bound, params->beta,
+                                               params->min_weight, tol2, max_iter);
+  advance_kernel<<<1, 1024, 0, st>>>(w, nb, 0);
+  RWB_LAUNCH_CHECK("setup kernels");
+  count_launches(3);
+
+  int* host = nullptr;
+  rc = pinned(&host);
+  if (rc) return rc;
+  RWB_CUDA(cudaMemcpyAsync(host, w.n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
+  RWB_CUDA(cudaStreamSynchronize(st));
+  int active = host[0];
+
+  cudaGraphExec_t exec = nullptr;
+  const bool use_graph = !(params->flags & RWB_SOLVE_NO_GRAPH);
+  if (use_graph && active > 0) {
+    cudaStream_t cap;
+    RWB_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      rc = launch_chunk(g, w, nb, list, k, tol2, max_iter, grid, cap);
+      cudaError_t e2 = cudaStreamEndCapture(cap, &graph);
+      if (e2 != cudaSuccess) e = e2;
+      if (rc == RWB_OK && e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+      if (graph) cudaGraphDestroy(graph);
+    }
+    cudaStreamDestroy(cap);
+    if (rc) return rc;
+    if (e != cudaSuccess) return cuda_fail(e, "graph capture of the CG iterations");
+  }
+
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  RWB_CUDA(cudaEventCreate(&ev0));
+  RWB_CUDA(cudaEventCreate(&ev1));
+  float cg_ms = 0.f;
+  int sweeps = 0;
+  while (active > 0 && sweeps < max_iter) {
+    RWB_CUDA(cudaEventRecord(ev0, st));
+    if (exec) {
+      cudaError_t e = cudaGraphLaunch(exec, st);
+      if (e != cudaSuccess) {
+        cudaGraphExecDestroy(exec);
+        return cuda_fail(e, "cudaGraphLaunch");
+      }
+    } else {
+      rc = launch_chunk(g, w, nb, list, k, tol2, max_iter, grid, st);
+      if (rc) return rc;
+    }
+    sweeps += k;
+    count_launches(2 * k + 1);
+    cudaError_t e = cudaEventRecord(ev1, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(host, w.n_active, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    float ms = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, ev0, ev1);
+    if (e != cudaSuccess) {
+      if (exec) cudaGraphExecDestroy(exec);
+      cudaEventDestroy(ev0);
+      cudaEventDestroy(ev1);
+      return cuda_fail(e, "convergence poll");
+    }
+    cg_ms += ms;
+    active = host[0];
+  }
+  if (exec) cudaGraphExecDestroy(exec);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+
+  finalize_kernel<<<(nb + 255) / 256, 256, 0, st>>>(w, nb);
+  epilogue_kernel<<<sgrid, block, 0, st>>>(g, w, list, seeds, bound, prob, labels);
+  stats_kernel<<<1, 1024, 0, st>>>(w, nb);
+  RWB_LAUNCH_CHECK("epilogue kernels");
+  count_launches(3);
+  if (stats) {
+    int hs[8];
+    unsigned long long unk = 0;
+    RWB_CUDA(cudaMemcpyAsync(hs, w.stat_i, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    RWB_CUDA(cudaMemcpyAsync(&unk, w.unknowns, sizeof(unk), cudaMemcpyDeviceToHost, st));
+    RWB_CUDA(cudaStreamSynchronize(st));
+    stats->bricks = nb;
+    stats->converged = hs[0];
+    stats->not_converged = hs[1];
+    stats->zero_rhs = hs[2];
+    stats->iterations_max = hs[3];
+    unsigned long long s64;
+    std::memcpy(&s64, hs + 4, sizeof(s64));
+    stats->iterations_sum = (int64_t)s64;
+    stats->unknowns = (int64_t)unk;
+    stats->sweeps = sweeps;
+    stats->cg_ms = cg_ms;
+  }
+  return RWB_OK;
+}

@@ -1,0 +1,277 @@
+"""Device-resident hot path: torch tensors in HBM -> librwb kernels.
+
+PyTorch only provides device memory and the current CUDA stream; every
+arithmetic step runs in the hand-written sm_100a kernels of librwb.so
+(`csrc/`), called through the C ABI of `include/rwb.h`.
+
+Level layout in HBM: one dense row-major tensor per pyramid level (f32
+intensity, u8 seeds, f32 probabilities), exactly the logical tensors of the
+reference's `TensorMetaData` (model.py:98-177); bricks are windows of the
+chunk grid.  The solver's brick-local workspace is a caller-owned uint8
+tensor (`Workspace`), reused across levels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _native
+from .config import RWConfig
+
+
+def _stream_handle():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t: torch.Tensor | None):
+    return ctypes.c_void_p(t.data_ptr() if t is not None else 0)
+
+
+def _check_tensor(t: torch.Tensor, dtype, name: str, ndim=None):
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (the random-walker path has no CPU fallback)")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if ndim is not None and t.dim() not in ndim:
+        raise ValueError(f"{name} must have {ndim} dims, got {t.dim()}")
+
+
+def coarse_shape(shape):
+    return tuple(-(-int(s) // 2) for s in shape)
+
+
+# ---------------------------------------------------------------------------
+# per-voxel operators
+
+
+def lod_down(level: torch.Tensor) -> torch.Tensor:
+    """Next coarser LOD level (bit-identical to the reference's conv+downsample)."""
+    _check_tensor(level, torch.float32, "level", (1, 2, 3))
+    lib = _native.lib()
+    out = torch.empty(coarse_shape(level.shape), dtype=torch.float32, device=level.device)
+    _native.check(lib.rwb_lod_down_f32(level.dim(), _native.int64_array(level.shape), _ptr(level), _ptr(out),
+                                       _stream_handle()))
+    return out
+
+
+def num_lod_levels(shape, chunk) -> int:
+    """Level count of the reference's `build_lod` stop rule (ops.py:720)."""
+    shape = [int(s) for s in shape]
+    n = 1
+    while any(s > c for s, c in zip(shape, chunk)):
+        shape = [-(-s // 2) for s in shape]
+        n += 1
+    return n
+
+
+def lod_chain(volume: torch.Tensor, chunk, levels: int | None = None) -> list:
+    total = num_lod_levels(volume.shape, chunk)
+    levels = total if levels is None else int(levels)
+    if not 1 <= levels <= total:
+        raise ValueError(f"levels={levels} outside 1..{total} for size {tuple(volume.shape)}, chunk {tuple(chunk)}")
+    out = [volume]
+    for _ in range(levels - 1):
+        out.append(lod_down(out[-1]))
+    return out
+
+
+def project_seeds(seeds: torch.Tensor) -> torch.Tensor:
+    _check_tensor(seeds, torch.uint8, "seeds", (1, 2, 3))
+    lib = _native.lib()
+    out = torch.empty(coarse_shape(seeds.shape), dtype=torch.uint8, device=seeds.device)
+    _native.check(lib.rwb_project_seeds_u8(seeds.dim(), _native.int64_array(seeds.shape), _ptr(seeds), _ptr(out),
+                                           _stream_handle()))
+    return out
+
+
+def upsample(parent: torch.Tensor, fine_shape, out: torch.Tensor | None = None) -> torch.Tensor:
+    _check_tensor(parent, torch.float32, "parent", (1, 2, 3))
+    fine_shape = tuple(int(s) for s in fine_shape)
+    if out is None:
+        out = torch.empty(fine_shape, dtype=torch.float32, device=parent.device)
+    _check_tensor(out, torch.float32, "out")
+    if tuple(out.shape) != fine_shape:
+        raise ValueError("out has the wrong shape")
+    lib = _native.lib()
+    _native.check(lib.rwb_upsample_f32(parent.dim(), _native.int64_array(parent.shape), _ptr(parent),
+                                       _native.int64_array(fine_shape), _ptr(out), _stream_handle()))
+    return out
+
+
+def edge_weights(volume: torch.Tensor, beta: float = 100.0, min_weight: float = 1e-6) -> torch.Tensor:
+    """Forward edge weights, lanes-last: shape volume.shape + (ndim,)."""
+    _check_tensor(volume, torch.float32, "volume", (1, 2, 3))
+    lib = _native.lib()
+    out = torch.empty(tuple(volume.shape) + (volume.dim(),), dtype=torch.float32, device=volume.device)
+    _native.check(lib.rwb_edge_weights_f32(volume.dim(), _native.int64_array(volume.shape), _ptr(volume),
+                                           float(beta), float(min_weight), _ptr(out), _stream_handle()))
+    return out
+
+
+def labels(prob: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    _check_tensor(prob, torch.float32, "prob")
+    if out is None:
+        out = torch.empty(prob.shape, dtype=torch.uint8, device=prob.device)
+    _check_tensor(out, torch.uint8, "out")
+    lib = _native.lib()
+    _native.check(lib.rwb_labels_u8(prob.numel(), _ptr(prob), _ptr(out), _stream_handle()))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# level solve
+
+
+class Workspace:
+    """Grow-only device scratch buffer for the brick solver."""
+
+    def __init__(self, device=None):
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.buffer = None
+
+    def get(self, nbytes: int) -> torch.Tensor:
+        if self.buffer is None or self.buffer.numel() < nbytes:
+            self.buffer = None
+            self.buffer = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+        return self.buffer
+
+    def release(self):
+        self.buffer = None
+
+
+def geometry(shape, brick, origin=None) -> _native.Geometry:
+    nd = len(shape)
+    if nd not in (2, 3):
+        raise ValueError("the random walker supports 2-D and 3-D levels")
+    if len(brick) != nd:
+        raise ValueError("brick dimensionality mismatch")
+    g = _native.Geometry()
+    g.ndim = nd
+    origin = origin or (0,) * nd
+    for i in range(nd):
+        g.size[i] = int(shape[i])
+        g.brick[i] = int(brick[i])
+        g.origin[i] = int(origin[i])
+    return g
+
+
+def brick_grid(shape, brick, origin=None):
+    origin = origin or (0,) * len(shape)
+    return tuple(-(-(int(s) - int(o)) // int(b)) for s, b, o in zip(shape, brick, origin))
+
+
+def workspace_bytes(shape, brick, n_bricks=-1, origin=None) -> int:
+    g = geometry(shape, brick, origin)
+    return int(_native.load_library().rwb_solve_workspace_bytes(ctypes.byref(g), int(n_bricks)))
+
+
+def solve_level(volume: torch.Tensor, seeds: torch.Tensor, brick, bound: torch.Tensor | None = None,
+                cfg: RWConfig = RWConfig(), *, brick_list: torch.Tensor | None = None, out: torch.Tensor | None = None,
+                labels_out: torch.Tensor | None = None, workspace: Workspace | None = None,
+                origin=None) -> tuple:
+    """Random-walker solve of (the listed bricks of) one level.
+
+    `bound` = upsampled parent probabilities (Dirichlet values outside each
+    brick and initial guess); None only when `brick` covers the level.
+    `out` may be `bound` itself (in-place).  Returns (prob, stats dict).
+    """
+    _check_tensor(volume, torch.float32, "volume", (2, 3))
+    _check_tensor(seeds, torch.uint8, "seeds")
+    if seeds.shape != volume.shape:
+        raise ValueError("seeds and volume shapes differ")
+    if bound is not None:
+        _check_tensor(bound, torch.float32, "bound")
+        if bound.shape != volume.shape:
+            raise ValueError("bound and volume shapes differ")
+    if out is None:
+        out = torch.empty(volume.shape, dtype=torch.float32, device=volume.device)
+    _check_tensor(out, torch.float32, "out")
+    if labels_out is not None:
+        _check_tensor(labels_out, torch.uint8, "labels_out")
+    n_list = -1
+    if brick_list is not None:
+        _check_tensor(brick_list, torch.int32, "brick_list", (1,))
+        n_list = brick_list.numel()
+    g = geometry(volume.shape, brick, origin)
+    if bound is None and any(n > 1 for n in brick_grid(volume.shape, brick, origin)):
+        raise ValueError("a brick-wise solve needs `bound` (the upsampled parent level)")
+    lib = _native.lib()
+    nbytes = int(lib.rwb_solve_workspace_bytes(ctypes.byref(g), n_list))
+    if nbytes == 0:
+        raise ValueError(f"invalid solver geometry: {_native.load_library().rwb_last_error().decode()}")
+    workspace = workspace or Workspace(volume.device)
+    ws = workspace.get(nbytes)
+    p = _native.SolveParams()
+    p.beta, p.min_weight, p.tol = float(cfg.beta), float(cfg.min_weight), float(cfg.tol)
+    p.max_iter, p.check_every = int(cfg.max_iter), int(cfg.check_every)
+    p.flags = 0 if cfg.use_graph else _native.SOLVE_NO_GRAPH
+    stats = _native.SolveStats()
+    _native.check(lib.rwb_solve_level(
+        ctypes.byref(g), _ptr(volume), _ptr(seeds), _ptr(bound), _ptr(brick_list), int(max(n_list, 0)),
+        ctypes.byref(p), _ptr(out), _ptr(labels_out), _ptr(ws), ctypes.c_size_t(ws.numel()),
+        ctypes.byref(stats), _stream_handle()))
+    return out, stats.as_dict()
+
+
+# ---------------------------------------------------------------------------
+# hierarchical driver
+
+
+@dataclass
+class HRWResult:
+    prob: torch.Tensor            # level-0 probabilities (f32)
+    labels: torch.Tensor | None   # level-0 labels (u8, p > 0.5)
+    levels: list                  # per-level probabilities, level 0 finest
+    volumes: list                 # LOD pyramid used
+    seeds: list                   # projected seeds per level
+    stats: list = field(default_factory=list)  # per-level solver stats (level 0 first)
+
+
+def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick, levels: int | None = None,
+                               cfg: RWConfig = RWConfig(), *, want_labels: bool = True,
+                               workspace: Workspace | None = None, brick_lists=None,
+                               exchange=None) -> HRWResult:
+    """Coarse-to-fine random walker (oracle/rw.py: hierarchical_random_walker).
+
+    The coarsest level is solved whole; each finer level is initialised and
+    bounded by the upsampled solution of the level above and solved brick
+    by brick.  `brick_lists[k]` (int32 device tensor) restricts level k to a
+    subset of bricks (multi-GPU sharding) and `exchange(k, prob_k)` is called
+    after level k is solved so the caller can complete the halo of the
+    parent level before it is upsampled (see sharding.py).
+    """
+    brick = tuple(int(b) for b in brick)
+    vols = lod_chain(volume, brick, levels)
+    seed_levels = [seeds]
+    for _ in range(len(vols) - 1):
+        seed_levels.append(project_seeds(seed_levels[-1]))
+    workspace = workspace or Workspace(volume.device)
+    nlev = len(vols)
+    probs = [None] * nlev
+    stats = [None] * nlev
+    top = nlev - 1
+    lab = None
+    top_labels = torch.empty(vols[top].shape, dtype=torch.uint8, device=volume.device) \
+        if (want_labels and top == 0) else None
+    probs[top], stats[top] = solve_level(vols[top], seed_levels[top], tuple(vols[top].shape), None, cfg,
+                                         labels_out=top_labels, workspace=workspace)
+    lab = top_labels
+    for k in range(top - 1, -1, -1):
+        if exchange is not None:
+            exchange(k + 1, probs[k + 1])
+        x = upsample(probs[k + 1], vols[k].shape)
+        lab_k = torch.empty(vols[k].shape, dtype=torch.uint8, device=volume.device) \
+            if (want_labels and k == 0) else None
+        bl = brick_lists[k] if brick_lists is not None else None
+        probs[k], stats[k] = solve_level(vols[k], seed_levels[k], brick, x, cfg, brick_list=bl, out=x,
+                                         labels_out=lab_k, workspace=workspace)
+        if k == 0:
+            lab = lab_k
+    return HRWResult(probs[0], lab, probs, vols, seed_levels, stats)
