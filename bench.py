@@ -38,7 +38,7 @@ WORKLOADS = {
     "c4": dict(shape=(1024, 1024, 1024), brick=(32, 32, 32), levels=4,
                desc="config 4: 1024^3 f32 two-blob phantom + noise, 4-level hierarchy (1024/512/256/128), "
                     "32^3 bricks, seeds S1",
-               sample=dict(shape=(128, 128, 128), levels=4)),
+               sample=dict(shape=(256, 256, 256), levels=4)),
     "c2": dict(shape=(256, 256, 256), brick=(32, 32, 32), levels=2,
                desc="config 2: 256^3 f32 two-blob phantom + noise, 2-level hierarchy, 32^3 bricks, seeds S1",
                sample=dict(shape=(128, 128, 128), levels=2)),

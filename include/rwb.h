@@ -67,7 +67,12 @@ typedef struct {
   int32_t flags;       /* RWB_SOLVE_* */
 } rwb_solve_params_t;
 
-#define RWB_SOLVE_NO_GRAPH 1 /* launch iterations directly instead of via a CUDA graph */
+#define RWB_SOLVE_NO_GRAPH 1  /* streaming solver: launch iterations directly, not via a CUDA graph */
+#define RWB_SOLVE_STREAMING 2 /* force the streaming solver even where the brick-resident one applies */
+
+/* Solver paths (rwb_solve_stats_t.path) */
+#define RWB_PATH_STREAMING 0 /* brick-batched CG, state in HBM, 2 launches per iteration */
+#define RWB_PATH_RESIDENT 1  /* one 32^3 brick per 8-CTA cluster, CG state on chip */
 
 typedef struct {
   int64_t bricks;          /* bricks solved by this call */
@@ -77,8 +82,11 @@ typedef struct {
   int64_t iterations_max;  /* max over bricks */
   int64_t iterations_sum;  /* sum over bricks (for algorithmic-byte accounting) */
   int64_t unknowns;        /* unseeded voxels solved for */
-  int32_t sweeps;          /* PCG iterations launched (= iterations_max rounded up to a poll) */
-  float cg_ms;             /* device time of the CG iteration launches (CUDA events on `stream`) */
+  int32_t sweeps;          /* streaming: CG iterations launched (iterations_max rounded up to a poll) */
+  float cg_ms;             /* device time of the solve launches (CUDA events on `stream`): streaming =
+                              the CG iteration kernels; resident = the whole on-chip brick solve */
+  int32_t path;            /* RWB_PATH_* that ran */
+  int32_t reserved;
 } rwb_solve_stats_t;
 
 int rwb_abi_version(void);
@@ -110,6 +118,16 @@ int rwb_project_seeds_u8(int32_t ndim, const int64_t* size, const uint8_t* fine,
 int rwb_upsample_f32(int32_t ndim, const int64_t* parent_size, const float* parent,
                      const int64_t* fine_size, float* fine, void* stream);
 
+/* Windowed prolongation for operator mode, where a chunk kernel only holds
+ * the parent chunks around its brick: computes the fine voxels
+ * [fine_origin, fine_origin + fine_window) of a level of size fine_size from
+ * the parent window [parent_origin, parent_origin + parent_window) of a parent
+ * level of size parent_size (taps use global coordinates, identical to
+ * rwb_upsample_f32; the parent window must cover them). */
+int rwb_upsample_window_f32(int32_t ndim, const int64_t* parent_size, const int64_t* parent_origin,
+                            const int64_t* parent_window, const float* parent, const int64_t* fine_size,
+                            const int64_t* fine_origin, const int64_t* fine_window, float* fine, void* stream);
+
 /* Forward edge weights, lanes-last (the ElementType(F32, ndim) payload layout,
  * model.py:66-80): weights[i*ndim + k] = max(exp(-beta*(I_i - I_{i+e_k})^2), min_weight),
  * 0 where i+e_k is outside the volume. */
@@ -119,8 +137,9 @@ int rwb_edge_weights_f32(int32_t ndim, const int64_t* size, const float* volume,
 /* labels[i] = prob[i] > 0.5 (cast_array semantics of a boolean, ops.py:44-52). */
 int rwb_labels_u8(int64_t n, const float* prob, uint8_t* labels, void* stream);
 
-/* Bytes of solver workspace for n_bricks bricks of `geom` (n_bricks < 0: all). */
-size_t rwb_solve_workspace_bytes(const rwb_geometry_t* geom, int64_t n_bricks);
+/* Bytes of solver workspace for n_bricks bricks of `geom` (n_bricks < 0: all)
+ * with the given RWB_SOLVE_* flags (the brick-resident path needs almost none). */
+size_t rwb_solve_workspace_bytes(const rwb_geometry_t* geom, int64_t n_bricks, int32_t flags);
 
 /* Random-walker solve of the listed bricks of one level.
  *  intensity : f32 level (size)         seeds : u8 level, 0/1/2
@@ -131,9 +150,14 @@ size_t rwb_solve_workspace_bytes(const rwb_geometry_t* geom, int64_t n_bricks);
  *  brick_list: device int32 row-major brick indices, or NULL for all bricks
  *              (n_bricks then ignored).  Listed bricks must be distinct.
  *  prob      : f32 level output; written only inside the listed bricks.  May
- *              alias `bound` (all reads of bound happen before any write).
+ *              alias `bound` on the streaming path only (all its reads of
+ *              bound happen before any write); the brick-resident path
+ *              solves bricks at different times and rejects aliasing.
  *  labels    : u8 level output (prob > 0.5) or NULL.
  *  stats     : host pointer or NULL.
+ * Path: 3-D levels with 32^3 bricks and more than one brick run the
+ * brick-resident solver (unless RWB_SOLVE_STREAMING); everything else —
+ * including every whole-level (coarsest) solve — runs the streaming solver.
  * Blocking on the host: returns when the listed bricks have converged (or hit
  * max_iter); all work is stream-ordered on `stream`. */
 int rwb_solve_level(const rwb_geometry_t* geom, const float* intensity, const uint8_t* seeds,

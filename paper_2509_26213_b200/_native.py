@@ -20,6 +20,8 @@ c_int32, c_int64, c_float, c_void_p, c_size_t = (
 
 ABI_VERSION = 1
 SOLVE_NO_GRAPH = 1
+SOLVE_STREAMING = 2
+PATH_STREAMING, PATH_RESIDENT = 0, 1
 
 # every symbol include/rwb.h declares, with (restype, argtypes)
 SIGNATURES = {
@@ -31,10 +33,12 @@ SIGNATURES = {
     "rwb_project_seeds_u8": (c_int32, [c_int32, ctypes.POINTER(c_int64), c_void_p, c_void_p, c_void_p]),
     "rwb_upsample_f32": (c_int32, [c_int32, ctypes.POINTER(c_int64), c_void_p, ctypes.POINTER(c_int64),
                                    c_void_p, c_void_p]),
+    "rwb_upsample_window_f32": (c_int32, [c_int32] + [ctypes.POINTER(c_int64)] * 3 + [c_void_p] +
+                                [ctypes.POINTER(c_int64)] * 3 + [c_void_p, c_void_p]),
     "rwb_edge_weights_f32": (c_int32, [c_int32, ctypes.POINTER(c_int64), c_void_p, c_float, c_float,
                                        c_void_p, c_void_p]),
     "rwb_labels_u8": (c_int32, [c_int64, c_void_p, c_void_p, c_void_p]),
-    "rwb_solve_workspace_bytes": (c_size_t, [c_void_p, c_int64]),
+    "rwb_solve_workspace_bytes": (c_size_t, [c_void_p, c_int64, c_int32]),
     "rwb_solve_level": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
                                   c_void_p, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]),
 }
@@ -67,10 +71,11 @@ class SolveParams(ctypes.Structure):
 class SolveStats(ctypes.Structure):
     _fields_ = [("bricks", c_int64), ("converged", c_int64), ("not_converged", c_int64),
                 ("zero_rhs", c_int64), ("iterations_max", c_int64), ("iterations_sum", c_int64),
-                ("unknowns", c_int64), ("sweeps", c_int32), ("cg_ms", c_float)]
+                ("unknowns", c_int64), ("sweeps", c_int32), ("cg_ms", c_float), ("path", c_int32),
+                ("reserved", c_int32)]
 
     def as_dict(self):
-        out = {name: int(getattr(self, name)) for name, _ in self._fields_ if name != "cg_ms"}
+        out = {name: int(getattr(self, name)) for name, _ in self._fields_ if name not in ("cg_ms", "reserved")}
         out["cg_ms"] = float(self.cg_ms)
         return out
 

@@ -17,10 +17,12 @@ class RWConfig:
     tol: float = 1e-6          # per-brick ||r|| <= tol * ||b|| on the Jacobi-scaled system
     max_iter: int = 10_000     # per-brick iteration cap
     check_every: int = 16      # CG iterations per convergence poll (one CUDA graph)
-    use_graph: bool = True     # run each poll interval as one CUDA graph launch
+    use_graph: bool = True     # streaming solver: run each poll interval as one CUDA graph launch
+    resident: bool = True      # 32^3 bricks: solve each brick on chip (8-CTA cluster) instead of streaming
 
     def params(self) -> dict:
         d = asdict(self)
         d.pop("check_every")
         d.pop("use_graph")
+        d.pop("resident")
         return {k: (float(v) if isinstance(v, float) else int(v)) for k, v in d.items()}

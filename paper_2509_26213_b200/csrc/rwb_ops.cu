@@ -198,6 +198,38 @@ __global__ void __launch_bounds__(256) upsample_kernel(const float* __restrict__
   fine[o] = tz.w0 * r0 + tz.w1 * r1;
 }
 
+// Windowed variant: fine voxels [fo, fo+fw) of a level whose parent has size
+// ps; the parent is given as the window [po, po+pw).  Taps are computed from
+// global coordinates (clamped to the full parent), then read from the window.
+__device__ __forceinline__ Taps up_taps_win(int g, int m, int po) {
+  Taps t = up_taps(g, m);
+  t.i0 -= po;
+  t.i1 -= po;
+  return t;
+}
+
+__global__ void __launch_bounds__(256) upsample_window_kernel(const float* __restrict__ parent, Shape3 ps, Shape3 po,
+                                                              Shape3 pw, float* __restrict__ fine, Shape3 fo,
+                                                              Shape3 fw, Shape3 fsz) {
+  long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= fw.count()) return;
+  int lx = (int)(o % fw.nx);
+  long long t = o / fw.nx;
+  int ly = (int)(t % fw.ny);
+  int lz = (int)(t / fw.ny);
+  Taps tz = fsz.nz > 1 ? up_taps_win(fo.nz + lz, ps.nz, po.nz) : Taps{0, 0, 1.0f, 0.0f};
+  Taps ty = fsz.ny > 1 ? up_taps_win(fo.ny + ly, ps.ny, po.ny) : Taps{0, 0, 1.0f, 0.0f};
+  Taps tx = up_taps_win(fo.nx + lx, ps.nx, po.nx);
+  const long long sxy = (long long)pw.ny * pw.nx;
+  auto row = [&](int z, int y) {
+    const float* p = parent + z * sxy + (long long)y * pw.nx;
+    return tx.w0 * __ldg(p + tx.i0) + tx.w1 * __ldg(p + tx.i1);
+  };
+  float r0 = ty.w0 * row(tz.i0, ty.i0) + ty.w1 * row(tz.i0, ty.i1);
+  float r1 = ty.w0 * row(tz.i1, ty.i0) + ty.w1 * row(tz.i1, ty.i1);
+  fine[o] = tz.w0 * r0 + tz.w1 * r1;
+}
+
 // ---------------------------------------------------------------------------
 // forward edge weights, lanes-last
 
@@ -305,6 +337,54 @@ extern "C" int rwb_upsample_f32(int32_t ndim, const int64_t* parent_size, const 
     return fail(RWB_ERR_INVALID, "fine size is not a 2x refinement of the parent size");
   upsample_kernel<<<ceil_div_u(fs.count(), 256), 256, 0, (cudaStream_t)stream>>>(parent, ps, fine, fs);
   RWB_LAUNCH_CHECK("upsample_kernel");
+  count_launches(1);
+  return RWB_OK;
+}
+
+static int shape_raw(int32_t ndim, const int64_t* v, bool allow_zero_origin, Shape3* out) {
+  int64_t s[3] = {allow_zero_origin ? 0 : 1, allow_zero_origin ? 0 : 1, allow_zero_origin ? 0 : 1};
+  if (!v) return fail(RWB_ERR_INVALID, "null shape");
+  for (int i = 0; i < ndim; ++i) {
+    if (v[i] < (allow_zero_origin ? 0 : 1) || v[i] > (1ll << 30)) return fail(RWB_ERR_INVALID, "window out of range");
+    s[3 - ndim + i] = v[i];
+  }
+  out->nz = (int)s[0];
+  out->ny = (int)s[1];
+  out->nx = (int)s[2];
+  return RWB_OK;
+}
+
+extern "C" int rwb_upsample_window_f32(int32_t ndim, const int64_t* parent_size, const int64_t* parent_origin,
+                                       const int64_t* parent_window, const float* parent, const int64_t* fine_size,
+                                       const int64_t* fine_origin, const int64_t* fine_window, float* fine,
+                                       void* stream) {
+  if (ndim < 1 || ndim > 3) return fail(RWB_ERR_INVALID, "ndim must be 1..3");
+  Shape3 ps, po, pw, fs, fo, fw, chk;
+  int rc = shape_raw(ndim, parent_size, false, &ps);
+  if (!rc) rc = shape_raw(ndim, parent_origin, true, &po);
+  if (!rc) rc = shape_raw(ndim, parent_window, false, &pw);
+  if (!rc) rc = shape_raw(ndim, fine_size, false, &fs);
+  if (!rc) rc = shape_raw(ndim, fine_origin, true, &fo);
+  if (!rc) rc = shape_raw(ndim, fine_window, false, &fw);
+  if (rc) return rc;
+  if (!parent || !fine) return fail(RWB_ERR_INVALID, "null pointer");
+  coarse_of(fs, &chk);
+  const int fd[3] = {fs.nz, fs.ny, fs.nx}, cd[3] = {chk.nz, chk.ny, chk.nx}, pd[3] = {ps.nz, ps.ny, ps.nx};
+  const int pod[3] = {po.nz, po.ny, po.nx}, pwd[3] = {pw.nz, pw.ny, pw.nx};
+  const int fod[3] = {fo.nz, fo.ny, fo.nx}, fwd[3] = {fw.nz, fw.ny, fw.nx};
+  for (int d = 3 - ndim; d < 3; ++d) {
+    if (cd[d] != pd[d]) return fail(RWB_ERR_INVALID, "fine size is not a 2x refinement of the parent size");
+    if (fod[d] + fwd[d] > fd[d] || pod[d] + pwd[d] > pd[d]) return fail(RWB_ERR_INVALID, "window outside the level");
+    // parent rows the taps of the fine window touch must lie inside the parent window
+    int g0 = fod[d], g1 = fod[d] + fwd[d] - 1;
+    int lo = (g0 & 1) ? g0 / 2 : (g0 / 2 > 0 ? g0 / 2 - 1 : 0);
+    int hi = (g1 & 1) ? (g1 / 2 + 1 < pd[d] ? g1 / 2 + 1 : pd[d] - 1) : g1 / 2;
+    if (fd[d] == 1) lo = hi = 0;
+    if (lo < pod[d] || hi >= pod[d] + pwd[d]) return fail(RWB_ERR_INVALID, "parent window does not cover the taps");
+  }
+  upsample_window_kernel<<<ceil_div_u(fw.count(), 256), 256, 0, (cudaStream_t)stream>>>(parent, ps, po, pw, fine, fo,
+                                                                                          fw, fs);
+  RWB_LAUNCH_CHECK("upsample_window_kernel");
   count_launches(1);
   return RWB_OK;
 }

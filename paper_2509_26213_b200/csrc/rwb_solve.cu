@@ -34,6 +34,7 @@
 #include <vector>
 
 #include "rwb_common.cuh"
+#include "rwb_resident.cuh"
 
 namespace rwb {
 
@@ -41,20 +42,6 @@ constexpr int TX = 32;  // threads along x (one warp per row segment)
 constexpr int TY = 8;   // threads along y
 constexpr int TZ = 8;   // z extent marched by each thread
 constexpr int NTHREADS = TX * TY;
-
-enum BrickState : int { ST_ACTIVE = 0, ST_CONVERGED = 1, ST_MAXITER = 2, ST_ZERO = 3 };
-
-struct Geo {
-  int nz, ny, nx;  // level
-  int bz, by, bx;  // brick box
-  int oz, oy, ox;  // brick grid origin
-  int gz, gy, gx;  // brick grid
-  int tz, ty, tx;  // tiles per brick
-  int tiles;
-  long long bvol;  // bz*by*bx
-  long long sxy;   // ny*nx
-  int is3d;
-};
 
 struct Work {
   float *y, *r, *p0, *p1, *q, *wx, *wy, *wz, *sc;
@@ -640,12 +627,90 @@ static int launch_chunk(const Geo& g, const Work& w, int nb, const int* list, in
 
 using namespace rwb;
 
-extern "C" size_t rwb_solve_workspace_bytes(const rwb_geometry_t* geom, int64_t n_bricks) {
+static bool use_resident(const Geo& g, long long total, int flags) {
+  return !(flags & RWB_SOLVE_STREAMING) && total > 1 && resident3d_supported(g);
+}
+
+// resident path: per-slot state/iters + counter/stats scratch only
+static size_t resident_bytes(long long nb) { return align_up(2 * (size_t)nb * sizeof(int), 256) + 256; }
+
+extern "C" size_t rwb_solve_workspace_bytes(const rwb_geometry_t* geom, int64_t n_bricks, int32_t flags) {
   Geo g;
   if (make_geo(geom, &g)) return 0;
   long long total = (long long)g.gz * g.gy * g.gx;
   long long nb = n_bricks < 0 ? total : n_bricks;
+  if (use_resident(g, total, flags)) return resident_bytes(nb);
   return layout(g, nb).total;
+}
+
+static int solve_resident(const Geo& g, const float* intensity, const uint8_t* seeds, const float* bound,
+                          const int32_t* list, int nb, const rwb_solve_params_t* params, float* prob,
+                          uint8_t* labels, void* workspace, rwb_solve_stats_t* stats, cudaStream_t st) {
+  char* base = (char*)workspace;
+  Work w;
+  std::memset(&w, 0, sizeof(w));
+  w.state = reinterpret_cast<int*>(base);
+  w.iters = w.state + nb;
+  char* misc = base + align_up(2 * (size_t)nb * sizeof(int), 256);
+  int* counter = reinterpret_cast<int*>(misc);
+  w.unknowns = reinterpret_cast<unsigned long long*>(misc + 8);
+  w.stat_i = reinterpret_cast<int*>(misc + 16);
+  RWB_CUDA(cudaMemsetAsync(misc, 0, 256, st));
+  ResidentArgs a;
+  a.g = g;
+  a.list = list;
+  a.nb = nb;
+  a.I = intensity;
+  a.S = seeds;
+  a.bound = bound;
+  a.prob = prob;
+  a.labels = labels;
+  a.beta = params->beta;
+  a.wmin = params->min_weight;
+  a.tol2 = params->tol * params->tol;
+  a.max_iter = params->max_iter;
+  a.state = w.state;
+  a.iters = w.iters;
+  a.counter = counter;
+  a.unknowns = w.unknowns;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  RWB_CUDA(cudaEventCreate(&ev0));
+  RWB_CUDA(cudaEventCreate(&ev1));
+  RWB_CUDA(cudaEventRecord(ev0, st));
+  int rc = launch_resident3d(a, st);
+  if (rc) {
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    return rc;
+  }
+  RWB_CUDA(cudaEventRecord(ev1, st));
+  stats_kernel<<<1, 1024, 0, st>>>(w, nb);
+  RWB_LAUNCH_CHECK("stats_kernel");
+  count_launches(1);
+  if (stats) {
+    int hs[8];
+    unsigned long long unk = 0;
+    RWB_CUDA(cudaMemcpyAsync(hs, w.stat_i, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    RWB_CUDA(cudaMemcpyAsync(&unk, w.unknowns, sizeof(unk), cudaMemcpyDeviceToHost, st));
+    RWB_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    RWB_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+    stats->bricks = nb;
+    stats->converged = hs[0];
+    stats->not_converged = hs[1];
+    stats->zero_rhs = hs[2];
+    stats->iterations_max = hs[3];
+    unsigned long long s64;
+    std::memcpy(&s64, hs + 4, sizeof(s64));
+    stats->iterations_sum = (int64_t)s64;
+    stats->unknowns = (int64_t)unk;
+    stats->sweeps = hs[3];
+    stats->cg_ms = ms;
+    stats->path = RWB_PATH_RESIDENT;
+  }
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  return RWB_OK;
 }
 
 extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensity, const uint8_t* seeds,
@@ -663,6 +728,18 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
   if (!(params->tol >= 0.f) || !(params->beta >= 0.f) || !(params->min_weight >= 0.f) || params->max_iter < 0)
     return fail(RWB_ERR_INVALID, "invalid solve parameters");
   if (nbl * (long long)g.tiles >= (1ll << 31)) return fail(RWB_ERR_INVALID, "too many bricks for one launch");
+  if (use_resident(g, total, params->flags)) {
+    // bricks are solved at different times by the persistent clusters: a brick's
+    // epilogue must not overwrite the bound a neighbour's setup still reads
+    if (bound && (const void*)prob == (const void*)bound)
+      return fail(RWB_ERR_INVALID, "prob must not alias bound on the brick-resident path");
+    if (workspace_bytes < resident_bytes(nbl))
+      return fail(RWB_ERR_WORKSPACE, "workspace too small: need " + std::to_string(resident_bytes(nbl)) + " bytes");
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    if (nbl == 0) return RWB_OK;
+    return solve_resident(g, intensity, seeds, bound, brick_list, (int)nbl, params, prob, labels, workspace, stats,
+                          (cudaStream_t)stream);
+  }
   const Layout L = layout(g, nbl);
   if (workspace_bytes < L.total)
     return fail(RWB_ERR_WORKSPACE, "workspace too small: need " + std::to_string(L.total) + " bytes");
@@ -776,6 +853,7 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
     stats->unknowns = (int64_t)unk;
     stats->sweeps = sweeps;
     stats->cg_ms = cg_ms;
+    stats->path = RWB_PATH_STREAMING;
   }
   return RWB_OK;
 }

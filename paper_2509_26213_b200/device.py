@@ -167,9 +167,16 @@ def brick_grid(shape, brick, origin=None):
     return tuple(-(-(int(s) - int(o)) // int(b)) for s, b, o in zip(shape, brick, origin))
 
 
-def workspace_bytes(shape, brick, n_bricks=-1, origin=None) -> int:
+def _flags(cfg: RWConfig) -> int:
+    f = 0 if cfg.use_graph else _native.SOLVE_NO_GRAPH
+    if not cfg.resident:
+        f |= _native.SOLVE_STREAMING
+    return f
+
+
+def workspace_bytes(shape, brick, n_bricks=-1, origin=None, cfg: RWConfig = RWConfig()) -> int:
     g = geometry(shape, brick, origin)
-    return int(_native.load_library().rwb_solve_workspace_bytes(ctypes.byref(g), int(n_bricks)))
+    return int(_native.load_library().rwb_solve_workspace_bytes(ctypes.byref(g), int(n_bricks), _flags(cfg)))
 
 
 def solve_level(volume: torch.Tensor, seeds: torch.Tensor, brick, bound: torch.Tensor | None = None,
@@ -203,7 +210,7 @@ def solve_level(volume: torch.Tensor, seeds: torch.Tensor, brick, bound: torch.T
     if bound is None and any(n > 1 for n in brick_grid(volume.shape, brick, origin)):
         raise ValueError("a brick-wise solve needs `bound` (the upsampled parent level)")
     lib = _native.lib()
-    nbytes = int(lib.rwb_solve_workspace_bytes(ctypes.byref(g), n_list))
+    nbytes = int(lib.rwb_solve_workspace_bytes(ctypes.byref(g), n_list, _flags(cfg)))
     if nbytes == 0:
         raise ValueError(f"invalid solver geometry: {_native.load_library().rwb_last_error().decode()}")
     workspace = workspace or Workspace(volume.device)
@@ -211,7 +218,7 @@ def solve_level(volume: torch.Tensor, seeds: torch.Tensor, brick, bound: torch.T
     p = _native.SolveParams()
     p.beta, p.min_weight, p.tol = float(cfg.beta), float(cfg.min_weight), float(cfg.tol)
     p.max_iter, p.check_every = int(cfg.max_iter), int(cfg.check_every)
-    p.flags = 0 if cfg.use_graph else _native.SOLVE_NO_GRAPH
+    p.flags = _flags(cfg)
     stats = _native.SolveStats()
     _native.check(lib.rwb_solve_level(
         ctypes.byref(g), _ptr(volume), _ptr(seeds), _ptr(bound), _ptr(brick_list), int(max(n_list, 0)),
@@ -270,8 +277,11 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
         lab_k = torch.empty(vols[k].shape, dtype=torch.uint8, device=volume.device) \
             if (want_labels and k == 0) else None
         bl = brick_lists[k] if brick_lists is not None else None
-        probs[k], stats[k] = solve_level(vols[k], seed_levels[k], brick, x, cfg, brick_list=bl, out=x,
+        # separate output: the brick-resident solver reads neighbour bounds while
+        # other bricks already write their results
+        probs[k], stats[k] = solve_level(vols[k], seed_levels[k], brick, x, cfg, brick_list=bl,
                                          labels_out=lab_k, workspace=workspace)
+        del x
         if k == 0:
             lab = lab_k
     return HRWResult(probs[0], lab, probs, vols, seed_levels, stats)

@@ -1,0 +1,418 @@
+"""Drop-in operators for the reference compute graph (`chunkcast`, operator mode).
+
+Factories in the idiom of `chunkcast.ops` (`pkg/src/chunkcast/ops.py`): pure
+functions returning reference `OperatorNode`s (`graph.py:18-51`) whose
+per-chunk `kernel(h, input_arrays, out)` runs the sm_100a kernels of librwb.
+A reference `Engine` resolves them unchanged: it calls `dependencies(h)`,
+pins the input chunks in RAM and runs the kernel on a worker thread
+(`engine.py:999-1076`); the kernel stages the chunk neighbourhood to the
+GPU, calls the C ABI and writes the result (including zero padding, as
+`ops.py:517-520` requires) into `out`.
+
+    import chunkcast
+    from paper_2509_26213_b200 import ops as rw
+
+    vol = chunkcast.ops.source_from_array(volume, (32, 32, 32))
+    seeds = chunkcast.ops.source_from_array(seed_labels, (32, 32, 32))
+    prob = rw.hierarchical_random_walker(vol, seeds, levels=4)   # LodPyramid of p_fg
+    labels = rw.rw_labels(prob.node(0))
+    engine.resolve(labels)
+
+Names and argument meaning follow the reference (`build_lod`,
+`downsample`-style footprints, `OperatorError` for invalid graphs); results
+are bit-identical to the device-batched path (`device.py`), which is the
+throughput path this operator mode wraps chunk by chunk.
+
+The reference package itself is needed (it owns `OperatorNode`/`Engine`):
+it is imported from the environment or from `baseline/_ref`.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+import sys
+
+import numpy as np
+
+from .config import RWConfig
+
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _chunkcast():
+    try:
+        import chunkcast  # noqa: F401
+    except ImportError:
+        ref = os.path.join(_ROOT, "baseline", "_ref")
+        if os.path.isdir(os.path.join(ref, "chunkcast")) and ref not in sys.path:
+            sys.path.append(ref)
+        import chunkcast  # noqa: F401
+    import chunkcast.graph
+    import chunkcast.model
+    import chunkcast.ops
+
+    return chunkcast
+
+
+def _error(msg):
+    return _chunkcast().ops.OperatorError(msg)
+
+
+# ---------------------------------------------------------------------------
+# host-side chunk assembly (dtype preserving) and device staging
+
+
+def _overlapping(md, begin, end):
+    """Chunk positions of `md` intersecting the in-level region [begin, end)."""
+    lo = [max(0, int(b)) // c for b, c in zip(begin, md.chunk_size)]
+    hi = [-(-min(int(e), s) // c) for e, s, c in zip(end, md.size, md.chunk_size)]
+    return [tuple(int(a + o) for a, o in zip(lo, off))
+            for off in np.ndindex(*[max(h - l, 0) for l, h in zip(lo, hi)])]
+
+
+def _gather(md, chunks: dict, begin, end) -> np.ndarray:
+    """Copy the logical elements of [begin, end) out of padded chunk payloads."""
+    shape = [e - b for b, e in zip(begin, end)]
+    lanes = md.element_type.lanes
+    out = np.empty(shape + ([lanes] if lanes > 1 else []), dtype=md.element_type.np_dtype)
+    for h, payload in chunks.items():
+        cb, ce = md.chunk_logical_region(h)
+        lo = [max(a, c) for a, c in zip(begin, cb)]
+        hi = [min(a, c) for a, c in zip(end, ce)]
+        if any(x >= y for x, y in zip(lo, hi)):
+            continue
+        src = tuple(slice(a - c, b - c) for a, b, c in zip(lo, hi, cb))
+        dst = tuple(slice(a - o, b - o) for a, b, o in zip(lo, hi, begin))
+        out[dst] = payload[src]
+    return out
+
+
+def _write_out(out: np.ndarray, region_shape, values: np.ndarray):
+    out[...] = 0
+    out[tuple(slice(0, n) for n in region_shape)] = values
+
+
+def _device():
+    import torch
+
+    from . import _native
+
+    _native.lib()  # loud failure without the library / an sm_100 device
+    return torch, torch.device("cuda", torch.cuda.current_device())
+
+
+def _to_dev(a: np.ndarray):
+    torch, dev = _device()
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def _from_dev(t) -> np.ndarray:
+    import torch
+
+    torch.cuda.current_stream().synchronize()
+    return t.cpu().numpy()
+
+
+def _dilated(md, h, r=1):
+    begin, end = md.chunk_logical_region(h)
+    return ([max(b - r, 0) for b in begin], [min(e + r, s) for e, s in zip(end, md.size)], begin, end)
+
+
+def _check_f32(node, what):
+    cc = _chunkcast()
+    if node.md.element_type != cc.model.F32:
+        raise _error(f"{what} must have scalar f32 elements, got {node.md.element_type}")
+
+
+def _check_u8(node, what):
+    cc = _chunkcast()
+    if node.md.element_type != cc.model.U8:
+        raise _error(f"{what} must have scalar u8 elements, got {node.md.element_type}")
+
+
+# ---------------------------------------------------------------------------
+# LOD pyramid
+
+
+def lod_down(input_node):
+    """Next coarser LOD level, fused conv([.25,.5,.25]^d, clamp) + 2x mean.
+
+    Bit-identical to ``downsample_mean(separable_conv(node, [SMOOTHING_KERNEL]*d))``
+    (`ops.py:714-727`), in one node and one GPU pass.
+    """
+    cc = _chunkcast()
+    _check_f32(input_node, "lod_down input")
+    md_in = input_node.md
+    size = tuple(-(-s // 2) for s in md_in.size)
+    md = cc.model.TensorMetaData(size, md_in.chunk_size, md_in.element_type)
+    emb = None
+    if input_node.embedding is not None:
+        emb = cc.model.EmbeddingData(tuple(sp * 2 for sp in input_node.embedding.spacing))
+
+    def src_window(h):
+        # coarse [b, e) reads fine 2b-1 .. 2e (conv radius 1); start on an even
+        # fine index so coarse j <-> fine 2j stays aligned in the window
+        begin, end = md.chunk_logical_region(h)
+        lo = [max(2 * b - 2, 0) for b in begin]
+        hi = [min(2 * e + 2, s) for e, s in zip(end, md_in.size)]
+        return lo, hi, begin, end
+
+    def dependencies(h):
+        lo, hi, _, _ = src_window(h)
+        return [_overlapping(md_in, lo, hi)]
+
+    def kernel(h, input_arrays, out):
+        from . import device
+
+        lo, hi, begin, end = src_window(h)
+        block = _gather(md_in, dict(zip(dependencies(h)[0], input_arrays[0])), lo, hi)
+        coarse = _from_dev(device.lod_down(_to_dev(block)))
+        off = [b - l // 2 for b, l in zip(begin, lo)]
+        sel = tuple(slice(o, o + e - b) for o, b, e in zip(off, begin, end))
+        _write_out(out, [e - b for b, e in zip(begin, end)], coarse[sel])
+
+    return cc.graph.OperatorNode(
+        name="rwb.lod_down", params={"kernel": [0.25, 0.5, 0.25], "border": "clamp", "factor": 2},
+        inputs=(input_node,), md=md, embedding=emb, dependencies=dependencies, kernel=kernel)
+
+
+def build_lod(input_node, embedding=None, smooth: bool = True, levels: int | None = None):
+    """`chunkcast.ops.build_lod` with the fused GPU level step (`ops.py:714-727`).
+
+    Same stop rule (halve until every dim fits one chunk) and the same level
+    values; `levels` optionally truncates the chain.
+    """
+    cc = _chunkcast()
+    if not smooth:
+        raise _error("the GPU LOD path implements the smoothed pyramid only (smooth=True)")
+    d = input_node.md.num_dims
+    emb = embedding if embedding is not None else input_node.embedding
+    if emb is None:
+        emb = cc.model.EmbeddingData((1.0,) * d)
+    elif not isinstance(emb, cc.model.EmbeddingData):
+        emb = cc.model.EmbeddingData(tuple(emb))
+    out = [(input_node, emb)]
+    node = input_node
+    while any(s > c for s, c in zip(node.md.size, node.md.chunk_size)):
+        if levels is not None and len(out) >= levels:
+            break
+        node = lod_down(node)
+        emb = cc.model.EmbeddingData(tuple(sp * 2 for sp in emb.spacing))
+        out.append((node, emb))
+    if levels is not None and len(out) < levels:
+        raise _error(f"levels={levels} but the pyramid of {input_node.md.size} has only {len(out)} levels")
+    return cc.ops.LodPyramid(tuple(out))
+
+
+# ---------------------------------------------------------------------------
+# random-walker operators
+
+
+def rw_weights(volume_node, beta: float = 100.0, min_weight: float = 1e-6):
+    """Forward edge weights max(exp(-beta dI^2), min_weight), F32 x ndim lanes (0 = no edge)."""
+    cc = _chunkcast()
+    _check_f32(volume_node, "rw_weights input")
+    d = volume_node.md.num_dims
+    if not 1 <= d <= 3:
+        raise _error("rw_weights supports 1-3 dimensions")
+    if not (beta >= 0 and min_weight >= 0):
+        raise _error("beta and min_weight must be >= 0")
+    md = cc.model.TensorMetaData(volume_node.md.size, volume_node.md.chunk_size, cc.model.Scalar.F32.vec(d)) \
+        if d > 1 else cc.model.TensorMetaData(volume_node.md.size, volume_node.md.chunk_size, cc.model.F32)
+    md_in = volume_node.md
+
+    def window(h):
+        begin, end = md.chunk_logical_region(h)
+        return list(begin), [min(e + 1, s) for e, s in zip(end, md_in.size)], begin, end
+
+    def dependencies(h):
+        lo, hi, _, _ = window(h)
+        return [_overlapping(md_in, lo, hi)]
+
+    def kernel(h, input_arrays, out):
+        from . import device
+
+        lo, hi, begin, end = window(h)
+        block = _gather(md_in, dict(zip(dependencies(h)[0], input_arrays[0])), lo, hi)
+        w = _from_dev(device.edge_weights(_to_dev(block), beta, min_weight))
+        # edges leaving the window but not the level were computed inside it;
+        # the window's last slab only exists to give the region's forward edges
+        sel = tuple(slice(0, e - b) for b, e in zip(begin, end))
+        vals = w[sel] if d > 1 else w[sel][..., 0]
+        _write_out(out, [e - b for b, e in zip(begin, end)], vals)
+
+    return cc.graph.OperatorNode(
+        name="rwb.weights", params={"beta": float(beta), "min_weight": float(min_weight)},
+        inputs=(volume_node,), md=md, embedding=volume_node.embedding, dependencies=dependencies, kernel=kernel)
+
+
+def project_seeds(seeds_node):
+    """Seed labels of the next coarser level (fg/bg if only fg/bg children, conflicts -> 0)."""
+    cc = _chunkcast()
+    _check_u8(seeds_node, "project_seeds input")
+    md_in = seeds_node.md
+    md = cc.model.TensorMetaData(tuple(-(-s // 2) for s in md_in.size), md_in.chunk_size, cc.model.U8)
+
+    def window(h):
+        begin, end = md.chunk_logical_region(h)
+        return [2 * b for b in begin], [min(2 * e, s) for e, s in zip(end, md_in.size)], begin, end
+
+    def dependencies(h):
+        lo, hi, _, _ = window(h)
+        return [_overlapping(md_in, lo, hi)]
+
+    def kernel(h, input_arrays, out):
+        from . import device
+
+        lo, hi, begin, end = window(h)
+        block = _gather(md_in, dict(zip(dependencies(h)[0], input_arrays[0])), lo, hi)
+        _write_out(out, [e - b for b, e in zip(begin, end)], _from_dev(device.project_seeds(_to_dev(block))))
+
+    emb = None
+    if seeds_node.embedding is not None:
+        emb = cc.model.EmbeddingData(tuple(sp * 2 for sp in seeds_node.embedding.spacing))
+    return cc.graph.OperatorNode(name="rwb.project_seeds", params={"rule": "conflict->unseeded"},
+                                 inputs=(seeds_node,), md=md, embedding=emb, dependencies=dependencies,
+                                 kernel=kernel)
+
+
+def _parent_window(lo, hi, parent_size):
+    """Parent index window the prolongation taps of fine [lo, hi) read (per dim)."""
+    out_lo, out_hi = [], []
+    for a, b, m in zip(lo, hi, parent_size):
+        ja = a // 2
+        first = ja if a % 2 else max(ja - 1, 0)
+        jb = (b - 1) // 2
+        last = min(jb + 1, m - 1) if (b - 1) % 2 else jb
+        out_lo.append(first)
+        out_hi.append(last + 1)
+    return out_lo, out_hi
+
+
+def random_walker(volume_node, seeds_node, parent=None, *, beta: float = 100.0, min_weight: float = 1e-6,
+                  tol: float = 1e-6, max_iter: int = 10_000):
+    """Random-walker foreground probability of one pyramid level (F32).
+
+    Without `parent` the level is one Dirichlet problem (the coarsest level;
+    every chunk request solves the whole level).  With `parent` (the F32
+    probability node of the next coarser level) every chunk is an
+    independent brick problem bounded and initialised by the upsampled
+    parent solution.
+    """
+    cc = _chunkcast()
+    _check_f32(volume_node, "random_walker volume")
+    _check_u8(seeds_node, "random_walker seeds")
+    md_in = volume_node.md
+    if seeds_node.md.size != md_in.size or seeds_node.md.chunk_size != md_in.chunk_size:
+        raise _error("volume and seeds must share size and chunking")
+    if md_in.num_dims not in (2, 3):
+        raise _error("the random walker supports 2-D and 3-D tensors")
+    if parent is not None:
+        _check_f32(parent, "random_walker parent")
+        if parent.md.size != tuple(-(-s // 2) for s in md_in.size):
+            raise _error("parent must be the next coarser level (size ceil(size/2))")
+    cfg = RWConfig(beta=float(beta), min_weight=float(min_weight), tol=float(tol), max_iter=int(max_iter))
+    md = cc.model.TensorMetaData(md_in.size, md_in.chunk_size, cc.model.F32)
+    inputs = (volume_node, seeds_node) + ((parent,) if parent is not None else ())
+
+    def dependencies(h):
+        if parent is None:
+            every = list(md_in.chunk_positions())
+            return [every, every]
+        lo, hi, _, _ = _dilated(md, h)
+        plo, phi = _parent_window(lo, hi, parent.md.size)
+        vol = _overlapping(md_in, lo, hi)
+        return [vol, vol, _overlapping(parent.md, plo, phi)]
+
+    def kernel(h, input_arrays, out):
+        from . import device
+
+        deps = dependencies(h)
+        begin, end = md.chunk_logical_region(h)
+        region = [e - b for b, e in zip(begin, end)]
+        if parent is None:
+            lo, hi = [0] * md.num_dims, list(md.size)
+            vol = _gather(md_in, dict(zip(deps[0], input_arrays[0])), lo, hi)
+            sd = _gather(seeds_node.md, dict(zip(deps[1], input_arrays[1])), lo, hi)
+            prob, _ = device.solve_level(_to_dev(vol), _to_dev(sd), tuple(md.size), None, cfg)
+            p = _from_dev(prob)
+            _write_out(out, region, p[tuple(slice(b, e) for b, e in zip(begin, end))])
+            return
+        lo, hi, _, _ = _dilated(md, h)
+        vol = _gather(md_in, dict(zip(deps[0], input_arrays[0])), lo, hi)
+        sd = _gather(seeds_node.md, dict(zip(deps[1], input_arrays[1])), lo, hi)
+        plo, phi = _parent_window(lo, hi, parent.md.size)
+        par = _gather(parent.md, dict(zip(deps[2], input_arrays[2])), plo, phi)
+        torch, dev = _device()
+        from . import _native
+
+        win = [b - a for a, b in zip(lo, hi)]
+        bound = torch.empty(win, dtype=torch.float32, device=dev)
+        par_d = _to_dev(par)
+        a64 = _native.int64_array
+        _native.check(_native.lib().rwb_upsample_window_f32(
+            len(win), a64(parent.md.size), a64(plo), a64([b - a for a, b in zip(plo, phi)]),
+            device._ptr(par_d), a64(md.size), a64(lo), a64(win), device._ptr(bound), device._stream_handle()))
+        # one brick of the window's grid is exactly this chunk: shift the grid origin
+        brick = tuple(md.chunk_size)
+        origin = tuple((b - a) - c if b > a else 0 for a, b, c in zip(lo, begin, brick))
+        grid = device.brick_grid(win, brick, origin)
+        coord = [1 if b > a else 0 for a, b in zip(lo, begin)]
+        index = 0
+        for c, gdim in zip(coord, grid):
+            index = index * gdim + c
+        blist = torch.tensor([index], dtype=torch.int32, device=dev)
+        prob, _ = device.solve_level(_to_dev(vol), _to_dev(sd), brick, bound, cfg, brick_list=blist,
+                                     origin=origin)
+        p = _from_dev(prob)
+        _write_out(out, region, p[tuple(slice(b - a, e - a) for a, b, e in zip(lo, begin, end))])
+
+    return cc.graph.OperatorNode(
+        name="rwb.random_walker", params=dict(cfg.params(), hierarchical=parent is not None),
+        inputs=inputs, md=md, embedding=volume_node.embedding, dependencies=dependencies, kernel=kernel)
+
+
+def hierarchical_random_walker(volume_node, seeds_node, levels: int | None = None, *, beta: float = 100.0,
+                               min_weight: float = 1e-6, tol: float = 1e-6, max_iter: int = 10_000,
+                               embedding=None):
+    """Pyramid of random-walker probabilities, level 0 finest (`LodPyramid`).
+
+    Coarsest level solved whole, every finer level brick by brick from the
+    upsampled level above — pulled lazily: resolving chunk h of level 0 only
+    computes the parent chunks its footprint needs.
+    """
+    cc = _chunkcast()
+    vol_pyr = build_lod(volume_node, embedding=embedding, levels=levels)
+    n = vol_pyr.num_levels
+    seeds = [seeds_node]
+    for _ in range(n - 1):
+        seeds.append(project_seeds(seeds[-1]))
+    kw = dict(beta=beta, min_weight=min_weight, tol=tol, max_iter=max_iter)
+    probs = [None] * n
+    probs[n - 1] = random_walker(vol_pyr.node(n - 1), seeds[n - 1], None, **kw)
+    for k in range(n - 2, -1, -1):
+        probs[k] = random_walker(vol_pyr.node(k), seeds[k], probs[k + 1], **kw)
+    return cc.ops.LodPyramid(tuple((probs[k], vol_pyr.embedding(k)) for k in range(n)))
+
+
+def rw_labels(prob_node):
+    """Segmentation labels: 1 where p > 0.5, else 0 (U8)."""
+    cc = _chunkcast()
+    _check_f32(prob_node, "rw_labels input")
+    md = cc.model.TensorMetaData(prob_node.md.size, prob_node.md.chunk_size, cc.model.U8)
+
+    def dependencies(h):
+        return [[tuple(h)]]
+
+    def kernel(h, input_arrays, out):
+        from . import device
+
+        out[...] = _from_dev(device.labels(_to_dev(np.ascontiguousarray(input_arrays[0][0]))))
+
+    return cc.graph.OperatorNode(name="rwb.labels", params={"threshold": 0.5}, inputs=(prob_node,), md=md,
+                                 embedding=prob_node.embedding, dependencies=dependencies, kernel=kernel)
+
+
+def level_voxels(pyramid) -> int:
+    return math.prod(pyramid.node(0).md.size)

@@ -40,24 +40,29 @@ def test_library_exports_every_declared_symbol(lib):
 def test_struct_layouts_match_header():
     assert ctypes.sizeof(_native.Geometry) == 8 + 3 * 8 * 3
     assert ctypes.sizeof(_native.SolveParams) == 24
-    assert ctypes.sizeof(_native.SolveStats) == 7 * 8 + 8  # ..., int32 sweeps, float cg_ms
+    assert ctypes.sizeof(_native.SolveStats) == 7 * 8 + 16  # ..., int32 sweeps, float cg_ms
 
 
 def test_workspace_size_query_needs_no_device(lib):
     from paper_2509_26213_b200 import device
 
-    n = device.workspace_bytes((64, 64, 64), (32, 32, 32))
+    from paper_2509_26213_b200.config import RWConfig
+
+    streaming = RWConfig(resident=False)
+    n = device.workspace_bytes((64, 64, 64), (32, 32, 32), cfg=streaming)
     # 9 f32 brick-local arrays (36 B/voxel) plus small per-brick scalars
     assert 36 * 64**3 <= n < 36 * 64**3 + 64 * 1024
+    # the brick-resident path keeps the CG state on chip: per-brick scalars only
+    assert device.workspace_bytes((64, 64, 64), (32, 32, 32)) < 4096
     n2 = device.workspace_bytes((128, 128), (64, 64))
     assert 32 * 128**2 <= n2 < 32 * 128**2 + 64 * 1024
-    assert device.workspace_bytes((64, 64, 64), (32, 32, 32), n_bricks=2) < n
+    assert device.workspace_bytes((64, 64, 64), (32, 32, 32), n_bricks=2, cfg=streaming) < n
 
 
 def test_invalid_geometry_reports_error(lib):
     g = _native.Geometry()
     g.ndim = 4
-    assert lib.rwb_solve_workspace_bytes(ctypes.byref(g), -1) == 0
+    assert lib.rwb_solve_workspace_bytes(ctypes.byref(g), -1, 0) == 0
     assert lib.rwb_labels_u8(-1, None, None, None) == -1
     assert b"negative" in lib.rwb_last_error()
 

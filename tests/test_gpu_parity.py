@@ -224,3 +224,72 @@ def test_label_swap_symmetry_gpu():
     a = device.hierarchical_random_walker(cuda(vol), cuda(seeds), (16, 16), 2, GPU_CFG).prob
     b = device.hierarchical_random_walker(cuda(vol), cuda(sw), (16, 16), 2, GPU_CFG).prob
     np.testing.assert_allclose(host(a) + host(b), 1.0, atol=2e-4)
+
+
+# -- brick-resident solver (32^3 bricks, 8-CTA clusters) ---------------------------------
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 64), (70, 40, 33), (32, 96, 45)])
+def test_resident_path_matches_oracle(rng, shape):
+    vol, seeds = _random_case(rng, shape)
+    bound = rng.random(shape).astype(np.float32)
+    ref = orw.solve_level(vol, seeds, (32, 32, 32), bound.astype(np.float64), TIGHT).prob
+    out, st = device.solve_level(cuda(vol), cuda(seeds), (32, 32, 32), cuda(bound), GPU_CFG)
+    assert st["path"] == 1 and st["not_converged"] == 0
+    got = host(out)
+    assert_rw_parity(got, ref)
+    assert np.all(got[seeds == 1] == 1.0) and np.all(got[seeds == 2] == 0.0)
+
+
+def test_resident_and_streaming_agree(rng):
+    vol = synthetic.phantom((96, 64, 64))
+    seeds = synthetic.seeds(vol.shape, "S2")
+    bound = cuda(rng.random(vol.shape).astype(np.float32))
+    a, sa = device.solve_level(cuda(vol), cuda(seeds), (32, 32, 32), bound, GPU_CFG)
+    b, sb = device.solve_level(cuda(vol), cuda(seeds), (32, 32, 32), bound,
+                               RWConfig(tol=GPU_CFG.tol, max_iter=GPU_CFG.max_iter, resident=False))
+    assert sa["path"] == 1 and sb["path"] == 0
+    assert np.abs(host(a) - host(b)).max() <= 2e-5
+    assert sa["unknowns"] == sb["unknowns"]
+    assert abs(sa["iterations_sum"] - sb["iterations_sum"]) <= 0.05 * sb["iterations_sum"]
+
+
+def test_resident_brick_subset_bytes_identical(rng):
+    vol, seeds = _random_case(rng, (64, 64, 96))
+    bound = cuda(rng.random(vol.shape).astype(np.float32))
+    full, _ = device.solve_level(cuda(vol), cuda(seeds), (32, 32, 32), bound, GPU_CFG)
+    full = host(full)
+    bid, nb = orw.brick_ids(vol.shape, (32, 32, 32))
+    for part in (np.arange(0, nb, 3), np.array([nb - 1, 0])):
+        out = torch.zeros_like(bound)
+        lst = torch.from_numpy(part.astype(np.int32)).cuda()
+        out, st = device.solve_level(cuda(vol), cuda(seeds), (32, 32, 32), bound, GPU_CFG, brick_list=lst, out=out)
+        sel = np.isin(bid, part)
+        np.testing.assert_array_equal(host(out)[sel], full[sel])
+
+
+def test_resident_zero_rhs_and_seeded_bricks():
+    vol = np.zeros((64, 32, 32), np.float32)
+    seeds = np.zeros(vol.shape, np.uint8)
+    seeds[:32] = 2
+    bound = np.zeros(vol.shape, np.float32)
+    out, st = device.solve_level(cuda(vol), cuda(seeds), (32, 32, 32), cuda(bound), GPU_CFG)
+    assert st["path"] == 1
+    assert np.all(host(out) == 0.0)
+    assert st["zero_rhs"] == 2
+
+
+def test_resident_hierarchy_vs_golden_c2_like():
+    vol = synthetic.phantom((96, 96, 96))
+    seeds = synthetic.seeds(vol.shape, "S1")
+    res = device.hierarchical_random_walker(cuda(vol), cuda(seeds), (32, 32, 32), 2, GPU_CFG)
+    ref = orw.hierarchical_random_walker(vol, seeds, (32, 32, 32), 2, TIGHT)
+    assert res.stats[0]["path"] == 1
+    assert_rw_parity(host(res.prob), ref.prob[0], host(res.labels))
+
+
+def test_resident_rejects_aliased_output(rng):
+    vol, seeds = _random_case(rng, (64, 32, 32))
+    bound = cuda(rng.random(vol.shape).astype(np.float32))
+    with pytest.raises(ValueError):
+        device.solve_level(cuda(vol), cuda(seeds), (32, 32, 32), bound, GPU_CFG, out=bound)
