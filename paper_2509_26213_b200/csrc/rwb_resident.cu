@@ -6,30 +6,36 @@
 // scaled edge weights, 10 floats per voxel = 1.25 MiB — fits in the register
 // files of 8 SMs (8 x 256 KB), so here a cluster of 8 CTAs owns one brick:
 // CTA `c` holds z-planes [4c, 4c+4), each of its 256 threads a 4(x) x 4(z)
-// block of voxels in registers.  HBM is touched once per brick: the setup
-// reads intensity, seeds and the parent bound (plus a one-voxel halo), the
-// epilogue writes probabilities and labels (~14 B/voxel in total instead of
-// 52 B/voxel/iteration).
+// block of voxels in registers.  HBM is touched once per brick: the inputs
+// (intensity, seeds, parent bound, each with a one-voxel halo) are staged into
+// shared memory — for the NEXT brick, with cp.async, while the current brick
+// iterates — and the epilogue writes probabilities and labels (~14 B/voxel
+// in total instead of 52 B/voxel/iteration).
+//
+// The iteration is the single-reduction CG of Chronopoulos & Gear (1989):
+// with w = A'r and s = A'p carried as vectors, both dot products of an
+// iteration, gamma = r.r and delta = w.r, are reduced together, and
+//   beta = gamma_new / gamma,  alpha = gamma_new / (delta - beta gamma_new / alpha),
+//   p = r + beta p,  s = w + beta s,  y += alpha p,  r -= alpha s,  w = A'r.
+// Latency, not bandwidth, bounds an on-chip brick solve (each iteration is a
+// chain of neighbour exchange -> SpMV -> cluster-wide reduction), and this
+// form has one cluster-wide reduction per iteration instead of two.
 //
 // Neighbour exchange per iteration (no cluster-wide barrier inside the loop):
 //   x: warp shuffles (lanes of a row are x-consecutive quads)
-//   y: p planes in shared memory (LDS.128 of the rows above / below)
-//   z: in-thread, except the slab faces: every iteration each CTA PUSHES its
-//      two r face planes into its z-neighbours' shared memory with
-//      `st.async ... mbarrier::complete_tx` (DSMEM stores that complete on
-//      the receiver's mbarrier); the receiver keeps its neighbours' p face
-//      values in registers and advances them itself, p_face <- r_face + beta
-//      p_face, so p never crosses CTAs.
-// Reductions: warp shuffles -> CTA partial -> one thread st.async's it into
-// slot `rank` of all 8 CTAs (again completing on their mbarriers) -> every
-// CTA waits on its own mbarrier and sums the 8 partials in the same order
-// (float64), so all CTAs take identical CG decisions (deterministic).
-// Per iteration: two local mbarrier waits (pq; rr + faces) instead of
-// cluster barriers with their release/acquire fences.
+//   y: r planes in shared memory (LDS.128 of the rows above / below)
+//   z: in-thread, except the slab faces: each CTA PUSHES its two r face
+//      planes into its z-neighbours' shared memory with `st.async ...
+//      mbarrier::complete_tx` (DSMEM stores that complete on the receiver's
+//      mbarrier).
+// Reduction: every warp shuffle-reduces its partials and lanes 0..7 st.async
+// them into slot [rank][warp] of all 8 CTAs; each CTA waits on its own
+// mbarrier and every warp sums the 64 partials with the same fixed shuffle
+// tree, so all CTAs take identical CG decisions (deterministic, independent
+// of brick scheduling).
 //
-// The arithmetic is the same Jacobi-scaled CG as the streaming kernels
-// (identical scale factors and scaled weights); only the summation order of
-// the dot products differs.
+// Same Jacobi-scaled system as the streaming kernels (identical scale factors
+// and scaled weights); the CG scalars are fp32 here (float64 there).
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -40,30 +46,61 @@ namespace cg = cooperative_groups;
 
 namespace rwb {
 
-constexpr int RB = 32;              // brick edge
-constexpr int RCL = 8;              // CTAs per cluster (per brick)
-constexpr int RPZ = RB / RCL;       // z planes per CTA
-constexpr int RQ = 4;               // x voxels per thread
-constexpr int RQN = RB / RQ;        // quads per row
-constexpr int RT = RQN * RB;        // threads per CTA (256)
-constexpr int RV = RQ * RPZ;        // voxels per thread (16)
+constexpr int RB = 32;          // brick edge
+constexpr int RCL = 8;          // CTAs per cluster (per brick)
+constexpr int RPZ = RB / RCL;   // z planes per CTA
+constexpr int RQ = 4;           // x voxels per thread
+constexpr int RQN = RB / RQ;    // quads per row
+constexpr int RT = RQN * RB;    // threads per CTA (256)
+constexpr int RW = RT / 32;     // warps per CTA
+constexpr int RV = RQ * RPZ;    // voxels per thread (16)
+constexpr int NPART = RCL * RW; // pushed partials per reduction (64)
+constexpr int TZS = RPZ + 2;    // staged tile: slab + 1-voxel halo
+constexpr int TYS = RB + 2;
+constexpr int TXS = RB + 2;
+constexpr int TILE = TZS * TYS * TXS;
+constexpr unsigned char OUTSIDE = 255;  // staged seed marker: voxel outside the level
 
 static_assert(RPZ == 4 && RQ == 4, "register blocking assumes 4x4 voxels per thread");
 
+}  // namespace rwb
+
+#ifdef RWB_TRACE
+// phase timestamps of cluster 0 (diagnostics build only)
+__device__ long long g_rwb_trace[8][64][8];
+__device__ long long g_rwb_btrace[8][16][10];
+#define TRACE(k)                                                                                   \
+  do {                                                                                             \
+    if (tid == 0 && blockIdx.x < RCL && trace_it < 64) g_rwb_trace[rank][trace_it][k] = clock64(); \
+  } while (0)
+#define BTRACE(k)                                                                                   \
+  do {                                                                                              \
+    if (tid == 0 && blockIdx.x < RCL && btrace_n < 16) g_rwb_btrace[rank][btrace_n][k] = clock64(); \
+  } while (0)
+#else
+#define TRACE(k) \
+  do {           \
+  } while (0)
+#define BTRACE(k) \
+  do {            \
+  } while (0)
+#endif
+
+namespace rwb {
+
 struct ResidentSmem {
-  float4 p[RPZ][RB][RQN];       // p planes of this slab (y neighbours)
-  float4 rface[2][2][RB][RQN];  // received r faces [parity][0 = from below, 1 = from above]
-  float4 rown[2][RB][RQN];      // setup: own r0 faces (read once by the neighbours)
-  float4 sc[RPZ][RB][RQN];      // setup: scale factors of the slab
-  float red[2][2][RCL];         // pushed partials [0 = pq, 1 = rr][parity][rank]
-  float red_setup[2][RCL];      // setup partials [0 = bb, 1 = rr0][rank]
-  float warp_part[2][RT / 32];
-  unsigned long long barA[2];   // mbarriers: pq partials, per parity
-  unsigned long long barB[2];   // mbarriers: rr partials + r faces, per parity
-  int brick;
+  float tI[2][TZS][TYS][TXS];           // staged intensity (double buffer: current / next brick)
+  float tB[2][TZS][TYS][TXS];           // staged parent bound
+  unsigned char tS[2][TZS][TYS][TXS];   // staged seeds (OUTSIDE = not in the level)
+  float4 rp[RPZ][RB][RQN];              // r planes of this slab (y neighbours of the SpMV)
+  float4 rface[2][2][RB][RQN];          // received r faces [parity][0 = from below, 1 = from above]
+  float4 sc[RPZ][RB][RQN];              // scale factors of the slab (setup exchange, epilogue)
+  __align__(16) float red[2][3][NPART]; // pushed partials [parity][gamma, delta, bb][rank*RW + warp]
+  unsigned long long barF[2];           // mbarriers: r faces from the z neighbours, per parity
+  unsigned long long barR[2];           // mbarriers: dot-product partials, per parity
 };
 
-// ---- PTX helpers: mbarriers and DSMEM st.async -----------------------------------
+// ---- PTX helpers ----------------------------------------------------------------
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -87,7 +124,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phas
   asm volatile(
       "{\n\t.reg .pred P1;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@!P1 bra.uni WAIT_%=;\n\t}" ::"r"(a),
       "r"(phase)
       : "memory");
@@ -107,67 +144,86 @@ __device__ __forceinline__ void st_async_v4(uint32_t remote, float4 v, uint32_t 
                : "memory");
 }
 
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 __device__ __forceinline__ float lane_of(const float4& v, int i) {
   return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
 }
 
 __device__ __forceinline__ float4 f4(float a, float b, float c, float d) { return make_float4(a, b, c, d); }
 
-// CTA-wide sum (fixed order) -> thread 0 (uses warp_part[phase]; caller syncs before reuse)
-__device__ __forceinline__ float cta_sum(ResidentSmem& sm, float v, int phase) {
+__device__ __forceinline__ float seedval(unsigned char s) { return s == 1 ? 1.f : 0.f; }
+
+__device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) sm.warp_part[phase][threadIdx.x >> 5] = v;
-  __syncthreads();
-  float s = 0.f;
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int w = 0; w < RT / 32; ++w) s += sm.warp_part[phase][w];
+  return v;
+}
+
+// Sum of the 64 pushed partials: lane l loads partials 2l, 2l+1 (one LDS.64)
+// and the warp reduces them with a fixed shuffle tree, so every warp of every
+// CTA gets the bit-identical total without a broadcast through shared memory.
+__device__ __forceinline__ float sum64(const float* red) {
+  const float2 v = reinterpret_cast<const float2*>(red)[threadIdx.x & 31];
+  return warp_sum(v.x + v.y);
+}
+
+// Stage the slab of brick `brick` (+ one-voxel halo) into buffer `buf`:
+// intensity and bound with cp.async (complete at the next wait_group), seeds
+// with plain loads (byte granularity) when `seeds_now`.
+__device__ __forceinline__ void stage_issue(const ResidentArgs& a, ResidentSmem& sm, int buf, int brick, int lz0,
+                                            bool seeds_now) {
+  const Geo& g = a.g;
+  const int hx = brick % g.gx, hy = (brick / g.gx) % g.gy, hz = brick / (g.gx * g.gy);
+  const int z0 = g.oz + hz * RB + lz0 - 1, y0 = g.oy + hy * RB - 1, x0 = g.ox + hx * RB - 1;
+  for (int idx = threadIdx.x; idx < TILE; idx += RT) {
+    const int tz = idx / (TYS * TXS), rem = idx - tz * (TYS * TXS);
+    const int ty = rem / TXS, tx = rem - ty * TXS;
+    const int z = z0 + tz, y = y0 + ty, x = x0 + tx;
+    const bool in = z >= 0 && z < g.nz && y >= 0 && y < g.ny && x >= 0 && x < g.nx;
+    if (in) {
+      const long long gi = (long long)z * g.sxy + (long long)y * g.nx + x;
+      cp_async4(&sm.tI[buf][tz][ty][tx], a.I + gi);
+      cp_async4(&sm.tB[buf][tz][ty][tx], a.bound + gi);
+      if (seeds_now) sm.tS[buf][tz][ty][tx] = __ldg(a.S + gi);
+    } else {
+      sm.tI[buf][tz][ty][tx] = 0.f;
+      sm.tB[buf][tz][ty][tx] = 0.f;
+      sm.tS[buf][tz][ty][tx] = OUTSIDE;
+    }
   }
-  return s;
+  cp_async_commit();
 }
 
-// setup: CTA partial pushed to slot `rank` of every CTA's red_setup[phase] (plain DSMEM
-// stores; the caller's cluster barrier publishes them)
-__device__ __forceinline__ void cluster_push(cg::cluster_group& cluster, ResidentSmem& sm, float v, int phase,
-                                             int par, int rank) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if ((threadIdx.x & 31) == 0) sm.warp_part[phase][threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x < RCL) {
-    float s = 0.f;
-#pragma unroll
-    for (int w = 0; w < RT / 32; ++w) s += sm.warp_part[phase][w];
-    float* dst = cluster.map_shared_rank(&sm.red_setup[phase][rank], (unsigned)threadIdx.x);
-    *dst = s;
+__device__ __forceinline__ void stage_seeds(const ResidentArgs& a, ResidentSmem& sm, int buf, int brick, int lz0) {
+  const Geo& g = a.g;
+  const int hx = brick % g.gx, hy = (brick / g.gx) % g.gy, hz = brick / (g.gx * g.gy);
+  const int z0 = g.oz + hz * RB + lz0 - 1, y0 = g.oy + hy * RB - 1, x0 = g.ox + hx * RB - 1;
+  for (int idx = threadIdx.x; idx < TILE; idx += RT) {
+    const int tz = idx / (TYS * TXS), rem = idx - tz * (TYS * TXS);
+    const int ty = rem / TXS, tx = rem - ty * TXS;
+    const int z = z0 + tz, y = y0 + ty, x = x0 + tx;
+    if (z >= 0 && z < g.nz && y >= 0 && y < g.ny && x >= 0 && x < g.nx)
+      sm.tS[buf][tz][ty][tx] = __ldg(a.S + (long long)z * g.sxy + (long long)y * g.nx + x);
   }
-  (void)par;
 }
 
-__device__ __forceinline__ double setup_total(const ResidentSmem& sm, int phase) {
-  double s = 0.0;
-#pragma unroll
-  for (int i = 0; i < RCL; ++i) s += (double)sm.red_setup[phase][i];
-  return s;
-}
-
-__device__ __forceinline__ double pushed_total(const ResidentSmem& sm, int phase, int par) {
-  double s = 0.0;
-#pragma unroll
-  for (int i = 0; i < RCL; ++i) s += (double)sm.red[phase][par][i];
-  return s;
-}
-
-__device__ __forceinline__ float seedval(uint8_t s) { return s == 1 ? 1.f : 0.f; }
-
-__global__ void __cluster_dims__(RCL, 1, 1) __launch_bounds__(RT, 1)
-    resident3d_kernel(ResidentArgs a) {
+__global__ void __cluster_dims__(RCL, 1, 1) __launch_bounds__(RT, 1) resident3d_kernel(ResidentArgs a) {
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ResidentSmem& sm = *reinterpret_cast<ResidentSmem*>(smem_raw);
   const int rank = (int)cluster.block_rank();
   const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
   const int ly = tid / RQN;  // row
   const int xq = tid % RQN;  // quad within the row
   const int lz0 = rank * RPZ;
@@ -175,69 +231,75 @@ __global__ void __cluster_dims__(RCL, 1, 1) __launch_bounds__(RT, 1)
   const float bw = a.beta, wmin = a.wmin;
   const ResidentSmem* below = rank > 0 ? cluster.map_shared_rank(&sm, rank - 1) : nullptr;
   const ResidentSmem* above = rank < RCL - 1 ? cluster.map_shared_rank(&sm, rank + 1) : nullptr;
-  const long long offs[6] = {-g.sxy, g.sxy, -(long long)g.nx, (long long)g.nx, -1, 1};
   const int nfaces = (rank > 0) + (rank < RCL - 1);
   const uint32_t face_bytes = (uint32_t)(RB * RQN * sizeof(float4));
+  const int cid = blockIdx.x / RCL, ncl = gridDim.x / RCL;
 
   if (tid == 0) {
-    mbar_init(&sm.barA[0], 1);
-    mbar_init(&sm.barA[1], 1);
-    mbar_init(&sm.barB[0], 1);
-    mbar_init(&sm.barB[1], 1);
+    mbar_init(&sm.barF[0], 1);
+    mbar_init(&sm.barF[1], 1);
+    mbar_init(&sm.barR[0], 1);
+    mbar_init(&sm.barR[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // remote addresses this thread pushes to
-  uint32_t red_dst[2][2] = {{0, 0}, {0, 0}}, barA_dst[2] = {0, 0}, barB_dst[2] = {0, 0};
   uint32_t face_dn_dst[2] = {0, 0}, face_up_dst[2] = {0, 0}, bar_dn[2] = {0, 0}, bar_up[2] = {0, 0};
+  uint32_t red_dst[2] = {0, 0}, barR_dst[2] = {0, 0};
 #pragma unroll
   for (int par = 0; par < 2; ++par) {
     if (rank > 0) {  // my plane 0 goes to the CTA below, as its "from above" face
       face_dn_dst[par] = mapa_u32(smem_u32(&sm.rface[par][1][ly][xq]), rank - 1);
-      bar_dn[par] = mapa_u32(smem_u32(&sm.barB[par]), rank - 1);
+      bar_dn[par] = mapa_u32(smem_u32(&sm.barF[par]), rank - 1);
     }
     if (rank < RCL - 1) {  // my last plane goes to the CTA above, as its "from below" face
       face_up_dst[par] = mapa_u32(smem_u32(&sm.rface[par][0][ly][xq]), rank + 1);
-      bar_up[par] = mapa_u32(smem_u32(&sm.barB[par]), rank + 1);
+      bar_up[par] = mapa_u32(smem_u32(&sm.barF[par]), rank + 1);
     }
-    if (tid < RCL) {  // thread t < 8 delivers the CTA partials to CTA t
-      red_dst[0][par] = mapa_u32(smem_u32(&sm.red[0][par][rank]), tid);
-      red_dst[1][par] = mapa_u32(smem_u32(&sm.red[1][par][rank]), tid);
-      barA_dst[par] = mapa_u32(smem_u32(&sm.barA[par]), tid);
-      barB_dst[par] = mapa_u32(smem_u32(&sm.barB[par]), tid);
+    if (lane < RCL) {  // lane t delivers this warp's partials to CTA t
+      red_dst[par] = mapa_u32(smem_u32(&sm.red[par][0][rank * RW + warp]), lane);
+      barR_dst[par] = mapa_u32(smem_u32(&sm.barR[par]), lane);
     }
   }
   cluster.sync();
-  unsigned gk = 0;  // iterations run by this cluster so far (drives mbarrier parities)
+  unsigned gk = 0;  // iterations run by this cluster so far (drives the mbarrier parities)
+#ifdef RWB_TRACE
+  int btrace_n = 0;
+#endif
 
-  while (true) {
-    if (rank == 0 && tid == 0) {
-      int b = atomicAdd(a.counter, 1);
-#pragma unroll
-      for (int r = 0; r < RCL; ++r) *cluster.map_shared_rank(&sm.brick, (unsigned)r) = b;
-    }
-    cluster.sync();
-    const int slot = sm.brick;
-    if (slot >= a.nb) break;
+  // static round-robin brick assignment; brick n+1 is staged while brick n iterates
+  int buf = 0;
+  if (cid < a.nb) stage_issue(a, sm, 0, a.list ? a.list[cid] : cid, lz0, true);
+  for (int slot = cid; slot < a.nb; slot += ncl, buf ^= 1) {
+    BTRACE(0);
     const int brick = a.list ? a.list[slot] : slot;
+    const int next = slot + ncl;
+    if (next < a.nb) {
+      stage_issue(a, sm, buf ^ 1, a.list ? a.list[next] : next, lz0, false);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    BTRACE(1);
     const int hx = brick % g.gx;
     const int hy = (brick / g.gx) % g.gy;
     const int hz = brick / (g.gx * g.gy);
     const int gz0 = g.oz + hz * RB + lz0, gy = g.oy + hy * RB + ly, gx0 = g.ox + hx * RB + xq * RQ;
-    const bool row_in = gy >= 0 && gy < g.ny;
-    auto in_level = [&](int z, int i) {
-      const int gz = gz0 + z, gx = gx0 + i;
-      return row_in && gz >= 0 && gz < g.nz && gx >= 0 && gx < g.nx;
-    };
-    auto gidx = [&](int z, int i) { return (long long)(gz0 + z) * g.sxy + (long long)gy * g.nx + (gx0 + i); };
-    // the six edge weights of voxel gi in the level (0 = no edge), order -z,+z,-y,+y,-x,+x
-    auto weights6 = [&](int z, int i, float c, long long gi, float* wn) {
-      const int gz = gz0 + z, gx = gx0 + i;
-      wn[0] = gz > 0 ? edge_weight(c, __ldg(a.I + gi - g.sxy), bw, wmin) : 0.f;
-      wn[1] = gz + 1 < g.nz ? edge_weight(c, __ldg(a.I + gi + g.sxy), bw, wmin) : 0.f;
-      wn[2] = gy > 0 ? edge_weight(c, __ldg(a.I + gi - g.nx), bw, wmin) : 0.f;
-      wn[3] = gy + 1 < g.ny ? edge_weight(c, __ldg(a.I + gi + g.nx), bw, wmin) : 0.f;
-      wn[4] = gx > 0 ? edge_weight(c, __ldg(a.I + gi - 1), bw, wmin) : 0.f;
-      wn[5] = gx + 1 < g.nx ? edge_weight(c, __ldg(a.I + gi + 1), bw, wmin) : 0.f;
+    const float(*tI)[TYS][TXS] = sm.tI[buf];
+    const float(*tB)[TYS][TXS] = sm.tB[buf];
+    const unsigned char(*tS)[TYS][TXS] = sm.tS[buf];
+    // staged-tile coordinates of voxel (z, i) of this thread: (z+1, ly+1, xq*4+i+1)
+    const int cy = ly + 1, cx0 = xq * RQ + 1;
+    // the six edge weights (0 = no edge), order -z,+z,-y,+y,-x,+x
+    auto weights6 = [&](int z, int i, float* wn) {
+      const int cz = z + 1, cx = cx0 + i;
+      const float c = tI[cz][cy][cx];
+      const int nz[6] = {cz - 1, cz + 1, cz, cz, cz, cz};
+      const int ny[6] = {cy, cy, cy - 1, cy + 1, cy, cy};
+      const int nx[6] = {cx, cx, cx, cx, cx - 1, cx + 1};
+#pragma unroll
+      for (int e = 0; e < 6; ++e)
+        wn[e] = tS[nz[e]][ny[e]][nx[e]] != OUTSIDE ? edge_weight(c, tI[nz[e]][ny[e]][nx[e]], bw, wmin) : 0.f;
     };
 
     // ---------------- setup 1: scale factors s = diag^-1/2 ----------------
@@ -248,11 +310,9 @@ __global__ void __cluster_dims__(RCL, 1, 1) __launch_bounds__(RT, 1)
       for (int i = 0; i < RQ; ++i) {
         const int v = z * RQ + i;
         scl[v] = 0.f;
-        if (!in_level(z, i)) continue;
-        const long long gi = gidx(z, i);
-        if (__ldg(a.S + gi) != 0) continue;
+        if (tS[z + 1][cy][cx0 + i] != 0) continue;  // seed or outside the level
         float wn[6];
-        weights6(z, i, __ldg(a.I + gi), gi, wn);
+        weights6(z, i, wn);
         float d = 0.f;
 #pragma unroll
         for (int e = 0; e < 6; ++e) d += wn[e];
@@ -260,12 +320,15 @@ __global__ void __cluster_dims__(RCL, 1, 1) __launch_bounds__(RT, 1)
       }
 #pragma unroll
     for (int z = 0; z < RPZ; ++z) sm.sc[z][ly][xq] = f4(scl[z * RQ], scl[z * RQ + 1], scl[z * RQ + 2], scl[z * RQ + 3]);
+    BTRACE(2);
     cluster.sync();
+    BTRACE(3);
 
     // ---------------- setup 2: scaled weights, r0 = S(b - L x0), y0 = x0 / s ----------------
-    float y[RV], r[RV], p[RV], q[RV];
+    float y[RV], r[RV], p[RV], sv[RV], w[RV];
     float wxf[RV], wyf[RV], wzf[RV], wyb[RV], wxb[RPZ], wzb[RQ];
     float bb_part = 0.f, rr_part = 0.f;
+    unsigned n_unk = 0;
 #pragma unroll
     for (int z = 0; z < RPZ; ++z) {
       const float4 sy_up = ly + 1 < RB ? sm.sc[z][ly + 1][xq] : f4(0, 0, 0, 0);
@@ -291,21 +354,26 @@ __global__ void __cluster_dims__(RCL, 1, 1) __launch_bounds__(RT, 1)
         y[v] = 0.f;
         r[v] = 0.f;
         if (si > 0.f) {
-          const long long gi = gidx(z, i);
-          const float x0 = a.bound ? __ldg(a.bound + gi) : 0.f;
+          ++n_unk;
+          const int cz = z + 1, cx = cx0 + i;
+          const int nz[6] = {cz - 1, cz + 1, cz, cz, cz, cz};
+          const int ny[6] = {cy, cy, cy - 1, cy + 1, cy, cy};
+          const int nx[6] = {cx, cx, cx, cx, cx - 1, cx + 1};
+          const float x0 = tB[cz][cy][cx];
           float wn[6];
-          weights6(z, i, __ldg(a.I + gi), gi, wn);
+          weights6(z, i, wn);
           float diag = 0.f, b = 0.f, acc = 0.f;
 #pragma unroll
           for (int e = 0; e < 6; ++e) {
             diag += wn[e];
             if (wn[e] == 0.f) continue;
+            const float bn = tB[nz[e]][ny[e]][nx[e]];
             if (nsc[e] > 0.f) {  // coupled unknown of this brick
               wp[e] = wn[e] * si * nsc[e];
-              acc += wn[e] * (a.bound ? __ldg(a.bound + gi + offs[e]) : 0.f);
+              acc += wn[e] * bn;
             } else {  // Dirichlet: seed, or outside the brick
-              const uint8_t s = __ldg(a.S + gi + offs[e]);
-              b += wn[e] * (s ? seedval(s) : (a.bound ? __ldg(a.bound + gi + offs[e]) : 0.f));
+              const unsigned char s = tS[nz[e]][ny[e]][nx[e]];
+              b += wn[e] * (s ? seedval(s) : bn);
             }
           }
           r[v] = si * (b + acc - diag * x0);
@@ -323,161 +391,198 @@ __global__ void __cluster_dims__(RCL, 1, 1) __launch_bounds__(RT, 1)
       }
     }
     {
-      unsigned n_unk = 0;
-#pragma unroll
-      for (int v = 0; v < RV; ++v) n_unk += scl[v] > 0.f;
-      n_unk = __reduce_add_sync(0xffffffffu, n_unk);
-      if ((tid & 31) == 0 && n_unk) atomicAdd(a.unknowns, (unsigned long long)n_unk);
+      const unsigned nu = __reduce_add_sync(0xffffffffu, n_unk);
+      if (lane == 0 && nu) atomicAdd(a.unknowns, (unsigned long long)nu);
     }
-    cluster_push(cluster, sm, bb_part, 0, 1, rank);
-    cluster_push(cluster, sm, rr_part, 1, 1, rank);
-    // p_0 = r_0: publish p_0 planes and the r0 faces (read once by the neighbours)
-#pragma unroll
-    for (int v = 0; v < RV; ++v) p[v] = r[v];
-#pragma unroll
-    for (int z = 0; z < RPZ; ++z) sm.p[z][ly][xq] = f4(p[z * RQ], p[z * RQ + 1], p[z * RQ + 2], p[z * RQ + 3]);
-    sm.rown[0][ly][xq] = f4(r[0], r[1], r[2], r[3]);
-    sm.rown[1][ly][xq] = f4(r[(RPZ - 1) * RQ], r[(RPZ - 1) * RQ + 1], r[(RPZ - 1) * RQ + 2], r[(RPZ - 1) * RQ + 3]);
-    cluster.sync();
-    const double bb = setup_total(sm, 0);
-    double rr = setup_total(sm, 1);
-    // neighbours' p_0 faces (= their r0 faces), then advanced locally every iteration
-    float4 pf_dn = below ? below->rown[1][ly][xq] : f4(0, 0, 0, 0);
-    float4 pf_up = above ? above->rown[0][ly][xq] : f4(0, 0, 0, 0);
-    int state = ST_ACTIVE, it = 0;
-    if (bb <= 0.0)
-      state = ST_ZERO;
-    else if (rr <= (double)a.tol2 * bb)
-      state = ST_CONVERGED;
-    else if (a.max_iter <= 0)
-      state = ST_MAXITER;
+    BTRACE(4);
+    BTRACE(5);
 
-    // ---------------- CG iterations ----------------
-    while (state == ST_ACTIVE) {
+    // ---------------- CG (Chronopoulos-Gear) ----------------
+    // pass 0 computes w0 = A'r0 and reduces gamma0 = r0.r0, delta0 = w0.r0 and
+    // ||S b||^2; pass k >= 1 first applies update k, then the same SpMV + reduction.
+    const uint32_t tx_faces = nfaces * face_bytes;
+    float gamma = 0.f, alpha = 0.f, beta = 0.f, thresh = 0.f;
+    int state = ST_ACTIVE, it = 0;
+#ifdef RWB_TRACE
+    int trace_it = (int)gk;
+#endif
+#pragma unroll
+    for (int v = 0; v < RV; ++v) {
+      p[v] = 0.f;
+      sv[v] = 0.f;
+      w[v] = 0.f;
+    }
+    for (int pass = 0;; ++pass) {
+      TRACE(0);
       const int par = gk & 1;
       const uint32_t ph = (gk >> 1) & 1;
       if (tid == 0) {
-        mbar_expect_tx(&sm.barA[par], RCL * 4);
-        mbar_expect_tx(&sm.barB[par], RCL * 4 + nfaces * face_bytes);
+        if (tx_faces) mbar_expect_tx(&sm.barF[par], tx_faces);
+        mbar_expect_tx(&sm.barR[par], 3 * NPART * 4);
       }
-      // q = A' p
-      float pq_part = 0.f;
+      if (pass > 0) {
 #pragma unroll
-      for (int z = 0; z < RPZ; ++z) {
-        const float4 pu = ly + 1 < RB ? sm.p[z][ly + 1][xq] : f4(0, 0, 0, 0);
-        const float4 pd = ly > 0 ? sm.p[z][ly - 1][xq] : f4(0, 0, 0, 0);
-        const float4 pzu =
-            z + 1 < RPZ ? f4(p[(z + 1) * RQ], p[(z + 1) * RQ + 1], p[(z + 1) * RQ + 2], p[(z + 1) * RQ + 3]) : pf_up;
-        const float4 pzd = z > 0 ? f4(p[(z - 1) * RQ], p[(z - 1) * RQ + 1], p[(z - 1) * RQ + 2], p[(z - 1) * RQ + 3])
-                                 : pf_dn;
-        const float pl = __shfl_up_sync(0xffffffffu, p[z * RQ + RQ - 1], 1);
-        const float pr = __shfl_down_sync(0xffffffffu, p[z * RQ], 1);
-#pragma unroll
-        for (int i = 0; i < RQ; ++i) {
-          const int v = z * RQ + i;
-          const float pxl = i > 0 ? p[v - 1] : pl;
-          const float pxr = i < RQ - 1 ? p[v + 1] : pr;
-          const float wxl = i > 0 ? wxf[v - 1] : wxb[z];
-          const float wzl = z > 0 ? wzf[v - RQ] : wzb[i];
-          float s = wxf[v] * pxr;
-          s = fmaf(wxl, pxl, s);
-          s = fmaf(wyf[v], lane_of(pu, i), s);
-          s = fmaf(wyb[v], lane_of(pd, i), s);
-          s = fmaf(wzf[v], lane_of(pzu, i), s);
-          s = fmaf(wzl, lane_of(pzd, i), s);
-          q[v] = p[v] - s;
-          pq_part = fmaf(p[v], q[v], pq_part);
+        for (int v = 0; v < RV; ++v) {
+          p[v] = fmaf(beta, p[v], r[v]);
+          sv[v] = fmaf(beta, sv[v], w[v]);
+          y[v] = fmaf(alpha, p[v], y[v]);
+          r[v] = fmaf(-alpha, sv[v], r[v]);
         }
       }
-      {
-        const float s = cta_sum(sm, pq_part, 0);
-        const float tot = __shfl_sync(0xffffffffu, s, 0);  // warp 0 holds thread 0's sum
-        if (tid < RCL) st_async_f32(par ? red_dst[0][1] : red_dst[0][0], tot, par ? barA_dst[1] : barA_dst[0]);
-      }
-      mbar_wait(&sm.barA[par], ph);
-      const double pq = pushed_total(sm, 0, par);
-      const float alpha = pq != 0.0 ? (float)(rr / pq) : 0.f;
-      float rr_part = 0.f;
+      // publish r: planes for the y neighbours, faces for the z neighbours
 #pragma unroll
-      for (int v = 0; v < RV; ++v) {
-        y[v] = fmaf(alpha, p[v], y[v]);
-        r[v] = fmaf(-alpha, q[v], r[v]);
-        rr_part = fmaf(r[v], r[v], rr_part);
-      }
+      for (int z = 0; z < RPZ; ++z) sm.rp[z][ly][xq] = f4(r[z * RQ], r[z * RQ + 1], r[z * RQ + 2], r[z * RQ + 3]);
       if (rank > 0)
         st_async_v4(par ? face_dn_dst[1] : face_dn_dst[0], f4(r[0], r[1], r[2], r[3]), par ? bar_dn[1] : bar_dn[0]);
       if (rank < RCL - 1)
         st_async_v4(par ? face_up_dst[1] : face_up_dst[0],
                     f4(r[(RPZ - 1) * RQ], r[(RPZ - 1) * RQ + 1], r[(RPZ - 1) * RQ + 2], r[(RPZ - 1) * RQ + 3]),
                     par ? bar_up[1] : bar_up[0]);
-      {
-        const float s = cta_sum(sm, rr_part, 1);
-        const float tot = __shfl_sync(0xffffffffu, s, 0);
-        if (tid < RCL) st_async_f32(par ? red_dst[1][1] : red_dst[1][0], tot, par ? barB_dst[1] : barB_dst[0]);
-      }
-      mbar_wait(&sm.barB[par], ph);
-      const double rr_new = pushed_total(sm, 1, par);
-      ++it;
-      ++gk;
-      if (rr_new <= (double)a.tol2 * bb) {
-        state = ST_CONVERGED;
-        break;
-      }
-      if (it >= a.max_iter) {
-        state = ST_MAXITER;
-        break;
-      }
-      const float beta = (float)(rr_new / rr);
-      rr = rr_new;
-      if (rank > 0) {
-        const float4 rn = sm.rface[par][0][ly][xq];
-        pf_dn = f4(fmaf(beta, pf_dn.x, rn.x), fmaf(beta, pf_dn.y, rn.y), fmaf(beta, pf_dn.z, rn.z),
-                   fmaf(beta, pf_dn.w, rn.w));
-      }
-      if (rank < RCL - 1) {
-        const float4 rn = sm.rface[par][1][ly][xq];
-        pf_up = f4(fmaf(beta, pf_up.x, rn.x), fmaf(beta, pf_up.y, rn.y), fmaf(beta, pf_up.z, rn.z),
-                   fmaf(beta, pf_up.w, rn.w));
-      }
-#pragma unroll
-      for (int v = 0; v < RV; ++v) p[v] = fmaf(beta, p[v], r[v]);
-#pragma unroll
-      for (int z = 0; z < RPZ; ++z) sm.p[z][ly][xq] = f4(p[z * RQ], p[z * RQ + 1], p[z * RQ + 2], p[z * RQ + 3]);
       __syncthreads();
+      TRACE(1);
+      // w = A'r: interior planes first, the two face planes once their neighbours arrived
+      float g4[RPZ] = {0.f, 0.f, 0.f, 0.f}, d4[RPZ] = {0.f, 0.f, 0.f, 0.f};
+      auto spmv_plane = [&](int z, const float4& rzu, const float4& rzd) {
+        const float4 ru = ly + 1 < RB ? sm.rp[z][ly + 1][xq] : f4(0, 0, 0, 0);
+        const float4 rd = ly > 0 ? sm.rp[z][ly - 1][xq] : f4(0, 0, 0, 0);
+        const float rl = __shfl_up_sync(0xffffffffu, r[z * RQ + RQ - 1], 1);
+        const float rr_ = __shfl_down_sync(0xffffffffu, r[z * RQ], 1);
+#pragma unroll
+        for (int i = 0; i < RQ; ++i) {
+          const int v = z * RQ + i;
+          const float rxl = i > 0 ? r[v - 1] : rl;
+          const float rxr = i < RQ - 1 ? r[v + 1] : rr_;
+          const float wxl = i > 0 ? wxf[v - 1] : wxb[z];
+          const float wzl = z > 0 ? wzf[v - RQ] : wzb[i];
+          float acc = wxf[v] * rxr;
+          acc = fmaf(wxl, rxl, acc);
+          acc = fmaf(wyf[v], lane_of(ru, i), acc);
+          acc = fmaf(wyb[v], lane_of(rd, i), acc);
+          acc = fmaf(wzf[v], lane_of(rzu, i), acc);
+          acc = fmaf(wzl, lane_of(rzd, i), acc);
+          w[v] = r[v] - acc;
+          g4[z] = fmaf(r[v], r[v], g4[z]);
+          d4[z] = fmaf(w[v], r[v], d4[z]);
+        }
+      };
+#pragma unroll
+      for (int z = 1; z < RPZ - 1; ++z)
+        spmv_plane(z, f4(r[(z + 1) * RQ], r[(z + 1) * RQ + 1], r[(z + 1) * RQ + 2], r[(z + 1) * RQ + 3]),
+                   f4(r[(z - 1) * RQ], r[(z - 1) * RQ + 1], r[(z - 1) * RQ + 2], r[(z - 1) * RQ + 3]));
+      if (tx_faces) mbar_wait(&sm.barF[par], ph);
+      TRACE(2);
+      spmv_plane(0, f4(r[RQ], r[RQ + 1], r[RQ + 2], r[RQ + 3]),
+                 below ? sm.rface[par][0][ly][xq] : f4(0, 0, 0, 0));
+      spmv_plane(RPZ - 1, above ? sm.rface[par][1][ly][xq] : f4(0, 0, 0, 0),
+                 f4(r[(RPZ - 2) * RQ], r[(RPZ - 2) * RQ + 1], r[(RPZ - 2) * RQ + 2], r[(RPZ - 2) * RQ + 3]));
+      TRACE(3);
+      {
+        const float gw = warp_sum((g4[0] + g4[1]) + (g4[2] + g4[3]));
+        const float dw = warp_sum((d4[0] + d4[1]) + (d4[2] + d4[3]));
+        const float bw_ = pass == 0 ? warp_sum(bb_part) : 0.f;
+        if (lane < RCL) {
+          const uint32_t dst = par ? red_dst[1] : red_dst[0], bar = par ? barR_dst[1] : barR_dst[0];
+          st_async_f32(dst, gw, bar);
+          st_async_f32(dst + NPART * 4, dw, bar);
+          st_async_f32(dst + 2 * NPART * 4, bw_, bar);
+        }
+      }
+      TRACE(4);
+      mbar_wait(&sm.barR[par], ph);
+      TRACE(5);
+      ++gk;
+      const float g_new = sum64(sm.red[par][0]);
+      const float delta = sum64(sm.red[par][1]);
+      if (pass == 0) {
+        const double bb = (double)sum64(sm.red[par][2]);
+        thresh = (float)((double)a.tol2 * bb);
+        if (bb <= 0.0) {
+          state = ST_ZERO;  // no Dirichlet coupling: the exact solution is 0
+          break;
+        }
+        if ((double)g_new <= (double)a.tol2 * bb) {
+          state = ST_CONVERGED;
+          break;
+        }
+        if (a.max_iter <= 0) {
+          state = ST_MAXITER;
+          break;
+        }
+        beta = 0.f;
+        alpha = delta != 0.f ? __fdividef(g_new, delta) : 0.f;
+      } else {
+        ++it;
+        if (g_new <= thresh) {
+          state = ST_CONVERGED;
+          break;
+        }
+        if (it >= a.max_iter) {
+          state = ST_MAXITER;
+          break;
+        }
+        // fast reciprocals: the scalars only need to be identical in every CTA
+        beta = __fdividef(g_new, gamma);
+        const float den = delta - beta * __fdividef(g_new, alpha);
+        alpha = den != 0.f ? __fdividef(g_new, den) : 0.f;
+      }
+      gamma = g_new;
+      TRACE(6);
+#ifdef RWB_TRACE
+      ++trace_it;
+#endif
     }
+    BTRACE(6);
 
     // ---------------- epilogue: x = s*y | seed value | bound ----------------
 #pragma unroll
-    for (int z = 0; z < RPZ; ++z)
+    for (int z = 0; z < RPZ; ++z) {
+      const int gz = gz0 + z;
 #pragma unroll
       for (int i = 0; i < RQ; ++i) {
         const int v = z * RQ + i;
-        if (!in_level(z, i)) continue;
-        const long long gi = gidx(z, i);
+        const unsigned char s = tS[z + 1][cy][cx0 + i];
+        if (s == OUTSIDE) continue;
         float x;
-        if (scl[v] > 0.f) {
+        if (scl[v] > 0.f)
           x = state == ST_ZERO ? 0.f : scl[v] * y[v];
-        } else {
-          const uint8_t s = __ldg(a.S + gi);
-          x = s ? seedval(s) : (a.bound ? __ldg(a.bound + gi) : 0.f);
-        }
+        else
+          x = s ? seedval(s) : tB[z + 1][cy][cx0 + i];
+        const long long gi = (long long)gz * g.sxy + (long long)gy * g.nx + (gx0 + i);
         a.prob[gi] = x;
         if (a.labels) a.labels[gi] = x > 0.5f ? 1 : 0;
       }
+    }
     if (rank == 0 && tid == 0) {
       a.state[slot] = state;
       a.iters[slot] = state == ST_ZERO ? 0 : it;
     }
-    // every DSMEM read of this brick is done before any CTA starts the next one
+    BTRACE(7);
+    // every DSMEM read of this brick (sc) is done before any CTA starts the
+    // next one; the staged seeds of the next brick are loaded after it
     cluster.sync();
+    if (next < a.nb) stage_seeds(a, sm, buf ^ 1, a.list ? a.list[next] : next, lz0);
+    BTRACE(8);
+#ifdef RWB_TRACE
+    ++btrace_n;
+#endif
   }
 }
+
+#ifdef RWB_TRACE
+extern "C" int rwb_trace_dump(long long* out) {  // 8*64*8 int64
+  return (int)cudaMemcpyFromSymbol(out, g_rwb_trace, sizeof(g_rwb_trace));
+}
+extern "C" int rwb_btrace_dump(long long* out) {  // 8*16*10 int64
+  return (int)cudaMemcpyFromSymbol(out, g_rwb_btrace, sizeof(g_rwb_btrace));
+}
+#endif
 
 int resident3d_supported(const Geo& g) { return g.is3d && g.bz == RB && g.by == RB && g.bx == RB; }
 
 int launch_resident3d(const ResidentArgs& a, cudaStream_t st) {
   static thread_local int clusters = 0;
   const int smem = (int)sizeof(ResidentSmem);
+  if (!a.bound) return fail(RWB_ERR_INVALID, "the brick-resident solver needs a bound");
   if (!clusters) {
     RWB_CUDA(cudaFuncSetAttribute(resident3d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     cudaLaunchConfig_t cfg = {};
@@ -496,7 +601,7 @@ int launch_resident3d(const ResidentArgs& a, cudaStream_t st) {
     if (n <= 0) return fail(RWB_ERR_UNSUPPORTED, "no 8-CTA cluster fits on this device");
     clusters = n;
   }
-  int grid_clusters = clusters < a.nb ? clusters : a.nb;
+  const int grid_clusters = clusters < a.nb ? clusters : a.nb;
   resident3d_kernel<<<grid_clusters * RCL, RT, smem, st>>>(a);
   RWB_LAUNCH_CHECK("resident3d_kernel");
   count_launches(1);
