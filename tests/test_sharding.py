@@ -120,3 +120,92 @@ def test_halo_exchange_gloo_world2():
     results = dict(q.get(timeout=5) for _ in procs)
     assert results == {0: True, 1: True}
     assert all(p.exitcode == 0 for p in procs)
+
+
+# -- the sharded hierarchical driver end to end, world_size 2 over gloo -------------------
+# The level operators are swapped for the float64 oracle on CPU tensors, so the
+# test exercises exactly the host logic that runs on GPUs: the shard plan, the
+# per-level brick lists, and the point-to-point halo exchange of parent planes.
+
+def _install_oracle_backend():
+    from oracle import lod as olod
+    from paper_2509_26213_b200 import device
+
+    def lod_down(level):
+        return torch.from_numpy(olod.lod_down(level.numpy()))
+
+    def project_seeds(seeds):
+        return torch.from_numpy(orw.project_seeds(seeds.numpy()))
+
+    def upsample(parent, fine_shape, out=None):
+        return torch.from_numpy(orw.upsample_linear(parent.numpy(), tuple(fine_shape)).astype(np.float32))
+
+    def solve_level(vol, seeds, brick, bound, cfg, *, brick_list=None, out=None, labels_out=None,
+                    workspace=None, origin=None):
+        params = orw.RWParams(beta=cfg.beta, min_weight=cfg.min_weight, tol=1e-10)
+        b = None if bound is None else bound.numpy().astype(np.float64)
+        res = orw.solve_level(vol.numpy(), seeds.numpy(), brick, b, params).prob.astype(np.float32)
+        if out is None:
+            out = torch.full(vol.shape, float("nan"))
+        if brick_list is None:
+            out.copy_(torch.from_numpy(res))
+        else:
+            bid, _ = orw.brick_ids(tuple(vol.shape), brick)
+            sel = torch.from_numpy(np.isin(bid, brick_list.numpy()))
+            out[sel] = torch.from_numpy(res)[sel]
+        if labels_out is not None:
+            labels_out.copy_(out > 0.5)
+        return out, {"bricks": 0, "cg_ms": 0.0, "iterations_sum": 0}
+
+    device.lod_down = lod_down
+    device.project_seeds = project_seeds
+    device.upsample = upsample
+    device.solve_level = solve_level
+
+
+def _sharded_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        _install_oracle_backend()
+        from paper_2509_26213_b200 import synthetic
+        from paper_2509_26213_b200.config import RWConfig
+
+        shape, brick, levels = (48, 16, 16), (8, 8, 8), 3
+        vol = synthetic.phantom(shape)
+        sd = synthetic.seeds(shape, "S1")
+        plan = sharding.ShardPlan.build(shape, brick, levels, rank, world)
+        for s in plan.shards:
+            if s is not None:
+                s.brick_list = torch.tensor(s.bricks[rank], dtype=torch.int32)
+        res = sharding.hierarchical_random_walker_sharded(torch.from_numpy(vol), torch.from_numpy(sd), plan,
+                                                          RWConfig(), want_labels=False)
+        z0, z1 = plan.owned_planes(0, rank)
+        q.put((rank, z0, z1, res.prob[z0:z1].numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_hierarchy_matches_single_process_gloo_world2():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    from paper_2509_26213_b200 import synthetic
+
+    shape = (48, 16, 16)
+    vol = synthetic.phantom(shape)
+    sd = synthetic.seeds(shape, "S1")
+    ref = orw.hierarchical_random_walker(vol, sd, (8, 8, 8), 3, orw.RWParams(tol=1e-10)).prob[0].astype(np.float32)
+    covered = np.zeros(shape[0], bool)
+    for rank, z0, z1, part in got:
+        assert not np.isnan(part).any()
+        np.testing.assert_array_equal(part, ref[z0:z1])
+        covered[z0:z1] = True
+    assert covered.all()
