@@ -69,10 +69,12 @@ typedef struct {
 
 #define RWB_SOLVE_NO_GRAPH 1  /* streaming solver: launch iterations directly, not via a CUDA graph */
 #define RWB_SOLVE_STREAMING 2 /* force the streaming solver even where the brick-resident one applies */
+#define RWB_SOLVE_NO_COOP 4   /* whole-level solves: graph-launched passes instead of one cooperative kernel */
 
 /* Solver paths (rwb_solve_stats_t.path) */
 #define RWB_PATH_STREAMING 0 /* brick-batched CG, state in HBM, 2 launches per iteration */
 #define RWB_PATH_RESIDENT 1  /* one 32^3 brick per 8-CTA cluster, CG state on chip */
+#define RWB_PATH_COOPERATIVE 2 /* single-brick (whole-level) solve: all iterations in one cooperative kernel */
 
 typedef struct {
   int64_t bricks;          /* bricks solved by this call */
@@ -156,8 +158,10 @@ size_t rwb_solve_workspace_bytes(const rwb_geometry_t* geom, int64_t n_bricks, i
  *  labels    : u8 level output (prob > 0.5) or NULL.
  *  stats     : host pointer or NULL.
  * Path: 3-D levels with 32^3 bricks and more than one brick run the
- * brick-resident solver (unless RWB_SOLVE_STREAMING); everything else —
- * including every whole-level (coarsest) solve — runs the streaming solver.
+ * brick-resident solver (unless RWB_SOLVE_STREAMING); whole-level (coarsest,
+ * single-brick) solves run the streaming passes inside one cooperative
+ * kernel (unless RWB_SOLVE_NO_COOP); everything else runs the streaming
+ * solver with graph-launched passes.
  * Blocking on the host: returns when the listed bricks have converged (or hit
  * max_iter); all work is stream-ordered on `stream`. */
 int rwb_solve_level(const rwb_geometry_t* geom, const float* intensity, const uint8_t* seeds,

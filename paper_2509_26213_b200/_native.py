@@ -21,7 +21,8 @@ c_int32, c_int64, c_float, c_void_p, c_size_t = (
 ABI_VERSION = 1
 SOLVE_NO_GRAPH = 1
 SOLVE_STREAMING = 2
-PATH_STREAMING, PATH_RESIDENT = 0, 1
+SOLVE_NO_COOP = 4
+PATH_STREAMING, PATH_RESIDENT, PATH_COOPERATIVE = 0, 1, 2
 
 # every symbol include/rwb.h declares, with (restype, argtypes)
 SIGNATURES = {

@@ -19,10 +19,12 @@ class RWConfig:
     check_every: int = 16      # CG iterations per convergence poll (one CUDA graph)
     use_graph: bool = True     # streaming solver: run each poll interval as one CUDA graph launch
     resident: bool = True      # 32^3 bricks: solve each brick on chip (8-CTA cluster) instead of streaming
+    cooperative: bool = True   # whole-level solves: one cooperative kernel for all iterations
 
     def params(self) -> dict:
         d = asdict(self)
         d.pop("check_every")
         d.pop("use_graph")
         d.pop("resident")
+        d.pop("cooperative")
         return {k: (float(v) if isinstance(v, float) else int(v)) for k, v in d.items()}

@@ -36,6 +36,9 @@
 #include "rwb_common.cuh"
 #include "rwb_resident.cuh"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace rwb {
 
 constexpr int TX = 32;  // threads along x (one warp per row segment)
@@ -401,6 +404,126 @@ __global__ void __launch_bounds__(NTHREADS) cg_pass2_kernel(Geo g, Work w, int n
   }
 }
 
+// ---------------------------------------------------------------------------
+// Whole-level (single-brick) solve as ONE cooperative persistent kernel: every
+// iteration's two passes are separated by grid-wide barriers instead of kernel
+// launches, and the level's working set (~36 B/voxel, 75 MB at 128^3) stays in
+// the 126 MB L2.  Loads of the vectors written inside the kernel are plain
+// (L1-cacheable) loads: the grid barrier's gpu-scope fence invalidates L1, and
+// within a pass they are read-only.  Per-block partials are reduced by every
+// block in the same fixed order (float64), so all blocks take the same
+// decisions and the result is deterministic.
+
+__device__ __forceinline__ double grid_total(const float* part, int n, double* bcast) {
+  // warp 0 sums all block partials in a fixed order; result broadcast through smem
+  if (threadIdx.y == 0) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += 32) s += (double)__ldcg(part + i);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (threadIdx.x == 0) *bcast = s;
+  }
+  __syncthreads();
+  const double v = *bcast;
+  __syncthreads();
+  return v;
+}
+
+__global__ void __launch_bounds__(NTHREADS) coop_cg_kernel(Geo g, Work w, float* part_pq, float* part_rr, float tol2,
+                                                           int max_iter) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double bcast;
+  const long long sbz = (long long)g.by * g.bx;
+  const double bb = w.bb[0];
+  double rr = w.rr[0];
+  int state = ST_ACTIVE;
+  if (bb <= 0.0)
+    state = ST_ZERO;
+  else if (rr <= (double)tol2 * bb)
+    state = ST_CONVERGED;
+  else if (max_iter <= 0)
+    state = ST_MAXITER;
+  int it = 0;
+  double rr_prev = 0.0;
+  while (state == ST_ACTIVE) {
+    const int par = it & 1;
+    const float* pin = par ? w.p1 : w.p0;
+    float* pout = par ? w.p0 : w.p1;
+    const float beta = (it == 0) ? 0.f : (float)(rr / rr_prev);
+    // pass 1: p <- r + beta p ; q = A'p ; p.q
+    float acc = 0.f;
+    for (int tile = blockIdx.x; tile < g.tiles; tile += gridDim.x) {
+      TileCtx c = tile_ctx(g, nullptr, 0, tile);
+      if (!c.col) continue;
+      const long long lbase = (long long)c.ly * g.bx + c.lx;
+      const bool hx0 = c.lx > 0, hx1 = c.lx + 1 < g.bx, hy0 = c.ly > 0, hy1 = c.ly + 1 < g.by;
+      auto pn_at = [&](long long i) { return w.r[i] + beta * pin[i]; };
+      long long li = lbase + (long long)c.lz0 * sbz;
+      float pm = (g.is3d && c.lz0 > 0) ? pn_at(li - sbz) : 0.f;
+      float wzm = (g.is3d && c.lz0 > 0) ? __ldg(w.wz + li - sbz) : 0.f;
+      float pc = pn_at(li);
+      for (int lz = c.lz0; lz < c.lz1; ++lz, li += sbz) {
+        const bool up = g.is3d && lz + 1 < g.bz;
+        float pp = up ? pn_at(li + sbz) : 0.f;
+        float wzc = up ? __ldg(w.wz + li) : 0.f;
+        float s = wzc * pp + wzm * pm;
+        if (hx1) s += __ldg(w.wx + li) * pn_at(li + 1);
+        if (hx0) s += __ldg(w.wx + li - 1) * pn_at(li - 1);
+        if (hy1) s += __ldg(w.wy + li) * pn_at(li + g.bx);
+        if (hy0) s += __ldg(w.wy + li - g.bx) * pn_at(li - g.bx);
+        const float q = pc - s;
+        pout[li] = pc;
+        w.q[li] = q;
+        acc += pc * q;
+        pm = pc;
+        pc = pp;
+        wzm = wzc;
+      }
+    }
+    {
+      const float2 sblk = block_sum2(acc, 0.f);
+      if (threadIdx.x == 0 && threadIdx.y == 0) part_pq[blockIdx.x] = sblk.x;
+    }
+    grid.sync();
+    __threadfence();
+    const double pq = grid_total(part_pq, gridDim.x, &bcast);
+    const float alpha = pq != 0.0 ? (float)(rr / pq) : 0.f;
+    // pass 2: y += alpha p ; r -= alpha q ; r.r
+    float acc2 = 0.f;
+    for (int tile = blockIdx.x; tile < g.tiles; tile += gridDim.x) {
+      TileCtx c = tile_ctx(g, nullptr, 0, tile);
+      if (!c.col) continue;
+      long long li = (long long)c.ly * g.bx + c.lx + (long long)c.lz0 * sbz;
+      for (int lz = c.lz0; lz < c.lz1; ++lz, li += sbz) {
+        const float y = w.y[li] + alpha * pout[li];
+        const float r = w.r[li] - alpha * w.q[li];
+        w.y[li] = y;
+        w.r[li] = r;
+        acc2 += r * r;
+      }
+    }
+    {
+      const float2 sblk = block_sum2(acc2, 0.f);
+      if (threadIdx.x == 0 && threadIdx.y == 0) part_rr[blockIdx.x] = sblk.x;
+    }
+    grid.sync();
+    __threadfence();
+    const double rr_new = grid_total(part_rr, gridDim.x, &bcast);
+    ++it;
+    if (rr_new <= (double)tol2 * bb)
+      state = ST_CONVERGED;
+    else if (it >= max_iter)
+      state = ST_MAXITER;
+    rr_prev = rr;
+    rr = rr_new;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) {
+    w.state[0] = state;
+    w.iters[0] = state == ST_ZERO ? 0 : it;
+    // the epilogue reads y from the buffer pass 2 last wrote: nothing else to do
+  }
+}
+
 // Single CTA: advance the iteration base by k and rebuild the compacted list
 // of active slots (stable order).
 __global__ void __launch_bounds__(1024) advance_kernel(Work w, int nb, int k) {
@@ -537,6 +660,8 @@ static int make_geo(const rwb_geometry_t* geom, Geo* g) {
   return RWB_OK;
 }
 
+constexpr int kCoopMaxBlocks = 4096;  // partial slots of the cooperative whole-level solve
+
 enum { L_Y, L_R, L_P0, L_P1, L_Q, L_WX, L_WY, L_WZ, L_SC, L_RR, L_PQ, L_BB, L_STATE, L_ITERS, L_TICKET,
        L_ALIST, L_PART, L_MISC, L_N };
 
@@ -551,7 +676,8 @@ static Layout layout(const Geo& g, long long nb) {
   const size_t sizes[L_N] = {vox, vox, vox, vox, vox, vox, vox, g.is3d ? vox : 0, vox,
                              2 * nb * sizeof(double), nb * sizeof(double), nb * sizeof(double),
                              nb * sizeof(int), nb * sizeof(int), nb * sizeof(unsigned), nb * sizeof(int),
-                             (size_t)nb * g.tiles * sizeof(float2), 64};
+                             std::max((size_t)nb * g.tiles * sizeof(float2), (size_t)2 * kCoopMaxBlocks * sizeof(float)),
+                             64};
   size_t o = 0;
   for (int i = 0; i < L_N; ++i) {
     L.off[i] = o;
@@ -620,6 +746,21 @@ static int launch_chunk(const Geo& g, const Work& w, int nb, const int* list, in
   }
   advance_kernel<<<1, 1024, 0, st>>>(w, nb, k);
   RWB_LAUNCH_CHECK("cg iteration kernels");
+  return RWB_OK;
+}
+
+static int coop_grid(int* grid) {
+  static thread_local int cached = 0;
+  if (!cached) {
+    int dev = 0, sms = 0, per = 0, coop = 0;
+    RWB_CUDA(cudaGetDevice(&dev));
+    RWB_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+    if (!coop) return fail(RWB_ERR_UNSUPPORTED, "device does not support cooperative launches");
+    RWB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, coop_cg_kernel, NTHREADS, 0));
+    cached = std::min(sms * std::max(per, 1), kCoopMaxBlocks);
+  }
+  *grid = cached;
   return RWB_OK;
 }
 
@@ -767,6 +908,53 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
   advance_kernel<<<1, 1024, 0, st>>>(w, nb, 0);
   RWB_LAUNCH_CHECK("setup kernels");
   count_launches(3);
+
+  if (total == 1 && !(params->flags & RWB_SOLVE_NO_COOP)) {
+    // whole-level solve: all iterations in one cooperative launch
+    int cgrid = 0;
+    rc = coop_grid(&cgrid);
+    if (rc) return rc;
+    cgrid = std::min(cgrid, std::max(g.tiles, 1));
+    float* part_pq = reinterpret_cast<float*>(w.part);
+    float* part_rr = part_pq + kCoopMaxBlocks;
+    float tol2v = tol2;
+    int max_iter_v = max_iter;
+    void* args[] = {&g, &w, &part_pq, &part_rr, &tol2v, &max_iter_v};
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    RWB_CUDA(cudaEventCreate(&ev0));
+    RWB_CUDA(cudaEventCreate(&ev1));
+    RWB_CUDA(cudaEventRecord(ev0, st));
+    RWB_CUDA(cudaLaunchCooperativeKernel((const void*)coop_cg_kernel, dim3(cgrid), block, args, 0, st));
+    RWB_CUDA(cudaEventRecord(ev1, st));
+    epilogue_kernel<<<sgrid, block, 0, st>>>(g, w, list, seeds, bound, prob, labels);
+    stats_kernel<<<1, 1024, 0, st>>>(w, nb);
+    RWB_LAUNCH_CHECK("cooperative solve");
+    count_launches(3);
+    if (stats) {
+      int hs[8];
+      unsigned long long unk = 0;
+      RWB_CUDA(cudaMemcpyAsync(hs, w.stat_i, sizeof(hs), cudaMemcpyDeviceToHost, st));
+      RWB_CUDA(cudaMemcpyAsync(&unk, w.unknowns, sizeof(unk), cudaMemcpyDeviceToHost, st));
+      RWB_CUDA(cudaStreamSynchronize(st));
+      float ms = 0.f;
+      RWB_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+      stats->bricks = nb;
+      stats->converged = hs[0];
+      stats->not_converged = hs[1];
+      stats->zero_rhs = hs[2];
+      stats->iterations_max = hs[3];
+      unsigned long long s64;
+      std::memcpy(&s64, hs + 4, sizeof(s64));
+      stats->iterations_sum = (int64_t)s64;
+      stats->unknowns = (int64_t)unk;
+      stats->sweeps = hs[3];
+      stats->cg_ms = ms;
+      stats->path = RWB_PATH_COOPERATIVE;
+    }
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    return RWB_OK;
+  }
 
   int* host = nullptr;
   rc = pinned(&host);

@@ -105,6 +105,26 @@ def upsample(parent: torch.Tensor, fine_shape, out: torch.Tensor | None = None) 
     return out
 
 
+def upsample_window(parent: torch.Tensor, fine_shape, z0: int, z1: int, out: torch.Tensor) -> torch.Tensor:
+    """Upsample only planes [z0, z1) (dim 0) of the fine level into `out` (full fine shape)."""
+    _check_tensor(parent, torch.float32, "parent", (2, 3))
+    _check_tensor(out, torch.float32, "out")
+    fine_shape = tuple(int(s) for s in fine_shape)
+    if tuple(out.shape) != fine_shape:
+        raise ValueError("out has the wrong shape")
+    if z1 <= z0:
+        return out
+    nd = parent.dim()
+    fo = [z0] + [0] * (nd - 1)
+    fw = [z1 - z0] + list(fine_shape[1:])
+    view = out[z0:z1]
+    lib = _native.lib()
+    a64 = _native.int64_array
+    _native.check(lib.rwb_upsample_window_f32(nd, a64(parent.shape), a64([0] * nd), a64(parent.shape), _ptr(parent),
+                                              a64(fine_shape), a64(fo), a64(fw), _ptr(view), _stream_handle()))
+    return out
+
+
 def edge_weights(volume: torch.Tensor, beta: float = 100.0, min_weight: float = 1e-6) -> torch.Tensor:
     """Forward edge weights, lanes-last: shape volume.shape + (ndim,)."""
     _check_tensor(volume, torch.float32, "volume", (1, 2, 3))
@@ -171,6 +191,8 @@ def _flags(cfg: RWConfig) -> int:
     f = 0 if cfg.use_graph else _native.SOLVE_NO_GRAPH
     if not cfg.resident:
         f |= _native.SOLVE_STREAMING
+    if not cfg.cooperative:
+        f |= _native.SOLVE_NO_COOP
     return f
 
 
@@ -244,7 +266,7 @@ class HRWResult:
 def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick, levels: int | None = None,
                                cfg: RWConfig = RWConfig(), *, want_labels: bool = True,
                                workspace: Workspace | None = None, brick_lists=None,
-                               exchange=None) -> HRWResult:
+                               exchange=None, upsample_planes=None) -> HRWResult:
     """Coarse-to-fine random walker (oracle/rw.py: hierarchical_random_walker).
 
     The coarsest level is solved whole; each finer level is initialised and
@@ -252,7 +274,8 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
     by brick.  `brick_lists[k]` (int32 device tensor) restricts level k to a
     subset of bricks (multi-GPU sharding) and `exchange(k, prob_k)` is called
     after level k is solved so the caller can complete the halo of the
-    parent level before it is upsampled (see sharding.py).
+    parent level before it is upsampled; `upsample_planes[k]` = (z0, z1)
+    limits the prolongation of level k to those planes (see sharding.py).
     """
     brick = tuple(int(b) for b in brick)
     vols = lod_chain(volume, brick, levels)
@@ -273,7 +296,12 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
     for k in range(top - 1, -1, -1):
         if exchange is not None:
             exchange(k + 1, probs[k + 1])
-        x = upsample(probs[k + 1], vols[k].shape)
+        win = upsample_planes[k] if upsample_planes is not None else None
+        if win is None:
+            x = upsample(probs[k + 1], vols[k].shape)
+        else:  # sharded: only the planes this rank's bricks (+ halo) read
+            x = upsample_window(probs[k + 1], vols[k].shape, win[0], win[1],
+                                torch.empty(vols[k].shape, dtype=torch.float32, device=volume.device))
         lab_k = torch.empty(vols[k].shape, dtype=torch.uint8, device=volume.device) \
             if (want_labels and k == 0) else None
         bl = brick_lists[k] if brick_lists is not None else None

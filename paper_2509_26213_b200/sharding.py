@@ -138,28 +138,41 @@ def halo_messages(plan: ShardPlan, level: int):
 
 
 def exchange_halo(plan: ShardPlan, level: int, prob: torch.Tensor, group=None):
-    """Receive the parent planes this rank needs from their owners (point to point)."""
+    """Receive the parent planes this rank needs from their owners (point to point).
+
+    NCCL moves device tensors directly (NVLink); backends without device
+    support for point-to-point (gloo: CPU tests, several ranks sharing one
+    GPU in tests) get the planes staged through host memory.
+    """
     import torch.distributed as dist
 
-    ops = []
-    for src, dst, a, b in halo_messages(plan, level):
+    msgs = halo_messages(plan, level)
+    if not msgs:
+        return
+    stage = prob.is_cuda and dist.get_backend(group) != "nccl"
+    sends, recvs = [], []
+    for src, dst, a, b in msgs:
         if src == plan.rank:
-            ops.append(dist.P2POp(dist.isend, prob[a:b].contiguous(), dst, group=group))
+            t = prob[a:b].contiguous()
+            sends.append((t.cpu() if stage else t, dst))
         elif dst == plan.rank:
-            ops.append(("recv", src, a, b))
-    recv_bufs = []
-    p2p = [op for op in ops if not isinstance(op, tuple)]
-    for op in ops:
-        if isinstance(op, tuple):
-            _, src, a, b = op
-            buf = torch.empty_like(prob[a:b])
-            recv_bufs.append((buf, a, b))
-            p2p.append(dist.P2POp(dist.irecv, buf, src, group=group))
-    if p2p:
-        for req in dist.batch_isend_irecv(p2p):
+            buf = torch.empty(prob[a:b].shape, dtype=prob.dtype, device="cpu" if stage else prob.device)
+            recvs.append((buf, src, a, b))
+    ops = [dist.P2POp(dist.isend, t, dst, group=group) for t, dst in sends]
+    ops += [dist.P2POp(dist.irecv, buf, src, group=group) for buf, src, _, _ in recvs]
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
             req.wait()
-    for buf, a, b in recv_bufs:
+    for buf, _, a, b in recvs:
         prob[a:b].copy_(buf)
+
+
+def upsample_planes(plan: ShardPlan, level: int):
+    """Planes of `level` (< L-1) this rank's bricks and their 1-voxel halo read."""
+    z0, z1 = plan.shards[level].planes[plan.rank]
+    if z1 <= z0:
+        return (0, 0)
+    return (max(z0 - 1, 0), min(z1 + 1, plan.shards[level].shape[0]))
 
 
 def hierarchical_random_walker_sharded(volume, seeds, plan: ShardPlan, cfg: RWConfig = RWConfig(), *,
@@ -168,9 +181,11 @@ def hierarchical_random_walker_sharded(volume, seeds, plan: ShardPlan, cfg: RWCo
     from . import device
 
     lists = [s.brick_list if s is not None else None for s in plan.shards]
+    windows = [upsample_planes(plan, k) if k < plan.levels - 1 else None for k in range(plan.levels)]
 
     def exchange(level, prob):
         exchange_halo(plan, level, prob, group)
 
     return device.hierarchical_random_walker(volume, seeds, plan.brick, plan.levels, cfg, want_labels=want_labels,
-                                             workspace=workspace, brick_lists=lists, exchange=exchange)
+                                             workspace=workspace, brick_lists=lists, exchange=exchange,
+                                             upsample_planes=windows)

@@ -293,3 +293,16 @@ def test_resident_rejects_aliased_output(rng):
     bound = cuda(rng.random(vol.shape).astype(np.float32))
     with pytest.raises(ValueError):
         device.solve_level(cuda(vol), cuda(seeds), (32, 32, 32), bound, GPU_CFG, out=bound)
+
+
+def test_cooperative_whole_level_matches_graph_path():
+    vol = synthetic.phantom((48, 40, 36))
+    seeds = synthetic.seeds(vol.shape, "S2")
+    ref = orw.solve_level(vol, seeds, vol.shape, None, TIGHT).prob
+    a, sa = device.solve_level(cuda(vol), cuda(seeds), vol.shape, None, GPU_CFG)
+    b, sb = device.solve_level(cuda(vol), cuda(seeds), vol.shape, None,
+                               RWConfig(tol=GPU_CFG.tol, max_iter=GPU_CFG.max_iter, cooperative=False))
+    assert sa["path"] == 2 and sb["path"] == 0
+    assert_rw_parity(host(a), ref)
+    assert_rw_parity(host(b), ref)
+    assert abs(sa["iterations_max"] - sb["iterations_max"]) <= 2

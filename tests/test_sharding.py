@@ -157,9 +157,16 @@ def _install_oracle_backend():
             labels_out.copy_(out > 0.5)
         return out, {"bricks": 0, "cg_ms": 0.0, "iterations_sum": 0}
 
+    def upsample_window(parent, fine_shape, z0, z1, out):
+        full = torch.from_numpy(orw.upsample_linear(parent.numpy(), tuple(fine_shape)).astype(np.float32))
+        out.fill_(float("nan"))  # planes outside the window must never be read
+        out[z0:z1] = full[z0:z1]
+        return out
+
     device.lod_down = lod_down
     device.project_seeds = project_seeds
     device.upsample = upsample
+    device.upsample_window = upsample_window
     device.solve_level = solve_level
 
 
