@@ -22,24 +22,24 @@ struct Geo {
   int is3d;
 };
 
+// The brick-resident CG engine works on the brick-local system the streaming
+// setup kernels build (slot-major, each brick box contiguous, x fastest).
 struct ResidentArgs {
-  Geo g;
-  const int* list;  // brick indices per slot, or null (slot == brick)
-  int nb;           // slots
-  const float* I;
-  const uint8_t* S;
-  const float* bound;
-  float* prob;
-  uint8_t* labels;
-  float beta, wmin, tol2;
+  const float* wx;        // scaled forward weights (0 across brick faces / at Dirichlet nodes)
+  const float* wy;
+  const float* wz;
+  const float* r0;        // initial scaled residual
+  float* y;               // in: y0 = x0 / s, out: the solution of the scaled system
+  const double* bb;       // per slot ||S b||^2
+  const int* alist;       // compacted slots still active after the setup
+  const int* n_active;
+  int* state;             // per slot
+  int* iters;             // per slot
+  float tol2;
   int max_iter;
-  int* state;    // [nb]
-  int* iters;    // [nb]
-  int* counter;  // work counter, zero before launch
-  unsigned long long* unknowns;
 };
 
 int resident3d_supported(const Geo& g);
-int launch_resident3d(const ResidentArgs& a, cudaStream_t st);
+int launch_resident3d(const ResidentArgs& a, int max_bricks, cudaStream_t st);
 
 }  // namespace rwb

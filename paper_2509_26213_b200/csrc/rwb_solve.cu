@@ -749,6 +749,31 @@ static int launch_chunk(const Geo& g, const Work& w, int nb, const int* list, in
   return RWB_OK;
 }
 
+// Copy the per-level stats to the host (synchronises the stream).
+static int read_stats(const Work& w, int nb, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1, int sweeps, int path,
+                      rwb_solve_stats_t* stats) {
+  int hs[8];
+  unsigned long long unk = 0;
+  RWB_CUDA(cudaMemcpyAsync(hs, w.stat_i, sizeof(hs), cudaMemcpyDeviceToHost, st));
+  RWB_CUDA(cudaMemcpyAsync(&unk, w.unknowns, sizeof(unk), cudaMemcpyDeviceToHost, st));
+  RWB_CUDA(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  if (ev0 && ev1) RWB_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+  stats->bricks = nb;
+  stats->converged = hs[0];
+  stats->not_converged = hs[1];
+  stats->zero_rhs = hs[2];
+  stats->iterations_max = hs[3];
+  unsigned long long s64;
+  std::memcpy(&s64, hs + 4, sizeof(s64));
+  stats->iterations_sum = (int64_t)s64;
+  stats->unknowns = (int64_t)unk;
+  stats->sweeps = sweeps ? sweeps : hs[3];
+  stats->cg_ms = ms;
+  stats->path = path;
+  return RWB_OK;
+}
+
 static int coop_grid(int* grid) {
   static thread_local int cached = 0;
   if (!cached) {
@@ -772,86 +797,13 @@ static bool use_resident(const Geo& g, long long total, int flags) {
   return !(flags & RWB_SOLVE_STREAMING) && total > 1 && resident3d_supported(g);
 }
 
-// resident path: per-slot state/iters + counter/stats scratch only
-static size_t resident_bytes(long long nb) { return align_up(2 * (size_t)nb * sizeof(int), 256) + 256; }
-
 extern "C" size_t rwb_solve_workspace_bytes(const rwb_geometry_t* geom, int64_t n_bricks, int32_t flags) {
   Geo g;
   if (make_geo(geom, &g)) return 0;
   long long total = (long long)g.gz * g.gy * g.gx;
   long long nb = n_bricks < 0 ? total : n_bricks;
-  if (use_resident(g, total, flags)) return resident_bytes(nb);
+  (void)flags;  // every path builds the brick-local system with the streaming setup kernels
   return layout(g, nb).total;
-}
-
-static int solve_resident(const Geo& g, const float* intensity, const uint8_t* seeds, const float* bound,
-                          const int32_t* list, int nb, const rwb_solve_params_t* params, float* prob,
-                          uint8_t* labels, void* workspace, rwb_solve_stats_t* stats, cudaStream_t st) {
-  char* base = (char*)workspace;
-  Work w;
-  std::memset(&w, 0, sizeof(w));
-  w.state = reinterpret_cast<int*>(base);
-  w.iters = w.state + nb;
-  char* misc = base + align_up(2 * (size_t)nb * sizeof(int), 256);
-  int* counter = reinterpret_cast<int*>(misc);
-  w.unknowns = reinterpret_cast<unsigned long long*>(misc + 8);
-  w.stat_i = reinterpret_cast<int*>(misc + 16);
-  RWB_CUDA(cudaMemsetAsync(misc, 0, 256, st));
-  ResidentArgs a;
-  a.g = g;
-  a.list = list;
-  a.nb = nb;
-  a.I = intensity;
-  a.S = seeds;
-  a.bound = bound;
-  a.prob = prob;
-  a.labels = labels;
-  a.beta = params->beta;
-  a.wmin = params->min_weight;
-  a.tol2 = params->tol * params->tol;
-  a.max_iter = params->max_iter;
-  a.state = w.state;
-  a.iters = w.iters;
-  a.counter = counter;
-  a.unknowns = w.unknowns;
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  RWB_CUDA(cudaEventCreate(&ev0));
-  RWB_CUDA(cudaEventCreate(&ev1));
-  RWB_CUDA(cudaEventRecord(ev0, st));
-  int rc = launch_resident3d(a, st);
-  if (rc) {
-    cudaEventDestroy(ev0);
-    cudaEventDestroy(ev1);
-    return rc;
-  }
-  RWB_CUDA(cudaEventRecord(ev1, st));
-  stats_kernel<<<1, 1024, 0, st>>>(w, nb);
-  RWB_LAUNCH_CHECK("stats_kernel");
-  count_launches(1);
-  if (stats) {
-    int hs[8];
-    unsigned long long unk = 0;
-    RWB_CUDA(cudaMemcpyAsync(hs, w.stat_i, sizeof(hs), cudaMemcpyDeviceToHost, st));
-    RWB_CUDA(cudaMemcpyAsync(&unk, w.unknowns, sizeof(unk), cudaMemcpyDeviceToHost, st));
-    RWB_CUDA(cudaStreamSynchronize(st));
-    float ms = 0.f;
-    RWB_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
-    stats->bricks = nb;
-    stats->converged = hs[0];
-    stats->not_converged = hs[1];
-    stats->zero_rhs = hs[2];
-    stats->iterations_max = hs[3];
-    unsigned long long s64;
-    std::memcpy(&s64, hs + 4, sizeof(s64));
-    stats->iterations_sum = (int64_t)s64;
-    stats->unknowns = (int64_t)unk;
-    stats->sweeps = hs[3];
-    stats->cg_ms = ms;
-    stats->path = RWB_PATH_RESIDENT;
-  }
-  cudaEventDestroy(ev0);
-  cudaEventDestroy(ev1);
-  return RWB_OK;
 }
 
 extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensity, const uint8_t* seeds,
@@ -869,18 +821,6 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
   if (!(params->tol >= 0.f) || !(params->beta >= 0.f) || !(params->min_weight >= 0.f) || params->max_iter < 0)
     return fail(RWB_ERR_INVALID, "invalid solve parameters");
   if (nbl * (long long)g.tiles >= (1ll << 31)) return fail(RWB_ERR_INVALID, "too many bricks for one launch");
-  if (use_resident(g, total, params->flags)) {
-    // bricks are solved at different times by the persistent clusters: a brick's
-    // epilogue must not overwrite the bound a neighbour's setup still reads
-    if (bound && (const void*)prob == (const void*)bound)
-      return fail(RWB_ERR_INVALID, "prob must not alias bound on the brick-resident path");
-    if (workspace_bytes < resident_bytes(nbl))
-      return fail(RWB_ERR_WORKSPACE, "workspace too small: need " + std::to_string(resident_bytes(nbl)) + " bytes");
-    if (stats) std::memset(stats, 0, sizeof(*stats));
-    if (nbl == 0) return RWB_OK;
-    return solve_resident(g, intensity, seeds, bound, brick_list, (int)nbl, params, prob, labels, workspace, stats,
-                          (cudaStream_t)stream);
-  }
   const Layout L = layout(g, nbl);
   if (workspace_bytes < L.total)
     return fail(RWB_ERR_WORKSPACE, "workspace too small: need " + std::to_string(L.total) + " bytes");
@@ -908,6 +848,45 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
   advance_kernel<<<1, 1024, 0, st>>>(w, nb, 0);
   RWB_LAUNCH_CHECK("setup kernels");
   count_launches(3);
+
+  if (use_resident(g, total, params->flags)) {
+    // every CG iteration of a brick on chip: one 8-CTA cluster per 32^3 brick
+    ResidentArgs ra;
+    ra.wx = w.wx;
+    ra.wy = w.wy;
+    ra.wz = w.wz;
+    ra.r0 = w.r;
+    ra.y = w.y;
+    ra.bb = w.bb;
+    ra.alist = w.alist;
+    ra.n_active = w.n_active;
+    ra.state = w.state;
+    ra.iters = w.iters;
+    ra.tol2 = tol2;
+    ra.max_iter = max_iter;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    RWB_CUDA(cudaEventCreate(&ev0));
+    RWB_CUDA(cudaEventCreate(&ev1));
+    RWB_CUDA(cudaEventRecord(ev0, st));
+    rc = launch_resident3d(ra, nb, st);
+    if (rc) {
+      cudaEventDestroy(ev0);
+      cudaEventDestroy(ev1);
+      return rc;
+    }
+    RWB_CUDA(cudaEventRecord(ev1, st));
+    epilogue_kernel<<<sgrid, block, 0, st>>>(g, w, list, seeds, bound, prob, labels);
+    stats_kernel<<<1, 1024, 0, st>>>(w, nb);
+    RWB_LAUNCH_CHECK("resident solve epilogue");
+    count_launches(2);
+    if (stats) {
+      rc = read_stats(w, nb, st, ev0, ev1, 0, RWB_PATH_RESIDENT, stats);
+      if (rc) return rc;
+    }
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    return RWB_OK;
+  }
 
   if (total == 1 && !(params->flags & RWB_SOLVE_NO_COOP)) {
     // whole-level solve: all iterations in one cooperative launch

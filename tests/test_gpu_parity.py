@@ -288,11 +288,15 @@ def test_resident_hierarchy_vs_golden_c2_like():
     assert_rw_parity(host(res.prob), ref.prob[0], host(res.labels))
 
 
-def test_resident_rejects_aliased_output(rng):
-    vol, seeds = _random_case(rng, (64, 32, 32))
+def test_resident_in_place_output(rng):
+    # the resident engine never touches `bound`; setup reads it, the epilogue writes prob
+    vol, seeds = _random_case(rng, (64, 32, 64))
     bound = cuda(rng.random(vol.shape).astype(np.float32))
-    with pytest.raises(ValueError):
-        device.solve_level(cuda(vol), cuda(seeds), (32, 32, 32), bound, GPU_CFG, out=bound)
+    ref, _ = device.solve_level(cuda(vol), cuda(seeds), (32, 32, 32), bound, GPU_CFG)
+    ref = host(ref)
+    out, st = device.solve_level(cuda(vol), cuda(seeds), (32, 32, 32), bound, GPU_CFG, out=bound)
+    assert st["path"] == 1
+    np.testing.assert_array_equal(host(out), ref)
 
 
 def test_cooperative_whole_level_matches_graph_path():

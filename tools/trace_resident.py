@@ -29,8 +29,10 @@ bbuf = (ctypes.c_longlong * (8 * 16 * 10))()
 lib.rwb_btrace_dump.argtypes = [ctypes.c_void_p]
 lib.rwb_btrace_dump(bbuf)
 b = np.frombuffer(bbuf, dtype=np.int64).reshape(8, 16, 10)
-bn = ["fetch", "setup1", "sc_sync", "setup2", "(unused)", "iterations", "epilogue", "end_sync"]
+bn = ["staging_wait", "registers", "iterations", "(0)", "(0)", "(0)", "writeback", "(0)"]
 for rank in (0, 7):
-    d = np.diff(b[rank, 1:12, :9], axis=1)
-    print("rank", rank, "median cycles per brick phase", dict(zip(bn, np.median(d, axis=0).astype(int))),
+    cols = [0, 1, 2, 6, 7]
+    d = np.diff(b[rank, 1:12][:, cols], axis=1)
+    bn2 = ["staging_wait", "registers", "iterations", "writeback"]
+    print("rank", rank, "median cycles per brick phase", dict(zip(bn2, np.median(d, axis=0).astype(int))),
           "brick", int(np.median(b[rank, 2:12, 0] - b[rank, 1:11, 0])))
