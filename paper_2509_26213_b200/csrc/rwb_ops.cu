@@ -40,11 +40,24 @@ int shape_from(int32_t ndim, const int64_t* size, Shape3* out) {
     s[3 - ndim + i] = size[i];
   }
   if (s[0] * s[1] * s[2] > (1ll << 40)) return fail(RWB_ERR_INVALID, "level too large");
+  if (s[0] > 65535 || s[1] > 65535 * 8) return fail(RWB_ERR_INVALID, "dimension too large for the 3-D launch grid");
   out->nz = (int)s[0];
   out->ny = (int)s[1];
   out->nx = (int)s[2];
   return RWB_OK;
 }
+
+// 3-D launch geometry for per-voxel kernels: block 32 (x) x 8 (y), grid over
+// (x tiles, y tiles, z) — no 64-bit index division in the kernels.
+constexpr int BX = 32, BY = 8;
+static inline dim3 grid3(const Shape3& s) { return dim3((s.nx + BX - 1) / BX, (s.ny + BY - 1) / BY, s.nz); }
+static const dim3 kBlock3(BX, BY, 1);
+
+#define VOXEL3(S, X, Y, Z)                    \
+  const int X = blockIdx.x * BX + threadIdx.x; \
+  const int Y = blockIdx.y * BY + threadIdx.y; \
+  const int Z = blockIdx.z;                    \
+  if (X >= (S).nx || Y >= (S).ny) return
 
 // ---------------------------------------------------------------------------
 // LOD step: f32(mean2(f32(conv3_clamp(x)))) with the reference's float64
@@ -66,12 +79,8 @@ __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? l
 template <bool HAS_Z, bool HAS_Y>
 __global__ void __launch_bounds__(256) lod_down_kernel(const float* __restrict__ src, Shape3 fs,
                                                        float* __restrict__ dst, Shape3 cs) {
-  long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= cs.count()) return;
-  int jx = (int)(o % cs.nx);
-  long long t = o / cs.nx;
-  int jy = (int)(t % cs.ny);
-  int jz = (int)(t / cs.ny);
+  VOXEL3(cs, jx, jy, jz);
+  const long long o = ((long long)jz * cs.ny + jy) * cs.nx + jx;
   // fine index windows 2j-1 .. 2j+2, clamped
   int zi[4], yi[4], xi[4];
 #pragma unroll
@@ -135,12 +144,8 @@ __global__ void __launch_bounds__(256) lod_down_kernel(const float* __restrict__
 
 __global__ void __launch_bounds__(256) project_seeds_kernel(const uint8_t* __restrict__ fine, Shape3 fs,
                                                             uint8_t* __restrict__ coarse, Shape3 cs) {
-  long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= cs.count()) return;
-  int jx = (int)(o % cs.nx);
-  long long t = o / cs.nx;
-  int jy = (int)(t % cs.ny);
-  int jz = (int)(t / cs.ny);
+  VOXEL3(cs, jx, jy, jz);
+  const long long o = ((long long)jz * cs.ny + jy) * cs.nx + jx;
   bool fg = false, bg = false;
   for (int z = 2 * jz; z < min(2 * jz + 2, fs.nz); ++z)
     for (int y = 2 * jy; y < min(2 * jy + 2, fs.ny); ++y)
@@ -179,12 +184,8 @@ __device__ __forceinline__ Taps up_taps(int g, int m) {
 
 __global__ void __launch_bounds__(256) upsample_kernel(const float* __restrict__ parent, Shape3 ps,
                                                        float* __restrict__ fine, Shape3 fs) {
-  long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= fs.count()) return;
-  int gx = (int)(o % fs.nx);
-  long long t = o / fs.nx;
-  int gy = (int)(t % fs.ny);
-  int gz = (int)(t / fs.ny);
+  VOXEL3(fs, gx, gy, gz);
+  const long long o = ((long long)gz * fs.ny + gy) * fs.nx + gx;
   Taps tz = fs.nz > 1 ? up_taps(gz, ps.nz) : Taps{0, 0, 1.0f, 0.0f};
   Taps ty = fs.ny > 1 ? up_taps(gy, ps.ny) : Taps{0, 0, 1.0f, 0.0f};
   Taps tx = up_taps(gx, ps.nx);
@@ -211,12 +212,8 @@ __device__ __forceinline__ Taps up_taps_win(int g, int m, int po) {
 __global__ void __launch_bounds__(256) upsample_window_kernel(const float* __restrict__ parent, Shape3 ps, Shape3 po,
                                                               Shape3 pw, float* __restrict__ fine, Shape3 fo,
                                                               Shape3 fw, Shape3 fsz) {
-  long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= fw.count()) return;
-  int lx = (int)(o % fw.nx);
-  long long t = o / fw.nx;
-  int ly = (int)(t % fw.ny);
-  int lz = (int)(t / fw.ny);
+  VOXEL3(fw, lx, ly, lz);
+  const long long o = ((long long)lz * fw.ny + ly) * fw.nx + lx;
   Taps tz = fsz.nz > 1 ? up_taps_win(fo.nz + lz, ps.nz, po.nz) : Taps{0, 0, 1.0f, 0.0f};
   Taps ty = fsz.ny > 1 ? up_taps_win(fo.ny + ly, ps.ny, po.ny) : Taps{0, 0, 1.0f, 0.0f};
   Taps tx = up_taps_win(fo.nx + lx, ps.nx, po.nx);
@@ -235,12 +232,8 @@ __global__ void __launch_bounds__(256) upsample_window_kernel(const float* __res
 
 __global__ void __launch_bounds__(256) edge_weights_kernel(const float* __restrict__ vol, Shape3 s, int ndim,
                                                            float beta, float wmin, float* __restrict__ w) {
-  long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= s.count()) return;
-  int x = (int)(o % s.nx);
-  long long t = o / s.nx;
-  int y = (int)(t % s.ny);
-  int z = (int)(t / s.ny);
+  VOXEL3(s, x, y, z);
+  const long long o = ((long long)z * s.ny + y) * s.nx + x;
   float c = vol[o];
   const long long sxy = (long long)s.ny * s.nx;
   float* out = w + o * ndim;
@@ -295,13 +288,12 @@ extern "C" int rwb_lod_down_f32(int32_t ndim, const int64_t* size, const float* 
   if (ndim == 1) cs.ny = fs.ny, cs.nz = fs.nz;
   if (ndim == 2) cs.nz = fs.nz;
   cudaStream_t st = (cudaStream_t)stream;
-  unsigned grid = ceil_div_u(cs.count(), 256);
   if (ndim == 3)
-    lod_down_kernel<true, true><<<grid, 256, 0, st>>>(src, fs, dst, cs);
+    lod_down_kernel<true, true><<<grid3(cs), kBlock3, 0, st>>>(src, fs, dst, cs);
   else if (ndim == 2)
-    lod_down_kernel<false, true><<<grid, 256, 0, st>>>(src, fs, dst, cs);
+    lod_down_kernel<false, true><<<grid3(cs), kBlock3, 0, st>>>(src, fs, dst, cs);
   else
-    lod_down_kernel<false, false><<<grid, 256, 0, st>>>(src, fs, dst, cs);
+    lod_down_kernel<false, false><<<grid3(cs), kBlock3, 0, st>>>(src, fs, dst, cs);
   RWB_LAUNCH_CHECK("lod_down_kernel");
   count_launches(1);
   return RWB_OK;
@@ -316,7 +308,7 @@ extern "C" int rwb_project_seeds_u8(int32_t ndim, const int64_t* size, const uin
   coarse_of(fs, &cs);
   if (ndim < 3) cs.nz = fs.nz;
   if (ndim < 2) cs.ny = fs.ny;
-  project_seeds_kernel<<<ceil_div_u(cs.count(), 256), 256, 0, (cudaStream_t)stream>>>(fine, fs, coarse, cs);
+  project_seeds_kernel<<<grid3(cs), kBlock3, 0, (cudaStream_t)stream>>>(fine, fs, coarse, cs);
   RWB_LAUNCH_CHECK("project_seeds_kernel");
   count_launches(1);
   return RWB_OK;
@@ -335,7 +327,7 @@ extern "C" int rwb_upsample_f32(int32_t ndim, const int64_t* parent_size, const 
   if (ndim < 2) chk.ny = fs.ny;
   if (chk.nz != ps.nz || chk.ny != ps.ny || chk.nx != ps.nx)
     return fail(RWB_ERR_INVALID, "fine size is not a 2x refinement of the parent size");
-  upsample_kernel<<<ceil_div_u(fs.count(), 256), 256, 0, (cudaStream_t)stream>>>(parent, ps, fine, fs);
+  upsample_kernel<<<grid3(fs), kBlock3, 0, (cudaStream_t)stream>>>(parent, ps, fine, fs);
   RWB_LAUNCH_CHECK("upsample_kernel");
   count_launches(1);
   return RWB_OK;
@@ -382,7 +374,7 @@ extern "C" int rwb_upsample_window_f32(int32_t ndim, const int64_t* parent_size,
     if (fd[d] == 1) lo = hi = 0;
     if (lo < pod[d] || hi >= pod[d] + pwd[d]) return fail(RWB_ERR_INVALID, "parent window does not cover the taps");
   }
-  upsample_window_kernel<<<ceil_div_u(fw.count(), 256), 256, 0, (cudaStream_t)stream>>>(parent, ps, po, pw, fine, fo,
+  upsample_window_kernel<<<grid3(fw), kBlock3, 0, (cudaStream_t)stream>>>(parent, ps, po, pw, fine, fo,
                                                                                           fw, fs);
   RWB_LAUNCH_CHECK("upsample_window_kernel");
   count_launches(1);
@@ -396,7 +388,7 @@ extern "C" int rwb_edge_weights_f32(int32_t ndim, const int64_t* size, const flo
   if (rc) return rc;
   if (!volume || !weights) return fail(RWB_ERR_INVALID, "null pointer");
   if (!(beta >= 0.0f) || !(min_weight >= 0.0f)) return fail(RWB_ERR_INVALID, "beta and min_weight must be >= 0");
-  edge_weights_kernel<<<ceil_div_u(s.count(), 256), 256, 0, (cudaStream_t)stream>>>(volume, s, ndim, beta,
+  edge_weights_kernel<<<grid3(s), kBlock3, 0, (cudaStream_t)stream>>>(volume, s, ndim, beta,
                                                                                      min_weight, weights);
   RWB_LAUNCH_CHECK("edge_weights_kernel");
   count_launches(1);

@@ -73,6 +73,7 @@ struct TileCtx {
   bool col;             // column inside the brick box
 };
 
+template <int TZv = TZ>
 __device__ __forceinline__ TileCtx tile_ctx(const Geo& g, const int* __restrict__ list, int slot, int tile) {
   TileCtx c;
   c.slot = slot;
@@ -91,8 +92,8 @@ __device__ __forceinline__ TileCtx tile_ctx(const Geo& g, const int* __restrict_
   int ttz = tt / g.ty;
   c.lx = ttx * TX + threadIdx.x;
   c.ly = tty * TY + threadIdx.y;
-  c.lz0 = ttz * TZ;
-  c.lz1 = min(c.lz0 + TZ, g.bz);
+  c.lz0 = ttz * TZv;
+  c.lz1 = min(c.lz0 + TZv, g.bz);
   c.col = c.lx < g.bx && c.ly < g.by;
   return c;
 }
@@ -101,6 +102,17 @@ __device__ __forceinline__ TileCtx tile_ctx(const Geo& g, const int* __restrict_
 __device__ __forceinline__ TileCtx tile_ctx(const Geo& g, const int* __restrict__ list) {
   int slot = blockIdx.x / g.tiles;
   return tile_ctx(g, list, slot, blockIdx.x - slot * g.tiles);
+}
+
+// setup kernels: one voxel per thread (tiles of a single z plane) for more
+// independent loads in flight; `setup_tiles(g)` tiles per brick
+constexpr int STZ = 4;  // z extent marched per setup thread
+__device__ __host__ __forceinline__ int setup_tiles(const Geo& g) { return ((g.bz + STZ - 1) / STZ) * g.ty * g.tx; }
+
+__device__ __forceinline__ TileCtx setup_ctx(const Geo& g, const int* __restrict__ list) {
+  const int st = setup_tiles(g);
+  int slot = blockIdx.x / st;
+  return tile_ctx<STZ>(g, list, slot, blockIdx.x - slot * st);
 }
 
 // block-wide sum of two floats -> thread 0
@@ -131,12 +143,13 @@ __device__ __forceinline__ float2 block_sum2(float a, float b) {
 // holds the brick totals in *sum0 / *sum1.  Ends with a CTA barrier so the
 // shared scratch can be reused by the next work item.
 __device__ __forceinline__ bool brick_reduce(const Geo& g, const Work& w, int slot, int tile, float a, float b,
-                                             double* sum0, double* sum1) {
+                                             double* sum0, double* sum1, int ntiles = -1) {
+  const int tiles = ntiles > 0 ? ntiles : g.tiles;
   __shared__ bool last;
   float2 s = block_sum2(a, b);
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   bool mine = false;
-  if (g.tiles == 1) {
+  if (tiles == 1) {
     if (tid == 0) {
       *sum0 = (double)s.x;
       *sum1 = (double)s.y;
@@ -146,17 +159,17 @@ __device__ __forceinline__ bool brick_reduce(const Geo& g, const Work& w, int sl
     return mine;
   }
   if (tid == 0) {
-    w.part[(long long)slot * g.tiles + tile] = s;
+    w.part[(long long)slot * tiles + tile] = s;
     __threadfence();
     unsigned t = atomicAdd(&w.ticket[slot], 1u);
-    last = (t == (unsigned)g.tiles - 1);
+    last = (t == (unsigned)tiles - 1);
   }
   __syncthreads();
   if (last && tid < 32) {
     __threadfence();
     double sa = 0.0, sb = 0.0;
-    const float2* p = w.part + (long long)slot * g.tiles;
-    for (int i = tid; i < g.tiles; i += 32) {
+    const float2* p = w.part + (long long)slot * tiles;
+    for (int i = tid; i < tiles; i += 32) {
       float2 v = __ldcg(p + i);
       sa += (double)v.x;
       sb += (double)v.y;
@@ -180,110 +193,147 @@ __device__ __forceinline__ bool brick_reduce(const Geo& g, const Work& w, int sl
 // ---------------------------------------------------------------------------
 // setup
 
-// Sum of the weights of all edges of voxel (z,y,x) inside the level, fixed
-// order -z,+z,-y,+y,-x,+x (K1 and K2 must produce bit-identical diagonals).
-__device__ __forceinline__ float level_diag(const Geo& g, const float* __restrict__ I, long long gi, int z, int y,
-                                            int x, float c, float beta, float wmin) {
-  float d = 0.f;
-  if (g.is3d) {
-    if (z > 0) d += edge_weight(c, __ldg(I + gi - g.sxy), beta, wmin);
-    if (z + 1 < g.nz) d += edge_weight(c, __ldg(I + gi + g.sxy), beta, wmin);
+// Neighbour addressing of one voxel for the setup kernels: the six neighbours in
+// the order -z,+z,-y,+y,-x,+x, whether each is in the level and in the brick,
+// and clamped (always valid) level / brick-local indices, so every neighbour
+// load can be issued unconditionally and in parallel.
+struct Nbrs {
+  long long g[6];   // level index (clamped to the voxel itself when outside)
+  long long l[6];   // brick-local index (clamped likewise)
+  bool lev[6];      // neighbour inside the level
+  bool brk[6];      // ... and inside this brick
+};
+
+__device__ __forceinline__ Nbrs neighbours(const Geo& g, long long gi, long long li, int gz, int gy, int gx, int lz,
+                                           int ly, int lx) {
+  Nbrs n;
+  const long long sbz = (long long)g.by * g.bx;
+  const long long dg[6] = {-g.sxy, g.sxy, -(long long)g.nx, (long long)g.nx, -1, 1};
+  const long long dl[6] = {-sbz, sbz, -(long long)g.bx, (long long)g.bx, -1, 1};
+  const bool lev[6] = {g.is3d && gz > 0, g.is3d && gz + 1 < g.nz, gy > 0, gy + 1 < g.ny, gx > 0, gx + 1 < g.nx};
+  const bool brk[6] = {lz > 0, lz + 1 < g.bz, ly > 0, ly + 1 < g.by, lx > 0, lx + 1 < g.bx};
+#pragma unroll
+  for (int e = 0; e < 6; ++e) {
+    n.lev[e] = lev[e];
+    n.brk[e] = lev[e] && brk[e];
+    n.g[e] = lev[e] ? gi + dg[e] : gi;
+    n.l[e] = n.brk[e] ? li + dl[e] : li;
   }
-  if (y > 0) d += edge_weight(c, __ldg(I + gi - g.nx), beta, wmin);
-  if (y + 1 < g.ny) d += edge_weight(c, __ldg(I + gi + g.nx), beta, wmin);
-  if (x > 0) d += edge_weight(c, __ldg(I + gi - 1), beta, wmin);
-  if (x + 1 < g.nx) d += edge_weight(c, __ldg(I + gi + 1), beta, wmin);
-  return d;
+  return n;
 }
 
 // K1: scale s = diag^-1/2 for unknowns, 0 for seeds / padding / isolated voxels.
+// The diagonal sums the six edge weights in the order -z,+z,-y,+y,-x,+x
+// (the brick-resident engine and the oracle use the same order).
 __global__ void __launch_bounds__(NTHREADS) setup_scale_kernel(Geo g, Work w, const int* __restrict__ list,
                                                                const float* __restrict__ I,
                                                                const uint8_t* __restrict__ S, float beta,
                                                                float wmin) {
-  TileCtx c = tile_ctx(g, list);
+  TileCtx c = setup_ctx(g, list);
   if (!c.col) return;
   const int gy = c.gy0 + c.ly, gx = c.gx0 + c.lx;
   const bool colin = gy >= 0 && gy < g.ny && gx >= 0 && gx < g.nx;
-  long long lbase = (long long)c.slot * g.bvol + (long long)c.ly * g.bx + c.lx;
-  for (int lz = c.lz0; lz < c.lz1; ++lz) {
-    long long li = lbase + (long long)lz * g.by * g.bx;
+  const long long sbz = (long long)g.by * g.bx;
+  float* __restrict__ sc = w.sc;
+  const long long lbase = (long long)c.slot * g.bvol + (long long)c.ly * g.bx + c.lx;
+#pragma unroll
+  for (int k = 0; k < STZ; ++k) {
+    const int lz = c.lz0 + k;
+    if (lz >= c.lz1) break;
+    const long long li = lbase + (long long)lz * sbz;
     const int gz = c.gz0 + lz;
     float s = 0.f;
     if (colin && gz >= 0 && gz < g.nz) {
-      long long gi = (long long)gz * g.sxy + (long long)gy * g.nx + gx;
-      if (S[gi] == 0) {
-        float d = level_diag(g, I, gi, gz, gy, gx, __ldg(I + gi), beta, wmin);
+      const long long gi = (long long)gz * g.sxy + (long long)gy * g.nx + gx;
+      const Nbrs n = neighbours(g, gi, li, gz, gy, gx, lz, c.ly, c.lx);
+      const float ci = __ldg(I + gi);
+      float In[6];
+#pragma unroll
+      for (int e = 0; e < 6; ++e) In[e] = __ldg(I + n.g[e]);
+      if (__ldg(S + gi) == 0) {
+        float d = 0.f;
+#pragma unroll
+        for (int e = 0; e < 6; ++e) d += n.lev[e] ? edge_weight(ci, In[e], beta, wmin) : 0.f;
         s = d > 0.f ? 1.0f / sqrtf(d) : 0.f;
       }
     }
-    w.sc[li] = s;
+    sc[li] = s;
   }
 }
 
 __device__ __forceinline__ float seed_value(uint8_t s) { return s == 1 ? 1.0f : 0.0f; }
 
-// K2: scaled forward weights, r0 = S(b - L x0), y0 = x0 / s, p = 0; per-brick
-// ||S b||^2 and ||r0||^2.
+// K2: scaled forward weights, r0 = S(b - L x0), y0 = x0 / s, (p = 0); per-brick
+// ||S b||^2 and ||r0||^2 and the brick's initial decision.
 __global__ void __launch_bounds__(NTHREADS) setup_system_kernel(Geo g, Work w, const int* __restrict__ list,
                                                                 const float* __restrict__ I,
                                                                 const uint8_t* __restrict__ S,
                                                                 const float* __restrict__ bound, float beta,
-                                                                float wmin, float tol2, int max_iter) {
-  TileCtx c = tile_ctx(g, list);
+                                                                float wmin, float tol2, int max_iter,
+                                                                int write_p) {
+  TileCtx c = setup_ctx(g, list);
   float acc_bb = 0.f, acc_rr = 0.f;
   unsigned n_unknown = 0;
   if (c.col) {
     const int gy = c.gy0 + c.ly, gx = c.gx0 + c.lx;
     const bool colin = gy >= 0 && gy < g.ny && gx >= 0 && gx < g.nx;
     const long long sbz = (long long)g.by * g.bx;
-    long long lbase = (long long)c.slot * g.bvol + (long long)c.ly * g.bx + c.lx;
-    for (int lz = c.lz0; lz < c.lz1; ++lz) {
-      long long li = lbase + (long long)lz * sbz;
+    const float* __restrict__ sc = w.sc;
+    float* __restrict__ wx = w.wx;
+    float* __restrict__ wy = w.wy;
+    float* __restrict__ wz = w.wz;
+    float* __restrict__ rv = w.r;
+    float* __restrict__ yv = w.y;
+    const long long lbase = (long long)c.slot * g.bvol + (long long)c.ly * g.bx + c.lx;
+#pragma unroll
+    for (int k = 0; k < STZ; ++k) {
+      const int lz = c.lz0 + k;
+      if (lz >= c.lz1) break;
+      const long long li = lbase + (long long)lz * sbz;
       const int gz = c.gz0 + lz;
-      float si = w.sc[li];
-      float wfx = 0.f, wfy = 0.f, wfz = 0.f, r = 0.f, y = 0.f;
+      const float si = sc[li];
+      float wf[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, r = 0.f, y = 0.f;
       if (si > 0.f && colin && gz >= 0 && gz < g.nz) {
         ++n_unknown;
-        long long gi = (long long)gz * g.sxy + (long long)gy * g.nx + gx;
+        const long long gi = (long long)gz * g.sxy + (long long)gy * g.nx + gx;
+        const Nbrs n = neighbours(g, gi, li, gz, gy, gx, lz, c.ly, c.lx);
         const float ci = __ldg(I + gi);
-        const float x0 = bound ? bound[gi] : 0.f;
-        float diag = 0.f, b = 0.f, acc = 0.f;
-        // neighbour visit in the same order as level_diag
-        auto visit = [&](bool inlevel, bool inbrick, long long gn, long long ln, float* fwd) {
-          if (!inlevel) return;
-          float wt = edge_weight(ci, __ldg(I + gn), beta, wmin);
-          diag += wt;
-          float sn = inbrick ? w.sc[ln] : 0.f;
-          if (sn > 0.f) {
-            acc += wt * (bound ? bound[gn] : 0.f);
-            if (fwd) *fwd = wt * si * sn;
-          } else {
-            uint8_t sv = S[gn];
-            float val = sv ? seed_value(sv) : (bound ? bound[gn] : 0.f);
-            b += wt * val;
-          }
-        };
-        if (g.is3d) {
-          visit(gz > 0, lz > 0, gi - g.sxy, li - sbz, nullptr);
-          visit(gz + 1 < g.nz, lz + 1 < g.bz, gi + g.sxy, li + sbz, &wfz);
+        const float x0 = bound ? __ldg(bound + gi) : 0.f;
+        float In[6], Bn[6], Sc[6];
+        uint8_t Sn[6];
+#pragma unroll
+        for (int e = 0; e < 6; ++e) {  // all neighbour loads issued together
+          In[e] = __ldg(I + n.g[e]);
+          Sn[e] = __ldg(S + n.g[e]);
+          Bn[e] = bound ? __ldg(bound + n.g[e]) : 0.f;
+          Sc[e] = sc[n.l[e]];
         }
-        visit(gy > 0, c.ly > 0, gi - g.nx, li - g.bx, nullptr);
-        visit(gy + 1 < g.ny, c.ly + 1 < g.by, gi + g.nx, li + g.bx, &wfy);
-        visit(gx > 0, c.lx > 0, gi - 1, li - 1, nullptr);
-        visit(gx + 1 < g.nx, c.lx + 1 < g.bx, gi + 1, li + 1, &wfx);
+        float diag = 0.f, b = 0.f, acc = 0.f;
+#pragma unroll
+        for (int e = 0; e < 6; ++e) {
+          if (!n.lev[e]) continue;
+          const float wt = edge_weight(ci, In[e], beta, wmin);
+          diag += wt;
+          const float sn = n.brk[e] ? Sc[e] : 0.f;
+          if (sn > 0.f) {  // coupled unknown of this brick
+            acc += wt * Bn[e];
+            wf[e] = wt * si * sn;
+          } else {  // Dirichlet: seed, or outside the brick
+            b += wt * (Sn[e] ? seed_value(Sn[e]) : Bn[e]);
+          }
+        }
         r = si * (b + acc - diag * x0);
         y = x0 / si;
-        float sb = si * b;
+        const float sb = si * b;
         acc_bb += sb * sb;
         acc_rr += r * r;
       }
-      w.wx[li] = wfx;
-      w.wy[li] = wfy;
-      if (g.is3d) w.wz[li] = wfz;
-      w.r[li] = r;
-      w.y[li] = y;
-      w.p0[li] = 0.f;
+      wx[li] = wf[5];
+      wy[li] = wf[3];
+      if (g.is3d) wz[li] = wf[1];
+      rv[li] = r;
+      yv[li] = y;
+      if (write_p) w.p0[li] = 0.f;  // only the streaming passes read p
     }
   }
   {
@@ -296,7 +346,7 @@ __global__ void __launch_bounds__(NTHREADS) setup_system_kernel(Geo g, Work w, c
       atomicAdd(w.unknowns, (unsigned long long)cta_unknown);
   }
   double bb, rr;
-  if (brick_reduce(g, w, c.slot, c.tile, acc_bb, acc_rr, &bb, &rr)) {
+  if (brick_reduce(g, w, c.slot, c.tile, acc_bb, acc_rr, &bb, &rr, setup_tiles(g))) {
     w.bb[c.slot] = bb;
     w.rr[c.slot] = rr;  // parity 0
     int st = ST_ACTIVE;
@@ -676,7 +726,8 @@ static Layout layout(const Geo& g, long long nb) {
   const size_t sizes[L_N] = {vox, vox, vox, vox, vox, vox, vox, g.is3d ? vox : 0, vox,
                              2 * nb * sizeof(double), nb * sizeof(double), nb * sizeof(double),
                              nb * sizeof(int), nb * sizeof(int), nb * sizeof(unsigned), nb * sizeof(int),
-                             std::max((size_t)nb * g.tiles * sizeof(float2), (size_t)2 * kCoopMaxBlocks * sizeof(float)),
+                             std::max((size_t)nb * std::max(g.tiles, setup_tiles(g)) * sizeof(float2),
+                                      (size_t)2 * kCoopMaxBlocks * sizeof(float)),
                              64};
   size_t o = 0;
   for (int i = 0; i < L_N; ++i) {
@@ -820,7 +871,8 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
   if (!bound && total > 1) return fail(RWB_ERR_INVALID, "bound may be NULL only for a single-brick level");
   if (!(params->tol >= 0.f) || !(params->beta >= 0.f) || !(params->min_weight >= 0.f) || params->max_iter < 0)
     return fail(RWB_ERR_INVALID, "invalid solve parameters");
-  if (nbl * (long long)g.tiles >= (1ll << 31)) return fail(RWB_ERR_INVALID, "too many bricks for one launch");
+  if (nbl * (long long)std::max(g.tiles, setup_tiles(g)) >= (1ll << 31))
+    return fail(RWB_ERR_INVALID, "too many bricks for one launch");
   const Layout L = layout(g, nbl);
   if (workspace_bytes < L.total)
     return fail(RWB_ERR_WORKSPACE, "workspace too small: need " + std::to_string(L.total) + " bytes");
@@ -841,15 +893,17 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
   // zero the scalar region (rr .. misc) in one memset
   RWB_CUDA(cudaMemsetAsync((char*)workspace + L.off[L_RR], 0, L.total - L.off[L_RR], st));
   const unsigned sgrid = (unsigned)((long long)nb * g.tiles);
+  const unsigned setup_grid = (unsigned)((long long)nb * setup_tiles(g));
   dim3 block(TX, TY);
-  setup_scale_kernel<<<sgrid, block, 0, st>>>(g, w, list, intensity, seeds, params->beta, params->min_weight);
-  setup_system_kernel<<<sgrid, block, 0, st>>>(g, w, list, intensity, seeds, bound, params->beta,
-                                               params->min_weight, tol2, max_iter);
+  setup_scale_kernel<<<setup_grid, block, 0, st>>>(g, w, list, intensity, seeds, params->beta, params->min_weight);
+  const bool resident = use_resident(g, total, params->flags);
+  setup_system_kernel<<<setup_grid, block, 0, st>>>(g, w, list, intensity, seeds, bound, params->beta,
+                                                    params->min_weight, tol2, max_iter, resident ? 0 : 1);
   advance_kernel<<<1, 1024, 0, st>>>(w, nb, 0);
   RWB_LAUNCH_CHECK("setup kernels");
   count_launches(3);
 
-  if (use_resident(g, total, params->flags)) {
+  if (resident) {
     // every CG iteration of a brick on chip: one 8-CTA cluster per 32^3 brick
     ResidentArgs ra;
     ra.wx = w.wx;
