@@ -160,71 +160,79 @@ __global__ void __launch_bounds__(256) project_seeds_kernel(const uint8_t* __res
 // ---------------------------------------------------------------------------
 // cell-centred multilinear prolongation (parent coordinate g/2 - 1/4, clamped)
 
-struct Taps {
-  int i0, i1;
-  float w0, w1;
-};
-
-__device__ __forceinline__ Taps up_taps(int g, int m) {
-  Taps t;
-  int j = g >> 1;
-  if (g & 1) {
-    t.i0 = j;
-    t.i1 = min(j + 1, m - 1);
-    t.w0 = 0.75f;
-    t.w1 = 0.25f;
-  } else {
-    t.i0 = max(j - 1, 0);
-    t.i1 = j;
-    t.w0 = 0.25f;
-    t.w1 = 0.75f;
+// One thread per PARENT voxel j: it reads the clamped 3x3x3 parent
+// neighbourhood once and writes the (up to) 2x2x2 fine voxels 2j, 2j+1 that
+// fall inside the fine window [fo, fo+fw) (taps 1/4, 3/4; x first, then y,
+// then z).  ~1/8 of the address arithmetic of a per-fine-voxel kernel, which
+// was instruction-bound.  The parent is addressed through a window
+// [po, po+pw) of the full parent of size ps; the fine output through the
+// window's own dense layout.  Full-level and windowed calls run this same
+// code, so every caller gets bit-identical values.
+__global__ void __launch_bounds__(256) upsample_kernel(const float* __restrict__ parent, Shape3 ps, Shape3 po,
+                                                       Shape3 pw, float* __restrict__ fine, Shape3 fs, Shape3 fo,
+                                                       Shape3 fw, Shape3 j0) {
+  const int jx = j0.nx + blockIdx.x * BX + threadIdx.x;
+  const int jy = j0.ny + blockIdx.y * BY + threadIdx.y;
+  const int jz = j0.nz + blockIdx.z;
+  if (jx >= ps.nx || jy >= ps.ny || jz >= ps.nz) return;
+  const long long psxy = (long long)pw.ny * pw.nx;
+  const int xm = max(jx - 1, 0) - po.nx, xc = jx - po.nx, xp = min(jx + 1, ps.nx - 1) - po.nx;
+  const int zz[3] = {max(jz - 1, 0) - po.nz, jz - po.nz, min(jz + 1, ps.nz - 1) - po.nz};
+  const int yy[3] = {max(jy - 1, 0) - po.ny, jy - po.ny, min(jy + 1, ps.ny - 1) - po.ny};
+  // x-interpolated parent rows: lo -> fine 2j (0.25 P[j-1] + 0.75 P[j]), hi -> 2j+1 (0.75 P[j] + 0.25 P[j+1])
+  float lo[3][3], hi[3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      const float* row = parent + zz[a] * psxy + (long long)yy[b] * pw.nx;
+      const float c = __ldg(row + xc), m = __ldg(row + xm), p = __ldg(row + xp);
+      lo[a][b] = __fmaf_rn(0.25f, m, __fmul_rn(0.75f, c));
+      hi[a][b] = __fmaf_rn(0.75f, c, __fmul_rn(0.25f, p));
+    }
+  // then y and z; a fine dimension of size 1 takes its single row unweighted
+  const bool fy2 = fs.ny > 1, fz2 = fs.nz > 1;
+#pragma unroll
+  for (int dz = 0; dz < 2; ++dz) {
+    const int gz = 2 * jz + dz;
+    if (gz >= fs.nz || gz < fo.nz || gz >= fo.nz + fw.nz) continue;
+    const int za = dz ? 1 : 0, zb = dz ? 2 : 1;
+    const float wa = fz2 ? (dz ? 0.75f : 0.25f) : 0.f, wb = fz2 ? (dz ? 0.25f : 0.75f) : 1.f;
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy) {
+      const int gy = 2 * jy + dy;
+      if (gy >= fs.ny || gy < fo.ny || gy >= fo.ny + fw.ny) continue;
+      const int ya = dy ? 1 : 0, yb = dy ? 2 : 1;
+      const float va = fy2 ? (dy ? 0.75f : 0.25f) : 0.f, vb = fy2 ? (dy ? 0.25f : 0.75f) : 1.f;
+      float f[2];
+#pragma unroll
+      for (int dx = 0; dx < 2; ++dx) {
+        const float(*xs)[3] = dx ? hi : lo;
+        const float ra = __fmaf_rn(va, xs[za][ya], __fmul_rn(vb, xs[za][yb]));
+        const float rb = __fmaf_rn(va, xs[zb][ya], __fmul_rn(vb, xs[zb][yb]));
+        f[dx] = __fmaf_rn(wa, ra, __fmul_rn(wb, rb));
+      }
+      const int gx = 2 * jx;
+      float* out = fine + ((long long)(gz - fo.nz) * fw.ny + (gy - fo.ny)) * fw.nx + (gx - fo.nx);
+      const bool in0 = gx >= fo.nx && gx < fo.nx + fw.nx;
+      const bool in1 = gx + 1 < fs.nx && gx + 1 >= fo.nx && gx + 1 < fo.nx + fw.nx;
+      if (in0 && in1 && (((uintptr_t)out) & 7) == 0) {
+        *reinterpret_cast<float2*>(out) = make_float2(f[0], f[1]);
+      } else {
+        if (in0) out[0] = f[0];
+        if (in1) out[1] = f[1];
+      }
+    }
   }
-  return t;
 }
 
-__global__ void __launch_bounds__(256) upsample_kernel(const float* __restrict__ parent, Shape3 ps,
-                                                       float* __restrict__ fine, Shape3 fs) {
-  VOXEL3(fs, gx, gy, gz);
-  const long long o = ((long long)gz * fs.ny + gy) * fs.nx + gx;
-  Taps tz = fs.nz > 1 ? up_taps(gz, ps.nz) : Taps{0, 0, 1.0f, 0.0f};
-  Taps ty = fs.ny > 1 ? up_taps(gy, ps.ny) : Taps{0, 0, 1.0f, 0.0f};
-  Taps tx = up_taps(gx, ps.nx);
-  const long long sxy = (long long)ps.ny * ps.nx;
-  auto row = [&](int z, int y) {
-    const float* p = parent + z * sxy + (long long)y * ps.nx;
-    return tx.w0 * __ldg(p + tx.i0) + tx.w1 * __ldg(p + tx.i1);
-  };
-  float r0 = ty.w0 * row(tz.i0, ty.i0) + ty.w1 * row(tz.i0, ty.i1);
-  float r1 = ty.w0 * row(tz.i1, ty.i0) + ty.w1 * row(tz.i1, ty.i1);
-  fine[o] = tz.w0 * r0 + tz.w1 * r1;
-}
-
-// Windowed variant: fine voxels [fo, fo+fw) of a level whose parent has size
-// ps; the parent is given as the window [po, po+pw).  Taps are computed from
-// global coordinates (clamped to the full parent), then read from the window.
-__device__ __forceinline__ Taps up_taps_win(int g, int m, int po) {
-  Taps t = up_taps(g, m);
-  t.i0 -= po;
-  t.i1 -= po;
-  return t;
-}
-
-__global__ void __launch_bounds__(256) upsample_window_kernel(const float* __restrict__ parent, Shape3 ps, Shape3 po,
-                                                              Shape3 pw, float* __restrict__ fine, Shape3 fo,
-                                                              Shape3 fw, Shape3 fsz) {
-  VOXEL3(fw, lx, ly, lz);
-  const long long o = ((long long)lz * fw.ny + ly) * fw.nx + lx;
-  Taps tz = fsz.nz > 1 ? up_taps_win(fo.nz + lz, ps.nz, po.nz) : Taps{0, 0, 1.0f, 0.0f};
-  Taps ty = fsz.ny > 1 ? up_taps_win(fo.ny + ly, ps.ny, po.ny) : Taps{0, 0, 1.0f, 0.0f};
-  Taps tx = up_taps_win(fo.nx + lx, ps.nx, po.nx);
-  const long long sxy = (long long)pw.ny * pw.nx;
-  auto row = [&](int z, int y) {
-    const float* p = parent + z * sxy + (long long)y * pw.nx;
-    return tx.w0 * __ldg(p + tx.i0) + tx.w1 * __ldg(p + tx.i1);
-  };
-  float r0 = ty.w0 * row(tz.i0, ty.i0) + ty.w1 * row(tz.i0, ty.i1);
-  float r1 = ty.w0 * row(tz.i1, ty.i0) + ty.w1 * row(tz.i1, ty.i1);
-  fine[o] = tz.w0 * r0 + tz.w1 * r1;
+static void launch_upsample(const float* parent, Shape3 ps, Shape3 po, Shape3 pw, float* fine, Shape3 fs, Shape3 fo,
+                            Shape3 fw, cudaStream_t st) {
+  // parent voxels whose fine children intersect the window
+  Shape3 j0{fo.nz >> 1, fo.ny >> 1, fo.nx >> 1};
+  Shape3 j1{(fo.nz + fw.nz + 1) >> 1, (fo.ny + fw.ny + 1) >> 1, (fo.nx + fw.nx + 1) >> 1};
+  dim3 grid((j1.nx - j0.nx + BX - 1) / BX, (j1.ny - j0.ny + BY - 1) / BY, j1.nz - j0.nz);
+  upsample_kernel<<<grid, kBlock3, 0, st>>>(parent, ps, po, pw, fine, fs, fo, fw, j0);
 }
 
 // ---------------------------------------------------------------------------
@@ -327,7 +335,7 @@ extern "C" int rwb_upsample_f32(int32_t ndim, const int64_t* parent_size, const 
   if (ndim < 2) chk.ny = fs.ny;
   if (chk.nz != ps.nz || chk.ny != ps.ny || chk.nx != ps.nx)
     return fail(RWB_ERR_INVALID, "fine size is not a 2x refinement of the parent size");
-  upsample_kernel<<<grid3(fs), kBlock3, 0, (cudaStream_t)stream>>>(parent, ps, fine, fs);
+  launch_upsample(parent, ps, Shape3{0, 0, 0}, ps, fine, fs, Shape3{0, 0, 0}, fs, (cudaStream_t)stream);
   RWB_LAUNCH_CHECK("upsample_kernel");
   count_launches(1);
   return RWB_OK;
@@ -374,9 +382,8 @@ extern "C" int rwb_upsample_window_f32(int32_t ndim, const int64_t* parent_size,
     if (fd[d] == 1) lo = hi = 0;
     if (lo < pod[d] || hi >= pod[d] + pwd[d]) return fail(RWB_ERR_INVALID, "parent window does not cover the taps");
   }
-  upsample_window_kernel<<<grid3(fw), kBlock3, 0, (cudaStream_t)stream>>>(parent, ps, po, pw, fine, fo,
-                                                                                          fw, fs);
-  RWB_LAUNCH_CHECK("upsample_window_kernel");
+  launch_upsample(parent, ps, po, pw, fine, fs, fo, fw, (cudaStream_t)stream);
+  RWB_LAUNCH_CHECK("upsample_kernel (window)");
   count_launches(1);
   return RWB_OK;
 }

@@ -310,3 +310,15 @@ def test_cooperative_whole_level_matches_graph_path():
     assert_rw_parity(host(a), ref)
     assert_rw_parity(host(b), ref)
     assert abs(sa["iterations_max"] - sb["iterations_max"]) <= 2
+
+
+def test_upsample_window_slabs_match_full(rng):
+    for fine in [(33, 20, 18), (40, 16)]:
+        parent = cuda(rng.random(device.coarse_shape(fine), dtype=np.float32))
+        full = host(device.upsample(parent, fine))
+        for z0, z1 in [(0, 5), (7, 8), (13, fine[0]), (0, fine[0])]:
+            out = torch.full(fine, float("nan"), device="cuda")
+            device.upsample_window(parent, fine, z0, z1, out)
+            got = host(out)
+            np.testing.assert_array_equal(got[z0:z1], full[z0:z1])
+            assert np.isnan(got[:z0]).all() and np.isnan(got[z1:]).all()
