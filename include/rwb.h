@@ -70,6 +70,7 @@ typedef struct {
 #define RWB_SOLVE_NO_GRAPH 1  /* streaming solver: launch iterations directly, not via a CUDA graph */
 #define RWB_SOLVE_STREAMING 2 /* force the streaming solver even where the brick-resident one applies */
 #define RWB_SOLVE_NO_COOP 4   /* whole-level solves: graph-launched passes instead of one cooperative kernel */
+#define RWB_SOLVE_CLUSTER16 8 /* brick-resident solver: 16-CTA clusters, 2 CTAs/SM (default 8-CTA, 1 CTA/SM) */
 
 /* Solver paths (rwb_solve_stats_t.path) */
 #define RWB_PATH_STREAMING 0 /* brick-batched CG, state in HBM, 2 launches per iteration */

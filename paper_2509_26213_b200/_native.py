@@ -22,6 +22,7 @@ ABI_VERSION = 1
 SOLVE_NO_GRAPH = 1
 SOLVE_STREAMING = 2
 SOLVE_NO_COOP = 4
+SOLVE_CLUSTER16 = 8
 PATH_STREAMING, PATH_RESIDENT, PATH_COOPERATIVE = 0, 1, 2
 
 # every symbol include/rwb.h declares, with (restype, argtypes)

@@ -50,18 +50,28 @@ namespace cg = cooperative_groups;
 namespace rwb {
 
 constexpr int RB = 32;           // brick edge
-constexpr int RCL = 8;           // CTAs per cluster (per brick)
-constexpr int RPZ = RB / RCL;    // z planes per CTA
 constexpr int RQ = 4;            // x voxels per thread
 constexpr int RQN = RB / RQ;     // quads per row
 constexpr int RT = RQN * RB;     // threads per CTA (256)
 constexpr int RW = RT / 32;      // warps per CTA
-constexpr int RV = RQ * RPZ;     // voxels per thread (16)
-constexpr int NPART = RCL * RW;  // pushed partials per reduction (64)
 constexpr int PLANE = RB * RB;   // floats per plane
-constexpr int SLAB = RPZ * PLANE;
 
-static_assert(RPZ == 4 && RQ == 4, "register blocking assumes 4x4 voxels per thread");
+// Two decompositions of a 32^3 brick:
+//   RPZ = 4: 8-CTA clusters, 4 z-planes (16 voxels) per thread, 1 CTA per SM,
+//            double-buffered staging (the next brick prefetched while iterating);
+//   RPZ = 2: 16-CTA clusters (non-portable size), 2 z-planes (8 voxels) per
+//            thread, half the registers, so two CTAs of DIFFERENT bricks share
+//            an SM and each hides the other's reduction latency.
+template <int RPZ_>
+struct RCfg {
+  static constexpr int RPZ = RPZ_;               // z planes per CTA
+  static constexpr int RCL = RB / RPZ;           // CTAs per cluster (per brick)
+  static constexpr int RV = RQ * RPZ;            // voxels per thread
+  static constexpr int NPART = RCL * RW;         // pushed partials per reduction
+  static constexpr int SLAB = RPZ * PLANE;
+  static constexpr int NBUF = RPZ == 4 ? 2 : 1;  // staging buffers
+  static constexpr int MINB = RPZ == 4 ? 1 : 2;  // CTAs per SM
+};
 
 }  // namespace rwb
 
@@ -69,13 +79,13 @@ static_assert(RPZ == 4 && RQ == 4, "register blocking assumes 4x4 voxels per thr
 // phase timestamps of cluster 0 (diagnostics build only)
 __device__ long long g_rwb_trace[8][64][8];
 __device__ long long g_rwb_btrace[8][16][10];
-#define TRACE(k)                                                                                   \
-  do {                                                                                             \
-    if (tid == 0 && blockIdx.x < RCL && trace_it < 64) g_rwb_trace[rank][trace_it][k] = clock64(); \
+#define TRACE(k)                                                                                      \
+  do {                                                                                                \
+    if (tid == 0 && blockIdx.x < 8 && rank < 8 && trace_it < 64) g_rwb_trace[rank][trace_it][k] = clock64(); \
   } while (0)
-#define BTRACE(k)                                                                                   \
-  do {                                                                                              \
-    if (tid == 0 && blockIdx.x < RCL && btrace_n < 16) g_rwb_btrace[rank][btrace_n][k] = clock64(); \
+#define BTRACE(k)                                                                                      \
+  do {                                                                                                 \
+    if (tid == 0 && blockIdx.x < 8 && rank < 8 && btrace_n < 16) g_rwb_btrace[rank][btrace_n][k] = clock64(); \
   } while (0)
 #else
 #define TRACE(k) \
@@ -88,15 +98,17 @@ __device__ long long g_rwb_btrace[8][16][10];
 
 namespace rwb {
 
+template <int RPZ>
 struct ResidentSmem {
-  float sx[2][SLAB];                     // staged scaled weights, double buffer (current / next brick)
-  float sy[2][SLAB];
-  float sz[2][PLANE + SLAB];             // z weights incl. the plane below the slab
-  float sr[2][SLAB];                     // staged r0
-  float sv[2][SLAB];                     // staged y0
-  float4 rp[RPZ][RB][RQN];               // r planes of this slab (y neighbours of the SpMV)
-  float4 rface[2][2][RB][RQN];           // received r faces [parity][0 = from below, 1 = from above]
-  __align__(16) float red[2][2][NPART];  // pushed partials [parity][gamma, delta][rank*RW + warp]
+  using C = RCfg<RPZ>;
+  float sx[C::NBUF][C::SLAB];              // staged scaled weights (double buffer: current / next brick)
+  float sy[C::NBUF][C::SLAB];
+  float sz[C::NBUF][PLANE + C::SLAB];      // z weights incl. the plane below the slab
+  float sr[C::NBUF][C::SLAB];              // staged r0
+  float sv[C::NBUF][C::SLAB];              // staged y0
+  float4 rp[RPZ][RB][RQN];                 // r planes of this slab (y neighbours of the SpMV)
+  float4 rface[2][2][RB][RQN];             // received r faces [parity][0 = from below, 1 = from above]
+  __align__(16) float red[2][2][C::NPART];  // pushed partials [parity][gamma, delta][rank*RW + warp]
   unsigned long long barF[2];            // mbarriers: r faces from the z neighbours, per parity
   unsigned long long barR[2];            // mbarriers: dot-product partials, per parity
   unsigned long long barL[2];            // mbarriers: bulk staging, per buffer
@@ -166,16 +178,27 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-// Sum of the 64 pushed partials: lane l loads partials 2l, 2l+1 (one LDS.64)
-// and the warp reduces them with a fixed shuffle tree, so every warp of every
-// CTA gets the bit-identical total without a broadcast through shared memory.
-__device__ __forceinline__ float sum64(const float* red) {
-  const float2 v = reinterpret_cast<const float2*>(red)[threadIdx.x & 31];
-  return warp_sum(v.x + v.y);
+// Sum of the N pushed partials (N = 64 or 128): lane l loads N/32 consecutive
+// partials with one vector load and the warp reduces them with a fixed
+// shuffle tree, so every warp of every CTA gets the bit-identical total
+// without a broadcast through shared memory.
+template <int N>
+__device__ __forceinline__ float sum_parts(const float* red) {
+  static_assert(N == 64 || N == 128, "partial count");
+  if constexpr (N == 64) {
+    const float2 v = reinterpret_cast<const float2*>(red)[threadIdx.x & 31];
+    return warp_sum(v.x + v.y);
+  } else {
+    const float4 v = reinterpret_cast<const float4*>(red)[threadIdx.x & 31];
+    return warp_sum((v.x + v.y) + (v.z + v.w));
+  }
 }
 
 // Stage the slab of `slot` into buffer `buf` (one thread issues; completes on barL[buf]).
-__device__ __forceinline__ void stage_slab(const ResidentArgs& a, ResidentSmem& sm, int buf, int slot, int rank) {
+template <int RPZ>
+__device__ __forceinline__ void stage_slab(const ResidentArgs& a, ResidentSmem<RPZ>& sm, int buf, int slot,
+                                           int rank) {
+  constexpr int SLAB = RCfg<RPZ>::SLAB;
   const long long base = (long long)slot * (RB * RB * RB) + (long long)rank * SLAB;
   const uint32_t slab_bytes = SLAB * 4;
   const uint32_t zbytes = rank > 0 ? slab_bytes + PLANE * 4 : slab_bytes;
@@ -190,10 +213,13 @@ __device__ __forceinline__ void stage_slab(const ResidentArgs& a, ResidentSmem& 
   bulk_g2s(sm.sv[buf], a.y + base, slab_bytes, &sm.barL[buf]);
 }
 
-__global__ void __cluster_dims__(RCL, 1, 1) __launch_bounds__(RT, 1) resident3d_kernel(ResidentArgs a) {
+template <int RPZ>
+__global__ void __launch_bounds__(RT, RCfg<RPZ>::MINB) resident3d_kernel(ResidentArgs a) {
+  using C = RCfg<RPZ>;
+  constexpr int RCL = C::RCL, RV = C::RV, NPART = C::NPART, SLAB = C::SLAB, NBUF = C::NBUF;
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  ResidentSmem& sm = *reinterpret_cast<ResidentSmem*>(smem_raw);
+  ResidentSmem<RPZ>& sm = *reinterpret_cast<ResidentSmem<RPZ>*>(smem_raw);
   const int rank = (int)cluster.block_rank();
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -215,8 +241,10 @@ __global__ void __cluster_dims__(RCL, 1, 1) __launch_bounds__(RT, 1) resident3d_
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (rank == 0)  // the CTA holding planes 0..3 has no plane below: zero it once
-    for (int i = tid; i < PLANE; i += RT) sm.sz[0][i] = sm.sz[1][i] = 0.f;
+  if (rank == 0)  // the CTA holding planes 0.. has no plane below: zero it once
+    for (int i = tid; i < PLANE; i += RT)
+#pragma unroll
+      for (int b = 0; b < NBUF; ++b) sm.sz[b][i] = 0.f;
   // remote addresses this thread pushes to
   uint32_t face_dn_dst[2] = {0, 0}, face_up_dst[2] = {0, 0}, bar_dn[2] = {0, 0}, bar_up[2] = {0, 0};
   uint32_t red_dst[2] = {0, 0}, barR_dst[2] = {0, 0};
@@ -243,11 +271,11 @@ __global__ void __cluster_dims__(RCL, 1, 1) __launch_bounds__(RT, 1) resident3d_
 #endif
 
   int buf = 0;
-  if (cid < n_act && tid == 0) stage_slab(a, sm, 0, a.alist[cid], rank);
-  for (int j = cid; j < n_act; j += ncl, buf ^= 1) {
+  if (cid < n_act && tid == 0) stage_slab<RPZ>(a, sm, 0, a.alist[cid], rank);
+  for (int j = cid; j < n_act; j += ncl, buf ^= (NBUF - 1)) {
     BTRACE(0);
     const int slot = a.alist[j];
-    if (j + ncl < n_act && tid == 0) stage_slab(a, sm, buf ^ 1, a.alist[j + ncl], rank);
+    if (NBUF == 2 && j + ncl < n_act && tid == 0) stage_slab<RPZ>(a, sm, buf ^ 1, a.alist[j + ncl], rank);
     if (buf) {
       mbar_wait(&sm.barL[1], uses1 & 1);
       ++uses1;
@@ -263,6 +291,7 @@ __global__ void __cluster_dims__(RCL, 1, 1) __launch_bounds__(RT, 1) resident3d_
 #pragma unroll
     for (int z = 0; z < RPZ; ++z) {
       const int o = z * PLANE + ly * RB + xq * RQ;
+      (void)SLAB;
       const float4 fx = *reinterpret_cast<const float4*>(&sm.sx[buf][o]);
       const float4 fy = *reinterpret_cast<const float4*>(&sm.sy[buf][o]);
       const float4 fz = *reinterpret_cast<const float4*>(&sm.sz[buf][PLANE + o]);
@@ -329,7 +358,9 @@ __global__ void __cluster_dims__(RCL, 1, 1) __launch_bounds__(RT, 1) resident3d_
       __syncthreads();
       TRACE(1);
       // w = A'r: interior planes first, the two face planes once their neighbours arrived
-      float g4[RPZ] = {0.f, 0.f, 0.f, 0.f}, d4[RPZ] = {0.f, 0.f, 0.f, 0.f};
+      float g4[RPZ], d4[RPZ];
+#pragma unroll
+      for (int z = 0; z < RPZ; ++z) g4[z] = d4[z] = 0.f;
       auto spmv_plane = [&](int z, const float4& rzu, const float4& rzd) {
         const float4 ru = ly + 1 < RB ? sm.rp[z][ly + 1][xq] : f4(0, 0, 0, 0);
         const float4 rd = ly > 0 ? sm.rp[z][ly - 1][xq] : f4(0, 0, 0, 0);
@@ -364,8 +395,14 @@ __global__ void __cluster_dims__(RCL, 1, 1) __launch_bounds__(RT, 1) resident3d_
                  f4(r[(RPZ - 2) * RQ], r[(RPZ - 2) * RQ + 1], r[(RPZ - 2) * RQ + 2], r[(RPZ - 2) * RQ + 3]));
       TRACE(3);
       {
-        const float gw = warp_sum((g4[0] + g4[1]) + (g4[2] + g4[3]));
-        const float dw = warp_sum((d4[0] + d4[1]) + (d4[2] + d4[3]));
+        float gs = 0.f, ds = 0.f;
+#pragma unroll
+        for (int z = 0; z < RPZ; ++z) {
+          gs += g4[z];
+          ds += d4[z];
+        }
+        const float gw = warp_sum(gs);
+        const float dw = warp_sum(ds);
         if (lane < RCL) {
           const uint32_t dst = par ? red_dst[1] : red_dst[0], bar = par ? barR_dst[1] : barR_dst[0];
           st_async_f32(dst, gw, bar);
@@ -376,8 +413,8 @@ __global__ void __cluster_dims__(RCL, 1, 1) __launch_bounds__(RT, 1) resident3d_
       mbar_wait(&sm.barR[par], ph);
       TRACE(5);
       ++gk;
-      const float g_new = sum64(sm.red[par][0]);
-      const float delta = sum64(sm.red[par][1]);
+      const float g_new = sum_parts<NPART>(sm.red[par][0]);
+      const float delta = sum_parts<NPART>(sm.red[par][1]);
       if (pass == 0) {
         // the setup already settled zero-rhs and converged-at-start bricks
         beta = 0.f;
@@ -420,9 +457,10 @@ __global__ void __cluster_dims__(RCL, 1, 1) __launch_bounds__(RT, 1) resident3d_
       a.state[slot] = state;
       a.iters[slot] = it;
     }
-    // the staging buffer just read is refilled two bricks later: every thread
+    // the staging buffer just read is refilled for a later brick: every thread
     // must be past its register loads first
     __syncthreads();
+    if (NBUF == 1 && j + ncl < n_act && tid == 0) stage_slab<RPZ>(a, sm, 0, a.alist[j + ncl], rank);
     BTRACE(7);
     BTRACE(8);
 #ifdef RWB_TRACE
@@ -442,33 +480,41 @@ extern "C" int rwb_btrace_dump(long long* out) {  // 8*16*10 int64
 
 int resident3d_supported(const Geo& g) { return g.is3d && g.bz == RB && g.by == RB && g.bx == RB; }
 
-int launch_resident3d(const ResidentArgs& a, int max_bricks, cudaStream_t st) {
+template <int RPZ>
+static int launch_resident(const ResidentArgs& a, int max_bricks, cudaStream_t st) {
+  constexpr int RCL = RCfg<RPZ>::RCL;
   static thread_local int clusters = 0;
-  const int smem = (int)sizeof(ResidentSmem);
+  const int smem = (int)sizeof(ResidentSmem<RPZ>);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = RCL;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.blockDim = dim3(RT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
   if (!clusters) {
-    RWB_CUDA(cudaFuncSetAttribute(resident3d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    cudaLaunchConfig_t cfg = {};
+    RWB_CUDA(cudaFuncSetAttribute(resident3d_kernel<RPZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    if (RCL > 8) RWB_CUDA(cudaFuncSetAttribute(resident3d_kernel<RPZ>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     cfg.gridDim = dim3(RCL * 1024, 1, 1);
-    cfg.blockDim = dim3(RT, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cudaLaunchAttribute attr;
-    attr.id = cudaLaunchAttributeClusterDimension;
-    attr.val.clusterDim.x = RCL;
-    attr.val.clusterDim.y = 1;
-    attr.val.clusterDim.z = 1;
-    cfg.attrs = &attr;
-    cfg.numAttrs = 1;
     int n = 0;
-    RWB_CUDA(cudaOccupancyMaxActiveClusters(&n, resident3d_kernel, &cfg));
-    if (n <= 0) return fail(RWB_ERR_UNSUPPORTED, "no 8-CTA cluster fits on this device");
+    RWB_CUDA(cudaOccupancyMaxActiveClusters(&n, resident3d_kernel<RPZ>, &cfg));
+    if (n <= 0) return fail(RWB_ERR_UNSUPPORTED, "no brick cluster fits on this device");
     clusters = n;
   }
   const int grid_clusters = clusters < max_bricks ? clusters : max_bricks;
   if (grid_clusters <= 0) return RWB_OK;
-  resident3d_kernel<<<grid_clusters * RCL, RT, smem, st>>>(a);
-  RWB_LAUNCH_CHECK("resident3d_kernel");
+  cfg.gridDim = dim3(grid_clusters * RCL, 1, 1);
+  RWB_CUDA(cudaLaunchKernelEx(&cfg, resident3d_kernel<RPZ>, a));
   count_launches(1);
   return RWB_OK;
+}
+
+int launch_resident3d(const ResidentArgs& a, int max_bricks, int variant, cudaStream_t st) {
+  return variant == 16 ? launch_resident<2>(a, max_bricks, st) : launch_resident<4>(a, max_bricks, st);
 }
 
 }  // namespace rwb

@@ -193,6 +193,10 @@ def _flags(cfg: RWConfig) -> int:
         f |= _native.SOLVE_STREAMING
     if not cfg.cooperative:
         f |= _native.SOLVE_NO_COOP
+    if cfg.cluster == 16:
+        f |= _native.SOLVE_CLUSTER16
+    elif cfg.cluster != 8:
+        raise ValueError("cluster must be 8 or 16")
     return f
 
 

@@ -322,3 +322,15 @@ def test_upsample_window_slabs_match_full(rng):
             got = host(out)
             np.testing.assert_array_equal(got[z0:z1], full[z0:z1])
             assert np.isnan(got[:z0]).all() and np.isnan(got[z1:]).all()
+
+
+@pytest.mark.parametrize("cluster", [8, 16])
+def test_resident_cluster_variants(rng, cluster):
+    vol = synthetic.phantom((64, 96, 64))
+    seeds = synthetic.seeds(vol.shape, "S1")
+    bound = rng.random(vol.shape).astype(np.float32)
+    ref = orw.solve_level(vol, seeds, (32, 32, 32), bound.astype(np.float64), TIGHT).prob
+    cfg = RWConfig(tol=GPU_CFG.tol, max_iter=GPU_CFG.max_iter, cluster=cluster)
+    out, st = device.solve_level(cuda(vol), cuda(seeds), (32, 32, 32), cuda(bound), cfg)
+    assert st["path"] == 1 and st["not_converged"] == 0
+    assert_rw_parity(host(out), ref)
