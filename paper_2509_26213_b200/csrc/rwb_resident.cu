@@ -52,25 +52,29 @@ namespace rwb {
 constexpr int RB = 32;           // brick edge
 constexpr int RQ = 4;            // x voxels per thread
 constexpr int RQN = RB / RQ;     // quads per row
-constexpr int RT = RQN * RB;     // threads per CTA (256)
-constexpr int RW = RT / 32;      // warps per CTA
+constexpr int RT = RQN * RB;     // threads per CTA z-group (one thread per row quad of a plane set)
 constexpr int PLANE = RB * RB;   // floats per plane
 
-// Two decompositions of a 32^3 brick:
-//   RPZ = 4: 8-CTA clusters, 4 z-planes (16 voxels) per thread, 1 CTA per SM,
-//            double-buffered staging (the next brick prefetched while iterating);
-//   RPZ = 2: 16-CTA clusters (non-portable size), 2 z-planes (8 voxels) per
-//            thread, half the registers, so two CTAs of DIFFERENT bricks share
-//            an SM and each hides the other's reduction latency.
-template <int RPZ_>
+// Decompositions of a 32^3 brick (RPZ z-planes per CTA, TZT z-planes per thread):
+//   <4,4>: 8-CTA clusters, 256 threads x 16 voxels, 1 CTA per SM, double-buffered
+//          staging (the next brick prefetched while iterating);
+//   <4,2>: 8-CTA clusters, 512 threads x 8 voxels: twice the warps per SM to hide
+//          the latency of each phase, the middle planes exchanged through smem;
+//   <2,2>: 16-CTA clusters (non-portable size), 256 threads x 8 voxels, two CTAs
+//          of DIFFERENT bricks per SM.
+template <int RPZ_, int TZT_>
 struct RCfg {
   static constexpr int RPZ = RPZ_;               // z planes per CTA
+  static constexpr int TZT = TZT_;               // z planes per thread
+  static constexpr int NZG = RPZ / TZT;          // thread z-groups per CTA
+  static constexpr int RTT = RT * NZG;           // threads per CTA
+  static constexpr int RW = RTT / 32;            // warps per CTA
   static constexpr int RCL = RB / RPZ;           // CTAs per cluster (per brick)
-  static constexpr int RV = RQ * RPZ;            // voxels per thread
+  static constexpr int RV = RQ * TZT;            // voxels per thread
   static constexpr int NPART = RCL * RW;         // pushed partials per reduction
   static constexpr int SLAB = RPZ * PLANE;
-  static constexpr int NBUF = RPZ == 4 ? 2 : 1;  // staging buffers
-  static constexpr int MINB = RPZ == 4 ? 1 : 2;  // CTAs per SM
+  static constexpr int MINB = RPZ == 2 ? 2 : 1;  // CTAs per SM
+  static constexpr int NBUF = MINB == 1 ? 2 : 1; // staging buffers (2: next brick prefetched)
 };
 
 }  // namespace rwb
@@ -98,9 +102,9 @@ __device__ long long g_rwb_btrace[8][16][10];
 
 namespace rwb {
 
-template <int RPZ>
+template <int RPZ, int TZT>
 struct ResidentSmem {
-  using C = RCfg<RPZ>;
+  using C = RCfg<RPZ, TZT>;
   float sx[C::NBUF][C::SLAB];              // staged scaled weights (double buffer: current / next brick)
   float sy[C::NBUF][C::SLAB];
   float sz[C::NBUF][PLANE + C::SLAB];      // z weights incl. the plane below the slab
@@ -195,10 +199,10 @@ __device__ __forceinline__ float sum_parts(const float* red) {
 }
 
 // Stage the slab of `slot` into buffer `buf` (one thread issues; completes on barL[buf]).
-template <int RPZ>
-__device__ __forceinline__ void stage_slab(const ResidentArgs& a, ResidentSmem<RPZ>& sm, int buf, int slot,
+template <int RPZ, int TZT>
+__device__ __forceinline__ void stage_slab(const ResidentArgs& a, ResidentSmem<RPZ, TZT>& sm, int buf, int slot,
                                            int rank) {
-  constexpr int SLAB = RCfg<RPZ>::SLAB;
+  constexpr int SLAB = RCfg<RPZ, TZT>::SLAB;
   const long long base = (long long)slot * (RB * RB * RB) + (long long)rank * SLAB;
   const uint32_t slab_bytes = SLAB * 4;
   const uint32_t zbytes = rank > 0 ? slab_bytes + PLANE * 4 : slab_bytes;
@@ -213,19 +217,22 @@ __device__ __forceinline__ void stage_slab(const ResidentArgs& a, ResidentSmem<R
   bulk_g2s(sm.sv[buf], a.y + base, slab_bytes, &sm.barL[buf]);
 }
 
-template <int RPZ>
-__global__ void __launch_bounds__(RT, RCfg<RPZ>::MINB) resident3d_kernel(ResidentArgs a) {
-  using C = RCfg<RPZ>;
-  constexpr int RCL = C::RCL, RV = C::RV, NPART = C::NPART, SLAB = C::SLAB, NBUF = C::NBUF;
+template <int RPZ, int TZT>
+__global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) resident3d_kernel(ResidentArgs a) {
+  using C = RCfg<RPZ, TZT>;
+  constexpr int RCL = C::RCL, RV = C::RV, NPART = C::NPART, NBUF = C::NBUF, RTT = C::RTT, NZG = C::NZG;
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  ResidentSmem<RPZ>& sm = *reinterpret_cast<ResidentSmem<RPZ>*>(smem_raw);
+  ResidentSmem<RPZ, TZT>& sm = *reinterpret_cast<ResidentSmem<RPZ, TZT>*>(smem_raw);
   const int rank = (int)cluster.block_rank();
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int ly = tid / RQN;  // row
-  const int xq = tid % RQN;  // quad within the row
+  const int zg = tid / RT;          // thread z-group: planes [zg*TZT, zg*TZT + TZT) of the slab
+  const int ly = (tid % RT) / RQN;  // row
+  const int xq = tid % RQN;         // quad within the row
+  const int pz0 = zg * TZT;
   const bool below = rank > 0, above = rank < RCL - 1;
+  const bool first_zg = zg == 0, last_zg = zg == NZG - 1;
   const int nfaces = (int)below + (int)above;
   const uint32_t face_bytes = (uint32_t)(RB * RQN * sizeof(float4));
   const uint32_t tx_faces = nfaces * face_bytes;
@@ -241,8 +248,8 @@ __global__ void __launch_bounds__(RT, RCfg<RPZ>::MINB) resident3d_kernel(Residen
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (rank == 0)  // the CTA holding planes 0.. has no plane below: zero it once
-    for (int i = tid; i < PLANE; i += RT)
+  if (rank == 0)  // the CTA holding plane 0 has no plane below: zero it once
+    for (int i = tid; i < PLANE; i += RTT)
 #pragma unroll
       for (int b = 0; b < NBUF; ++b) sm.sz[b][i] = 0.f;
   // remote addresses this thread pushes to
@@ -250,16 +257,16 @@ __global__ void __launch_bounds__(RT, RCfg<RPZ>::MINB) resident3d_kernel(Residen
   uint32_t red_dst[2] = {0, 0}, barR_dst[2] = {0, 0};
 #pragma unroll
   for (int par = 0; par < 2; ++par) {
-    if (below) {  // my plane 0 goes to the CTA below, as its "from above" face
+    if (below && first_zg) {  // slab plane 0 goes to the CTA below, as its "from above" face
       face_dn_dst[par] = mapa_u32(smem_u32(&sm.rface[par][1][ly][xq]), rank - 1);
       bar_dn[par] = mapa_u32(smem_u32(&sm.barF[par]), rank - 1);
     }
-    if (above) {  // my last plane goes to the CTA above, as its "from below" face
+    if (above && last_zg) {  // the last slab plane goes to the CTA above, as its "from below" face
       face_up_dst[par] = mapa_u32(smem_u32(&sm.rface[par][0][ly][xq]), rank + 1);
       bar_up[par] = mapa_u32(smem_u32(&sm.barF[par]), rank + 1);
     }
     if (lane < RCL) {  // lane t delivers this warp's partials to CTA t
-      red_dst[par] = mapa_u32(smem_u32(&sm.red[par][0][rank * RW + warp]), lane);
+      red_dst[par] = mapa_u32(smem_u32(&sm.red[par][0][rank * C::RW + warp]), lane);
       barR_dst[par] = mapa_u32(smem_u32(&sm.barR[par]), lane);
     }
   }
@@ -271,11 +278,11 @@ __global__ void __launch_bounds__(RT, RCfg<RPZ>::MINB) resident3d_kernel(Residen
 #endif
 
   int buf = 0;
-  if (cid < n_act && tid == 0) stage_slab<RPZ>(a, sm, 0, a.alist[cid], rank);
+  if (cid < n_act && tid == 0) stage_slab<RPZ, TZT>(a, sm, 0, a.alist[cid], rank);
   for (int j = cid; j < n_act; j += ncl, buf ^= (NBUF - 1)) {
     BTRACE(0);
     const int slot = a.alist[j];
-    if (NBUF == 2 && j + ncl < n_act && tid == 0) stage_slab<RPZ>(a, sm, buf ^ 1, a.alist[j + ncl], rank);
+    if (NBUF == 2 && j + ncl < n_act && tid == 0) stage_slab<RPZ, TZT>(a, sm, buf ^ 1, a.alist[j + ncl], rank);
     if (buf) {
       mbar_wait(&sm.barL[1], uses1 & 1);
       ++uses1;
@@ -287,11 +294,11 @@ __global__ void __launch_bounds__(RT, RCfg<RPZ>::MINB) resident3d_kernel(Residen
 
     // ---------------- registers from the staged slab ----------------
     float y[RV], r[RV], p[RV], sv[RV], w[RV];
-    float wxf[RV], wyf[RV], wzf[RV], wyb[RV], wxb[RPZ], wzb[RQ];
+    float wxf[RV], wyf[RV], wzf[RV], wyb[RV], wxb[TZT], wzb[RQ];
 #pragma unroll
-    for (int z = 0; z < RPZ; ++z) {
-      const int o = z * PLANE + ly * RB + xq * RQ;
-      (void)SLAB;
+    for (int z = 0; z < TZT; ++z) {
+      const int pz = pz0 + z;
+      const int o = pz * PLANE + ly * RB + xq * RQ;
       const float4 fx = *reinterpret_cast<const float4*>(&sm.sx[buf][o]);
       const float4 fy = *reinterpret_cast<const float4*>(&sm.sy[buf][o]);
       const float4 fz = *reinterpret_cast<const float4*>(&sm.sz[buf][PLANE + o]);
@@ -299,7 +306,7 @@ __global__ void __launch_bounds__(RT, RCfg<RPZ>::MINB) resident3d_kernel(Residen
       const float4 fr = *reinterpret_cast<const float4*>(&sm.sr[buf][o]);
       const float4 fv = *reinterpret_cast<const float4*>(&sm.sv[buf][o]);
       wxb[z] = xq > 0 ? sm.sx[buf][o - 1] : 0.f;
-      if (z == 0) {
+      if (z == 0) {  // -z weights of the thread's first plane (sz[0] is the plane below the slab)
         const float4 fzb = *reinterpret_cast<const float4*>(&sm.sz[buf][o]);
 #pragma unroll
         for (int i = 0; i < RQ; ++i) wzb[i] = lane_of(fzb, i);
@@ -346,24 +353,27 @@ __global__ void __launch_bounds__(RT, RCfg<RPZ>::MINB) resident3d_kernel(Residen
           r[v] = fmaf(-alpha, sv[v], r[v]);
         }
       }
-      // publish r: planes for the y neighbours, faces for the z neighbours
+      // publish r: planes for the y (and cross-group z) neighbours, faces for the z neighbours
 #pragma unroll
-      for (int z = 0; z < RPZ; ++z) sm.rp[z][ly][xq] = f4(r[z * RQ], r[z * RQ + 1], r[z * RQ + 2], r[z * RQ + 3]);
-      if (below)
+      for (int z = 0; z < TZT; ++z)
+        sm.rp[pz0 + z][ly][xq] = f4(r[z * RQ], r[z * RQ + 1], r[z * RQ + 2], r[z * RQ + 3]);
+      if (below && first_zg)
         st_async_v4(par ? face_dn_dst[1] : face_dn_dst[0], f4(r[0], r[1], r[2], r[3]), par ? bar_dn[1] : bar_dn[0]);
-      if (above)
+      if (above && last_zg)
         st_async_v4(par ? face_up_dst[1] : face_up_dst[0],
-                    f4(r[(RPZ - 1) * RQ], r[(RPZ - 1) * RQ + 1], r[(RPZ - 1) * RQ + 2], r[(RPZ - 1) * RQ + 3]),
+                    f4(r[(TZT - 1) * RQ], r[(TZT - 1) * RQ + 1], r[(TZT - 1) * RQ + 2], r[(TZT - 1) * RQ + 3]),
                     par ? bar_up[1] : bar_up[0]);
       __syncthreads();
       TRACE(1);
-      // w = A'r: interior planes first, the two face planes once their neighbours arrived
-      float g4[RPZ], d4[RPZ];
+      // w = A'r: planes whose z neighbours are in this CTA first, the slab faces once their
+      // neighbours arrived
+      float g4[TZT], d4[TZT];
 #pragma unroll
-      for (int z = 0; z < RPZ; ++z) g4[z] = d4[z] = 0.f;
+      for (int z = 0; z < TZT; ++z) g4[z] = d4[z] = 0.f;
       auto spmv_plane = [&](int z, const float4& rzu, const float4& rzd) {
-        const float4 ru = ly + 1 < RB ? sm.rp[z][ly + 1][xq] : f4(0, 0, 0, 0);
-        const float4 rd = ly > 0 ? sm.rp[z][ly - 1][xq] : f4(0, 0, 0, 0);
+        const int pz = pz0 + z;
+        const float4 ru = ly + 1 < RB ? sm.rp[pz][ly + 1][xq] : f4(0, 0, 0, 0);
+        const float4 rd = ly > 0 ? sm.rp[pz][ly - 1][xq] : f4(0, 0, 0, 0);
         const float rl = __shfl_up_sync(0xffffffffu, r[z * RQ + RQ - 1], 1);
         const float rr_ = __shfl_down_sync(0xffffffffu, r[z * RQ], 1);
 #pragma unroll
@@ -384,20 +394,34 @@ __global__ void __launch_bounds__(RT, RCfg<RPZ>::MINB) resident3d_kernel(Residen
           d4[z] = fmaf(w[v], r[v], d4[z]);
         }
       };
+      auto reg_plane = [&](int z) { return f4(r[z * RQ], r[z * RQ + 1], r[z * RQ + 2], r[z * RQ + 3]); };
+      // z neighbour of thread plane z in direction d (+1 / -1) that lives in this CTA
+      auto zn_local = [&](int z, int d) {
+        const int zt = z + d;
+        if (zt >= 0 && zt < TZT) return reg_plane(zt);
+        return sm.rp[pz0 + zt][ly][xq];  // another z-group of this CTA
+      };
+      const bool face_dn = first_zg, face_up = last_zg;  // thread planes touching the slab faces
 #pragma unroll
-      for (int z = 1; z < RPZ - 1; ++z)
-        spmv_plane(z, f4(r[(z + 1) * RQ], r[(z + 1) * RQ + 1], r[(z + 1) * RQ + 2], r[(z + 1) * RQ + 3]),
-                   f4(r[(z - 1) * RQ], r[(z - 1) * RQ + 1], r[(z - 1) * RQ + 2], r[(z - 1) * RQ + 3]));
-      if (tx_faces) mbar_wait(&sm.barF[par], ph);
+      for (int z = 0; z < TZT; ++z) {
+        const bool needs_dn = z == 0 && face_dn, needs_up = z == TZT - 1 && face_up;
+        if (!needs_dn && !needs_up) spmv_plane(z, zn_local(z, +1), zn_local(z, -1));
+      }
+      if (tx_faces && (face_dn || face_up)) mbar_wait(&sm.barF[par], ph);
       TRACE(2);
-      spmv_plane(0, f4(r[RQ], r[RQ + 1], r[RQ + 2], r[RQ + 3]), below ? sm.rface[par][0][ly][xq] : f4(0, 0, 0, 0));
-      spmv_plane(RPZ - 1, above ? sm.rface[par][1][ly][xq] : f4(0, 0, 0, 0),
-                 f4(r[(RPZ - 2) * RQ], r[(RPZ - 2) * RQ + 1], r[(RPZ - 2) * RQ + 2], r[(RPZ - 2) * RQ + 3]));
+#pragma unroll
+      for (int z = 0; z < TZT; ++z) {
+        const bool needs_dn = z == 0 && face_dn, needs_up = z == TZT - 1 && face_up;
+        if (!needs_dn && !needs_up) continue;
+        const float4 up = needs_up ? (above ? sm.rface[par][1][ly][xq] : f4(0, 0, 0, 0)) : zn_local(z, +1);
+        const float4 dn = needs_dn ? (below ? sm.rface[par][0][ly][xq] : f4(0, 0, 0, 0)) : zn_local(z, -1);
+        spmv_plane(z, up, dn);
+      }
       TRACE(3);
       {
         float gs = 0.f, ds = 0.f;
 #pragma unroll
-        for (int z = 0; z < RPZ; ++z) {
+        for (int z = 0; z < TZT; ++z) {
           gs += g4[z];
           ds += d4[z];
         }
@@ -447,10 +471,10 @@ __global__ void __launch_bounds__(RT, RCfg<RPZ>::MINB) resident3d_kernel(Residen
     BTRACE(6);
     // ---------------- y back to the brick-local workspace ----------------
     {
-      const long long base = (long long)slot * (RB * RB * RB) + (long long)rank * SLAB;
+      const long long base = (long long)slot * (RB * RB * RB) + (long long)rank * C::SLAB;
 #pragma unroll
-      for (int z = 0; z < RPZ; ++z)
-        *reinterpret_cast<float4*>(a.y + base + z * PLANE + ly * RB + xq * RQ) =
+      for (int z = 0; z < TZT; ++z)
+        *reinterpret_cast<float4*>(a.y + base + (pz0 + z) * PLANE + ly * RB + xq * RQ) =
             f4(y[z * RQ], y[z * RQ + 1], y[z * RQ + 2], y[z * RQ + 3]);
     }
     if (rank == 0 && tid == 0) {
@@ -460,7 +484,7 @@ __global__ void __launch_bounds__(RT, RCfg<RPZ>::MINB) resident3d_kernel(Residen
     // the staging buffer just read is refilled for a later brick: every thread
     // must be past its register loads first
     __syncthreads();
-    if (NBUF == 1 && j + ncl < n_act && tid == 0) stage_slab<RPZ>(a, sm, 0, a.alist[j + ncl], rank);
+    if (NBUF == 1 && j + ncl < n_act && tid == 0) stage_slab<RPZ, TZT>(a, sm, 0, a.alist[j + ncl], rank);
     BTRACE(7);
     BTRACE(8);
 #ifdef RWB_TRACE
@@ -480,41 +504,46 @@ extern "C" int rwb_btrace_dump(long long* out) {  // 8*16*10 int64
 
 int resident3d_supported(const Geo& g) { return g.is3d && g.bz == RB && g.by == RB && g.bx == RB; }
 
-template <int RPZ>
+template <int RPZ, int TZT>
 static int launch_resident(const ResidentArgs& a, int max_bricks, cudaStream_t st) {
-  constexpr int RCL = RCfg<RPZ>::RCL;
+  using C = RCfg<RPZ, TZT>;
   static thread_local int clusters = 0;
-  const int smem = (int)sizeof(ResidentSmem<RPZ>);
+  const int smem = (int)sizeof(ResidentSmem<RPZ, TZT>);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeClusterDimension;
-  attr.val.clusterDim.x = RCL;
+  attr.val.clusterDim.x = C::RCL;
   attr.val.clusterDim.y = 1;
   attr.val.clusterDim.z = 1;
-  cfg.blockDim = dim3(RT, 1, 1);
+  cfg.blockDim = dim3(C::RTT, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
   if (!clusters) {
-    RWB_CUDA(cudaFuncSetAttribute(resident3d_kernel<RPZ>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    if (RCL > 8) RWB_CUDA(cudaFuncSetAttribute(resident3d_kernel<RPZ>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    cfg.gridDim = dim3(RCL * 1024, 1, 1);
+    RWB_CUDA(cudaFuncSetAttribute(resident3d_kernel<RPZ, TZT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    if (C::RCL > 8)
+      RWB_CUDA(cudaFuncSetAttribute(resident3d_kernel<RPZ, TZT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    cfg.gridDim = dim3(C::RCL * 1024, 1, 1);
     int n = 0;
-    RWB_CUDA(cudaOccupancyMaxActiveClusters(&n, resident3d_kernel<RPZ>, &cfg));
+    RWB_CUDA(cudaOccupancyMaxActiveClusters(&n, resident3d_kernel<RPZ, TZT>, &cfg));
     if (n <= 0) return fail(RWB_ERR_UNSUPPORTED, "no brick cluster fits on this device");
     clusters = n;
   }
   const int grid_clusters = clusters < max_bricks ? clusters : max_bricks;
   if (grid_clusters <= 0) return RWB_OK;
-  cfg.gridDim = dim3(grid_clusters * RCL, 1, 1);
-  RWB_CUDA(cudaLaunchKernelEx(&cfg, resident3d_kernel<RPZ>, a));
+  cfg.gridDim = dim3(grid_clusters * C::RCL, 1, 1);
+  RWB_CUDA(cudaLaunchKernelEx(&cfg, resident3d_kernel<RPZ, TZT>, a));
   count_launches(1);
   return RWB_OK;
 }
 
 int launch_resident3d(const ResidentArgs& a, int max_bricks, int variant, cudaStream_t st) {
-  return variant == 16 ? launch_resident<2>(a, max_bricks, st) : launch_resident<4>(a, max_bricks, st);
+  switch (variant) {
+    case 16: return launch_resident<2, 2>(a, max_bricks, st);
+    case 512: return launch_resident<4, 2>(a, max_bricks, st);
+    default: return launch_resident<4, 4>(a, max_bricks, st);
+  }
 }
 
 }  // namespace rwb

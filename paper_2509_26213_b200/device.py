@@ -195,8 +195,10 @@ def _flags(cfg: RWConfig) -> int:
         f |= _native.SOLVE_NO_COOP
     if cfg.cluster == 16:
         f |= _native.SOLVE_CLUSTER16
+    elif cfg.cluster == 512:  # 8-CTA clusters, 512 threads per CTA
+        f |= _native.SOLVE_SPLIT_Z
     elif cfg.cluster != 8:
-        raise ValueError("cluster must be 8 or 16")
+        raise ValueError("cluster must be 8, 16 or 512")
     return f
 
 

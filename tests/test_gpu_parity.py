@@ -324,7 +324,7 @@ def test_upsample_window_slabs_match_full(rng):
             assert np.isnan(got[:z0]).all() and np.isnan(got[z1:]).all()
 
 
-@pytest.mark.parametrize("cluster", [8, 16])
+@pytest.mark.parametrize("cluster", [8, 16, 512])
 def test_resident_cluster_variants(rng, cluster):
     vol = synthetic.phantom((64, 96, 64))
     seeds = synthetic.seeds(vol.shape, "S1")

@@ -8,7 +8,7 @@ from paper_2509_26213_b200 import device, synthetic
 from paper_2509_26213_b200.config import RWConfig
 vol = synthetic.phantom_device((1024,) * 3); sd = synthetic.seeds_device((1024,) * 3)
 ws = device.Workspace()
-for cl in (8, 16, 8, 16):
+for cl in (8, 512, 16, 8, 512):
     cfg = RWConfig(cluster=cl)
     res = device.hierarchical_random_walker(vol, sd, (32, 32, 32), 4, cfg, workspace=ws)
     torch.cuda.synchronize()
