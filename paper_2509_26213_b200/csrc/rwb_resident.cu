@@ -111,7 +111,7 @@ struct ResidentSmem {
   float sr[C::NBUF][C::SLAB];              // staged r0
   float sv[C::NBUF][C::SLAB];              // staged y0
   float4 rp[RPZ][RB][RQN];                 // r planes of this slab (y neighbours of the SpMV)
-  float4 rface[2][2][RB][RQN];             // received r faces [parity][0 = from below, 1 = from above]
+  float4 rface[2][2][RB][RQN];             // received faces [parity][0 = from below, 1 = from above]
   __align__(16) float red[2][2][C::NPART];  // pushed partials [parity][gamma, delta][rank*RW + warp]
   unsigned long long barF[2];            // mbarriers: r faces from the z neighbours, per parity
   unsigned long long barR[2];            // mbarriers: dot-product partials, per parity
@@ -189,13 +189,23 @@ __device__ __forceinline__ float warp_sum(float v) {
 template <int N>
 __device__ __forceinline__ float sum_parts(const float* red) {
   static_assert(N == 64 || N == 128, "partial count");
+  // each lane of an aligned group of 8 lanes sums N/8 partials (vector loads), then
+  // three butterfly steps inside the group: every lane ends with the same total in
+  // the same order, with 3 dependent shuffles instead of 5
+  const float4* v = reinterpret_cast<const float4*>(red) + (threadIdx.x & 7) * (N / 32);
+  float s;
   if constexpr (N == 64) {
-    const float2 v = reinterpret_cast<const float2*>(red)[threadIdx.x & 31];
-    return warp_sum(v.x + v.y);
+    const float4 a = v[0], b = v[1];
+    s = ((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w));
   } else {
-    const float4 v = reinterpret_cast<const float4*>(red)[threadIdx.x & 31];
-    return warp_sum((v.x + v.y) + (v.z + v.w));
+    const float4 a = v[0], b = v[1], c = v[2], d = v[3];
+    s = (((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w))) +
+        (((c.x + c.y) + (c.z + c.w)) + ((d.x + d.y) + (d.z + d.w)));
   }
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
+  s += __shfl_xor_sync(0xffffffffu, s, 4);
+  return s;
 }
 
 // Stage the slab of `slot` into buffer `buf` (one thread issues; completes on barL[buf]).
@@ -259,11 +269,11 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
   for (int par = 0; par < 2; ++par) {
     if (below && first_zg) {  // slab plane 0 goes to the CTA below, as its "from above" face
       face_dn_dst[par] = mapa_u32(smem_u32(&sm.rface[par][1][ly][xq]), rank - 1);
-      bar_dn[par] = mapa_u32(smem_u32(&sm.barF[par]), rank - 1);
+      bar_dn[par] = mapa_u32(smem_u32(&sm.barR[par]), rank - 1);
     }
     if (above && last_zg) {  // the last slab plane goes to the CTA above, as its "from below" face
       face_up_dst[par] = mapa_u32(smem_u32(&sm.rface[par][0][ly][xq]), rank + 1);
-      bar_up[par] = mapa_u32(smem_u32(&sm.barF[par]), rank + 1);
+      bar_up[par] = mapa_u32(smem_u32(&sm.barR[par]), rank + 1);
     }
     if (lane < RCL) {  // lane t delivers this warp's partials to CTA t
       red_dst[par] = mapa_u32(smem_u32(&sm.red[par][0][rank * C::RW + warp]), lane);
@@ -329,10 +339,44 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
     BTRACE(2);
 
     // ---------------- CG (Chronopoulos-Gear) ----------------
-    // pass 0 computes w0 = A'r0 and reduces gamma0 = r0.r0, delta0 = w0.r0;
-    // pass k >= 1 first applies update k, then the same SpMV + reduction.
-    float gamma = 0.f, alpha = 0.f, beta = 0.f;
+    // One cluster-wide exchange per iteration: right after the SpMV w = A'r each
+    // CTA pushes its dot partials AND its two face planes of w.  A CTA keeps its
+    // own copies of the neighbours' face values of r and s (r0 exchanged once per
+    // brick) and advances them with the same fmaf as their owner,
+    //   s_face <- w_face + beta s_face,   r_face <- r_face - alpha s_face,
+    // so they stay bit-identical and the next SpMV needs no second exchange.
+    // (Pushing r faces as well would double the DSMEM volume, which at ~20 B/cycle
+    // per SM is what bounds the exchange.)
+    float gamma = 0.f, alpha = 0.f;
     int state = ST_ACTIVE, it = 0;
+    float4 rf_dn = f4(0, 0, 0, 0), rf_up = f4(0, 0, 0, 0);  // neighbours' r at my faces
+    float4 sf_dn = f4(0, 0, 0, 0), sf_up = f4(0, 0, 0, 0);  // ... and their s
+    const float4 z4 = f4(0, 0, 0, 0);
+    auto plane4 = [&](const float* v, int z) { return f4(v[z * RQ], v[z * RQ + 1], v[z * RQ + 2], v[z * RQ + 3]); };
+    // publish r0: planes for the y / cross-group z neighbours, faces through a one-time exchange
+#pragma unroll
+    for (int z = 0; z < TZT; ++z) sm.rp[pz0 + z][ly][xq] = plane4(r, z);
+    {
+      const int par = gk & 1;
+      const uint32_t ph = (gk >> 1) & 1;
+      if (tid == 0) mbar_expect_tx(&sm.barR[par], tx_faces + 2 * NPART * 4);
+      if (below && first_zg) st_async_v4(par ? face_dn_dst[1] : face_dn_dst[0], plane4(r, 0), par ? bar_dn[1] : bar_dn[0]);
+      if (above && last_zg)
+        st_async_v4(par ? face_up_dst[1] : face_up_dst[0], plane4(r, TZT - 1), par ? bar_up[1] : bar_up[0]);
+      // complete the phase's partial slots with zeros (this exchange carries no dot products)
+      if (warp == 0 && lane < RCL) {
+        const uint32_t dst = par ? red_dst[1] : red_dst[0], bar = par ? barR_dst[1] : barR_dst[0];
+        for (int wv = 0; wv < C::RW; ++wv) {
+          st_async_f32(dst + wv * 4, 0.f, bar);
+          st_async_f32(dst + NPART * 4 + wv * 4, 0.f, bar);
+        }
+      }
+      mbar_wait(&sm.barR[par], ph);
+      ++gk;
+      if (first_zg && below) rf_dn = sm.rface[par][0][ly][xq];
+      if (last_zg && above) rf_up = sm.rface[par][1][ly][xq];
+      __syncthreads();  // own r planes published
+    }
 #ifdef RWB_TRACE
     int trace_it = (int)gk;
 #endif
@@ -340,40 +384,18 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
       TRACE(0);
       const int par = gk & 1;
       const uint32_t ph = (gk >> 1) & 1;
-      if (tid == 0) {
-        if (tx_faces) mbar_expect_tx(&sm.barF[par], tx_faces);
-        mbar_expect_tx(&sm.barR[par], 2 * NPART * 4);
-      }
-      if (pass > 0) {
-#pragma unroll
-        for (int v = 0; v < RV; ++v) {
-          p[v] = fmaf(beta, p[v], r[v]);
-          sv[v] = fmaf(beta, sv[v], w[v]);
-          y[v] = fmaf(alpha, p[v], y[v]);
-          r[v] = fmaf(-alpha, sv[v], r[v]);
-        }
-      }
-      // publish r: planes for the y (and cross-group z) neighbours, faces for the z neighbours
-#pragma unroll
-      for (int z = 0; z < TZT; ++z)
-        sm.rp[pz0 + z][ly][xq] = f4(r[z * RQ], r[z * RQ + 1], r[z * RQ + 2], r[z * RQ + 3]);
-      if (below && first_zg)
-        st_async_v4(par ? face_dn_dst[1] : face_dn_dst[0], f4(r[0], r[1], r[2], r[3]), par ? bar_dn[1] : bar_dn[0]);
-      if (above && last_zg)
-        st_async_v4(par ? face_up_dst[1] : face_up_dst[0],
-                    f4(r[(TZT - 1) * RQ], r[(TZT - 1) * RQ + 1], r[(TZT - 1) * RQ + 2], r[(TZT - 1) * RQ + 3]),
-                    par ? bar_up[1] : bar_up[0]);
-      __syncthreads();
-      TRACE(1);
-      // w = A'r: planes whose z neighbours are in this CTA first, the slab faces once their
-      // neighbours arrived
+      if (tid == 0) mbar_expect_tx(&sm.barR[par], tx_faces + 2 * NPART * 4);
+      // w = A'r
       float g4[TZT], d4[TZT];
 #pragma unroll
       for (int z = 0; z < TZT; ++z) g4[z] = d4[z] = 0.f;
-      auto spmv_plane = [&](int z, const float4& rzu, const float4& rzd) {
+#pragma unroll
+      for (int z = 0; z < TZT; ++z) {
         const int pz = pz0 + z;
-        const float4 ru = ly + 1 < RB ? sm.rp[pz][ly + 1][xq] : f4(0, 0, 0, 0);
-        const float4 rd = ly > 0 ? sm.rp[pz][ly - 1][xq] : f4(0, 0, 0, 0);
+        const float4 ru = ly + 1 < RB ? sm.rp[pz][ly + 1][xq] : z4;
+        const float4 rd = ly > 0 ? sm.rp[pz][ly - 1][xq] : z4;
+        const float4 rzu = z + 1 < TZT ? plane4(r, z + 1) : (pz + 1 < RPZ ? sm.rp[pz + 1][ly][xq] : rf_up);
+        const float4 rzd = z > 0 ? plane4(r, z - 1) : (pz > 0 ? sm.rp[pz - 1][ly][xq] : rf_dn);
         const float rl = __shfl_up_sync(0xffffffffu, r[z * RQ + RQ - 1], 1);
         const float rr_ = __shfl_down_sync(0xffffffffu, r[z * RQ], 1);
 #pragma unroll
@@ -393,31 +415,13 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
           g4[z] = fmaf(r[v], r[v], g4[z]);
           d4[z] = fmaf(w[v], r[v], d4[z]);
         }
-      };
-      auto reg_plane = [&](int z) { return f4(r[z * RQ], r[z * RQ + 1], r[z * RQ + 2], r[z * RQ + 3]); };
-      // z neighbour of thread plane z in direction d (+1 / -1) that lives in this CTA
-      auto zn_local = [&](int z, int d) {
-        const int zt = z + d;
-        if (zt >= 0 && zt < TZT) return reg_plane(zt);
-        return sm.rp[pz0 + zt][ly][xq];  // another z-group of this CTA
-      };
-      const bool face_dn = first_zg, face_up = last_zg;  // thread planes touching the slab faces
-#pragma unroll
-      for (int z = 0; z < TZT; ++z) {
-        const bool needs_dn = z == 0 && face_dn, needs_up = z == TZT - 1 && face_up;
-        if (!needs_dn && !needs_up) spmv_plane(z, zn_local(z, +1), zn_local(z, -1));
       }
-      if (tx_faces && (face_dn || face_up)) mbar_wait(&sm.barF[par], ph);
-      TRACE(2);
-#pragma unroll
-      for (int z = 0; z < TZT; ++z) {
-        const bool needs_dn = z == 0 && face_dn, needs_up = z == TZT - 1 && face_up;
-        if (!needs_dn && !needs_up) continue;
-        const float4 up = needs_up ? (above ? sm.rface[par][1][ly][xq] : f4(0, 0, 0, 0)) : zn_local(z, +1);
-        const float4 dn = needs_dn ? (below ? sm.rface[par][0][ly][xq] : f4(0, 0, 0, 0)) : zn_local(z, -1);
-        spmv_plane(z, up, dn);
-      }
-      TRACE(3);
+      TRACE(1);
+      // push the faces of w, then the dot partials, all onto the peers' barR[par]
+      if (below && first_zg)
+        st_async_v4(par ? face_dn_dst[1] : face_dn_dst[0], plane4(w, 0), par ? bar_dn[1] : bar_dn[0]);
+      if (above && last_zg)
+        st_async_v4(par ? face_up_dst[1] : face_up_dst[0], plane4(w, TZT - 1), par ? bar_up[1] : bar_up[0]);
       {
         float gs = 0.f, ds = 0.f;
 #pragma unroll
@@ -433,12 +437,13 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
           st_async_f32(dst + NPART * 4, dw, bar);
         }
       }
-      TRACE(4);
+      TRACE(2);
       mbar_wait(&sm.barR[par], ph);
-      TRACE(5);
+      TRACE(3);
       ++gk;
       const float g_new = sum_parts<NPART>(sm.red[par][0]);
       const float delta = sum_parts<NPART>(sm.red[par][1]);
+      float beta;
       if (pass == 0) {
         // the setup already settled zero-rhs and converged-at-start bricks
         beta = 0.f;
@@ -448,7 +453,6 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
           break;
         }
       } else {
-        ++it;
         if (g_new <= thresh) {
           state = ST_CONVERGED;
           break;
@@ -463,6 +467,34 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
         alpha = den != 0.f ? __fdividef(g_new, den) : 0.f;
       }
       gamma = g_new;
+      TRACE(4);
+      // update k: p = r + beta p, s = w + beta s, y += alpha p, r -= alpha s (and the neighbour faces)
+#pragma unroll
+      for (int v = 0; v < RV; ++v) {
+        p[v] = fmaf(beta, p[v], r[v]);
+        sv[v] = fmaf(beta, sv[v], w[v]);
+        y[v] = fmaf(alpha, p[v], y[v]);
+        r[v] = fmaf(-alpha, sv[v], r[v]);
+      }
+      ++it;
+      if (first_zg && below) {
+        const float4 wn = sm.rface[par][0][ly][xq];
+        sf_dn = f4(fmaf(beta, sf_dn.x, wn.x), fmaf(beta, sf_dn.y, wn.y), fmaf(beta, sf_dn.z, wn.z), fmaf(beta, sf_dn.w, wn.w));
+        rf_dn = f4(fmaf(-alpha, sf_dn.x, rf_dn.x), fmaf(-alpha, sf_dn.y, rf_dn.y), fmaf(-alpha, sf_dn.z, rf_dn.z),
+                   fmaf(-alpha, sf_dn.w, rf_dn.w));
+      }
+      if (last_zg && above) {
+        const float4 wn = sm.rface[par][1][ly][xq];
+        sf_up = f4(fmaf(beta, sf_up.x, wn.x), fmaf(beta, sf_up.y, wn.y), fmaf(beta, sf_up.z, wn.z), fmaf(beta, sf_up.w, wn.w));
+        rf_up = f4(fmaf(-alpha, sf_up.x, rf_up.x), fmaf(-alpha, sf_up.y, rf_up.y), fmaf(-alpha, sf_up.z, rf_up.z),
+                   fmaf(-alpha, sf_up.w, rf_up.w));
+      }
+      // publish the new r planes (previous readers finished before the wait: their
+      // partials were part of it)
+#pragma unroll
+      for (int z = 0; z < TZT; ++z) sm.rp[pz0 + z][ly][xq] = plane4(r, z);
+      __syncthreads();
+      TRACE(5);
       TRACE(6);
 #ifdef RWB_TRACE
       ++trace_it;

@@ -17,7 +17,7 @@ lib = _native.load_library()
 lib.rwb_trace_dump.argtypes = [ctypes.c_void_p]
 print("rc", lib.rwb_trace_dump(buf))
 t = np.frombuffer(buf, dtype=np.int64).reshape(8, 64, 8)
-names = ["update+publish", "interior_spmv+waitF", "face_spmv", "warp_sums+push", "waitR", "scalars"]
+names = ["spmv", "warp_sums+push", "wait", "scalars", "update+publish", "-"]
 for rank in (0, 3, 7):
     d = np.diff(t[rank][:, :7], axis=1)[5:40]
     tot = (t[rank, 6:41, 0] - t[rank, 5:40, 0])
