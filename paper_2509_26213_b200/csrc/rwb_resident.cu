@@ -189,23 +189,13 @@ __device__ __forceinline__ float warp_sum(float v) {
 template <int N>
 __device__ __forceinline__ float sum_parts(const float* red) {
   static_assert(N == 64 || N == 128, "partial count");
-  // each lane of an aligned group of 8 lanes sums N/8 partials (vector loads), then
-  // three butterfly steps inside the group: every lane ends with the same total in
-  // the same order, with 3 dependent shuffles instead of 5
-  const float4* v = reinterpret_cast<const float4*>(red) + (threadIdx.x & 7) * (N / 32);
-  float s;
   if constexpr (N == 64) {
-    const float4 a = v[0], b = v[1];
-    s = ((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w));
+    const float2 v = reinterpret_cast<const float2*>(red)[threadIdx.x & 31];
+    return warp_sum(v.x + v.y);
   } else {
-    const float4 a = v[0], b = v[1], c = v[2], d = v[3];
-    s = (((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w))) +
-        (((c.x + c.y) + (c.z + c.w)) + ((d.x + d.y) + (d.z + d.w)));
+    const float4 v = reinterpret_cast<const float4*>(red)[threadIdx.x & 31];
+    return warp_sum((v.x + v.y) + (v.z + v.w));
   }
-  s += __shfl_xor_sync(0xffffffffu, s, 1);
-  s += __shfl_xor_sync(0xffffffffu, s, 2);
-  s += __shfl_xor_sync(0xffffffffu, s, 4);
-  return s;
 }
 
 // Stage the slab of `slot` into buffer `buf` (one thread issues; completes on barL[buf]).
