@@ -362,6 +362,245 @@ __global__ void __launch_bounds__(NTHREADS) setup_system_kernel(Geo g, Work w, c
 }
 
 // ---------------------------------------------------------------------------
+// Fused setup, one CTA per brick (brick x, y extents <= 32): thread (lx, ly)
+// owns a column and marches z.  Both setup kernels above compute all six
+// edge weights of every voxel twice (12 exponentials) and exchange the scale
+// factors through HBM; here each voxel computes its forward x/y/z and backward
+// y weights once (4 exponentials; backward x comes by shuffle, backward z from
+// the previous plane), the scale factors of plane a are computed one plane
+// ahead of the system of plane a-1, and the y neighbours' values travel
+// through shared memory.  Same arithmetic, same summation order (-z,+z,-y,+y,
+// -x,+x) as setup_scale/setup_system, so the outputs are bit-identical.
+constexpr int FB = 32;  // max brick extent in x and y for the fused setup
+
+__device__ __forceinline__ bool in_level(const Geo& g, int z, int y, int x) {
+  return z >= 0 && z < g.nz && y >= 0 && y < g.ny && x >= 0 && x < g.nx;
+}
+
+// What a column needs from HBM for one plane besides its intensity: its seed
+// and bound, and on the brick's x / y faces the cross-brick neighbour (a lane
+// lies on at most one x face and one y face: bricks are >= 2 wide).  Loaded
+// one plane AHEAD of use (intensity two planes ahead), so the marching loop
+// does not wait on fresh global loads.
+struct PlaneIn {
+  float B, hxI, hxB, hyI, hyB;
+  unsigned S, hxS, hyS;
+};
+
+__global__ void __launch_bounds__(FB * FB, 1) setup_brick_kernel(Geo g, Work w, const int* __restrict__ list,
+                                                                 const float* __restrict__ I,
+                                                                 const uint8_t* __restrict__ S,
+                                                                 const float* __restrict__ B, float beta, float wmin,
+                                                                 float tol2, int max_iter, int write_p) {
+  __shared__ float sI[FB][FB + 1];
+  __shared__ float sWy[FB][FB + 1];
+  __shared__ float sSc[2][FB][FB + 1];
+  __shared__ float sB[2][FB][FB + 1];
+  __shared__ unsigned char sS[2][FB][FB + 4];
+  __shared__ float red[2][FB];
+  __shared__ unsigned red_unk[FB];
+  const int slot = blockIdx.x;
+  const int brick = list ? list[slot] : slot;
+  const int hx = brick % g.gx, hy = (brick / g.gx) % g.gy, hz = brick / (g.gx * g.gy);
+  const int gz0 = g.oz + hz * g.bz, gy0 = g.oy + hy * g.by, gx0 = g.ox + hx * g.bx;
+  const int lx = threadIdx.x, ly = threadIdx.y;
+  const int gx = gx0 + lx, gy = gy0 + ly;
+  const bool col = lx < g.bx && ly < g.by;
+  const bool colin = col && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny;
+  const bool fxm = lx == 0, fxp = lx + 1 == g.bx, fym = ly == 0, fyp = ly + 1 == g.by;  // brick-face lanes
+  const bool exm = gx > 0, exp_ = gx + 1 < g.nx, eym = gy > 0, eyp = gy + 1 < g.ny;  // neighbour in level
+  // the cross-brick neighbour a face lane loads: x offset -1 / +1, y offset -nx / +nx
+  const bool hasx = (fxm && exm) || (fxp && exp_), hasy = (fym && eym) || (fyp && eyp);
+  const long long dx = fxm ? -1 : 1, dy = fym ? -(long long)g.nx : (long long)g.nx;
+  const long long sbz = (long long)g.by * g.bx;
+  const long long lcol = (long long)slot * g.bvol + (long long)ly * g.bx + lx;
+  auto wgt = [&](float a, float b) { return edge_weight(a, b, beta, wmin); };
+  auto gidx = [&](int gz) { return ((long long)gz * g.ny + gy) * g.nx + gx; };
+  auto inz = [&](int gz) { return colin && gz >= 0 && gz < g.nz; };
+  auto load_I = [&](int gz) { return inz(gz) ? __ldg(I + gidx(gz)) : 0.f; };
+  auto load_plane = [&](int gz, PlaneIn& p) {
+    p.B = p.hxI = p.hxB = p.hyI = p.hyB = 0.f;
+    p.S = 255u, p.hxS = p.hyS = 0u;
+    if (!inz(gz)) return;
+    const long long gi = gidx(gz);
+    p.S = __ldg(S + gi);
+    p.B = B ? __ldg(B + gi) : 0.f;
+    if (hasx) { p.hxI = __ldg(I + gi + dx); p.hxS = __ldg(S + gi + dx); p.hxB = B ? __ldg(B + gi + dx) : 0.f; }
+    if (hasy) { p.hyI = __ldg(I + gi + dy); p.hyS = __ldg(S + gi + dy); p.hyB = B ? __ldg(B + gi + dy) : 0.f; }
+  };
+
+  // plane -1 (cross-brick z neighbour of plane 0: values only), plane 0, intensity of plane 1.
+  // Plane -1's seed/bound start in the "plane z" slots: the first rotation moves them to z-1.
+  PlaneIn pa, pn;
+  const float I_below = load_I(gz0 - 1);
+  unsigned S_zm = 255u, S_z = 255u;
+  float B_zm = 0.f, B_z = 0.f;
+  if (inz(gz0 - 1)) {
+    S_z = __ldg(S + gidx(gz0 - 1));
+    B_z = B ? __ldg(B + gidx(gz0 - 1)) : 0.f;
+  }
+  load_plane(gz0, pa);
+  float Ia = load_I(gz0), Inext = load_I(gz0 + 1);
+  float wzf_prev = 0.f;  // forward z weight of plane a-1 (= backward z weight of plane a)
+  // system-step (plane z = a-1) registers
+  float z_wxf = 0.f, z_wyf = 0.f, z_wzf = 0.f, z_wxb = 0.f, z_wyb = 0.f, z_wzb = 0.f;
+  float sc_zm = 0.f, sc_z = 0.f, hxB_z = 0.f, hyB_z = 0.f;
+  unsigned hxS_z = 0u, hyS_z = 0u;
+  float acc_bb = 0.f, acc_rr = 0.f;
+  unsigned n_unknown = 0;
+
+  for (int a = 0; a <= g.bz; ++a) {
+    const int gza = gz0 + a;
+    const bool pa_in = a < g.bz;
+    const bool va = pa_in && inz(gza);
+    // prefetch: plane a+1 (seeds, bounds, face neighbours) and the intensity of plane a+2
+    load_plane(gza + 1, pn);
+    const float In2 = a + 2 <= g.bz ? load_I(gza + 2) : 0.f;
+    // ---------------- phase 1: weights and scale of plane a ----------------
+    float sca = 0.f, wxf = 0.f, wyf = 0.f, wzf = 0.f, wxb = 0.f, wyb = 0.f, wzb = 0.f;
+    if (pa_in) {
+      sI[ly][lx] = Ia;
+      __syncthreads();
+      const float Ixp_sh = __shfl_down_sync(0xffffffffu, Ia, 1);
+      if (va) {
+        const bool haszp = g.is3d && gza + 1 < g.nz;
+        wxf = exp_ ? wgt(Ia, fxp ? pa.hxI : Ixp_sh) : 0.f;
+        wyf = eyp ? wgt(Ia, fyp ? pa.hyI : sI[ly + 1][lx]) : 0.f;
+        wzf = haszp ? wgt(Ia, Inext) : 0.f;
+      }
+      sWy[ly][lx] = wyf;
+      __syncthreads();
+      const float wxf_sh = __shfl_up_sync(0xffffffffu, wxf, 1);
+      if (va) {
+        const bool haszm = g.is3d && gza > 0;
+        wxb = exm ? (fxm ? wgt(Ia, pa.hxI) : wxf_sh) : 0.f;
+        wyb = eym ? (fym ? wgt(Ia, pa.hyI) : sWy[ly - 1][lx]) : 0.f;
+        wzb = haszm ? (a > 0 ? wzf_prev : wgt(Ia, I_below)) : 0.f;
+        const float d = ((((wzb + wzf) + wyb) + wyf) + wxb) + wxf;
+        sca = (pa.S == 0 && d > 0.f) ? 1.0f / sqrtf(d) : 0.f;
+      }
+      sSc[a & 1][ly][lx] = sca;
+      sB[a & 1][ly][lx] = pa.B;
+      sS[a & 1][ly][lx] = (unsigned char)pa.S;
+      wzf_prev = wzf;
+      __syncthreads();
+    }
+    // ---------------- phase 2: the system of plane z = a-1 ----------------
+    const int z = a - 1;
+    if (z >= 0) {
+      const int gz = gz0 + z;
+      const bool vz = inz(gz);
+      const float scx_l = __shfl_up_sync(0xffffffffu, sc_z, 1), scx_r = __shfl_down_sync(0xffffffffu, sc_z, 1);
+      const float Bx_l = __shfl_up_sync(0xffffffffu, B_z, 1), Bx_r = __shfl_down_sync(0xffffffffu, B_z, 1);
+      const unsigned Sx_l = __shfl_up_sync(0xffffffffu, S_z, 1), Sx_r = __shfl_down_sync(0xffffffffu, S_z, 1);
+      const long long li = lcol + (long long)z * sbz;
+      float wfx = 0.f, wfy = 0.f, wfz = 0.f, r = 0.f, y = 0.f;
+      if (vz && sc_z > 0.f) {
+        ++n_unknown;
+        const int zb = z & 1;
+        const float si = sc_z, x0 = B_z;
+        float diag = 0.f, b = 0.f, acc = 0.f;
+        auto visit = [&](float wt, bool exists, bool inbrick, float sn, unsigned sv, float bn, float* fwd) {
+          if (!exists) return;
+          diag += wt;
+          if (inbrick && sn > 0.f) {
+            acc += wt * bn;
+            if (fwd) *fwd = wt * si * sn;
+          } else {
+            b += wt * (sv ? seed_value((uint8_t)sv) : bn);
+          }
+        };
+        // -z, +z (beyond the brick: the prefetched neighbour planes)
+        visit(z_wzb, g.is3d && gz > 0, z > 0, sc_zm, S_zm, B_zm, nullptr);
+        visit(z_wzf, g.is3d && gz + 1 < g.nz, z + 1 < g.bz, sca, pa.S, pa.B, &wfz);
+        // -y, +y
+        if (fym)
+          visit(z_wyb, eym, false, 0.f, hyS_z, hyB_z, nullptr);
+        else
+          visit(z_wyb, eym, true, sSc[zb][ly - 1][lx], sS[zb][ly - 1][lx], sB[zb][ly - 1][lx], nullptr);
+        if (fyp)
+          visit(z_wyf, eyp, false, 0.f, hyS_z, hyB_z, &wfy);
+        else
+          visit(z_wyf, eyp, true, sSc[zb][ly + 1][lx], sS[zb][ly + 1][lx], sB[zb][ly + 1][lx], &wfy);
+        // -x, +x
+        if (fxm)
+          visit(z_wxb, exm, false, 0.f, hxS_z, hxB_z, nullptr);
+        else
+          visit(z_wxb, exm, true, scx_l, Sx_l, Bx_l, nullptr);
+        if (fxp)
+          visit(z_wxf, exp_, false, 0.f, hxS_z, hxB_z, &wfx);
+        else
+          visit(z_wxf, exp_, true, scx_r, Sx_r, Bx_r, &wfx);
+        r = si * (b + acc - diag * x0);
+        y = x0 / si;
+        const float sb = si * b;
+        acc_bb += sb * sb;
+        acc_rr += r * r;
+      }
+      if (col) {
+        w.wx[li] = wfx;
+        w.wy[li] = wfy;
+        if (g.is3d) w.wz[li] = wfz;
+        w.r[li] = r;
+        w.y[li] = y;
+        w.sc[li] = vz ? sc_z : 0.f;
+        if (write_p) w.p0[li] = 0.f;
+      }
+    }
+    // rotate: plane a becomes plane z of the next system step
+    z_wxf = wxf, z_wyf = wyf, z_wzf = wzf, z_wxb = wxb, z_wyb = wyb, z_wzb = wzb;
+    sc_zm = sc_z;
+    sc_z = sca;
+    B_zm = B_z;
+    B_z = pa.B;
+    S_zm = S_z;
+    S_z = pa.S;
+    hxB_z = pa.hxB, hyB_z = pa.hyB, hxS_z = pa.hxS, hyS_z = pa.hyS;
+    pa = pn;
+    Ia = Inext;
+    Inext = In2;
+  }
+  // per-brick ||S b||^2, ||r0||^2 and the brick's initial decision
+  float bb = acc_bb, rr = acc_rr;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    bb += __shfl_xor_sync(0xffffffffu, bb, o);
+    rr += __shfl_xor_sync(0xffffffffu, rr, o);
+  }
+  const unsigned nu = __reduce_add_sync(0xffffffffu, n_unknown);
+  if (lx == 0) {
+    red[0][ly] = bb;
+    red[1][ly] = rr;
+    red_unk[ly] = nu;
+  }
+  __syncthreads();
+  if (ly == 0) {
+    double sbb = (double)red[0][lx], srr = (double)red[1][lx];
+    unsigned su = red_unk[lx];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      sbb += __shfl_xor_sync(0xffffffffu, sbb, o);
+      srr += __shfl_xor_sync(0xffffffffu, srr, o);
+    }
+    su = __reduce_add_sync(0xffffffffu, su);
+    if (lx == 0) {
+      if (su) atomicAdd(w.unknowns, (unsigned long long)su);
+      w.bb[slot] = sbb;
+      w.rr[slot] = srr;  // parity 0
+      int st = ST_ACTIVE;
+      if (sbb <= 0.0)
+        st = ST_ZERO;
+      else if (srr <= (double)tol2 * sbb)
+        st = ST_CONVERGED;
+      else if (max_iter <= 0)
+        st = ST_MAXITER;
+      w.state[slot] = st;
+      w.iters[slot] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // CG passes.  Persistent grid: CTAs stride over the work items
 // (active brick, tile) of the compacted active list; the list is rebuilt
 // between graph chunks, so converged bricks stop costing launches.
@@ -895,10 +1134,15 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
   const unsigned sgrid = (unsigned)((long long)nb * g.tiles);
   const unsigned setup_grid = (unsigned)((long long)nb * setup_tiles(g));
   dim3 block(TX, TY);
-  setup_scale_kernel<<<setup_grid, block, 0, st>>>(g, w, list, intensity, seeds, params->beta, params->min_weight);
   const bool resident = use_resident(g, total, params->flags);
-  setup_system_kernel<<<setup_grid, block, 0, st>>>(g, w, list, intensity, seeds, bound, params->beta,
-                                                    params->min_weight, tol2, max_iter, resident ? 0 : 1);
+  if (g.bx <= FB && g.by <= FB && g.bx >= 2 && g.by >= 2 && !(params->flags & RWB_SOLVE_SETUP2)) {
+    setup_brick_kernel<<<nb, dim3(FB, FB), 0, st>>>(g, w, list, intensity, seeds, bound, params->beta,
+                                                     params->min_weight, tol2, max_iter, resident ? 0 : 1);
+  } else {
+    setup_scale_kernel<<<setup_grid, block, 0, st>>>(g, w, list, intensity, seeds, params->beta, params->min_weight);
+    setup_system_kernel<<<setup_grid, block, 0, st>>>(g, w, list, intensity, seeds, bound, params->beta,
+                                                      params->min_weight, tol2, max_iter, resident ? 0 : 1);
+  }
   advance_kernel<<<1, 1024, 0, st>>>(w, nb, 0);
   RWB_LAUNCH_CHECK("setup kernels");
   count_launches(3);

@@ -193,6 +193,8 @@ def _flags(cfg: RWConfig) -> int:
         f |= _native.SOLVE_STREAMING
     if not cfg.cooperative:
         f |= _native.SOLVE_NO_COOP
+    if not cfg.fused_setup:
+        f |= _native.SOLVE_SETUP2
     if cfg.cluster == 16:
         f |= _native.SOLVE_CLUSTER16
     elif cfg.cluster == 512:  # 8-CTA clusters, 512 threads per CTA

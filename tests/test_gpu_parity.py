@@ -334,3 +334,16 @@ def test_resident_cluster_variants(rng, cluster):
     out, st = device.solve_level(cuda(vol), cuda(seeds), (32, 32, 32), cuda(bound), cfg)
     assert st["path"] == 1 and st["not_converged"] == 0
     assert_rw_parity(host(out), ref)
+
+
+@pytest.mark.parametrize("shape,brick", [((70, 40, 33), (32, 32, 32)), ((48, 40, 36), (16, 16, 16)),
+                                         ((90, 70), (32, 32)), ((20, 18, 16), (20, 18, 16))])
+def test_fused_setup_matches_two_kernel_setup(rng, shape, brick):
+    vol, seeds = _random_case(rng, shape)
+    whole = tuple(brick) == tuple(shape)
+    bound = None if whole else cuda(rng.random(shape).astype(np.float32))
+    a, sa = device.solve_level(cuda(vol), cuda(seeds), brick, bound, GPU_CFG)
+    b, sb = device.solve_level(cuda(vol), cuda(seeds), brick, bound,
+                               RWConfig(tol=GPU_CFG.tol, max_iter=GPU_CFG.max_iter, fused_setup=False))
+    assert np.abs(host(a) - host(b)).max() <= 2e-6
+    assert sa["unknowns"] == sb["unknowns"]
