@@ -24,9 +24,13 @@ int cuda_fail(cudaError_t err, const char* what);
     if (err__ != cudaSuccess) return ::rwb::cuda_fail(err__, #call); \
   } while (0)
 
+// RWB_DEBUG_SYNC=1 in the environment: synchronise after every checked launch
+// so an asynchronous fault is reported at the launch that caused it.
+bool debug_sync();
 #define RWB_LAUNCH_CHECK(what)                           \
   do {                                                   \
     cudaError_t err__ = cudaGetLastError();              \
+    if (err__ == cudaSuccess && ::rwb::debug_sync()) err__ = cudaDeviceSynchronize(); \
     if (err__ != cudaSuccess) return ::rwb::cuda_fail(err__, what); \
   } while (0)
 

@@ -9,6 +9,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "rwb_common.cuh"
@@ -30,6 +31,14 @@ int fail(int code, const std::string& msg) {
 int cuda_fail(cudaError_t err, const char* what) {
   g_last_error = std::string(what) + ": " + cudaGetErrorName(err) + " (" + cudaGetErrorString(err) + ")";
   return RWB_ERR_CUDA;
+}
+
+bool debug_sync() {
+  static const bool on = [] {
+    const char* e = std::getenv("RWB_DEBUG_SYNC");
+    return e && *e && *e != '0';
+  }();
+  return on;
 }
 
 int shape_from(int32_t ndim, const int64_t* size, Shape3* out) {

@@ -25,6 +25,8 @@
 // last CTA of a brick to finish (atomic ticket) sums the partials in a fixed
 // order in float64.  Results are therefore independent of which other bricks
 // share the launch (multi-GPU sharding gives bit-identical bytes).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -363,7 +365,7 @@ __global__ void __launch_bounds__(NTHREADS) setup_system_kernel(Geo g, Work w, c
 
 // ---------------------------------------------------------------------------
 // Fused setup, one CTA per brick (brick x, y extents <= 32): thread (lx, ly)
-// owns a column and marches z.  Both setup kernels above compute all six
+// owns a column and marches z.  The two setup kernels above compute all six
 // edge weights of every voxel twice (12 exponentials) and exchange the scale
 // factors through HBM; here each voxel computes its forward x/y/z and backward
 // y weights once (4 exponentials; backward x comes by shuffle, backward z from
@@ -371,134 +373,181 @@ __global__ void __launch_bounds__(NTHREADS) setup_system_kernel(Geo g, Work w, c
 // ahead of the system of plane a-1, and the y neighbours' values travel
 // through shared memory.  Same arithmetic, same summation order (-z,+z,-y,+y,
 // -x,+x) as setup_scale/setup_system, so the outputs are bit-identical.
-constexpr int FB = 32;  // max brick extent in x and y for the fused setup
+//
+// Inputs arrive by TMA: for every plane, one elected thread loads the
+// tile of intensity, bound and seeds that covers the brick's plane plus its
+// one-voxel x/y halo (the x start rounded down to 16 B: TMA tile boxes must
+// start 16 B aligned), out-of-level parts zero-filled by the tensor map, into
+// a ring of SR stages, each completing on its own mbarrier, SR-4 planes ahead
+// of use.  One CTA per SM marches 33 planes with two barriers each, so it is
+// the ring depth, not the warps, that keeps enough bytes in flight to stream
+// at HBM rate (a one-plane register prefetch reached about a fifth of it).
+constexpr int FB = 32;                 // max brick extent in x and y for the fused setup
+constexpr int SR = 8;                  // ring stages (planes)
+constexpr int SRX = 40, SRY = FB + 2;  // f32 tile box: x [gx0-4, gx0+36), y [gy0-1, gy0+33)
+constexpr int SRXS = 64;               // u8 seed tile box: x [gx0-16, gx0+48)
+constexpr int SRX0 = 4, SRXS0 = 16;    // tile column of x = gx0
+constexpr int SR_F32 = ((SRX * SRY * 4 + 127) / 128) * 128;  // bytes per f32 stage (128 B aligned)
+constexpr int SR_U8 = ((SRXS * SRY + 127) / 128) * 128;
+constexpr int SETUP_MAX_TILES = 256;  // (bz / STZ) * (by / TY) tiles of the two-kernel reduction order
 
-__device__ __forceinline__ bool in_level(const Geo& g, int z, int y, int x) {
-  return z >= 0 && z < g.nz && y >= 0 && y < g.ny && x >= 0 && x < g.nx;
-}
-
-// What a column needs from HBM for one plane besides its intensity: its seed
-// and bound, and on the brick's x / y faces the cross-brick neighbour (a lane
-// lies on at most one x face and one y face: bricks are >= 2 wide).  Loaded
-// one plane AHEAD of use (intensity two planes ahead), so the marching loop
-// does not wait on fresh global loads.
-struct PlaneIn {
-  float B, hxI, hxB, hyI, hyB;
-  unsigned S, hxS, hyS;
+struct SetupSmem {
+  float I[SR][SR_F32 / 4];
+  float B[SR][SR_F32 / 4];
+  unsigned char S[SR][SR_U8];
+  unsigned long long bar[SR];
+  float Wy[FB][FB + 1];
+  float Sc[3][FB][FB + 1];
+  float2 rowpart[FB];          // per-row (warp) sums of the current 4-plane chunk
+  float2 tpart[SETUP_MAX_TILES];  // per setup-tile sums, in setup_system_kernel's tile order
+  unsigned red_unk[FB];
 };
 
-__global__ void __launch_bounds__(FB * FB, 1) setup_brick_kernel(Geo g, Work w, const int* __restrict__ list,
-                                                                 const float* __restrict__ I,
-                                                                 const uint8_t* __restrict__ S,
-                                                                 const float* __restrict__ B, float beta, float wmin,
-                                                                 float tol2, int max_iter, int write_p) {
-  __shared__ float sI[FB][FB + 1];
-  __shared__ float sWy[FB][FB + 1];
-  __shared__ float sSc[2][FB][FB + 1];
-  __shared__ float sB[2][FB][FB + 1];
-  __shared__ unsigned char sS[2][FB][FB + 4];
-  __shared__ float red[2][FB];
-  __shared__ unsigned red_unk[FB];
+struct SetupMaps {
+  CUtensorMap I, B, S;  // 3-D tiled maps over the level (x fastest)
+};
+
+__device__ __forceinline__ void setup_tma_plane(const SetupMaps& m, SetupSmem& sm, bool has_b, int stage, int gx0,
+                                                int y, int z) {
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&sm.bar[stage]);
+  const uint32_t bytes = (has_b ? 2u : 1u) * (SRX * SRY * 4) + SRXS * SRY;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  int x = gx0 - SRX0;
+  auto load = [&](const CUtensorMap* map, void* dst) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(bar)
+        : "memory");
+  };
+  load(&m.I, sm.I[stage]);
+  if (has_b) load(&m.B, sm.B[stage]);
+  x = gx0 - SRXS0;
+  load(&m.S, sm.S[stage]);
+}
+
+__device__ __forceinline__ void setup_wait(SetupSmem& sm, int stage, uint32_t parity) {
+  const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&sm.bar[stage]);
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra.uni WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(FB * FB, 1) setup_brick_kernel(const __grid_constant__ SetupMaps maps, Geo g,
+                                                                 Work w, const int* __restrict__ list, bool has_b,
+                                                                 float beta, float wmin, float tol2, int max_iter,
+                                                                 int write_p) {
+  extern __shared__ __align__(128) unsigned char setup_smem_raw[];
+  SetupSmem& sm = *reinterpret_cast<SetupSmem*>(setup_smem_raw);
   const int slot = blockIdx.x;
   const int brick = list ? list[slot] : slot;
   const int hx = brick % g.gx, hy = (brick / g.gx) % g.gy, hz = brick / (g.gx * g.gy);
   const int gz0 = g.oz + hz * g.bz, gy0 = g.oy + hy * g.by, gx0 = g.ox + hx * g.bx;
   const int lx = threadIdx.x, ly = threadIdx.y;
+  const int tid = ly * FB + lx;
   const int gx = gx0 + lx, gy = gy0 + ly;
   const bool col = lx < g.bx && ly < g.by;
   const bool colin = col && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny;
   const bool fxm = lx == 0, fxp = lx + 1 == g.bx, fym = ly == 0, fyp = ly + 1 == g.by;  // brick-face lanes
   const bool exm = gx > 0, exp_ = gx + 1 < g.nx, eym = gy > 0, eyp = gy + 1 < g.ny;  // neighbour in level
-  // the cross-brick neighbour a face lane loads: x offset -1 / +1, y offset -nx / +nx
-  const bool hasx = (fxm && exm) || (fxp && exp_), hasy = (fym && eym) || (fyp && eyp);
-  const long long dx = fxm ? -1 : 1, dy = fym ? -(long long)g.nx : (long long)g.nx;
   const long long sbz = (long long)g.by * g.bx;
   const long long lcol = (long long)slot * g.bvol + (long long)ly * g.bx + lx;
   auto wgt = [&](float a, float b) { return edge_weight(a, b, beta, wmin); };
-  auto gidx = [&](int gz) { return ((long long)gz * g.ny + gy) * g.nx + gx; };
   auto inz = [&](int gz) { return colin && gz >= 0 && gz < g.nz; };
-  auto load_I = [&](int gz) { return inz(gz) ? __ldg(I + gidx(gz)) : 0.f; };
-  auto load_plane = [&](int gz, PlaneIn& p) {
-    p.B = p.hxI = p.hxB = p.hyI = p.hyB = 0.f;
-    p.S = 255u, p.hxS = p.hyS = 0u;
-    if (!inz(gz)) return;
-    const long long gi = gidx(gz);
-    p.S = __ldg(S + gi);
-    p.B = B ? __ldg(B + gi) : 0.f;
-    if (hasx) { p.hxI = __ldg(I + gi + dx); p.hxS = __ldg(S + gi + dx); p.hxB = B ? __ldg(B + gi + dx) : 0.f; }
-    if (hasy) { p.hyI = __ldg(I + gi + dy); p.hyS = __ldg(S + gi + dy); p.hyB = B ? __ldg(B + gi + dy) : 0.f; }
+  // plane p in [-1, bz] lives in stage (p + 1) % SR, use (p + 1) / SR; tile row ty = voxel y gy0-1+ty
+  auto stage_of = [](int p) { return (p + 1) % SR; };
+  auto tI = [&](int p, int dy, int dx) { return sm.I[stage_of(p)][(ly + 1 + dy) * SRX + SRX0 + lx + dx]; };
+  auto tB = [&](int p, int dy, int dx) {
+    return has_b ? sm.B[stage_of(p)][(ly + 1 + dy) * SRX + SRX0 + lx + dx] : 0.f;
   };
+  auto tS = [&](int p, int dy, int dx) { return (unsigned)sm.S[stage_of(p)][(ly + 1 + dy) * SRXS + SRXS0 + lx + dx]; };
+  auto wait_plane = [&](int p) { setup_wait(sm, stage_of(p), (uint32_t)(((p + 1) / SR) & 1)); };
+  const int last = g.bz;  // planes -1 .. bz are loaded
 
-  // plane -1 (cross-brick z neighbour of plane 0: values only), plane 0, intensity of plane 1.
-  // Plane -1's seed/bound start in the "plane z" slots: the first rotation moves them to z-1.
-  PlaneIn pa, pn;
-  const float I_below = load_I(gz0 - 1);
-  unsigned S_zm = 255u, S_z = 255u;
-  float B_zm = 0.f, B_z = 0.f;
-  if (inz(gz0 - 1)) {
-    S_z = __ldg(S + gidx(gz0 - 1));
-    B_z = B ? __ldg(B + gidx(gz0 - 1)) : 0.f;
+  if (tid == 0) {
+    for (int s = 0; s < SR; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&sm.bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int p = -1; p <= min(last, SR - 4); ++p) setup_tma_plane(maps, sm, has_b, stage_of(p), gx0, gy0 - 1, gz0 + p);
   }
-  load_plane(gz0, pa);
-  float Ia = load_I(gz0), Inext = load_I(gz0 + 1);
+  __syncthreads();
+  wait_plane(-1);
+  wait_plane(0);
+
   float wzf_prev = 0.f;  // forward z weight of plane a-1 (= backward z weight of plane a)
-  // system-step (plane z = a-1) registers
+  // system-step (plane z = a-1) registers: its weights and the scale factors of z-1, z
   float z_wxf = 0.f, z_wyf = 0.f, z_wzf = 0.f, z_wxb = 0.f, z_wyb = 0.f, z_wzb = 0.f;
-  float sc_zm = 0.f, sc_z = 0.f, hxB_z = 0.f, hyB_z = 0.f;
-  unsigned hxS_z = 0u, hyS_z = 0u;
+  float sc_zm = 0.f, sc_z = 0.f;
   float acc_bb = 0.f, acc_rr = 0.f;
   unsigned n_unknown = 0;
+  // ||S b||^2 and ||r0||^2 are reduced in exactly the order of setup_system_kernel
+  // (per thread over a 4-plane chunk, warp tree per row, 8 rows in sequence per
+  // tile, tiles in float64 by brick_reduce), so both setups give the same bits
+  // and the CG that starts from them the same trajectory.
+  const int ty8 = (g.by + TY - 1) / TY;
+  int pending_chunk = -1;
+  auto tile_sums = [&]() {  // after a barrier: rows of the flushed chunk -> its tiles
+    if (pending_chunk >= 0 && tid < ty8) {
+      float2 s = make_float2(0.f, 0.f);
+      for (int r8 = 0; r8 < TY; ++r8) {
+        s.x += sm.rowpart[tid * TY + r8].x;
+        s.y += sm.rowpart[tid * TY + r8].y;
+      }
+      sm.tpart[pending_chunk * ty8 + tid] = s;
+    }
+    if (pending_chunk >= 0) __syncthreads();  // rowpart free for the next flush (uniform branch)
+    pending_chunk = -1;
+  };
 
   for (int a = 0; a <= g.bz; ++a) {
+    tile_sums();
     const int gza = gz0 + a;
     const bool pa_in = a < g.bz;
     const bool va = pa_in && inz(gza);
-    // prefetch: plane a+1 (seeds, bounds, face neighbours) and the intensity of plane a+2
-    load_plane(gza + 1, pn);
-    const float In2 = a + 2 <= g.bz ? load_I(gza + 2) : 0.f;
+    // refill: plane a+SR-3 replaces plane a-3, whose last reader (step a-1) every thread has left
+    if (tid == 0 && a + SR - 3 <= last)
+      setup_tma_plane(maps, sm, has_b, stage_of(a + SR - 3), gx0, gy0 - 1, gz0 + a + SR - 3);
+    if (a + 1 <= last) wait_plane(a + 1);
     // ---------------- phase 1: weights and scale of plane a ----------------
     float sca = 0.f, wxf = 0.f, wyf = 0.f, wzf = 0.f, wxb = 0.f, wyb = 0.f, wzb = 0.f;
     if (pa_in) {
-      sI[ly][lx] = Ia;
-      __syncthreads();
-      const float Ixp_sh = __shfl_down_sync(0xffffffffu, Ia, 1);
+      const float Ia = tI(a, 0, 0);
       if (va) {
         const bool haszp = g.is3d && gza + 1 < g.nz;
-        wxf = exp_ ? wgt(Ia, fxp ? pa.hxI : Ixp_sh) : 0.f;
-        wyf = eyp ? wgt(Ia, fyp ? pa.hyI : sI[ly + 1][lx]) : 0.f;
-        wzf = haszp ? wgt(Ia, Inext) : 0.f;
+        wxf = exp_ ? wgt(Ia, tI(a, 0, 1)) : 0.f;
+        wyf = eyp ? wgt(Ia, tI(a, 1, 0)) : 0.f;
+        wzf = haszp ? wgt(Ia, tI(a + 1, 0, 0)) : 0.f;
       }
-      sWy[ly][lx] = wyf;
+      sm.Wy[ly][lx] = wyf;
       __syncthreads();
       const float wxf_sh = __shfl_up_sync(0xffffffffu, wxf, 1);
       if (va) {
         const bool haszm = g.is3d && gza > 0;
-        wxb = exm ? (fxm ? wgt(Ia, pa.hxI) : wxf_sh) : 0.f;
-        wyb = eym ? (fym ? wgt(Ia, pa.hyI) : sWy[ly - 1][lx]) : 0.f;
-        wzb = haszm ? (a > 0 ? wzf_prev : wgt(Ia, I_below)) : 0.f;
+        wxb = exm ? (fxm ? wgt(Ia, tI(a, 0, -1)) : wxf_sh) : 0.f;
+        wyb = eym ? (fym ? wgt(Ia, tI(a, -1, 0)) : sm.Wy[ly - 1][lx]) : 0.f;
+        wzb = haszm ? (a > 0 ? wzf_prev : wgt(Ia, tI(-1, 0, 0))) : 0.f;
         const float d = ((((wzb + wzf) + wyb) + wyf) + wxb) + wxf;
-        sca = (pa.S == 0 && d > 0.f) ? 1.0f / sqrtf(d) : 0.f;
+        sca = (tS(a, 0, 0) == 0 && d > 0.f) ? 1.0f / sqrtf(d) : 0.f;
       }
-      sSc[a & 1][ly][lx] = sca;
-      sB[a & 1][ly][lx] = pa.B;
-      sS[a & 1][ly][lx] = (unsigned char)pa.S;
+      sm.Sc[a % 3][ly][lx] = sca;
       wzf_prev = wzf;
-      __syncthreads();
     }
     // ---------------- phase 2: the system of plane z = a-1 ----------------
     const int z = a - 1;
     if (z >= 0) {
       const int gz = gz0 + z;
       const bool vz = inz(gz);
-      const float scx_l = __shfl_up_sync(0xffffffffu, sc_z, 1), scx_r = __shfl_down_sync(0xffffffffu, sc_z, 1);
-      const float Bx_l = __shfl_up_sync(0xffffffffu, B_z, 1), Bx_r = __shfl_down_sync(0xffffffffu, B_z, 1);
-      const unsigned Sx_l = __shfl_up_sync(0xffffffffu, S_z, 1), Sx_r = __shfl_down_sync(0xffffffffu, S_z, 1);
       const long long li = lcol + (long long)z * sbz;
       float wfx = 0.f, wfy = 0.f, wfz = 0.f, r = 0.f, y = 0.f;
       if (vz && sc_z > 0.f) {
         ++n_unknown;
-        const int zb = z & 1;
-        const float si = sc_z, x0 = B_z;
+        const int zs = z % 3;
+        const float si = sc_z, x0 = tB(z, 0, 0);
         float diag = 0.f, b = 0.f, acc = 0.f;
         auto visit = [&](float wt, bool exists, bool inbrick, float sn, unsigned sv, float bn, float* fwd) {
           if (!exists) return;
@@ -510,32 +559,30 @@ __global__ void __launch_bounds__(FB * FB, 1) setup_brick_kernel(Geo g, Work w, 
             b += wt * (sv ? seed_value((uint8_t)sv) : bn);
           }
         };
-        // -z, +z (beyond the brick: the prefetched neighbour planes)
-        visit(z_wzb, g.is3d && gz > 0, z > 0, sc_zm, S_zm, B_zm, nullptr);
-        visit(z_wzf, g.is3d && gz + 1 < g.nz, z + 1 < g.bz, sca, pa.S, pa.B, &wfz);
-        // -y, +y
-        if (fym)
-          visit(z_wyb, eym, false, 0.f, hyS_z, hyB_z, nullptr);
-        else
-          visit(z_wyb, eym, true, sSc[zb][ly - 1][lx], sS[zb][ly - 1][lx], sB[zb][ly - 1][lx], nullptr);
-        if (fyp)
-          visit(z_wyf, eyp, false, 0.f, hyS_z, hyB_z, &wfy);
-        else
-          visit(z_wyf, eyp, true, sSc[zb][ly + 1][lx], sS[zb][ly + 1][lx], sB[zb][ly + 1][lx], &wfy);
-        // -x, +x
-        if (fxm)
-          visit(z_wxb, exm, false, 0.f, hxS_z, hxB_z, nullptr);
-        else
-          visit(z_wxb, exm, true, scx_l, Sx_l, Bx_l, nullptr);
-        if (fxp)
-          visit(z_wxf, exp_, false, 0.f, hxS_z, hxB_z, &wfx);
-        else
-          visit(z_wxf, exp_, true, scx_r, Sx_r, Bx_r, &wfx);
+        // -z, +z (beyond the brick: the neighbour planes of the ring)
+        visit(z_wzb, g.is3d && gz > 0, z > 0, sc_zm, tS(z - 1, 0, 0), tB(z - 1, 0, 0), nullptr);
+        visit(z_wzf, g.is3d && gz + 1 < g.nz, z + 1 < g.bz, sca, tS(a, 0, 0), tB(a, 0, 0), &wfz);
+        // -y, +y, -x, +x (beyond the brick face: the tile halo)
+        visit(z_wyb, eym, !fym, fym ? 0.f : sm.Sc[zs][ly - 1][lx], tS(z, -1, 0), tB(z, -1, 0), nullptr);
+        visit(z_wyf, eyp, !fyp, fyp ? 0.f : sm.Sc[zs][ly + 1][lx], tS(z, 1, 0), tB(z, 1, 0), &wfy);
+        visit(z_wxb, exm, !fxm, fxm ? 0.f : sm.Sc[zs][ly][lx - 1], tS(z, 0, -1), tB(z, 0, -1), nullptr);
+        visit(z_wxf, exp_, !fxp, fxp ? 0.f : sm.Sc[zs][ly][lx + 1], tS(z, 0, 1), tB(z, 0, 1), &wfx);
         r = si * (b + acc - diag * x0);
         y = x0 / si;
         const float sb = si * b;
         acc_bb += sb * sb;
         acc_rr += r * r;
+      }
+      if (z % STZ == STZ - 1 || z == g.bz - 1) {  // chunk complete: row sums
+        float bb = acc_bb, rr = acc_rr;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          bb += __shfl_xor_sync(0xffffffffu, bb, o);
+          rr += __shfl_xor_sync(0xffffffffu, rr, o);
+        }
+        if (lx == 0) sm.rowpart[ly] = make_float2(bb, rr);
+        acc_bb = acc_rr = 0.f;
+        pending_chunk = z / STZ;
       }
       if (col) {
         w.wx[li] = wfx;
@@ -551,38 +598,31 @@ __global__ void __launch_bounds__(FB * FB, 1) setup_brick_kernel(Geo g, Work w, 
     z_wxf = wxf, z_wyf = wyf, z_wzf = wzf, z_wxb = wxb, z_wyb = wyb, z_wzb = wzb;
     sc_zm = sc_z;
     sc_z = sca;
-    B_zm = B_z;
-    B_z = pa.B;
-    S_zm = S_z;
-    S_z = pa.S;
-    hxB_z = pa.hxB, hyB_z = pa.hyB, hxS_z = pa.hxS, hyS_z = pa.hyS;
-    pa = pn;
-    Ia = Inext;
-    Inext = In2;
+    __syncthreads();
   }
-  // per-brick ||S b||^2, ||r0||^2 and the brick's initial decision
-  float bb = acc_bb, rr = acc_rr;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    bb += __shfl_xor_sync(0xffffffffu, bb, o);
-    rr += __shfl_xor_sync(0xffffffffu, rr, o);
-  }
+  // per-brick ||S b||^2, ||r0||^2 (brick_reduce's order) and the brick's initial decision
+  tile_sums();
   const unsigned nu = __reduce_add_sync(0xffffffffu, n_unknown);
-  if (lx == 0) {
-    red[0][ly] = bb;
-    red[1][ly] = rr;
-    red_unk[ly] = nu;
-  }
+  if (lx == 0) sm.red_unk[ly] = nu;
   __syncthreads();
   if (ly == 0) {
-    double sbb = (double)red[0][lx], srr = (double)red[1][lx];
-    unsigned su = red_unk[lx];
+    const int tiles = ((g.bz + STZ - 1) / STZ) * ty8;
+    double sbb = 0.0, srr = 0.0;
+    if (tiles == 1) {
+      sbb = (double)sm.tpart[0].x;
+      srr = (double)sm.tpart[0].y;
+    } else {
+      for (int i = lx; i < tiles; i += 32) {
+        sbb += (double)sm.tpart[i].x;
+        srr += (double)sm.tpart[i].y;
+      }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      sbb += __shfl_xor_sync(0xffffffffu, sbb, o);
-      srr += __shfl_xor_sync(0xffffffffu, srr, o);
+      for (int o = 16; o > 0; o >>= 1) {
+        sbb += __shfl_xor_sync(0xffffffffu, sbb, o);
+        srr += __shfl_xor_sync(0xffffffffu, srr, o);
+      }
     }
-    su = __reduce_add_sync(0xffffffffu, su);
+    unsigned su = __reduce_add_sync(0xffffffffu, sm.red_unk[lx]);
     if (lx == 0) {
       if (su) atomicAdd(w.unknowns, (unsigned long long)su);
       w.bb[slot] = sbb;
@@ -598,6 +638,38 @@ __global__ void __launch_bounds__(FB * FB, 1) setup_brick_kernel(Geo g, Work w, 
       w.iters[slot] = 0;
     }
   }
+}
+
+// Tensor maps for the fused setup; false when the level's layout does not
+// meet TMA's rules (16 B aligned bases, row pitches and box x starts) — the
+// caller then uses the two-kernel setup.
+static bool make_setup_maps(const Geo& g, const float* I, const uint8_t* S, const float* B, SetupMaps* m) {
+  if (g.bx > FB || g.by > FB || ((g.bz + STZ - 1) / STZ) * ((g.by + TY - 1) / TY) > SETUP_MAX_TILES) return false;
+  if (g.ox % 16 || (g.gx > 1 && g.bx % 16)) return false;  // every brick's x start 16-voxel aligned
+  if (g.nx % 16 || ((uintptr_t)I & 15) || ((uintptr_t)S & 15) || ((uintptr_t)B & 15)) return false;
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  auto enc = [&](CUtensorMap* map, const void* base, CUtensorMapDataType dt, int esz, int boxx) {
+    const cuuint64_t dims[3] = {(cuuint64_t)g.nx, (cuuint64_t)g.ny, (cuuint64_t)g.nz};
+    const cuuint64_t strides[2] = {(cuuint64_t)g.nx * esz, (cuuint64_t)g.nx * g.ny * esz};
+    const cuuint32_t box[3] = {(cuuint32_t)boxx, (cuuint32_t)SRY, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    return encode(map, dt, 3, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  };
+  std::memset(m, 0, sizeof(*m));
+  if (!enc(&m->I, I, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, SRX)) return false;
+  if (B && !enc(&m->B, B, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, SRX)) return false;
+  if (!enc(&m->S, S, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1, SRXS)) return false;
+  return true;
 }
 
 // ---------------------------------------------------------------------------
@@ -1135,9 +1207,18 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
   const unsigned setup_grid = (unsigned)((long long)nb * setup_tiles(g));
   dim3 block(TX, TY);
   const bool resident = use_resident(g, total, params->flags);
-  if (g.bx <= FB && g.by <= FB && g.bx >= 2 && g.by >= 2 && !(params->flags & RWB_SOLVE_SETUP2)) {
-    setup_brick_kernel<<<nb, dim3(FB, FB), 0, st>>>(g, w, list, intensity, seeds, bound, params->beta,
-                                                     params->min_weight, tol2, max_iter, resident ? 0 : 1);
+  SetupMaps maps;
+  if (!(params->flags & RWB_SOLVE_SETUP2) && make_setup_maps(g, intensity, seeds, bound, &maps)) {
+    static bool smem_set = false;
+    if (!smem_set) {
+      RWB_CUDA(cudaFuncSetAttribute(setup_brick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sizeof(SetupSmem)));
+      smem_set = true;
+    }
+    setup_brick_kernel<<<nb, dim3(FB, FB), sizeof(SetupSmem), st>>>(maps, g, w, list, bound != nullptr, params->beta,
+                                                                   params->min_weight, tol2, max_iter,
+                                                                   resident ? 0 : 1);
+    RWB_LAUNCH_CHECK("fused setup kernel");
   } else {
     setup_scale_kernel<<<setup_grid, block, 0, st>>>(g, w, list, intensity, seeds, params->beta, params->min_weight);
     setup_system_kernel<<<setup_grid, block, 0, st>>>(g, w, list, intensity, seeds, bound, params->beta,
@@ -1166,7 +1247,8 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
     RWB_CUDA(cudaEventCreate(&ev0));
     RWB_CUDA(cudaEventCreate(&ev1));
     RWB_CUDA(cudaEventRecord(ev0, st));
-    rc = launch_resident3d(ra, nb, (params->flags & RWB_SOLVE_CLUSTER16) ? 16 : ((params->flags & RWB_SOLVE_SPLIT_Z) ? 512 : 8), st);
+    rc = launch_resident3d(ra, nb, (params->flags & RWB_SOLVE_CLUSTER16) ? 16 : ((params->flags & RWB_SOLVE_SPLIT_Z) ? 512 : 8),
+                           (params->flags & RWB_SOLVE_PIPELINED) != 0, st);
     if (rc) {
       cudaEventDestroy(ev0);
       cudaEventDestroy(ev1);

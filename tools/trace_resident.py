@@ -9,7 +9,8 @@ from paper_2509_26213_b200 import device, synthetic
 from paper_2509_26213_b200.config import RWConfig
 shape = (256, 256, 256)
 vol = synthetic.phantom_device(shape); sd = synthetic.seeds_device(shape, "S1")
-res = device.hierarchical_random_walker(vol, sd, (32, 32, 32), 2, RWConfig())
+PIPE = "pipe" in sys.argv[1:]
+res = device.hierarchical_random_walker(vol, sd, (32, 32, 32), 2, RWConfig(pipelined=PIPE))
 torch.cuda.synchronize()
 print(res.stats[0])
 buf = (ctypes.c_longlong * (8 * 64 * 8))()
@@ -18,8 +19,12 @@ lib.rwb_trace_dump.argtypes = [ctypes.c_void_p]
 print("rc", lib.rwb_trace_dump(buf))
 t = np.frombuffer(buf, dtype=np.int64).reshape(8, 64, 8)
 names = ["spmv", "warp_sums+push", "wait", "scalars", "update+publish", "-"]
+ncol = 7
+if PIPE:
+    names = ["push_partials", "spmv+push_faces", "wait", "scalars", "update+faces+sync"]
+    ncol = 6
 for rank in (0, 3, 7):
-    d = np.diff(t[rank][:, :7], axis=1)[5:40]
+    d = np.diff(t[rank][:, :ncol], axis=1)[5:40]
     tot = (t[rank, 6:41, 0] - t[rank, 5:40, 0])
     print("rank", rank, "median cycles per phase", dict(zip(names, np.median(d, axis=0).astype(int))), "iter", int(np.median(tot)))
 st = t[:, 5:40, 0]
