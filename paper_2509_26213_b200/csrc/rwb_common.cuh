@@ -47,13 +47,21 @@ void count_launches(long long n);
 
 inline unsigned ceil_div_u(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 
-// Edge weight of the Grady random walker: max(exp(-beta*(a-b)^2), w_min).
-// __expf (one MUFU.EX2): relative error ~|beta d^2| * 2^-23, i.e. <= 1e-6 for
-// every weight above w_min = 1e-6, far inside the 1e-4 probability bar; it is
-// symmetric in (a, b), so both endpoints of an edge compute identical bits.
+// Edge weight of the Grady random walker: max(exp(-beta*(a-b)^2), w_min) as
+// max(2^((d * c) * d), w_min) with c = -beta log2(e), one MUFU.EX2 (.ftz: an
+// output below 2^-126 is flushed to 0, then clamped to w_min anyway).  Relative
+// error ~|beta d^2| * 2^-22, i.e. a few 1e-6 for every weight above
+// w_min = 1e-6, far inside the 1e-4 probability bar; it is symmetric in (a, b),
+// so both endpoints of an edge compute identical bits.
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float edge_weight(float a, float b, float beta, float wmin) {
-  float d = a - b;
-  return fmaxf(__expf(-beta * d * d), wmin);
+  const float c = -beta * 1.44269504088896341f;
+  const float d = a - b;
+  return fmaxf(ex2_ftz((d * c) * d), wmin);
 }
 
 }  // namespace rwb

@@ -195,6 +195,17 @@ __device__ __forceinline__ bool brick_reduce(const Geo& g, const Work& w, int sl
 // ---------------------------------------------------------------------------
 // setup
 
+__device__ __forceinline__ float seed_value(uint8_t s) { return s == 1 ? 1.0f : 0.0f; }
+
+// Shared by both setups (bit-identical systems).  s = diag^-1/2 by MUFU.RSQ
+// (~1 ulp; the float64 oracle is matched to the solve tolerance, not bits);
+// r0 = s (b + acc - diag x0); y0 = x0 / s = x0 diag s.
+__device__ __forceinline__ float jacobi_scale(float d) { return rsqrtf(d); }
+__device__ __forceinline__ float initial_residual(float si, float b, float acc, float diag, float x0) {
+  return si * fmaf(-diag, x0, b + acc);
+}
+__device__ __forceinline__ float initial_y(float x0, float si, float diag) { return x0 * (diag * si); }
+
 // Neighbour addressing of one voxel for the setup kernels: the six neighbours in
 // the order -z,+z,-y,+y,-x,+x, whether each is in the level and in the brick,
 // and clamped (always valid) level / brick-local indices, so every neighbour
@@ -256,14 +267,14 @@ __global__ void __launch_bounds__(NTHREADS) setup_scale_kernel(Geo g, Work w, co
         float d = 0.f;
 #pragma unroll
         for (int e = 0; e < 6; ++e) d += n.lev[e] ? edge_weight(ci, In[e], beta, wmin) : 0.f;
-        s = d > 0.f ? 1.0f / sqrtf(d) : 0.f;
+        s = d > 0.f ? jacobi_scale(d) : 0.f;
       }
     }
     sc[li] = s;
   }
 }
 
-__device__ __forceinline__ float seed_value(uint8_t s) { return s == 1 ? 1.0f : 0.0f; }
+
 
 // K2: scaled forward weights, r0 = S(b - L x0), y0 = x0 / s, (p = 0); per-brick
 // ||S b||^2 and ||r0||^2 and the brick's initial decision.
@@ -318,14 +329,14 @@ __global__ void __launch_bounds__(NTHREADS) setup_system_kernel(Geo g, Work w, c
           diag += wt;
           const float sn = n.brk[e] ? Sc[e] : 0.f;
           if (sn > 0.f) {  // coupled unknown of this brick
-            acc += wt * Bn[e];
+            acc = fmaf(wt, Bn[e], acc);
             wf[e] = wt * si * sn;
           } else {  // Dirichlet: seed, or outside the brick
-            b += wt * (Sn[e] ? seed_value(Sn[e]) : Bn[e]);
+            b = fmaf(wt, Sn[e] ? seed_value(Sn[e]) : Bn[e], b);
           }
         }
-        r = si * (b + acc - diag * x0);
-        y = x0 / si;
+        r = initial_residual(si, b, acc, diag, x0);
+        y = initial_y(x0, si, diag);
         const float sb = si * b;
         acc_bb += sb * sb;
         acc_rr += r * r;
@@ -364,43 +375,50 @@ __global__ void __launch_bounds__(NTHREADS) setup_system_kernel(Geo g, Work w, c
 }
 
 // ---------------------------------------------------------------------------
-// Fused setup, one CTA per brick (brick x, y extents <= 32): thread (lx, ly)
-// owns a column and marches z.  The two setup kernels above compute all six
-// edge weights of every voxel twice (12 exponentials) and exchange the scale
-// factors through HBM; here each voxel computes its forward x/y/z and backward
-// y weights once (4 exponentials; backward x comes by shuffle, backward z from
-// the previous plane), the scale factors of plane a are computed one plane
-// ahead of the system of plane a-1, and the y neighbours' values travel
-// through shared memory.  Same arithmetic, same summation order (-z,+z,-y,+y,
-// -x,+x) as setup_scale/setup_system, so the outputs are bit-identical.
+// Fused setup, one CTA per brick (brick x, y extents <= 32, x a multiple of 4):
+// thread (xq, ly) owns a row quad of 4 x-voxels and marches z.  The two setup
+// kernels above compute all six edge weights of every voxel twice (12
+// exponentials) and exchange the scale factors through HBM; here each voxel
+// computes its forward x/y/z and backward y weights (4 exponentials; backward
+// x comes from the quad neighbour, backward z from the previous plane), the
+// scale factors and Dirichlet values of plane a are computed one plane ahead
+// of the system of plane a-1 and reach the y / quad-edge neighbours through
+// shared memory.  Same arithmetic, same summation order (-z,+z,-y,+y,-x,+x) and
+// the same reduction order for ||S b||^2 and ||r0||^2 as setup_scale /
+// setup_system, so the outputs are bit-identical.
 //
-// Inputs arrive by TMA: for every plane, one elected thread loads the
-// tile of intensity, bound and seeds that covers the brick's plane plus its
-// one-voxel x/y halo (the x start rounded down to 16 B: TMA tile boxes must
-// start 16 B aligned), out-of-level parts zero-filled by the tensor map, into
-// a ring of SR stages, each completing on its own mbarrier, SR-4 planes ahead
-// of use.  One CTA per SM marches 33 planes with two barriers each, so it is
-// the ring depth, not the warps, that keeps enough bytes in flight to stream
-// at HBM rate (a one-plane register prefetch reached about a fifth of it).
+// Inputs arrive by TMA: for every plane, one elected thread loads the tile of
+// intensity, bound and seeds that covers the brick's plane plus its one-voxel
+// x/y halo (the x start rounded down to 16 B: TMA tile boxes must start 16 B
+// aligned), out-of-level parts zero-filled by the tensor map, into a ring of
+// SR stages, each completing on its own mbarrier, SR-4 planes ahead of use.
+// Quads make every shared-memory access and global store 16 B wide and spread
+// the per-plane bookkeeping over 4 voxels; two CTAs fit on an SM.
 constexpr int FB = 32;                 // max brick extent in x and y for the fused setup
-constexpr int SR = 8;                  // ring stages (planes)
+constexpr int SQ = 4;                  // x voxels per thread
+constexpr int SQN = FB / SQ;           // quads per row
+constexpr int STH = SQN * FB;          // threads per CTA
+constexpr int SR = 6;                  // ring stages (planes)
 constexpr int SRX = 40, SRY = FB + 2;  // f32 tile box: x [gx0-4, gx0+36), y [gy0-1, gy0+33)
 constexpr int SRXS = 64;               // u8 seed tile box: x [gx0-16, gx0+48)
 constexpr int SRX0 = 4, SRXS0 = 16;    // tile column of x = gx0
 constexpr int SR_F32 = ((SRX * SRY * 4 + 127) / 128) * 128;  // bytes per f32 stage (128 B aligned)
 constexpr int SR_U8 = ((SRXS * SRY + 127) / 128) * 128;
-constexpr int SETUP_MAX_TILES = 256;  // (bz / STZ) * (by / TY) tiles of the two-kernel reduction order
+constexpr int SPX = 4, SPW = FB + 8;   // padded Sc / Dv rows: column SPX + x, halo at SPX-1 and SPX+bx
+constexpr int SETUP_MAX_TILES = 256;   // (bz / STZ) * (by / TY) tiles of the two-kernel reduction order
 
 struct SetupSmem {
   float I[SR][SR_F32 / 4];
   float B[SR][SR_F32 / 4];
   unsigned char S[SR][SR_U8];
   unsigned long long bar[SR];
-  float Wy[FB][FB + 1];
-  float Sc[3][FB][FB + 1];
-  float2 rowpart[FB];          // per-row (warp) sums of the current 4-plane chunk
+  // per plane (2 alternating): scale factors and Dirichlet values (seed value,
+  // else bound) with a one-voxel halo; Sc's halo stays 0 (cross-brick = never coupled)
+  __align__(16) float Sc[2][SRY][SPW];
+  __align__(16) float Dv[2][SRY][SPW];
+  float2 rowpart[FB];             // per-row sums of the current 4-plane chunk
   float2 tpart[SETUP_MAX_TILES];  // per setup-tile sums, in setup_system_kernel's tile order
-  unsigned red_unk[FB];
+  unsigned red_unk[STH / 32];
 };
 
 struct SetupMaps {
@@ -437,34 +455,59 @@ __device__ __forceinline__ void setup_wait(SetupSmem& sm, int stage, uint32_t pa
       : "memory");
 }
 
-__global__ void __launch_bounds__(FB * FB, 1) setup_brick_kernel(const __grid_constant__ SetupMaps maps, Geo g,
-                                                                 Work w, const int* __restrict__ list, bool has_b,
-                                                                 float beta, float wmin, float tol2, int max_iter,
-                                                                 int write_p) {
+__device__ __forceinline__ float q4(const float4& v, int i) { return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w)); }
+
+__global__ void __launch_bounds__(STH, 2) setup_brick_kernel(const __grid_constant__ SetupMaps maps, Geo g, Work w,
+                                                             const int* __restrict__ list, bool has_b, float beta,
+                                                             float wmin, float tol2, int max_iter, int write_p) {
   extern __shared__ __align__(128) unsigned char setup_smem_raw[];
   SetupSmem& sm = *reinterpret_cast<SetupSmem*>(setup_smem_raw);
   const int slot = blockIdx.x;
   const int brick = list ? list[slot] : slot;
   const int hx = brick % g.gx, hy = (brick / g.gx) % g.gy, hz = brick / (g.gx * g.gy);
   const int gz0 = g.oz + hz * g.bz, gy0 = g.oy + hy * g.by, gx0 = g.ox + hx * g.bx;
-  const int lx = threadIdx.x, ly = threadIdx.y;
-  const int tid = ly * FB + lx;
-  const int gx = gx0 + lx, gy = gy0 + ly;
-  const bool col = lx < g.bx && ly < g.by;
-  const bool colin = col && gx >= 0 && gx < g.nx && gy >= 0 && gy < g.ny;
-  const bool fxm = lx == 0, fxp = lx + 1 == g.bx, fym = ly == 0, fyp = ly + 1 == g.by;  // brick-face lanes
-  const bool exm = gx > 0, exp_ = gx + 1 < g.nx, eym = gy > 0, eyp = gy + 1 < g.ny;  // neighbour in level
+  const int tid = threadIdx.x;
+  const int xq = tid % SQN, ly = tid / SQN;
+  const int lx0 = xq * SQ;  // brick-local x of voxel 0 of the quad
+  const int gy = gy0 + ly;
+  const bool col = lx0 < g.bx && ly < g.by;  // quads lie wholly inside or outside (bx % 4 == 0)
+  const bool rowin = gy >= 0 && gy < g.ny;
+  const bool fxm = lx0 == 0, fxp = lx0 + SQ == g.bx, fym = ly == 0, fyp = ly + 1 == g.by;  // brick-face lanes
+  const bool eym = gy > 0, eyp = gy + 1 < g.ny;
+  bool colin[SQ], exm[SQ], exp_[SQ];
+#pragma unroll
+  for (int i = 0; i < SQ; ++i) {
+    const int gx = gx0 + lx0 + i;
+    colin[i] = col && rowin && gx >= 0 && gx < g.nx;
+    exm[i] = gx > 0;
+    exp_[i] = gx + 1 < g.nx;
+  }
   const long long sbz = (long long)g.by * g.bx;
-  const long long lcol = (long long)slot * g.bvol + (long long)ly * g.bx + lx;
+  const long long lcol = (long long)slot * g.bvol + (long long)ly * g.bx + lx0;
   auto wgt = [&](float a, float b) { return edge_weight(a, b, beta, wmin); };
-  auto inz = [&](int gz) { return colin && gz >= 0 && gz < g.nz; };
   // plane p in [-1, bz] lives in stage (p + 1) % SR, use (p + 1) / SR; tile row ty = voxel y gy0-1+ty
   auto stage_of = [](int p) { return (p + 1) % SR; };
-  auto tI = [&](int p, int dy, int dx) { return sm.I[stage_of(p)][(ly + 1 + dy) * SRX + SRX0 + lx + dx]; };
-  auto tB = [&](int p, int dy, int dx) {
-    return has_b ? sm.B[stage_of(p)][(ly + 1 + dy) * SRX + SRX0 + lx + dx] : 0.f;
+  auto rowI = [&](int p, int dy) { return &sm.I[stage_of(p)][(ly + 1 + dy) * SRX + SRX0 + lx0]; };
+  auto rowB = [&](int p, int dy) { return &sm.B[stage_of(p)][(ly + 1 + dy) * SRX + SRX0 + lx0]; };
+  auto ldI4 = [&](int p, int dy) { return *reinterpret_cast<const float4*>(rowI(p, dy)); };
+  auto ldB4 = [&](int p, int dy) {
+    return has_b ? *reinterpret_cast<const float4*>(rowB(p, dy)) : make_float4(0.f, 0.f, 0.f, 0.f);
   };
-  auto tS = [&](int p, int dy, int dx) { return (unsigned)sm.S[stage_of(p)][(ly + 1 + dy) * SRXS + SRXS0 + lx + dx]; };
+  auto ldS4 = [&](int p, int dy) {  // the quad's 4 seed bytes
+    return *reinterpret_cast<const unsigned*>(&sm.S[stage_of(p)][(ly + 1 + dy) * SRXS + SRXS0 + lx0]);
+  };
+  auto sbyte = [](unsigned s4, int i) { return (s4 >> (8 * i)) & 0xffu; };
+  auto dval1 = [](unsigned s, float b) { return s ? seed_value((uint8_t)s) : b; };  // Dirichlet value
+  auto dval4 = [&](int p, int dy) {
+    const unsigned s4 = ldS4(p, dy);
+    const float4 b4 = ldB4(p, dy);
+    return make_float4(dval1(sbyte(s4, 0), b4.x), dval1(sbyte(s4, 1), b4.y), dval1(sbyte(s4, 2), b4.z),
+                       dval1(sbyte(s4, 3), b4.w));
+  };
+  auto dval_x = [&](int p, int dx) {  // x halo voxel (dx = -1 or 4) of the quad's row
+    const unsigned s = sm.S[stage_of(p)][(ly + 1) * SRXS + SRXS0 + lx0 + dx];
+    return dval1(s, has_b ? rowB(p, 0)[dx] : 0.f);
+  };
   auto wait_plane = [&](int p) { setup_wait(sm, stage_of(p), (uint32_t)(((p + 1) / SR) & 1)); };
   const int last = g.bz;  // planes -1 .. bz are loaded
 
@@ -475,20 +518,34 @@ __global__ void __launch_bounds__(FB * FB, 1) setup_brick_kernel(const __grid_co
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     for (int p = -1; p <= min(last, SR - 4); ++p) setup_tma_plane(maps, sm, has_b, stage_of(p), gx0, gy0 - 1, gz0 + p);
   }
+  for (int i = tid; i < 2 * SRY * SPW; i += STH) {
+    (&sm.Sc[0][0][0])[i] = 0.f;
+    (&sm.Dv[0][0][0])[i] = 0.f;
+  }
   __syncthreads();
   wait_plane(-1);
   wait_plane(0);
 
-  float wzf_prev = 0.f;  // forward z weight of plane a-1 (= backward z weight of plane a)
-  // system-step (plane z = a-1) registers: its weights and the scale factors of z-1, z
-  float z_wxf = 0.f, z_wyf = 0.f, z_wzf = 0.f, z_wxb = 0.f, z_wyb = 0.f, z_wzb = 0.f;
-  float sc_zm = 0.f, sc_z = 0.f;
-  float acc_bb = 0.f, acc_rr = 0.f;
+  // system-step (plane z = a-1) registers: its weights, scale factors and
+  // Dirichlet values of the own quad at z-1 and z
+  float z_wxf[SQ], z_wyf[SQ], z_wzf[SQ], z_wxb[SQ], z_wyb[SQ], z_wzb[SQ];
+  float sc_zm[SQ], sc_z[SQ], dv_zm[SQ], dv_z[SQ];
+  float acc_bb[SQ], acc_rr[SQ];
+  {
+    const float4 dm = dval4(-1, 0);
+#pragma unroll
+    for (int i = 0; i < SQ; ++i) {
+      z_wxf[i] = z_wyf[i] = z_wzf[i] = z_wxb[i] = z_wyb[i] = z_wzb[i] = 0.f;
+      sc_zm[i] = sc_z[i] = dv_zm[i] = 0.f;
+      dv_z[i] = q4(dm, i);
+      acc_bb[i] = acc_rr[i] = 0.f;
+    }
+  }
   unsigned n_unknown = 0;
   // ||S b||^2 and ||r0||^2 are reduced in exactly the order of setup_system_kernel
-  // (per thread over a 4-plane chunk, warp tree per row, 8 rows in sequence per
-  // tile, tiles in float64 by brick_reduce), so both setups give the same bits
-  // and the CG that starts from them the same trajectory.
+  // (per voxel over a 4-plane chunk, xor tree over the 32 x of a row, 8 rows in
+  // sequence per tile, tiles in float64 by brick_reduce), so both setups give
+  // the same bits and the CG that starts from them the same trajectory.
   const int ty8 = (g.by + TY - 1) / TY;
   int pending_chunk = -1;
   auto tile_sums = [&]() {  // after a barrier: rows of the flushed chunk -> its tiles
@@ -508,111 +565,150 @@ __global__ void __launch_bounds__(FB * FB, 1) setup_brick_kernel(const __grid_co
     tile_sums();
     const int gza = gz0 + a;
     const bool pa_in = a < g.bz;
-    const bool va = pa_in && inz(gza);
+    const bool zin = gza >= 0 && gza < g.nz;
     // refill: plane a+SR-3 replaces plane a-3, whose last reader (step a-1) every thread has left
     if (tid == 0 && a + SR - 3 <= last)
       setup_tma_plane(maps, sm, has_b, stage_of(a + SR - 3), gx0, gy0 - 1, gz0 + a + SR - 3);
     if (a + 1 <= last) wait_plane(a + 1);
-    // ---------------- phase 1: weights and scale of plane a ----------------
-    float sca = 0.f, wxf = 0.f, wyf = 0.f, wzf = 0.f, wxb = 0.f, wyb = 0.f, wzb = 0.f;
+    // ---------------- phase 1: weights, scale and Dirichlet values of plane a ----------------
+    float sca[SQ], wxf[SQ], wyf[SQ], wzf[SQ], wxb[SQ], wyb[SQ], wzb[SQ];
+    const float4 dva4 = dval4(a, 0);
+    float dva[SQ] = {dva4.x, dva4.y, dva4.z, dva4.w};
+#pragma unroll
+    for (int i = 0; i < SQ; ++i) sca[i] = wxf[i] = wyf[i] = wzf[i] = wxb[i] = wyb[i] = wzb[i] = 0.f;
     if (pa_in) {
-      const float Ia = tI(a, 0, 0);
-      if (va) {
-        const bool haszp = g.is3d && gza + 1 < g.nz;
-        wxf = exp_ ? wgt(Ia, tI(a, 0, 1)) : 0.f;
-        wyf = eyp ? wgt(Ia, tI(a, 1, 0)) : 0.f;
-        wzf = haszp ? wgt(Ia, tI(a + 1, 0, 0)) : 0.f;
+      const int ab = a & 1;
+      if (col && rowin && zin) {
+        const float4 I4 = ldI4(a, 0), Iy4 = ldI4(a, 1), Iym4 = ldI4(a, -1), Iz4 = ldI4(a + 1, 0);
+        const float Ixr = rowI(a, 0)[SQ], Ixl = rowI(a, 0)[-1];
+        const unsigned s4 = ldS4(a, 0);
+        const bool haszp = g.is3d && gza + 1 < g.nz, haszm = g.is3d && gza > 0;
+        float4 Izm4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (a == 0 && haszm) Izm4 = ldI4(-1, 0);
+#pragma unroll
+        for (int i = 0; i < SQ; ++i) {
+          if (!colin[i]) continue;
+          const float Ii = q4(I4, i);
+          const float Ixp = i + 1 < SQ ? q4(I4, i + 1) : Ixr;
+          wxf[i] = exp_[i] ? wgt(Ii, Ixp) : 0.f;
+          wyf[i] = eyp ? wgt(Ii, q4(Iy4, i)) : 0.f;
+          wzf[i] = haszp ? wgt(Ii, q4(Iz4, i)) : 0.f;
+          wxb[i] = exm[i] ? (i > 0 ? wxf[i - 1] : wgt(Ii, Ixl)) : 0.f;
+          wyb[i] = eym ? wgt(Ii, q4(Iym4, i)) : 0.f;
+          wzb[i] = haszm ? (a > 0 ? z_wzf[i] : wgt(Ii, q4(Izm4, i))) : 0.f;
+          const float d = ((((wzb[i] + wzf[i]) + wyb[i]) + wyf[i]) + wxb[i]) + wxf[i];
+          sca[i] = (sbyte(s4, i) == 0 && d > 0.f) ? jacobi_scale(d) : 0.f;
+        }
+        *reinterpret_cast<float4*>(&sm.Sc[ab][ly + 1][SPX + lx0]) = make_float4(sca[0], sca[1], sca[2], sca[3]);
       }
-      sm.Wy[ly][lx] = wyf;
-      __syncthreads();
-      const float wxf_sh = __shfl_up_sync(0xffffffffu, wxf, 1);
-      if (va) {
-        const bool haszm = g.is3d && gza > 0;
-        wxb = exm ? (fxm ? wgt(Ia, tI(a, 0, -1)) : wxf_sh) : 0.f;
-        wyb = eym ? (fym ? wgt(Ia, tI(a, -1, 0)) : sm.Wy[ly - 1][lx]) : 0.f;
-        wzb = haszm ? (a > 0 ? wzf_prev : wgt(Ia, tI(-1, 0, 0))) : 0.f;
-        const float d = ((((wzb + wzf) + wyb) + wyf) + wxb) + wxf;
-        sca = (tS(a, 0, 0) == 0 && d > 0.f) ? 1.0f / sqrtf(d) : 0.f;
-      }
-      sm.Sc[a % 3][ly][lx] = sca;
-      wzf_prev = wzf;
+      *reinterpret_cast<float4*>(&sm.Dv[ab][ly + 1][SPX + lx0]) = dva4;
+      if (fxm) sm.Dv[ab][ly + 1][SPX - 1] = dval_x(a, -1);  // x / y halo of the brick face lanes
+      if (fxp) sm.Dv[ab][ly + 1][SPX + g.bx] = dval_x(a, SQ);
+      if (fym) *reinterpret_cast<float4*>(&sm.Dv[ab][0][SPX + lx0]) = dval4(a, -1);
+      if (fyp) *reinterpret_cast<float4*>(&sm.Dv[ab][ly + 2][SPX + lx0]) = dval4(a, 1);
     }
     // ---------------- phase 2: the system of plane z = a-1 ----------------
     const int z = a - 1;
     if (z >= 0) {
-      const int gz = gz0 + z;
-      const bool vz = inz(gz);
+      const bool vrow = col && rowin && gz0 + z >= 0 && gz0 + z < g.nz;
       const long long li = lcol + (long long)z * sbz;
-      float wfx = 0.f, wfy = 0.f, wfz = 0.f, r = 0.f, y = 0.f;
-      if (vz && sc_z > 0.f) {
-        ++n_unknown;
-        const int zs = z % 3;
-        const float si = sc_z, x0 = tB(z, 0, 0);
-        float diag = 0.f, b = 0.f, acc = 0.f;
-        auto visit = [&](float wt, bool exists, bool inbrick, float sn, unsigned sv, float bn, float* fwd) {
-          if (!exists) return;
-          diag += wt;
-          if (inbrick && sn > 0.f) {
-            acc += wt * bn;
-            if (fwd) *fwd = wt * si * sn;
-          } else {
-            b += wt * (sv ? seed_value((uint8_t)sv) : bn);
-          }
-        };
-        // -z, +z (beyond the brick: the neighbour planes of the ring)
-        visit(z_wzb, g.is3d && gz > 0, z > 0, sc_zm, tS(z - 1, 0, 0), tB(z - 1, 0, 0), nullptr);
-        visit(z_wzf, g.is3d && gz + 1 < g.nz, z + 1 < g.bz, sca, tS(a, 0, 0), tB(a, 0, 0), &wfz);
-        // -y, +y, -x, +x (beyond the brick face: the tile halo)
-        visit(z_wyb, eym, !fym, fym ? 0.f : sm.Sc[zs][ly - 1][lx], tS(z, -1, 0), tB(z, -1, 0), nullptr);
-        visit(z_wyf, eyp, !fyp, fyp ? 0.f : sm.Sc[zs][ly + 1][lx], tS(z, 1, 0), tB(z, 1, 0), &wfy);
-        visit(z_wxb, exm, !fxm, fxm ? 0.f : sm.Sc[zs][ly][lx - 1], tS(z, 0, -1), tB(z, 0, -1), nullptr);
-        visit(z_wxf, exp_, !fxp, fxp ? 0.f : sm.Sc[zs][ly][lx + 1], tS(z, 0, 1), tB(z, 0, 1), &wfx);
-        r = si * (b + acc - diag * x0);
-        y = x0 / si;
-        const float sb = si * b;
-        acc_bb += sb * sb;
-        acc_rr += r * r;
-      }
-      if (z % STZ == STZ - 1 || z == g.bz - 1) {  // chunk complete: row sums
-        float bb = acc_bb, rr = acc_rr;
+      float wfx[SQ], wfy[SQ], wfz[SQ], r[SQ], y[SQ], scw[SQ];
+      const int zb = z & 1;
+      const float4 scm = *reinterpret_cast<const float4*>(&sm.Sc[zb][ly][SPX + lx0]);
+      const float4 scp = *reinterpret_cast<const float4*>(&sm.Sc[zb][ly + 2][SPX + lx0]);
+      const float4 dvm = *reinterpret_cast<const float4*>(&sm.Dv[zb][ly][SPX + lx0]);
+      const float4 dvp = *reinterpret_cast<const float4*>(&sm.Dv[zb][ly + 2][SPX + lx0]);
+      const float scl = sm.Sc[zb][ly + 1][SPX + lx0 - 1], scr = sm.Sc[zb][ly + 1][SPX + lx0 + SQ];
+      const float dvl = sm.Dv[zb][ly + 1][SPX + lx0 - 1], dvr = sm.Dv[zb][ly + 1][SPX + lx0 + SQ];
+      const float4 xb4 = ldB4(z, 0);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          bb += __shfl_xor_sync(0xffffffffu, bb, o);
-          rr += __shfl_xor_sync(0xffffffffu, rr, o);
+      for (int i = 0; i < SQ; ++i) {
+        wfx[i] = wfy[i] = wfz[i] = r[i] = y[i] = 0.f;
+        scw[i] = 0.f;
+        const bool vz = vrow && colin[i];
+        if (vz) scw[i] = sc_z[i];
+        if (vz && sc_z[i] > 0.f) {
+          ++n_unknown;
+          const float si = sc_z[i], x0 = q4(xb4, i);
+          float diag = 0.f, b = 0.f, acc = 0.f;
+          // One neighbour, branch-free: a missing neighbour has weight 0 (phase
+          // 1), which adds exact zeros, so the non-zero terms are summed in the
+          // same order as setup_system_kernel's skipping loop.  A coupled
+          // neighbour is an unknown, so its Dirichlet value is its bound.
+          auto visit = [&](float wt, float sn, float dv) {
+            diag += wt;
+            const bool coupled = sn > 0.f;
+            acc = coupled ? fmaf(wt, dv, acc) : acc;
+            b = coupled ? b : fmaf(wt, dv, b);
+            return coupled ? wt * si * sn : 0.f;
+          };
+          visit(z_wzb[i], z > 0 ? sc_zm[i] : 0.f, dv_zm[i]);
+          wfz[i] = visit(z_wzf[i], z + 1 < g.bz ? sca[i] : 0.f, dva[i]);
+          visit(z_wyb[i], q4(scm, i), q4(dvm, i));
+          wfy[i] = visit(z_wyf[i], q4(scp, i), q4(dvp, i));
+          visit(z_wxb[i], i > 0 ? sc_z[i - 1] : scl, i > 0 ? dv_z[i - 1] : dvl);
+          wfx[i] = visit(z_wxf[i], i + 1 < SQ ? sc_z[i + 1] : scr, i + 1 < SQ ? dv_z[i + 1] : dvr);
+          r[i] = initial_residual(si, b, acc, diag, x0);
+          y[i] = initial_y(x0, si, diag);
+          const float sb = si * b;
+          acc_bb[i] += sb * sb;
+          acc_rr[i] += r[i] * r[i];
         }
-        if (lx == 0) sm.rowpart[ly] = make_float2(bb, rr);
-        acc_bb = acc_rr = 0.f;
+      }
+      if (z % STZ == STZ - 1 || z == g.bz - 1) {  // chunk complete: row sums in the xor-tree order
+        float bb[SQ], rr[SQ];
+#pragma unroll
+        for (int i = 0; i < SQ; ++i) {
+          bb[i] = acc_bb[i];
+          rr[i] = acc_rr[i];
+#pragma unroll
+          for (int o = SQN / 2; o > 0; o >>= 1) {  // x ^ 16, 8, 4 = quad ^ 4, 2, 1
+            bb[i] += __shfl_xor_sync(0xffffffffu, bb[i], o);
+            rr[i] += __shfl_xor_sync(0xffffffffu, rr[i], o);
+          }
+          acc_bb[i] = acc_rr[i] = 0.f;
+        }
+        // x ^ 2, then x ^ 1, inside the quad
+        const float b0 = bb[0] + bb[2], b1 = bb[1] + bb[3], r0 = rr[0] + rr[2], r1 = rr[1] + rr[3];
+        if (xq == 0) sm.rowpart[ly] = make_float2(b0 + b1, r0 + r1);
         pending_chunk = z / STZ;
       }
       if (col) {
-        w.wx[li] = wfx;
-        w.wy[li] = wfy;
-        if (g.is3d) w.wz[li] = wfz;
-        w.r[li] = r;
-        w.y[li] = y;
-        w.sc[li] = vz ? sc_z : 0.f;
-        if (write_p) w.p0[li] = 0.f;
+        *reinterpret_cast<float4*>(w.wx + li) = make_float4(wfx[0], wfx[1], wfx[2], wfx[3]);
+        *reinterpret_cast<float4*>(w.wy + li) = make_float4(wfy[0], wfy[1], wfy[2], wfy[3]);
+        if (g.is3d) *reinterpret_cast<float4*>(w.wz + li) = make_float4(wfz[0], wfz[1], wfz[2], wfz[3]);
+        *reinterpret_cast<float4*>(w.r + li) = make_float4(r[0], r[1], r[2], r[3]);
+        *reinterpret_cast<float4*>(w.y + li) = make_float4(y[0], y[1], y[2], y[3]);
+        *reinterpret_cast<float4*>(w.sc + li) = make_float4(scw[0], scw[1], scw[2], scw[3]);
+        if (write_p) *reinterpret_cast<float4*>(w.p0 + li) = make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
     // rotate: plane a becomes plane z of the next system step
-    z_wxf = wxf, z_wyf = wyf, z_wzf = wzf, z_wxb = wxb, z_wyb = wyb, z_wzb = wzb;
-    sc_zm = sc_z;
-    sc_z = sca;
+#pragma unroll
+    for (int i = 0; i < SQ; ++i) {
+      z_wxf[i] = wxf[i], z_wyf[i] = wyf[i], z_wzf[i] = wzf[i];
+      z_wxb[i] = wxb[i], z_wyb[i] = wyb[i], z_wzb[i] = wzb[i];
+      sc_zm[i] = sc_z[i];
+      sc_z[i] = sca[i];
+      dv_zm[i] = dv_z[i];
+      dv_z[i] = dva[i];
+    }
     __syncthreads();
   }
   // per-brick ||S b||^2, ||r0||^2 (brick_reduce's order) and the brick's initial decision
   tile_sums();
   const unsigned nu = __reduce_add_sync(0xffffffffu, n_unknown);
-  if (lx == 0) sm.red_unk[ly] = nu;
+  if ((tid & 31) == 0) sm.red_unk[tid >> 5] = nu;
   __syncthreads();
-  if (ly == 0) {
+  if (tid < 32) {
+    const int lane = tid;
     const int tiles = ((g.bz + STZ - 1) / STZ) * ty8;
     double sbb = 0.0, srr = 0.0;
     if (tiles == 1) {
       sbb = (double)sm.tpart[0].x;
       srr = (double)sm.tpart[0].y;
     } else {
-      for (int i = lx; i < tiles; i += 32) {
+      for (int i = lane; i < tiles; i += 32) {
         sbb += (double)sm.tpart[i].x;
         srr += (double)sm.tpart[i].y;
       }
@@ -622,8 +718,8 @@ __global__ void __launch_bounds__(FB * FB, 1) setup_brick_kernel(const __grid_co
         srr += __shfl_xor_sync(0xffffffffu, srr, o);
       }
     }
-    unsigned su = __reduce_add_sync(0xffffffffu, sm.red_unk[lx]);
-    if (lx == 0) {
+    const unsigned su = __reduce_add_sync(0xffffffffu, lane < STH / 32 ? sm.red_unk[lane] : 0u);
+    if (lane == 0) {
       if (su) atomicAdd(w.unknowns, (unsigned long long)su);
       w.bb[slot] = sbb;
       w.rr[slot] = srr;  // parity 0
@@ -644,7 +740,8 @@ __global__ void __launch_bounds__(FB * FB, 1) setup_brick_kernel(const __grid_co
 // meet TMA's rules (16 B aligned bases, row pitches and box x starts) — the
 // caller then uses the two-kernel setup.
 static bool make_setup_maps(const Geo& g, const float* I, const uint8_t* S, const float* B, SetupMaps* m) {
-  if (g.bx > FB || g.by > FB || ((g.bz + STZ - 1) / STZ) * ((g.by + TY - 1) / TY) > SETUP_MAX_TILES) return false;
+  if (g.bx > FB || g.by > FB || g.bx % SQ || ((g.bz + STZ - 1) / STZ) * ((g.by + TY - 1) / TY) > SETUP_MAX_TILES)
+    return false;
   if (g.ox % 16 || (g.gx > 1 && g.bx % 16)) return false;  // every brick's x start 16-voxel aligned
   if (g.nx % 16 || ((uintptr_t)I & 15) || ((uintptr_t)S & 15) || ((uintptr_t)B & 15)) return false;
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -1215,7 +1312,7 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
                                     (int)sizeof(SetupSmem)));
       smem_set = true;
     }
-    setup_brick_kernel<<<nb, dim3(FB, FB), sizeof(SetupSmem), st>>>(maps, g, w, list, bound != nullptr, params->beta,
+    setup_brick_kernel<<<nb, STH, sizeof(SetupSmem), st>>>(maps, g, w, list, bound != nullptr, params->beta,
                                                                    params->min_weight, tol2, max_iter,
                                                                    resident ? 0 : 1);
     RWB_LAUNCH_CHECK("fused setup kernel");
