@@ -200,7 +200,11 @@ __device__ __forceinline__ float seed_value(uint8_t s) { return s == 1 ? 1.0f : 
 // Shared by both setups (bit-identical systems).  s = diag^-1/2 by MUFU.RSQ
 // (~1 ulp; the float64 oracle is matched to the solve tolerance, not bits);
 // r0 = s (b + acc - diag x0); y0 = x0 / s = x0 diag s.
-__device__ __forceinline__ float jacobi_scale(float d) { return rsqrtf(d); }
+__device__ __forceinline__ float jacobi_scale(float d) {  // d >= w_min > 0: no denormal path needed
+  float s;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(d));
+  return s;
+}
 __device__ __forceinline__ float initial_residual(float si, float b, float acc, float diag, float x0) {
   return si * fmaf(-diag, x0, b + acc);
 }
@@ -338,8 +342,8 @@ __global__ void __launch_bounds__(NTHREADS) setup_system_kernel(Geo g, Work w, c
         r = initial_residual(si, b, acc, diag, x0);
         y = initial_y(x0, si, diag);
         const float sb = si * b;
-        acc_bb += sb * sb;
-        acc_rr += r * r;
+        acc_bb = fmaf(sb, sb, acc_bb);
+        acc_rr = fmaf(r, r, acc_rr);
       }
       wx[li] = wf[5];
       wy[li] = wf[3];
@@ -561,6 +565,7 @@ __global__ void __launch_bounds__(STH, 2) setup_brick_kernel(const __grid_consta
     pending_chunk = -1;
   };
 
+#pragma unroll 2
   for (int a = 0; a <= g.bz; ++a) {
     tile_sums();
     const int gza = gz0 + a;
@@ -585,19 +590,21 @@ __global__ void __launch_bounds__(STH, 2) setup_brick_kernel(const __grid_consta
         const bool haszp = g.is3d && gza + 1 < g.nz, haszm = g.is3d && gza > 0;
         float4 Izm4 = make_float4(0.f, 0.f, 0.f, 0.f);
         if (a == 0 && haszm) Izm4 = ldI4(-1, 0);
+        // branch-free: every lane computes all four voxels (tile values are
+        // finite, zero outside the level) and masks the voxels outside the level
 #pragma unroll
         for (int i = 0; i < SQ; ++i) {
-          if (!colin[i]) continue;
           const float Ii = q4(I4, i);
           const float Ixp = i + 1 < SQ ? q4(I4, i + 1) : Ixr;
-          wxf[i] = exp_[i] ? wgt(Ii, Ixp) : 0.f;
-          wyf[i] = eyp ? wgt(Ii, q4(Iy4, i)) : 0.f;
-          wzf[i] = haszp ? wgt(Ii, q4(Iz4, i)) : 0.f;
-          wxb[i] = exm[i] ? (i > 0 ? wxf[i - 1] : wgt(Ii, Ixl)) : 0.f;
-          wyb[i] = eym ? wgt(Ii, q4(Iym4, i)) : 0.f;
-          wzb[i] = haszm ? (a > 0 ? z_wzf[i] : wgt(Ii, q4(Izm4, i))) : 0.f;
+          const float fx = wgt(Ii, Ixp);
+          wxf[i] = colin[i] && exp_[i] ? fx : 0.f;
+          wyf[i] = colin[i] && eyp ? wgt(Ii, q4(Iy4, i)) : 0.f;
+          wzf[i] = colin[i] && haszp ? wgt(Ii, q4(Iz4, i)) : 0.f;
+          wxb[i] = colin[i] && exm[i] ? (i > 0 ? wxf[i - 1] : wgt(Ii, Ixl)) : 0.f;
+          wyb[i] = colin[i] && eym ? wgt(Ii, q4(Iym4, i)) : 0.f;
+          wzb[i] = colin[i] && haszm ? (a > 0 ? z_wzf[i] : wgt(Ii, q4(Izm4, i))) : 0.f;
           const float d = ((((wzb[i] + wzf[i]) + wyb[i]) + wyf[i]) + wxb[i]) + wxf[i];
-          sca[i] = (sbyte(s4, i) == 0 && d > 0.f) ? jacobi_scale(d) : 0.f;
+          sca[i] = (colin[i] && sbyte(s4, i) == 0 && d > 0.f) ? jacobi_scale(d) : 0.f;
         }
         *reinterpret_cast<float4*>(&sm.Sc[ab][ly + 1][SPX + lx0]) = make_float4(sca[0], sca[1], sca[2], sca[3]);
       }
@@ -623,12 +630,12 @@ __global__ void __launch_bounds__(STH, 2) setup_brick_kernel(const __grid_consta
       const float4 xb4 = ldB4(z, 0);
 #pragma unroll
       for (int i = 0; i < SQ; ++i) {
-        wfx[i] = wfy[i] = wfz[i] = r[i] = y[i] = 0.f;
-        scw[i] = 0.f;
         const bool vz = vrow && colin[i];
-        if (vz) scw[i] = sc_z[i];
-        if (vz && sc_z[i] > 0.f) {
-          ++n_unknown;
+        scw[i] = vz ? sc_z[i] : 0.f;
+        // branch-free: computed for every voxel, kept for the unknowns (sc > 0)
+        const bool unk = vz && sc_z[i] > 0.f;
+        n_unknown += unk;
+        {
           const float si = sc_z[i], x0 = q4(xb4, i);
           float diag = 0.f, b = 0.f, acc = 0.f;
           // One neighbour, branch-free: a missing neighbour has weight 0 (phase
@@ -643,16 +650,20 @@ __global__ void __launch_bounds__(STH, 2) setup_brick_kernel(const __grid_consta
             return coupled ? wt * si * sn : 0.f;
           };
           visit(z_wzb[i], z > 0 ? sc_zm[i] : 0.f, dv_zm[i]);
-          wfz[i] = visit(z_wzf[i], z + 1 < g.bz ? sca[i] : 0.f, dva[i]);
+          const float fz = visit(z_wzf[i], z + 1 < g.bz ? sca[i] : 0.f, dva[i]);
           visit(z_wyb[i], q4(scm, i), q4(dvm, i));
-          wfy[i] = visit(z_wyf[i], q4(scp, i), q4(dvp, i));
+          const float fy = visit(z_wyf[i], q4(scp, i), q4(dvp, i));
           visit(z_wxb[i], i > 0 ? sc_z[i - 1] : scl, i > 0 ? dv_z[i - 1] : dvl);
-          wfx[i] = visit(z_wxf[i], i + 1 < SQ ? sc_z[i + 1] : scr, i + 1 < SQ ? dv_z[i + 1] : dvr);
-          r[i] = initial_residual(si, b, acc, diag, x0);
-          y[i] = initial_y(x0, si, diag);
+          const float fx = visit(z_wxf[i], i + 1 < SQ ? sc_z[i + 1] : scr, i + 1 < SQ ? dv_z[i + 1] : dvr);
+          const float ri = initial_residual(si, b, acc, diag, x0);
           const float sb = si * b;
-          acc_bb[i] += sb * sb;
-          acc_rr[i] += r[i] * r[i];
+          wfx[i] = unk ? fx : 0.f;
+          wfy[i] = unk ? fy : 0.f;
+          wfz[i] = unk ? fz : 0.f;
+          r[i] = unk ? ri : 0.f;
+          y[i] = unk ? initial_y(x0, si, diag) : 0.f;
+          acc_bb[i] = unk ? fmaf(sb, sb, acc_bb[i]) : acc_bb[i];
+          acc_rr[i] = unk ? fmaf(ri, ri, acc_rr[i]) : acc_rr[i];
         }
       }
       if (z % STZ == STZ - 1 || z == g.bz - 1) {  // chunk complete: row sums in the xor-tree order
