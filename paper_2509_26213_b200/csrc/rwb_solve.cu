@@ -879,29 +879,35 @@ __global__ void __launch_bounds__(NTHREADS) cg_pass2_kernel(Geo g, Work w, int n
 // launches, and the level's working set (~36 B/voxel, 75 MB at 128^3) stays in
 // the 126 MB L2.  Loads of the vectors written inside the kernel are plain
 // (L1-cacheable) loads: the grid barrier's gpu-scope fence invalidates L1, and
-// within a pass they are read-only.  Per-block partials are reduced by every
-// block in the same fixed order (float64), so all blocks take the same
-// decisions and the result is deterministic.
+// within a pass they are read-only.  Work items (kCoopTZ planes of a tile) are
+// spread evenly over the blocks.  After each barrier every block reduces all
+// per-block partials in the same fixed order (float64; every thread one wide
+// load, then a fixed tree), so all blocks take the same decisions and the
+// result is deterministic.  (A single-sweep Chronopoulos-Gear variant needs
+// r, s, w double-buffered — 11 vectors, 92 MB at 128^3 — and fell out of L2:
+// 38 GB of DRAM traffic per solve instead of 0.14 GB; it was slower.)
+constexpr int kCoopTZ = 4;            // z planes per work item of the cooperative sweeps
+constexpr int kCoopMaxBlocks = 4096;  // partial slots of the cooperative whole-level solve
 
-__device__ __forceinline__ double grid_total(const float* part, int n, double* bcast) {
-  // warp 0 sums all block partials in a fixed order; result broadcast through smem
-  if (threadIdx.y == 0) {
-    double s = 0.0;
-    for (int i = threadIdx.x; i < n; i += 32) s += (double)__ldcg(part + i);
+__device__ __forceinline__ double coop_total(const float* part, int n, double* sh) {
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  double a = 0.0;
+  for (int i = tid; i < n; i += NTHREADS) a += (double)__ldcg(part + i);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (threadIdx.x == 0) *bcast = s;
-  }
+  for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+  __syncthreads();  // sh free from its previous use
+  if ((tid & 31) == 0) sh[tid >> 5] = a;
   __syncthreads();
-  const double v = *bcast;
-  __syncthreads();
-  return v;
+  double t = 0.0;
+#pragma unroll
+  for (int wv = 0; wv < NTHREADS / 32; ++wv) t += sh[wv];
+  return t;
 }
 
-__global__ void __launch_bounds__(NTHREADS) coop_cg_kernel(Geo g, Work w, float* part_pq, float* part_rr, float tol2,
-                                                           int max_iter) {
+__global__ void __launch_bounds__(NTHREADS) coop_cg_kernel(Geo g, Work w, float* part_pq, float* part_rr, int n_items,
+                                                           float tol2, int max_iter) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ double bcast;
+  __shared__ double sh[NTHREADS / 32];
   const long long sbz = (long long)g.by * g.bx;
   const double bb = w.bb[0];
   double rr = w.rr[0];
@@ -921,8 +927,8 @@ __global__ void __launch_bounds__(NTHREADS) coop_cg_kernel(Geo g, Work w, float*
     const float beta = (it == 0) ? 0.f : (float)(rr / rr_prev);
     // pass 1: p <- r + beta p ; q = A'p ; p.q
     float acc = 0.f;
-    for (int tile = blockIdx.x; tile < g.tiles; tile += gridDim.x) {
-      TileCtx c = tile_ctx(g, nullptr, 0, tile);
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      TileCtx c = tile_ctx<kCoopTZ>(g, nullptr, 0, item);
       if (!c.col) continue;
       const long long lbase = (long long)c.ly * g.bx + c.lx;
       const bool hx0 = c.lx > 0, hx1 = c.lx + 1 < g.bx, hy0 = c.ly > 0, hy1 = c.ly + 1 < g.by;
@@ -954,13 +960,12 @@ __global__ void __launch_bounds__(NTHREADS) coop_cg_kernel(Geo g, Work w, float*
       if (threadIdx.x == 0 && threadIdx.y == 0) part_pq[blockIdx.x] = sblk.x;
     }
     grid.sync();
-    __threadfence();
-    const double pq = grid_total(part_pq, gridDim.x, &bcast);
+    const double pq = coop_total(part_pq, gridDim.x, sh);
     const float alpha = pq != 0.0 ? (float)(rr / pq) : 0.f;
     // pass 2: y += alpha p ; r -= alpha q ; r.r
     float acc2 = 0.f;
-    for (int tile = blockIdx.x; tile < g.tiles; tile += gridDim.x) {
-      TileCtx c = tile_ctx(g, nullptr, 0, tile);
+    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+      TileCtx c = tile_ctx<kCoopTZ>(g, nullptr, 0, item);
       if (!c.col) continue;
       long long li = (long long)c.ly * g.bx + c.lx + (long long)c.lz0 * sbz;
       for (int lz = c.lz0; lz < c.lz1; ++lz, li += sbz) {
@@ -976,8 +981,7 @@ __global__ void __launch_bounds__(NTHREADS) coop_cg_kernel(Geo g, Work w, float*
       if (threadIdx.x == 0 && threadIdx.y == 0) part_rr[blockIdx.x] = sblk.x;
     }
     grid.sync();
-    __threadfence();
-    const double rr_new = grid_total(part_rr, gridDim.x, &bcast);
+    const double rr_new = coop_total(part_rr, gridDim.x, sh);
     ++it;
     if (rr_new <= (double)tol2 * bb)
       state = ST_CONVERGED;
@@ -1129,7 +1133,6 @@ static int make_geo(const rwb_geometry_t* geom, Geo* g) {
   return RWB_OK;
 }
 
-constexpr int kCoopMaxBlocks = 4096;  // partial slots of the cooperative whole-level solve
 
 enum { L_Y, L_R, L_P0, L_P1, L_Q, L_WX, L_WY, L_WZ, L_SC, L_RR, L_PQ, L_BB, L_STATE, L_ITERS, L_TICKET,
        L_ALIST, L_PART, L_MISC, L_N };
@@ -1381,12 +1384,15 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
     int cgrid = 0;
     rc = coop_grid(&cgrid);
     if (rc) return rc;
-    cgrid = std::min(cgrid, std::max(g.tiles, 1));
+    // work items of kCoopTZ planes, spread evenly: every block gets the same number
+    int n_items = ((g.bz + kCoopTZ - 1) / kCoopTZ) * g.ty * g.tx;
+    const int rounds = (n_items + cgrid - 1) / cgrid;
+    cgrid = (n_items + rounds - 1) / rounds;
     float* part_pq = reinterpret_cast<float*>(w.part);
     float* part_rr = part_pq + kCoopMaxBlocks;
     float tol2v = tol2;
     int max_iter_v = max_iter;
-    void* args[] = {&g, &w, &part_pq, &part_rr, &tol2v, &max_iter_v};
+    void* args[] = {&g, &w, &part_pq, &part_rr, &n_items, &tol2v, &max_iter_v};
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     RWB_CUDA(cudaEventCreate(&ev0));
     RWB_CUDA(cudaEventCreate(&ev1));
