@@ -296,6 +296,103 @@ extern "C" int rwb_device_info(int32_t* sm_count, int32_t* cc_major, int32_t* cc
   return RWB_OK;
 }
 
+// 3-D LOD step, separable and staged through shared memory: a CTA owns a
+// coarse 8 (y) x 32 (x) column block and marches LZC coarse planes.  Per
+// coarse plane: (1) z-conv of the two child fine planes at every (y, x) of the
+// fine window incl. the 1-voxel clamp halo (18 x 66), each thread carrying two
+// fine values per column from the previous plane, so every fine voxel is read
+// once; (2) y-conv of the 16 child rows; (3) per output, the x-conv of its 8
+// children and the pairwise means.  Every intermediate is computed from the
+// same operands in the same order as lod_down_kernel (A = conv_z, B = conv_y(A),
+// C = f32(conv_x(B))), so the result is bit-identical; each conv is evaluated
+// once per fine position instead of up to 8 times.
+constexpr int LCX = 32, LCY = 8, LZC = 8;                // coarse tile and planes per CTA
+constexpr int LFX = 2 * LCX + 2, LFY = 2 * LCY + 2;      // fine window 66 x 18
+constexpr int LCOLS = LFX * LFY;                          // fine columns per CTA (1188)
+constexpr int LTH = LCX * LCY;                            // threads (one output each)
+constexpr int LCPT = (LCOLS + LTH - 1) / LTH;             // columns per thread (5)
+
+__global__ void __launch_bounds__(LTH) lod_down3_kernel(const float* __restrict__ src, Shape3 fs,
+                                                        float* __restrict__ dst, Shape3 cs) {
+  __shared__ double A[2][LFY][LFX];
+  __shared__ double B[2][2 * LCY][LFX];
+  const int tid = threadIdx.x;
+  const int cx0 = blockIdx.x * LCX, cy0 = blockIdx.y * LCY, cz0 = blockIdx.z * LZC;
+  const int fx0 = 2 * cx0 - 1, fy0 = 2 * cy0 - 1;
+  const long long sxy = (long long)fs.ny * fs.nx;
+  // this thread's fine columns (clamped level offsets) and the two fine values carried between planes
+  long long colo[LCPT];
+  bool colv[LCPT];
+  float c1[LCPT], c2[LCPT];
+#pragma unroll
+  for (int k = 0; k < LCPT; ++k) {
+    const int c = tid + k * LTH;
+    colv[k] = c < LCOLS;
+    const int ty = colv[k] ? c / LFX : 0, tx = colv[k] ? c % LFX : 0;
+    colo[k] = (long long)clampi(fy0 + ty, 0, fs.ny - 1) * fs.nx + clampi(fx0 + tx, 0, fs.nx - 1);
+    c1[k] = c2[k] = 0.f;
+  }
+  const int oy = tid / LCX, ox = tid % LCX;
+  const int jy = cy0 + oy, jx = cx0 + ox;
+  const int zend = min(cz0 + LZC, cs.nz);
+  for (int jz = cz0; jz < zend; ++jz) {
+    // (1) z-conv: fine planes 2jz-1 .. 2jz+2 (clamped); the first two carried from jz-1
+    const long long z2 = (long long)clampi(2 * jz + 1, 0, fs.nz - 1) * sxy;
+    const long long z3 = (long long)clampi(2 * jz + 2, 0, fs.nz - 1) * sxy;
+    const bool first = jz == cz0;
+    const long long z0 = (long long)clampi(2 * jz - 1, 0, fs.nz - 1) * sxy;
+    const long long z1 = (long long)clampi(2 * jz, 0, fs.nz - 1) * sxy;
+#pragma unroll
+    for (int k = 0; k < LCPT; ++k) {
+      if (!colv[k]) continue;
+      const float* s = src + colo[k];
+      const float v0 = first ? __ldg(s + z0) : c1[k];
+      const float v1 = first ? __ldg(s + z1) : c2[k];
+      const float v2 = __ldg(s + z2), v3 = __ldg(s + z3);
+      const int c = tid + k * LTH, ty = c / LFX, tx = c % LFX;
+      A[0][ty][tx] = conv3(v0, v1, v2);
+      A[1][ty][tx] = conv3(v1, v2, v3);
+      c1[k] = v2;
+      c2[k] = v3;
+    }
+    __syncthreads();
+    // (2) y-conv of the 16 child rows of both child planes
+    for (int e = tid; e < 2 * 2 * LCY * LFX; e += LTH) {
+      const int cz = e / (2 * LCY * LFX), rem = e % (2 * LCY * LFX), r = rem / LFX, tx = rem % LFX;
+      B[cz][r][tx] = conv3(A[cz][r][tx], A[cz][r + 1][tx], A[cz][r + 2][tx]);
+    }
+    __syncthreads();
+    // (3) x-conv of this output's 8 children, then the pairwise means (z, y, x)
+    if (jy < cs.ny && jx < cs.nx) {
+      float C[2][2][2];
+#pragma unroll
+      for (int cz = 0; cz < 2; ++cz)
+#pragma unroll
+        for (int cy = 0; cy < 2; ++cy)
+#pragma unroll
+          for (int cx = 0; cx < 2; ++cx) {
+            const double* b = &B[cz][2 * oy + cy][2 * ox + cx];
+            C[cz][cy][cx] = (float)conv3(b[0], b[1], b[2]);
+          }
+      const int ncz = (2 * jz + 1 < fs.nz) ? 2 : 1;
+      const int ncy = (2 * jy + 1 < fs.ny) ? 2 : 1;
+      const int ncx = (2 * jx + 1 < fs.nx) ? 2 : 1;
+      double m0[2][2];
+#pragma unroll
+      for (int cy = 0; cy < 2; ++cy)
+#pragma unroll
+        for (int cx = 0; cx < 2; ++cx)
+          m0[cy][cx] = ncz == 2 ? ((double)C[0][cy][cx] + (double)C[1][cy][cx]) * 0.5 : (double)C[0][cy][cx];
+      double m1[2];
+#pragma unroll
+      for (int cx = 0; cx < 2; ++cx) m1[cx] = ncy == 2 ? (m0[0][cx] + m0[1][cx]) * 0.5 : m0[0][cx];
+      const double m2 = ncx == 2 ? (m1[0] + m1[1]) * 0.5 : m1[0];
+      dst[((long long)jz * cs.ny + jy) * cs.nx + jx] = (float)m2;
+    }
+    __syncthreads();  // A and B are rewritten by the next plane
+  }
+}
+
 extern "C" int rwb_lod_down_f32(int32_t ndim, const int64_t* size, const float* src, float* dst, void* stream) {
   Shape3 fs, cs;
   int rc = shape_from(ndim, size, &fs);
@@ -306,7 +403,8 @@ extern "C" int rwb_lod_down_f32(int32_t ndim, const int64_t* size, const float* 
   if (ndim == 2) cs.nz = fs.nz;
   cudaStream_t st = (cudaStream_t)stream;
   if (ndim == 3)
-    lod_down_kernel<true, true><<<grid3(cs), kBlock3, 0, st>>>(src, fs, dst, cs);
+    lod_down3_kernel<<<dim3((cs.nx + LCX - 1) / LCX, (cs.ny + LCY - 1) / LCY, (cs.nz + LZC - 1) / LZC), LTH, 0, st>>>(
+        src, fs, dst, cs);
   else if (ndim == 2)
     lod_down_kernel<false, true><<<grid3(cs), kBlock3, 0, st>>>(src, fs, dst, cs);
   else
