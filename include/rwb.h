@@ -73,7 +73,6 @@ typedef struct {
 #define RWB_SOLVE_CLUSTER16 8 /* brick-resident solver: 16-CTA clusters, 2 CTAs/SM (default 8-CTA, 1 CTA/SM) */
 #define RWB_SOLVE_SPLIT_Z 16  /* brick-resident solver: 8-CTA clusters with 512 threads x 8 voxels per CTA */
 #define RWB_SOLVE_SETUP2 32   /* build the system with the two-kernel setup instead of the fused per-brick one */
-#define RWB_SOLVE_PIPELINED 64 /* brick-resident solver: pipelined CG (reduction overlapped with the SpMV) */
 
 /* Solver paths (rwb_solve_stats_t.path) */
 #define RWB_PATH_STREAMING 0 /* brick-batched CG, state in HBM, 2 launches per iteration */

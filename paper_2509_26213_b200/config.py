@@ -21,7 +21,6 @@ class RWConfig:
     resident: bool = True      # 32^3 bricks: solve each brick on chip (8-CTA cluster) instead of streaming
     cooperative: bool = True   # whole-level solves: one cooperative kernel for all iterations
     fused_setup: bool = True   # build the brick system with the fused per-brick setup kernel
-    pipelined: bool = False    # resident solver: pipelined CG (dot products overlapped with the SpMV)
     cluster: int = 8           # resident solver: CTAs per brick cluster (8: 1 CTA/SM; 16: 2 CTAs/SM, measured 1.7x slower)
 
     def params(self) -> dict:
@@ -32,5 +31,4 @@ class RWConfig:
         d.pop("cooperative")
         d.pop("cluster")
         d.pop("fused_setup")
-        d.pop("pipelined")
         return {k: (float(v) if isinstance(v, float) else int(v)) for k, v in d.items()}

@@ -34,11 +34,14 @@
 //      into its z-neighbours' shared memory with `st.async ...
 //      mbarrier::complete_tx` (DSMEM stores completing on the receiver's
 //      mbarrier).
-// Reduction: every warp shuffle-reduces its partials and lanes 0..7 st.async
-// them into slot [rank][warp] of all 8 CTAs; each CTA waits on its own
-// mbarrier and every warp sums the 64 partials with the same fixed shuffle
-// tree, so all CTAs take identical CG decisions (deterministic, independent
-// of brick scheduling and of which other bricks are solved).
+// Reduction: every warp shuffle-reduces its partials, warp 0 adds the warps'
+// sums in a fixed order and its lanes 0..7 st.async the CTA's pair into slot
+// [rank] of all 8 CTAs; each CTA waits on its own mbarrier and every thread
+// adds the 8 pairs in the same fixed tree (broadcast loads, no shuffles), so
+// all CTAs take identical CG decisions (deterministic, independent of brick
+// scheduling and of which other bricks are solved).  The scalar recurrences
+// use approximate reciprocals, 1/gamma and 1/alpha computed one iteration
+// ahead, so only one MUFU.RCP sits on the critical path.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -71,7 +74,7 @@ struct RCfg {
   static constexpr int RW = RTT / 32;            // warps per CTA
   static constexpr int RCL = RB / RPZ;           // CTAs per cluster (per brick)
   static constexpr int RV = RQ * TZT;            // voxels per thread
-  static constexpr int NPART = RCL * RW;         // pushed partials per reduction
+  static constexpr int NPART = RCL;              // pushed partials per reduction (one per CTA)
   static constexpr int SLAB = RPZ * PLANE;
   static constexpr int MINB = RPZ == 2 ? 2 : 1;  // CTAs per SM
   static constexpr int NBUF = MINB == 1 ? 2 : 1; // staging buffers (2: next brick prefetched)
@@ -111,9 +114,9 @@ struct ResidentSmem {
   float sr[C::NBUF][C::SLAB];              // staged r0
   float sv[C::NBUF][C::SLAB];              // staged y0
   float4 rp[RPZ][RB][RQN];                 // r planes of this slab (y neighbours of the SpMV)
-  float4 rp2[RPZ][RB][RQN];                // pipelined kernel: second buffer of the published planes
   float4 rface[2][2][RB][RQN];             // received faces [parity][0 = from below, 1 = from above]
-  __align__(16) float red[2][2][C::NPART];  // pushed partials [parity][gamma, delta][rank*RW + warp]
+  __align__(16) float red[2][2][C::NPART];  // pushed partials [parity][gamma, delta][rank]
+  float2 wpart[C::RW];                      // this CTA's per-warp (gamma, delta) before the CTA sum
   unsigned long long barF[2];            // mbarriers: r faces from the z neighbours, per parity
   unsigned long long barR[2];            // mbarriers: dot-product partials, per parity
   unsigned long long barL[2];            // mbarriers: bulk staging, per buffer
@@ -183,20 +186,26 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-// Sum of the N pushed partials (N = 64 or 128): lane l loads N/32 consecutive
-// partials with one vector load and the warp reduces them with a fixed
-// shuffle tree, so every warp of every CTA gets the bit-identical total
-// without a broadcast through shared memory.
+// Sum of the N pushed per-CTA partials (N = 8 or 16): every thread loads all
+// of them (broadcast LDS.128) and adds them in the same fixed tree, so every
+// warp of every CTA gets the bit-identical total.
 template <int N>
 __device__ __forceinline__ float sum_parts(const float* red) {
-  static_assert(N == 64 || N == 128, "partial count");
-  if constexpr (N == 64) {
-    const float2 v = reinterpret_cast<const float2*>(red)[threadIdx.x & 31];
-    return warp_sum(v.x + v.y);
-  } else {
-    const float4 v = reinterpret_cast<const float4*>(red)[threadIdx.x & 31];
-    return warp_sum((v.x + v.y) + (v.z + v.w));
+  static_assert(N == 8 || N == 16, "partial count");
+  const float4* v = reinterpret_cast<const float4*>(red);
+  const float4 a = v[0], b = v[1];
+  float s = ((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w));
+  if constexpr (N == 16) {
+    const float4 c = v[2], d = v[3];
+    s += ((c.x + c.y) + (c.z + c.w)) + ((d.x + d.y) + (d.z + d.w));
   }
+  return s;
+}
+
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 // Stage the slab of `slot` into buffer `buf` (one thread issues; completes on barL[buf]).
@@ -266,8 +275,8 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
       face_up_dst[par] = mapa_u32(smem_u32(&sm.rface[par][0][ly][xq]), rank + 1);
       bar_up[par] = mapa_u32(smem_u32(&sm.barR[par]), rank + 1);
     }
-    if (lane < RCL) {  // lane t delivers this warp's partials to CTA t
-      red_dst[par] = mapa_u32(smem_u32(&sm.red[par][0][rank * C::RW + warp]), lane);
+    if (warp == 0 && lane < RCL) {  // lane t of warp 0 delivers this CTA's partials to CTA t
+      red_dst[par] = mapa_u32(smem_u32(&sm.red[par][0][rank]), lane);
       barR_dst[par] = mapa_u32(smem_u32(&sm.barR[par]), lane);
     }
   }
@@ -338,7 +347,7 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
     // so they stay bit-identical and the next SpMV needs no second exchange.
     // (Pushing r faces as well would double the DSMEM volume, which at ~20 B/cycle
     // per SM is what bounds the exchange.)
-    float gamma = 0.f, alpha = 0.f;
+    float gamma = 0.f, alpha = 0.f, rgamma = 0.f, ralpha = 0.f;
     int state = ST_ACTIVE, it = 0;
     float4 rf_dn = f4(0, 0, 0, 0), rf_up = f4(0, 0, 0, 0);  // neighbours' r at my faces
     float4 sf_dn = f4(0, 0, 0, 0), sf_up = f4(0, 0, 0, 0);  // ... and their s
@@ -357,10 +366,8 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
       // complete the phase's partial slots with zeros (this exchange carries no dot products)
       if (warp == 0 && lane < RCL) {
         const uint32_t dst = par ? red_dst[1] : red_dst[0], bar = par ? barR_dst[1] : barR_dst[0];
-        for (int wv = 0; wv < C::RW; ++wv) {
-          st_async_f32(dst + wv * 4, 0.f, bar);
-          st_async_f32(dst + NPART * 4 + wv * 4, 0.f, bar);
-        }
+        st_async_f32(dst, 0.f, bar);
+        st_async_f32(dst + NPART * 4, 0.f, bar);
       }
       mbar_wait(&sm.barR[par], ph);
       ++gk;
@@ -420,12 +427,24 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
           gs += g4[z];
           ds += d4[z];
         }
+        // warp sums -> CTA sum (fixed order) -> one st.async pair per CTA into every CTA
         const float gw = warp_sum(gs);
         const float dw = warp_sum(ds);
-        if (lane < RCL) {
-          const uint32_t dst = par ? red_dst[1] : red_dst[0], bar = par ? barR_dst[1] : barR_dst[0];
-          st_async_f32(dst, gw, bar);
-          st_async_f32(dst + NPART * 4, dw, bar);
+        if (lane == 0) sm.wpart[warp] = make_float2(gw, dw);
+        asm volatile("bar.sync 1, %0;" ::"n"(RTT) : "memory");
+        if (warp == 0) {
+          float gc = 0.f, dc = 0.f;
+#pragma unroll
+          for (int wv = 0; wv < C::RW; ++wv) {
+            const float2 v = sm.wpart[wv];
+            gc += v.x;
+            dc += v.y;
+          }
+          if (lane < RCL) {
+            const uint32_t dst = par ? red_dst[1] : red_dst[0], bar = par ? barR_dst[1] : barR_dst[0];
+            st_async_f32(dst, gc, bar);
+            st_async_f32(dst + NPART * 4, dc, bar);
+          }
         }
       }
       TRACE(2);
@@ -438,7 +457,7 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
       if (pass == 0) {
         // the setup already settled zero-rhs and converged-at-start bricks
         beta = 0.f;
-        alpha = delta != 0.f ? __fdividef(g_new, delta) : 0.f;
+        alpha = delta != 0.f ? g_new * rcp_ftz(delta) : 0.f;
         if (a.max_iter <= 0) {
           state = ST_MAXITER;
           break;
@@ -452,12 +471,15 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
           state = ST_MAXITER;
           break;
         }
-        // fast reciprocals: the scalars only need to be identical in every CTA
-        beta = __fdividef(g_new, gamma);
-        const float den = delta - beta * __fdividef(g_new, alpha);
-        alpha = den != 0.f ? __fdividef(g_new, den) : 0.f;
+        // fast reciprocals, 1/gamma and 1/alpha taken off the critical path in the
+        // previous iteration: the scalars only need to be identical in every CTA
+        beta = g_new * rgamma;
+        const float den = delta - beta * (g_new * ralpha);
+        alpha = den != 0.f ? g_new * rcp_ftz(den) : 0.f;
       }
       gamma = g_new;
+      rgamma = rcp_ftz(g_new);
+      ralpha = rcp_ftz(alpha);
       TRACE(4);
       // update k: p = r + beta p, s = w + beta s, y += alpha p, r -= alpha s (and the neighbour faces)
 #pragma unroll
@@ -516,319 +538,6 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
   }
 }
 
-// ---- pipelined variant ------------------------------------------------------------
-//
-// Pipelined CG (Ghysels & Vanroose 2014, unpreconditioned on the Jacobi-scaled
-// system): w = A'r and z = A'w are carried as recurrences, so the SpMV of an
-// iteration, q = A'w, does not depend on that iteration's dot products.  Each
-// iteration pushes its partials (gamma = r.r, delta = w.r) FIRST, then runs
-// the SpMV while the cluster-wide reduction is in flight, then waits:
-//   beta = gamma / gamma_prev,  alpha = gamma / (delta - beta gamma / alpha_prev)
-//   z = q + beta z,  s = w + beta s,  p = r + beta p,
-//   y += alpha p,  r -= alpha s,  w -= alpha z.
-// Slab-face values of w for the next SpMV are advanced locally from the
-// neighbours' pushed q faces (zf = qf + beta zf, wf -= alpha zf, the same fmaf
-// as their owner), which travel on a separate mbarrier (barF) and are waited
-// for only after the update, so neither the reduction nor the face transfer is
-// on the iteration's critical path.  The published planes alternate between two
-// buffers (rp / rp2) because the partials no longer prove that every warp has
-// left the previous SpMV.
-template <int RPZ, int TZT>
-__global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) resident3d_pipe_kernel(ResidentArgs a) {
-  using C = RCfg<RPZ, TZT>;
-  constexpr int RCL = C::RCL, RV = C::RV, NPART = C::NPART, NBUF = C::NBUF, RTT = C::RTT, NZG = C::NZG;
-  cg::cluster_group cluster = cg::this_cluster();
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  ResidentSmem<RPZ, TZT>& sm = *reinterpret_cast<ResidentSmem<RPZ, TZT>*>(smem_raw);
-  const int rank = (int)cluster.block_rank();
-  const int tid = threadIdx.x;
-  const int warp = tid >> 5, lane = tid & 31;
-  const int zg = tid / RT;
-  const int ly = (tid % RT) / RQN;
-  const int xq = tid % RQN;
-  const int pz0 = zg * TZT;
-  const bool below = rank > 0, above = rank < RCL - 1;
-  const bool first_zg = zg == 0, last_zg = zg == NZG - 1;
-  const bool push_dn = below && first_zg, push_up = above && last_zg;
-  const int nfaces = (int)below + (int)above;
-  const uint32_t tx_faces = nfaces * (uint32_t)(RB * RQN * sizeof(float4));
-  const int cid = blockIdx.x / RCL, ncl = gridDim.x / RCL;
-  const int n_act = *a.n_active;
-
-  if (tid == 0) {
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&sm.barF[i], 1);
-      mbar_init(&sm.barR[i], 1);
-      mbar_init(&sm.barL[i], 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (rank == 0)
-    for (int i = tid; i < PLANE; i += RTT)
-#pragma unroll
-      for (int b = 0; b < NBUF; ++b) sm.sz[b][i] = 0.f;
-  uint32_t face_dn_dst[2] = {0, 0}, face_up_dst[2] = {0, 0}, bar_dn[2] = {0, 0}, bar_up[2] = {0, 0};
-  uint32_t red_dst[2] = {0, 0}, barR_dst[2] = {0, 0};
-#pragma unroll
-  for (int par = 0; par < 2; ++par) {
-    if (push_dn) {
-      face_dn_dst[par] = mapa_u32(smem_u32(&sm.rface[par][1][ly][xq]), rank - 1);
-      bar_dn[par] = mapa_u32(smem_u32(&sm.barF[par]), rank - 1);
-    }
-    if (push_up) {
-      face_up_dst[par] = mapa_u32(smem_u32(&sm.rface[par][0][ly][xq]), rank + 1);
-      bar_up[par] = mapa_u32(smem_u32(&sm.barF[par]), rank + 1);
-    }
-    if (lane < RCL) {
-      red_dst[par] = mapa_u32(smem_u32(&sm.red[par][0][rank * C::RW + warp]), lane);
-      barR_dst[par] = mapa_u32(smem_u32(&sm.barR[par]), lane);
-    }
-  }
-  cluster.sync();
-  unsigned kf = 0, kr = 0;        // completed uses of barF / barR (parities)
-  unsigned uses0 = 0, uses1 = 0;  // completed uses of each staging buffer
-#ifdef RWB_TRACE
-  int btrace_n = 0;
-#endif
-  const float4 z4 = f4(0, 0, 0, 0);
-  auto plane4 = [&](const float* v, int z) { return f4(v[z * RQ], v[z * RQ + 1], v[z * RQ + 2], v[z * RQ + 3]); };
-  // one face exchange on barF: push planes 0 / TZT-1 of v, wait, return the received faces
-  auto face_push = [&](const float* v) {
-    const int par = kf & 1;
-    if (push_dn) st_async_v4(par ? face_dn_dst[1] : face_dn_dst[0], plane4(v, 0), par ? bar_dn[1] : bar_dn[0]);
-    if (push_up) st_async_v4(par ? face_up_dst[1] : face_up_dst[0], plane4(v, TZT - 1), par ? bar_up[1] : bar_up[0]);
-  };
-  auto face_wait = [&](float4& f_dn, float4& f_up) {
-    const int par = kf & 1;
-    mbar_wait(&sm.barF[par], (kf >> 1) & 1);
-    f_dn = push_dn ? sm.rface[par][0][ly][xq] : z4;
-    f_up = push_up ? sm.rface[par][1][ly][xq] : z4;
-    ++kf;
-  };
-  auto face_expect = [&]() {
-    if (tid == 0) mbar_expect_tx(&sm.barF[kf & 1], tx_faces);
-  };
-
-  int buf = 0;
-  if (cid < n_act && tid == 0) stage_slab<RPZ, TZT>(a, sm, 0, a.alist[cid], rank);
-  for (int j = cid; j < n_act; j += ncl, buf ^= (NBUF - 1)) {
-    BTRACE(0);
-    const int slot = a.alist[j];
-    if (NBUF == 2 && j + ncl < n_act && tid == 0) stage_slab<RPZ, TZT>(a, sm, buf ^ 1, a.alist[j + ncl], rank);
-    if (buf) {
-      mbar_wait(&sm.barL[1], uses1 & 1);
-      ++uses1;
-    } else {
-      mbar_wait(&sm.barL[0], uses0 & 1);
-      ++uses0;
-    }
-    BTRACE(1);
-
-    float y[RV], r[RV], p[RV], sv[RV], w[RV], zv[RV], q[RV];
-    float wxf[RV], wyf[RV], wzf[RV], wyb[RV], wxb[TZT], wzb[RQ];
-#pragma unroll
-    for (int z = 0; z < TZT; ++z) {
-      const int pz = pz0 + z;
-      const int o = pz * PLANE + ly * RB + xq * RQ;
-      const float4 fx = *reinterpret_cast<const float4*>(&sm.sx[buf][o]);
-      const float4 fy = *reinterpret_cast<const float4*>(&sm.sy[buf][o]);
-      const float4 fz = *reinterpret_cast<const float4*>(&sm.sz[buf][PLANE + o]);
-      const float4 fyb = ly > 0 ? *reinterpret_cast<const float4*>(&sm.sy[buf][o - RB]) : z4;
-      const float4 fr = *reinterpret_cast<const float4*>(&sm.sr[buf][o]);
-      const float4 fv = *reinterpret_cast<const float4*>(&sm.sv[buf][o]);
-      wxb[z] = xq > 0 ? sm.sx[buf][o - 1] : 0.f;
-      if (z == 0) {
-        const float4 fzb = *reinterpret_cast<const float4*>(&sm.sz[buf][o]);
-#pragma unroll
-        for (int i = 0; i < RQ; ++i) wzb[i] = lane_of(fzb, i);
-      }
-#pragma unroll
-      for (int i = 0; i < RQ; ++i) {
-        const int v = z * RQ + i;
-        wxf[v] = lane_of(fx, i);
-        wyf[v] = lane_of(fy, i);
-        wzf[v] = lane_of(fz, i);
-        wyb[v] = lane_of(fyb, i);
-        r[v] = lane_of(fr, i);
-        y[v] = lane_of(fv, i);
-        p[v] = 0.f;
-        sv[v] = 0.f;
-        zv[v] = 0.f;
-      }
-    }
-    const float thresh = (float)((double)a.tol2 * a.bb[slot]);
-    BTRACE(2);
-
-    // out = A' in (brick-local), planes[] = the published copy of `in`, f_dn / f_up its neighbours' faces
-    auto spmv = [&](const float* in, float* out, float4 (*planes)[RB][RQN], const float4& f_dn, const float4& f_up) {
-#pragma unroll
-      for (int z = 0; z < TZT; ++z) {
-        const int pz = pz0 + z;
-        const float4 ru = ly + 1 < RB ? planes[pz][ly + 1][xq] : z4;
-        const float4 rd = ly > 0 ? planes[pz][ly - 1][xq] : z4;
-        const float4 rzu = z + 1 < TZT ? plane4(in, z + 1) : (pz + 1 < RPZ ? planes[pz + 1][ly][xq] : f_up);
-        const float4 rzd = z > 0 ? plane4(in, z - 1) : (pz > 0 ? planes[pz - 1][ly][xq] : f_dn);
-        const float rl = __shfl_up_sync(0xffffffffu, in[z * RQ + RQ - 1], 1);
-        const float rr_ = __shfl_down_sync(0xffffffffu, in[z * RQ], 1);
-#pragma unroll
-        for (int i = 0; i < RQ; ++i) {
-          const int v = z * RQ + i;
-          const float rxl = i > 0 ? in[v - 1] : rl;
-          const float rxr = i < RQ - 1 ? in[v + 1] : rr_;
-          const float wxl = i > 0 ? wxf[v - 1] : wxb[z];
-          const float wzl = z > 0 ? wzf[v - RQ] : wzb[i];
-          float acc = wxf[v] * rxr;
-          acc = fmaf(wxl, rxl, acc);
-          acc = fmaf(wyf[v], lane_of(ru, i), acc);
-          acc = fmaf(wyb[v], lane_of(rd, i), acc);
-          acc = fmaf(wzf[v], lane_of(rzu, i), acc);
-          acc = fmaf(wzl, lane_of(rzd, i), acc);
-          out[v] = in[v] - acc;
-        }
-      }
-    };
-    auto publish = [&](const float* v, float4 (*planes)[RB][RQN]) {
-#pragma unroll
-      for (int z = 0; z < TZT; ++z) planes[pz0 + z][ly][xq] = plane4(v, z);
-    };
-    auto push_partials = [&](float gs, float ds) {
-      const int par = kr & 1;
-      if (tid == 0) mbar_expect_tx(&sm.barR[par], 2 * NPART * 4);
-      const float gw = warp_sum(gs);
-      const float dw = warp_sum(ds);
-      if (lane < RCL) {
-        const uint32_t dst = par ? red_dst[1] : red_dst[0], bar = par ? barR_dst[1] : barR_dst[0];
-        st_async_f32(dst, gw, bar);
-        st_async_f32(dst + NPART * 4, dw, bar);
-      }
-    };
-
-    // ---- start: r0 faces, w0 = A'r0, w0 faces ----
-    float4 wf_dn, wf_up, zf_dn = z4, zf_up = z4;
-    publish(r, sm.rp);
-    face_expect();
-    face_push(r);
-    face_wait(wf_dn, wf_up);  // (r0 faces)
-    __syncthreads();
-    spmv(r, w, sm.rp, wf_dn, wf_up);
-    face_expect();
-    face_push(w);
-    publish(w, sm.rp2);
-    float gs = 0.f, ds = 0.f;
-#pragma unroll
-    for (int v = 0; v < RV; ++v) {
-      gs = fmaf(r[v], r[v], gs);
-      ds = fmaf(w[v], r[v], ds);
-    }
-    face_wait(wf_dn, wf_up);
-    __syncthreads();
-
-    float gamma = 0.f, alpha = 0.f;
-    int state = ST_ACTIVE, it = 0;
-#ifdef RWB_TRACE
-    int trace_it = (int)kr;
-#endif
-    for (int pass = 0;; ++pass) {
-      TRACE(0);
-      float4 (*cur)[RB][RQN] = (pass & 1) ? sm.rp : sm.rp2;
-      float4 (*nxt)[RB][RQN] = (pass & 1) ? sm.rp2 : sm.rp;
-      push_partials(gs, ds);
-      face_expect();
-      TRACE(1);
-      spmv(w, q, cur, wf_dn, wf_up);
-      face_push(q);
-      TRACE(2);
-      {
-        const int par = kr & 1;
-        mbar_wait(&sm.barR[par], (kr >> 1) & 1);
-        ++kr;
-      }
-      TRACE(3);
-      const float g_new = sum_parts<NPART>(sm.red[(kr - 1) & 1][0]);
-      const float delta = sum_parts<NPART>(sm.red[(kr - 1) & 1][1]);
-      float beta;
-      bool stop = false;
-      if (pass == 0) {
-        beta = 0.f;
-        alpha = delta != 0.f ? __fdividef(g_new, delta) : 0.f;
-        if (a.max_iter <= 0) {
-          state = ST_MAXITER;
-          stop = true;
-        }
-      } else {
-        if (g_new <= thresh) {
-          state = ST_CONVERGED;
-          stop = true;
-        } else if (it >= a.max_iter) {
-          state = ST_MAXITER;
-          stop = true;
-        }
-        beta = __fdividef(g_new, gamma);
-        const float den = delta - beta * __fdividef(g_new, alpha);
-        alpha = den != 0.f ? __fdividef(g_new, den) : 0.f;
-      }
-      if (stop) {  // consume this iteration's face exchange so the barrier phases stay paired
-        float4 d0, d1;
-        face_wait(d0, d1);
-        break;
-      }
-      gamma = g_new;
-      TRACE(4);
-      gs = 0.f;
-      ds = 0.f;
-#pragma unroll
-      for (int v = 0; v < RV; ++v) {
-        zv[v] = fmaf(beta, zv[v], q[v]);
-        sv[v] = fmaf(beta, sv[v], w[v]);
-        p[v] = fmaf(beta, p[v], r[v]);
-        y[v] = fmaf(alpha, p[v], y[v]);
-        r[v] = fmaf(-alpha, sv[v], r[v]);
-        w[v] = fmaf(-alpha, zv[v], w[v]);
-        gs = fmaf(r[v], r[v], gs);
-        ds = fmaf(w[v], r[v], ds);
-      }
-      ++it;
-      publish(w, nxt);
-      {
-        float4 qn_dn, qn_up;
-        face_wait(qn_dn, qn_up);
-        zf_dn = f4(fmaf(beta, zf_dn.x, qn_dn.x), fmaf(beta, zf_dn.y, qn_dn.y), fmaf(beta, zf_dn.z, qn_dn.z),
-                   fmaf(beta, zf_dn.w, qn_dn.w));
-        wf_dn = f4(fmaf(-alpha, zf_dn.x, wf_dn.x), fmaf(-alpha, zf_dn.y, wf_dn.y), fmaf(-alpha, zf_dn.z, wf_dn.z),
-                   fmaf(-alpha, zf_dn.w, wf_dn.w));
-        zf_up = f4(fmaf(beta, zf_up.x, qn_up.x), fmaf(beta, zf_up.y, qn_up.y), fmaf(beta, zf_up.z, qn_up.z),
-                   fmaf(beta, zf_up.w, qn_up.w));
-        wf_up = f4(fmaf(-alpha, zf_up.x, wf_up.x), fmaf(-alpha, zf_up.y, wf_up.y), fmaf(-alpha, zf_up.z, wf_up.z),
-                   fmaf(-alpha, zf_up.w, wf_up.w));
-      }
-      __syncthreads();
-      TRACE(5);
-#ifdef RWB_TRACE
-      ++trace_it;
-#endif
-    }
-    BTRACE(6);
-    {
-      const long long base = (long long)slot * (RB * RB * RB) + (long long)rank * C::SLAB;
-#pragma unroll
-      for (int z = 0; z < TZT; ++z)
-        *reinterpret_cast<float4*>(a.y + base + (pz0 + z) * PLANE + ly * RB + xq * RQ) =
-            f4(y[z * RQ], y[z * RQ + 1], y[z * RQ + 2], y[z * RQ + 3]);
-    }
-    if (rank == 0 && tid == 0) {
-      a.state[slot] = state;
-      a.iters[slot] = it;
-    }
-    __syncthreads();
-    if (NBUF == 1 && j + ncl < n_act && tid == 0) stage_slab<RPZ, TZT>(a, sm, 0, a.alist[j + ncl], rank);
-    BTRACE(7);
-#ifdef RWB_TRACE
-    ++btrace_n;
-#endif
-  }
-}
-
 #ifdef RWB_TRACE
 extern "C" int rwb_trace_dump(long long* out) {  // 8*64*8 int64
   return (int)cudaMemcpyFromSymbol(out, g_rwb_trace, sizeof(g_rwb_trace));
@@ -840,11 +549,11 @@ extern "C" int rwb_btrace_dump(long long* out) {  // 8*16*10 int64
 
 int resident3d_supported(const Geo& g) { return g.is3d && g.bz == RB && g.by == RB && g.bx == RB; }
 
-template <int RPZ, int TZT, bool PIPE>
+template <int RPZ, int TZT>
 static int launch_resident(const ResidentArgs& a, int max_bricks, cudaStream_t st) {
   using C = RCfg<RPZ, TZT>;
   static thread_local int clusters = 0;
-  auto kern = PIPE ? resident3d_pipe_kernel<RPZ, TZT> : resident3d_kernel<RPZ, TZT>;
+  auto kern = resident3d_kernel<RPZ, TZT>;
   const int smem = (int)sizeof(ResidentSmem<RPZ, TZT>);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr;
@@ -874,18 +583,11 @@ static int launch_resident(const ResidentArgs& a, int max_bricks, cudaStream_t s
   return RWB_OK;
 }
 
-int launch_resident3d(const ResidentArgs& a, int max_bricks, int variant, bool pipelined, cudaStream_t st) {
-  if (pipelined) {
-    switch (variant) {
-      case 16: return launch_resident<2, 2, true>(a, max_bricks, st);
-      case 512: return launch_resident<4, 2, true>(a, max_bricks, st);
-      default: return launch_resident<4, 4, true>(a, max_bricks, st);
-    }
-  }
+int launch_resident3d(const ResidentArgs& a, int max_bricks, int variant, cudaStream_t st) {
   switch (variant) {
-    case 16: return launch_resident<2, 2, false>(a, max_bricks, st);
-    case 512: return launch_resident<4, 2, false>(a, max_bricks, st);
-    default: return launch_resident<4, 4, false>(a, max_bricks, st);
+    case 16: return launch_resident<2, 2>(a, max_bricks, st);
+    case 512: return launch_resident<4, 2>(a, max_bricks, st);
+    default: return launch_resident<4, 4>(a, max_bricks, st);
   }
 }
 

@@ -41,7 +41,6 @@ struct ResidentArgs {
 
 int resident3d_supported(const Geo& g);
 // variant: 8 = 8-CTA clusters (4 planes per CTA), 16 = 16-CTA clusters (2 planes per CTA, 2 CTAs/SM)
-// pipelined: Ghysels-Vanroose pipelined CG (reduction overlapped with the SpMV) instead of Chronopoulos-Gear
-int launch_resident3d(const ResidentArgs& a, int max_bricks, int variant, bool pipelined, cudaStream_t st);
+int launch_resident3d(const ResidentArgs& a, int max_bricks, int variant, cudaStream_t st);
 
 }  // namespace rwb

@@ -1358,8 +1358,7 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
     RWB_CUDA(cudaEventCreate(&ev0));
     RWB_CUDA(cudaEventCreate(&ev1));
     RWB_CUDA(cudaEventRecord(ev0, st));
-    rc = launch_resident3d(ra, nb, (params->flags & RWB_SOLVE_CLUSTER16) ? 16 : ((params->flags & RWB_SOLVE_SPLIT_Z) ? 512 : 8),
-                           (params->flags & RWB_SOLVE_PIPELINED) != 0, st);
+    rc = launch_resident3d(ra, nb, (params->flags & RWB_SOLVE_CLUSTER16) ? 16 : ((params->flags & RWB_SOLVE_SPLIT_Z) ? 512 : 8), st);
     if (rc) {
       cudaEventDestroy(ev0);
       cudaEventDestroy(ev1);

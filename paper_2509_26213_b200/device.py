@@ -195,8 +195,6 @@ def _flags(cfg: RWConfig) -> int:
         f |= _native.SOLVE_NO_COOP
     if not cfg.fused_setup:
         f |= _native.SOLVE_SETUP2
-    if cfg.pipelined:
-        f |= _native.SOLVE_PIPELINED
     if cfg.cluster == 16:
         f |= _native.SOLVE_CLUSTER16
     elif cfg.cluster == 512:  # 8-CTA clusters, 512 threads per CTA

@@ -324,14 +324,13 @@ def test_upsample_window_slabs_match_full(rng):
             assert np.isnan(got[:z0]).all() and np.isnan(got[z1:]).all()
 
 
-@pytest.mark.parametrize("pipelined", [False, True])
 @pytest.mark.parametrize("cluster", [8, 16, 512])
-def test_resident_cluster_variants(rng, cluster, pipelined):
+def test_resident_cluster_variants(rng, cluster):
     vol = synthetic.phantom((64, 96, 64))
     seeds = synthetic.seeds(vol.shape, "S1")
     bound = rng.random(vol.shape).astype(np.float32)
     ref = orw.solve_level(vol, seeds, (32, 32, 32), bound.astype(np.float64), TIGHT).prob
-    cfg = RWConfig(tol=GPU_CFG.tol, max_iter=GPU_CFG.max_iter, cluster=cluster, pipelined=pipelined)
+    cfg = RWConfig(tol=GPU_CFG.tol, max_iter=GPU_CFG.max_iter, cluster=cluster)
     out, st = device.solve_level(cuda(vol), cuda(seeds), (32, 32, 32), cuda(bound), cfg)
     assert st["path"] == 1 and st["not_converged"] == 0
     assert_rw_parity(host(out), ref)

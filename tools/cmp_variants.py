@@ -12,7 +12,7 @@ import torch  # noqa: E402
 from paper_2509_26213_b200 import device, synthetic  # noqa: E402
 from paper_2509_26213_b200.config import RWConfig  # noqa: E402
 
-variants = [a.split("=", 1) for a in sys.argv[1:]] or [["cg", "{}"], ["pipe", '{"pipelined": true}']]
+variants = [a.split("=", 1) for a in sys.argv[1:]] or [["cg", "{}"]]
 n = int(os.environ.get("CMP_N", "1024"))
 vol = synthetic.phantom_device((n,) * 3)
 sd = synthetic.seeds_device((n,) * 3)
