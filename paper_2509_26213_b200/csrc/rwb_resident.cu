@@ -120,6 +120,7 @@ struct ResidentSmem {
   unsigned long long barF[2];            // mbarriers: r faces from the z neighbours, per parity
   unsigned long long barR[2];            // mbarriers: dot-product partials, per parity
   unsigned long long barL[2];            // mbarriers: bulk staging, per buffer
+  unsigned long long barS[2];            // mbarriers: Jacobi scales staged into sr[] for the epilogue
 };
 
 // ---- PTX helpers ----------------------------------------------------------------
@@ -255,6 +256,7 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
       mbar_init(&sm.barF[i], 1);
       mbar_init(&sm.barR[i], 1);
       mbar_init(&sm.barL[i], 1);
+      mbar_init(&sm.barS[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -283,6 +285,7 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
   cluster.sync();  // barriers initialised and the zero plane written before any remote access
   unsigned gk = 0;  // CG passes run by this cluster so far (drives the exchange-barrier parities)
   unsigned uses0 = 0, uses1 = 0;  // completed uses of each staging buffer (barL parities)
+  unsigned usesS0 = 0, usesS1 = 0;  // ... and of the scale copies (barS parities)
 #ifdef RWB_TRACE
   int btrace_n = 0;
 #endif
@@ -373,7 +376,14 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
       ++gk;
       if (first_zg && below) rf_dn = sm.rface[par][0][ly][xq];
       if (last_zg && above) rf_up = sm.rface[par][1][ly][xq];
-      __syncthreads();  // own r planes published
+      __syncthreads();  // own r planes published; every thread has left the staged slab
+    }
+    // the staged r0 is in registers: fetch the slab's Jacobi scales into its place
+    // while the brick iterates (the epilogue at the end needs them)
+    if (tid == 0) {
+      const long long base = (long long)slot * (RB * RB * RB) + (long long)rank * C::SLAB;
+      mbar_expect_tx(&sm.barS[buf], C::SLAB * 4);
+      bulk_g2s(sm.sr[buf], a.sc + base, C::SLAB * 4, &sm.barS[buf]);
     }
 #ifdef RWB_TRACE
     int trace_it = (int)gk;
@@ -514,13 +524,46 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
 #endif
     }
     BTRACE(6);
-    // ---------------- y back to the brick-local workspace ----------------
+    // ---------------- epilogue: probabilities and labels straight into the level ----------------
     {
-      const long long base = (long long)slot * (RB * RB * RB) + (long long)rank * C::SLAB;
+      if (buf) {
+        mbar_wait(&sm.barS[1], usesS1 & 1);
+        ++usesS1;
+      } else {
+        mbar_wait(&sm.barS[0], usesS0 & 1);
+        ++usesS0;
+      }
+      const int brick = a.list ? a.list[slot] : slot;
+      const int hx = brick % a.gx, hy = (brick / a.gx) % a.gy, hz = brick / (a.gx * a.gy);
+      const int gy = a.oy + hy * RB + ly, gx0 = a.ox + hx * RB + xq * RQ;
+      const bool row_in = gy >= 0 && gy < a.ny;
+      const bool quad_in = gx0 >= 0 && gx0 + RQ <= a.nx;
 #pragma unroll
-      for (int z = 0; z < TZT; ++z)
-        *reinterpret_cast<float4*>(a.y + base + (pz0 + z) * PLANE + ly * RB + xq * RQ) =
-            f4(y[z * RQ], y[z * RQ + 1], y[z * RQ + 2], y[z * RQ + 3]);
+      for (int z = 0; z < TZT; ++z) {
+        const int gz = a.oz + hz * RB + rank * RPZ + pz0 + z;
+        if (!row_in || gz < 0 || gz >= a.nz) continue;
+        const float4 s4 = *reinterpret_cast<const float4*>(&sm.sr[buf][(pz0 + z) * PLANE + ly * RB + xq * RQ]);
+        float pv[RQ];
+#pragma unroll
+        for (int i = 0; i < RQ; ++i) {
+          const float s = lane_of(s4, i), yv = y[z * RQ + i];
+          pv[i] = s > 0.f ? s * yv : yv;
+        }
+        const long long gi = ((long long)gz * a.ny + gy) * a.nx + gx0;
+        if (quad_in && (gi & 3) == 0) {
+          *reinterpret_cast<float4*>(a.prob + gi) = f4(pv[0], pv[1], pv[2], pv[3]);
+          if (a.labels)
+            *reinterpret_cast<uchar4*>(a.labels + gi) =
+                make_uchar4(pv[0] > 0.5f, pv[1] > 0.5f, pv[2] > 0.5f, pv[3] > 0.5f);
+        } else {
+#pragma unroll
+          for (int i = 0; i < RQ; ++i) {
+            if (gx0 + i < 0 || gx0 + i >= a.nx) continue;
+            a.prob[gi + i] = pv[i];
+            if (a.labels) a.labels[gi + i] = pv[i] > 0.5f ? 1 : 0;
+          }
+        }
+      }
     }
     if (rank == 0 && tid == 0) {
       a.state[slot] = state;

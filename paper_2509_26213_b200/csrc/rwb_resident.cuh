@@ -29,7 +29,8 @@ struct ResidentArgs {
   const float* wy;
   const float* wz;
   const float* r0;        // initial scaled residual
-  float* y;               // in: y0 = x0 / s, out: the solution of the scaled system
+  const float* y;         // y0 = x0 / s (unknowns), the final value (other voxels)
+  const float* sc;        // Jacobi scale s (0: not an unknown)
   const double* bb;       // per slot ||S b||^2
   const int* alist;       // compacted slots still active after the setup
   const int* n_active;
@@ -37,6 +38,13 @@ struct ResidentArgs {
   int* iters;             // per slot
   float tol2;
   int max_iter;
+  // results straight into the level: prob = s y (unknowns) or y, labels = prob > 0.5
+  float* prob;
+  uint8_t* labels;        // may be null
+  const int* list;        // slot -> brick id (null: identity)
+  int nz, ny, nx;         // level
+  int oz, oy, ox;         // brick grid origin
+  int gy, gx;             // brick grid extents in y, x
 };
 
 int resident3d_supported(const Geo& g);

@@ -344,6 +344,12 @@ __global__ void __launch_bounds__(NTHREADS) setup_system_kernel(Geo g, Work w, c
         const float sb = si * b;
         acc_bb = fmaf(sb, sb, acc_bb);
         acc_rr = fmaf(r, r, acc_rr);
+      } else if (colin && gz >= 0 && gz < g.nz) {
+        // not an unknown: y holds the voxel's final value (seed value, else bound),
+        // which no CG path changes (its r, p, s, w stay exactly 0)
+        const long long gi = (long long)gz * g.sxy + (long long)gy * g.nx + gx;
+        const uint8_t sv = __ldg(S + gi);
+        y = sv ? seed_value(sv) : (bound ? __ldg(bound + gi) : 0.f);
       }
       wx[li] = wf[5];
       wy[li] = wf[3];
@@ -661,7 +667,8 @@ __global__ void __launch_bounds__(STH, 2) setup_brick_kernel(const __grid_consta
           wfy[i] = unk ? fy : 0.f;
           wfz[i] = unk ? fz : 0.f;
           r[i] = unk ? ri : 0.f;
-          y[i] = unk ? initial_y(x0, si, diag) : 0.f;
+          // not an unknown: y holds the voxel's final value (seed value, else bound)
+          y[i] = unk ? initial_y(x0, si, diag) : (vz ? dv_z[i] : 0.f);
           acc_bb[i] = unk ? fmaf(sb, sb, acc_bb[i]) : acc_bb[i];
           acc_rr[i] = unk ? fmaf(ri, ri, acc_rr[i]) : acc_rr[i];
         }
@@ -1015,6 +1022,8 @@ __global__ void __launch_bounds__(1024) advance_kernel(Work w, int nb, int k) {
     int off = 0;
     for (int i = 0; i < wid; ++i) off += warp_tot[i];
     if (a) w.alist[base + off + pre] = s;
+    // the settled slots fill the list from its end: alist[nb-1-i], i = their rank
+    if (s < nb && !a) w.alist[nb - 1 - (start - base - off - pre + threadIdx.x)] = s;
     __syncthreads();
     if (threadIdx.x == 0) {
       int t = 0;
@@ -1038,11 +1047,9 @@ __global__ void finalize_kernel(Work w, int nb) {
 }
 
 // prob = seed value | s*y | 0 (zero-rhs brick) | bound (isolated voxel)
-__global__ void __launch_bounds__(NTHREADS) epilogue_kernel(Geo g, Work w, const int* __restrict__ list,
-                                                            const uint8_t* __restrict__ S,
-                                                            const float* __restrict__ bound,
-                                                            float* __restrict__ prob, uint8_t* __restrict__ labels) {
-  TileCtx c = tile_ctx(g, list);
+// prob / labels of one tile of a brick from the brick-local solution
+__device__ __forceinline__ void epilogue_tile(const Geo& g, const Work& w, const TileCtx& c, float* __restrict__ prob,
+                                              uint8_t* __restrict__ labels) {
   if (!c.col) return;
   const int gy = c.gy0 + c.ly, gx = c.gx0 + c.lx;
   if (gy < 0 || gy >= g.ny || gx < 0 || gx >= g.nx) return;
@@ -1053,17 +1060,29 @@ __global__ void __launch_bounds__(NTHREADS) epilogue_kernel(Geo g, Work w, const
     const int gz = c.gz0 + lz;
     if (gz < 0 || gz >= g.nz) continue;
     long long gi = (long long)gz * g.sxy + (long long)gy * g.nx + gx;
-    uint8_t sv = S[gi];
-    float s = w.sc[li];
-    float p;
-    if (sv)
-      p = seed_value(sv);
-    else if (s > 0.f)
-      p = st == ST_ZERO ? 0.f : s * w.y[li];
-    else
-      p = bound ? bound[gi] : 0.f;
+    const float s = w.sc[li];
+    const float y = w.y[li];  // an unknown's scaled solution, else the final value (setup)
+    const float p = s > 0.f ? (st == ST_ZERO ? 0.f : s * y) : y;
     prob[gi] = p;
     if (labels) labels[gi] = p > 0.5f ? 1 : 0;
+  }
+}
+
+__global__ void __launch_bounds__(NTHREADS) epilogue_kernel(Geo g, Work w, const int* __restrict__ list,
+                                                            float* __restrict__ prob, uint8_t* __restrict__ labels) {
+  epilogue_tile(g, w, tile_ctx(g, list), prob, labels);
+}
+
+// Epilogue of the bricks the setup already settled (zero rhs, converged at
+// start): the brick-resident engine writes its own bricks' results.  The
+// settled slots sit at the end of the active list (advance_kernel).
+__global__ void __launch_bounds__(NTHREADS) settled_epilogue_kernel(Geo g, Work w, const int* __restrict__ list, int nb,
+                                                                    float* __restrict__ prob,
+                                                                    uint8_t* __restrict__ labels) {
+  const int n_items = (nb - *w.n_active) * g.tiles;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int slot = w.alist[nb - 1 - item / g.tiles];
+    epilogue_tile(g, w, tile_ctx(g, list, slot, item % g.tiles), prob, labels);
   }
 }
 
@@ -1354,6 +1373,15 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
     ra.iters = w.iters;
     ra.tol2 = tol2;
     ra.max_iter = max_iter;
+    ra.sc = w.sc;
+    ra.prob = prob;
+    ra.labels = labels;
+    ra.list = list;
+    ra.nz = g.nz, ra.ny = g.ny, ra.nx = g.nx;
+    ra.oz = g.oz, ra.oy = g.oy, ra.ox = g.ox;
+    ra.gy = g.gy, ra.gx = g.gx;
+    // bricks the setup settled are finished here; the engine writes its own bricks' results
+    settled_epilogue_kernel<<<grid, block, 0, st>>>(g, w, list, nb, prob, labels);
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     RWB_CUDA(cudaEventCreate(&ev0));
     RWB_CUDA(cudaEventCreate(&ev1));
@@ -1365,7 +1393,6 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
       return rc;
     }
     RWB_CUDA(cudaEventRecord(ev1, st));
-    epilogue_kernel<<<sgrid, block, 0, st>>>(g, w, list, seeds, bound, prob, labels);
     stats_kernel<<<1, 1024, 0, st>>>(w, nb);
     RWB_LAUNCH_CHECK("resident solve epilogue");
     count_launches(2);
@@ -1398,7 +1425,7 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
     RWB_CUDA(cudaEventRecord(ev0, st));
     RWB_CUDA(cudaLaunchCooperativeKernel((const void*)coop_cg_kernel, dim3(cgrid), block, args, 0, st));
     RWB_CUDA(cudaEventRecord(ev1, st));
-    epilogue_kernel<<<sgrid, block, 0, st>>>(g, w, list, seeds, bound, prob, labels);
+    epilogue_kernel<<<sgrid, block, 0, st>>>(g, w, list, prob, labels);
     stats_kernel<<<1, 1024, 0, st>>>(w, nb);
     RWB_LAUNCH_CHECK("cooperative solve");
     count_launches(3);
@@ -1492,7 +1519,7 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
   cudaEventDestroy(ev1);
 
   finalize_kernel<<<(nb + 255) / 256, 256, 0, st>>>(w, nb);
-  epilogue_kernel<<<sgrid, block, 0, st>>>(g, w, list, seeds, bound, prob, labels);
+  epilogue_kernel<<<sgrid, block, 0, st>>>(g, w, list, prob, labels);
   stats_kernel<<<1, 1024, 0, st>>>(w, nb);
   RWB_LAUNCH_CHECK("epilogue kernels");
   count_launches(3);
