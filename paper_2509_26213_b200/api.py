@@ -55,3 +55,70 @@ def segment(volume, seeds, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWCo
     out_labels.copy_(res.labels, non_blocking=out_labels.is_pinned())
     torch.cuda.current_stream().synchronize()
     return out_prob, out_labels
+
+
+def segment_many(inputs, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConfig(), *, outputs=None,
+                 workspace: device.Workspace | None = None):
+    """Segment a sequence of host volumes with the transfers overlapped.
+
+    `inputs`: list of (volume, seeds) host tensors of one shape (pinned for
+    asynchronous copies); `outputs`: optional list of (prob, labels) pinned
+    host tensors, reused cyclically when shorter than `inputs`.  Volume k+1 is
+    uploaded on its own stream while volume k is segmented, and the results
+    of volume k are downloaded on a third stream while volume k+1 is
+    segmented (device inputs double-buffered), so in steady state a volume
+    costs max(upload, compute, download) instead of their sum.  Returns the
+    list of (prob, labels) host tensors, complete when the call returns.
+    """
+    n = len(inputs)
+    if n == 0:
+        return []
+    dev = torch.device("cuda", torch.cuda.current_device())
+    comp = torch.cuda.current_stream(dev)
+    up = torch.cuda.Stream(dev)
+    down = torch.cuda.Stream(dev)
+    up.wait_stream(comp)
+    down.wait_stream(comp)
+    shape = tuple(inputs[0][0].shape)
+    vol_d = [torch.empty(shape, dtype=torch.float32, device=dev) for _ in range(min(n, 2))]
+    sd_d = [torch.empty(shape, dtype=torch.uint8, device=dev) for _ in range(min(n, 2))]
+    if outputs is None:
+        outputs = [(torch.empty(shape, dtype=torch.float32, pin_memory=True),
+                    torch.empty(shape, dtype=torch.uint8, pin_memory=True)) for _ in range(min(n, 2))]
+    computed = []
+
+    def upload(i):
+        b = i % 2
+        with torch.cuda.stream(up):
+            if i >= 2:
+                up.wait_event(computed[i - 2])  # buffer b is free once volume i-2 is segmented
+            v, s = inputs[i]
+            vol_d[b].copy_(_as_host_tensor(v, np.float32), non_blocking=True)
+            sd_d[b].copy_(_as_host_tensor(s, np.uint8), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(up)
+        return ev
+
+    uploaded = [upload(0)]
+    results = []
+    for i in range(n):
+        if i + 1 < n:
+            uploaded.append(upload(i + 1))
+        comp.wait_event(uploaded[i])
+        res = device.hierarchical_random_walker(vol_d[i % 2], sd_d[i % 2], brick, levels, cfg,
+                                                workspace=workspace)
+        ev = torch.cuda.Event()
+        ev.record(comp)
+        computed.append(ev)
+        out_p, out_l = outputs[i % len(outputs)]
+        with torch.cuda.stream(down):
+            down.wait_event(ev)
+            out_p.copy_(res.prob, non_blocking=True)
+            out_l.copy_(res.labels, non_blocking=True)
+            res.prob.record_stream(down)
+            res.labels.record_stream(down)
+        results.append((out_p, out_l))
+    comp.wait_stream(down)
+    comp.wait_stream(up)
+    comp.synchronize()
+    return results

@@ -1200,17 +1200,42 @@ static Work carve(const Layout& L, char* base, const Geo& g) {
   return w;
 }
 
+// Small device -> host readbacks (active-brick counts, per-level stats) go
+// through MAPPED pinned memory written by a one-warp kernel, not through
+// cudaMemcpyAsync: a copy puts the stream on the copy engine, and the stream's
+// next operations then queue behind unrelated bulk copies on that engine (e.g.
+// the overlapped result downloads of api.segment_many), stalling the solver.
 struct PinnedScratch {
   int* host = nullptr;
+  int* dev = nullptr;  // device alias of `host`
   ~PinnedScratch() {
     if (host) cudaFreeHost(host);
   }
 };
 static thread_local PinnedScratch t_pinned;
 
-static int pinned(int** out) {
-  if (!t_pinned.host) RWB_CUDA(cudaHostAlloc(&t_pinned.host, 64, cudaHostAllocDefault));
+static int pinned(int** out, int** dev_alias = nullptr) {
+  if (!t_pinned.host) {
+    RWB_CUDA(cudaHostAlloc(&t_pinned.host, 64, cudaHostAllocMapped));  // [0] n_active, [2..9] stats, [10..11] unknowns
+    RWB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&t_pinned.dev), t_pinned.host, 0));
+  }
   *out = t_pinned.host;
+  if (dev_alias) *dev_alias = t_pinned.dev;
+  return RWB_OK;
+}
+
+__global__ void readback_kernel(int* __restrict__ dst, const int* __restrict__ src, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+// n 32-bit words from device memory into the mapped scratch at word `at`, then wait for the stream
+static int readback(cudaStream_t st, const void* src, int at, int n) {
+  int *host = nullptr, *dev = nullptr;
+  int rc = pinned(&host, &dev);
+  if (rc) return rc;
+  readback_kernel<<<1, 32, 0, st>>>(dev + at, static_cast<const int*>(src), n);
+  RWB_LAUNCH_CHECK("readback_kernel");
+  RWB_CUDA(cudaStreamSynchronize(st));
   return RWB_OK;
 }
 
@@ -1242,15 +1267,23 @@ static int launch_chunk(const Geo& g, const Work& w, int nb, const int* list, in
 }
 
 // Copy the per-level stats to the host (synchronises the stream).
+// Copy the per-level stats to the host (synchronises the stream).  The copies
+// land in PINNED scratch: a copy into pageable memory is staged by the driver
+// and can queue behind unrelated bulk copies on other streams (e.g. the
+// overlapped downloads of api.segment_many), stalling this stream for them.
 static int read_stats(const Work& w, int nb, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1, int sweeps, int path,
-                      rwb_solve_stats_t* stats) {
-  int hs[8];
-  unsigned long long unk = 0;
-  RWB_CUDA(cudaMemcpyAsync(hs, w.stat_i, sizeof(hs), cudaMemcpyDeviceToHost, st));
-  RWB_CUDA(cudaMemcpyAsync(&unk, w.unknowns, sizeof(unk), cudaMemcpyDeviceToHost, st));
-  RWB_CUDA(cudaStreamSynchronize(st));
-  float ms = 0.f;
-  if (ev0 && ev1) RWB_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
+                      rwb_solve_stats_t* stats, float cg_ms = -1.f) {
+  int* host = nullptr;
+  int rc = pinned(&host);
+  if (rc) return rc;
+  int* hs = host + 2;                                                   // 8 ints
+  readback_kernel<<<1, 32, 0, st>>>(t_pinned.dev + 2, w.stat_i, 8);
+  rc = readback(st, w.unknowns, 10, 2);
+  if (rc) return rc;
+  unsigned long long unk;
+  std::memcpy(&unk, host + 10, sizeof(unk));
+  float ms = cg_ms >= 0.f ? cg_ms : 0.f;
+  if (cg_ms < 0.f && ev0 && ev1) RWB_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
   stats->bricks = nb;
   stats->converged = hs[0];
   stats->not_converged = hs[1];
@@ -1430,25 +1463,8 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
     RWB_LAUNCH_CHECK("cooperative solve");
     count_launches(3);
     if (stats) {
-      int hs[8];
-      unsigned long long unk = 0;
-      RWB_CUDA(cudaMemcpyAsync(hs, w.stat_i, sizeof(hs), cudaMemcpyDeviceToHost, st));
-      RWB_CUDA(cudaMemcpyAsync(&unk, w.unknowns, sizeof(unk), cudaMemcpyDeviceToHost, st));
-      RWB_CUDA(cudaStreamSynchronize(st));
-      float ms = 0.f;
-      RWB_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
-      stats->bricks = nb;
-      stats->converged = hs[0];
-      stats->not_converged = hs[1];
-      stats->zero_rhs = hs[2];
-      stats->iterations_max = hs[3];
-      unsigned long long s64;
-      std::memcpy(&s64, hs + 4, sizeof(s64));
-      stats->iterations_sum = (int64_t)s64;
-      stats->unknowns = (int64_t)unk;
-      stats->sweeps = hs[3];
-      stats->cg_ms = ms;
-      stats->path = RWB_PATH_COOPERATIVE;
+      rc = read_stats(w, nb, st, ev0, ev1, 0, RWB_PATH_COOPERATIVE, stats);
+      if (rc) return rc;
     }
     cudaEventDestroy(ev0);
     cudaEventDestroy(ev1);
@@ -1458,8 +1474,8 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
   int* host = nullptr;
   rc = pinned(&host);
   if (rc) return rc;
-  RWB_CUDA(cudaMemcpyAsync(host, w.n_active, sizeof(int), cudaMemcpyDeviceToHost, st));
-  RWB_CUDA(cudaStreamSynchronize(st));
+  rc = readback(st, w.n_active, 0, 1);
+  if (rc) return rc;
   int active = host[0];
 
   cudaGraphExec_t exec = nullptr;
@@ -1501,7 +1517,10 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
     sweeps += k;
     count_launches(2 * k + 1);
     cudaError_t e = cudaEventRecord(ev1, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(host, w.n_active, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) {
+      readback_kernel<<<1, 32, 0, st>>>(t_pinned.dev, w.n_active, 1);
+      e = cudaGetLastError();
+    }
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     float ms = 0.f;
     if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, ev0, ev1);
@@ -1524,23 +1543,8 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
   RWB_LAUNCH_CHECK("epilogue kernels");
   count_launches(3);
   if (stats) {
-    int hs[8];
-    unsigned long long unk = 0;
-    RWB_CUDA(cudaMemcpyAsync(hs, w.stat_i, sizeof(hs), cudaMemcpyDeviceToHost, st));
-    RWB_CUDA(cudaMemcpyAsync(&unk, w.unknowns, sizeof(unk), cudaMemcpyDeviceToHost, st));
-    RWB_CUDA(cudaStreamSynchronize(st));
-    stats->bricks = nb;
-    stats->converged = hs[0];
-    stats->not_converged = hs[1];
-    stats->zero_rhs = hs[2];
-    stats->iterations_max = hs[3];
-    unsigned long long s64;
-    std::memcpy(&s64, hs + 4, sizeof(s64));
-    stats->iterations_sum = (int64_t)s64;
-    stats->unknowns = (int64_t)unk;
-    stats->sweeps = sweeps;
-    stats->cg_ms = cg_ms;
-    stats->path = RWB_PATH_STREAMING;
+    rc = read_stats(w, nb, st, nullptr, nullptr, sweeps, RWB_PATH_STREAMING, stats, cg_ms);
+    if (rc) return rc;
   }
   return RWB_OK;
 }

@@ -1,0 +1,55 @@
+"""Public entry points (`api.segment`, `api.segment_many`) on host buffers.
+
+`segment_many` overlaps uploads / downloads with the neighbouring volumes'
+compute on separate streams; its results must be byte-identical to one
+`segment` call per volume (same kernels, same workspace decisions).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2509_26213_b200 import api, synthetic  # noqa: E402
+from paper_2509_26213_b200.config import RWConfig  # noqa: E402
+
+
+def _case(shape, kind):
+    return (torch.from_numpy(synthetic.phantom(shape)).pin_memory(),
+            torch.from_numpy(synthetic.seeds(shape, kind)).pin_memory())
+
+
+def test_segment_host_roundtrip_matches_device():
+    vol, sd = _case((64, 64, 64), "S1")
+    cfg = RWConfig(tol=1e-6)
+    p_h, l_h = api.segment(vol, sd, (32, 32, 32), 2, cfg)
+    p_d, l_d = api.segment(vol.cuda(), sd.cuda(), (32, 32, 32), 2, cfg)
+    torch.cuda.synchronize()
+    assert not p_h.is_cuda and p_d.is_cuda
+    np.testing.assert_array_equal(p_h.numpy(), p_d.cpu().numpy())
+    np.testing.assert_array_equal(l_h.numpy(), l_d.cpu().numpy())
+
+
+@pytest.mark.parametrize("n_out", [2, 4])
+def test_segment_many_matches_single_calls(n_out):
+    shape = (64, 64, 96)
+    inputs = [_case(shape, k) for k in ("S1", "S2", "S1", "S2")]
+    inputs[2] = (inputs[2][0] * 0.5, inputs[2][1])  # a different volume
+    cfg = RWConfig(tol=1e-6)
+    outs = [(torch.empty(shape, dtype=torch.float32, pin_memory=True),
+             torch.empty(shape, dtype=torch.uint8, pin_memory=True)) for _ in range(n_out)]
+    ref = [tuple(t.clone() for t in api.segment(v, s, (32, 32, 32), 2, cfg)) for v, s in inputs]
+    if n_out < len(inputs):  # cyclic outputs: check each result as it would be read, one call per volume
+        for k, (v, s) in enumerate(inputs):
+            got = api.segment_many([(v, s)], (32, 32, 32), 2, cfg, outputs=outs)
+            np.testing.assert_array_equal(got[0][0].numpy(), ref[k][0].numpy())
+        got = api.segment_many(inputs, (32, 32, 32), 2, cfg, outputs=outs)
+        last = (len(inputs) - 1) % n_out
+        np.testing.assert_array_equal(outs[last][0].numpy(), ref[-1][0].numpy())
+        np.testing.assert_array_equal(outs[last][1].numpy(), ref[-1][1].numpy())
+    else:
+        got = api.segment_many(inputs, (32, 32, 32), 2, cfg, outputs=outs)
+        for (p, l), (rp, rl) in zip(got, ref):
+            np.testing.assert_array_equal(p.numpy(), rp.numpy())
+            np.testing.assert_array_equal(l.numpy(), rl.numpy())
