@@ -54,6 +54,22 @@ UNIT = "voxel/s"
 BETA, WMIN, TOL = 100.0, 1e-6, 1e-6
 
 
+# algorithmic bytes per unknown voxel per PCG iteration (fp32, forward-edge weights
+# and the inverse diagonal stored): 3-D 56 B, 2-D 52 B.  (Our streaming kernels need 52 / 48 B: the
+# Jacobi-scaled system has a unit diagonal.)
+ALG_BYTES_PER_UNKNOWN_ITER = {3: 56, 2: 52}
+
+
+def load_traffic(config, level_key):
+    """ncu DRAM bytes (read + write) of the dominant launch, from the committed profile, if present."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(config, {}).get(level_key)
+    except (OSError, ValueError):
+        return None
+
+
 def load_peak():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -213,9 +229,11 @@ def run_ours(args, wl, rank, world):
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = lib.rwb_kernel_launches()
-    # per solver path: device ms, algorithmic HBM bytes, streaming-equivalent CG bytes
-    acc = {p: {"ms": 0.0, "bytes": 0.0, "cg_equiv_bytes": 0.0, "launches": 0} for p in ("streaming", "resident")}
-    bpvi = sharding.cg_bytes_per_voxel_iter(len(shape))
+    # per level solve (one resident / cooperative launch, or the streaming CG launches of a level):
+    # device ms and SURVEY.md 8(d) algorithmic bytes = 56 B (3-D; 52 B 2-D) per unknown voxel per
+    # PCG iteration, counted exactly on the device (sum over bricks of unknowns x iterations)
+    acc = {}
+    alg_b = ALG_BYTES_PER_UNKNOWN_ITER[len(shape)]
     with ClockSampler(local) as clocks:
         torch.cuda.synchronize()
         barrier()
@@ -225,19 +243,11 @@ def run_ours(args, wl, rank, world):
             for k, st in enumerate(res.stats):
                 if st is None:
                     continue
-                bvol = math.prod(res.volumes[k].shape) if k == len(res.stats) - 1 else math.prod(brick)
-                cg_equiv = bpvi * bvol * st["iterations_sum"]
-                if st["path"] == 1:
-                    a = acc["resident"]
-                    # one read of intensity, bound (f32) and seeds (u8), one write of the probabilities
-                    # (+ labels on level 0), per brick voxel solved
-                    a["bytes"] += (4 + 4 + 1 + 4 + (1 if k == 0 else 0)) * bvol * st["bricks"]
-                else:
-                    a = acc["streaming"]
-                    a["bytes"] += cg_equiv
+                a = acc.setdefault(k, {"ms": 0.0, "alg_bytes": 0.0, "unknown_iterations": 0, "path": st["path"],
+                                       "voxels": math.prod(res.volumes[k].shape)})
                 a["ms"] += st["cg_ms"]
-                a["cg_equiv_bytes"] += cg_equiv
-                a["launches"] += 1
+                a["alg_bytes"] += alg_b * st["unknown_iterations"]
+                a["unknown_iterations"] += st["unknown_iterations"]
         ev1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -286,30 +296,34 @@ def run_ours(args, wl, rank, world):
         del vol_h, seeds_h, outs
 
     peak, peak_src = load_peak()
+    path_name = {0: "streaming cg_pass1/cg_pass2", 1: "resident3d_kernel", 2: "coop_cg_kernel"}
     kernels = {}
-    for name, a in acc.items():
+    for k, a in sorted(acc.items()):
         if a["ms"] <= 0:
             continue
-        gbs = a["bytes"] / (a["ms"] / 1e3) / 1e9
-        kernels[name] = {
-            "ms_per_step": a["ms"] / args.steps, "share_of_step": a["ms"] / ms_max,
-            "achieved_gbs": gbs, "frac": gbs / peak,
-            "cg_voxel_iter_per_s": a["cg_equiv_bytes"] / bpvi / (a["ms"] / 1e3),
-            "streaming_equivalent_gbs": a["cg_equiv_bytes"] / (a["ms"] / 1e3) / 1e9,
+        gbs = a["alg_bytes"] / (a["ms"] / 1e3) / 1e9
+        kernels[f"level{k}"] = {
+            "kernel": path_name.get(a["path"], "?"), "ms_per_step": a["ms"] / args.steps,
+            "share_of_step": a["ms"] / ms_max, "achieved_gbs": gbs, "frac": gbs / peak,
+            "unknown_iterations_per_step": a["unknown_iterations"] // args.steps,
+            # what actually crosses HBM when the CG state is on chip: intensity, bound, seeds in,
+            # probabilities (+ labels) out, once per solve
+            "hbm_gbs_if_resident": 14 * a["voxels"] / (a["ms"] / args.steps / 1e3) / 1e9 if a["path"] == 1 else None,
         }
     dom = max(kernels, key=lambda n: kernels[n]["ms_per_step"])
     dk = kernels[dom]
-    if dom == "resident":
-        desc = ("resident3d_kernel: whole 32^3-brick Jacobi-PCG solves on 8-CTA clusters (levels 0..L-2); "
-                "algorithmic bytes = 13 B per brick voxel (+1 B labels on level 0) read/written once per solve; "
-                "the CG state never leaves the SMs, so this kernel is bound by the latency of its per-iteration "
-                "cluster reduction, not by HBM (see streaming_equivalent_gbs)")
-    else:
-        desc = ("cg_pass1 + cg_pass2 (streaming Jacobi-PCG): algorithmic bytes = %d B per brick voxel per "
-                "iteration x per-brick iterations" % bpvi)
-    roofline = {"bound": "hbm", "kernel": desc, "achieved": dk["achieved_gbs"], "peak": peak, "unit": "GB/s",
-                "frac": dk["frac"], "traffic": None, "peak_source": peak_src,
-                "traffic_note": "ncu dram bytes per launch: see profiles/ (null here: per-launch sizes vary by level)",
+    traffic = load_traffic(args.config, dom)
+    roofline = {"bound": "hbm", "achieved": dk["achieved_gbs"], "peak": peak, "unit": "GB/s", "frac": dk["frac"],
+                "traffic": traffic,
+                "kernel": f"{dk['kernel']} ({dom}, the step's largest launch)",
+                "algorithmic_bytes": f"{alg_b} B per unknown voxel per PCG iteration (SURVEY.md 8(d)) x "
+                                     f"{dk['unknown_iterations_per_step']} unknown-iterations per launch",
+                "peak_source": peak_src,
+                "note": ("frac > 1: the brick-resident engine keeps every CG vector of a brick in registers/SMEM "
+                         "of an 8-CTA cluster, so per-iteration traffic never reaches HBM; the HBM roofline of "
+                         "the streaming algorithm (the 8(d) bytes) is beaten, and the kernel is bound by the "
+                         "latency of its per-iteration cluster reduction instead. traffic = ncu DRAM bytes of "
+                         "this launch (profiles/)"),
                 "kernels": kernels}
 
     cpu = None

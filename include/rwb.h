@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define RWB_ABI_VERSION 1
+#define RWB_ABI_VERSION 2
 
 enum {
   RWB_OK = 0,
@@ -92,6 +92,8 @@ typedef struct {
                               the CG iteration kernels; resident = the whole on-chip brick solve */
   int32_t path;            /* RWB_PATH_* that ran */
   int32_t reserved;
+  int64_t unknown_iterations; /* sum over bricks of unknowns x iterations: the PCG work done, in
+                                 unknown-voxel iterations (algorithmic-byte accounting) */
 } rwb_solve_stats_t;
 
 int rwb_abi_version(void);

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(LIB_DIR, "librwb.so")
 c_int32, c_int64, c_float, c_void_p, c_size_t = (
     ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p, ctypes.c_size_t)
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 SOLVE_NO_GRAPH = 1
 SOLVE_STREAMING = 2
 SOLVE_NO_COOP = 4
@@ -76,7 +76,7 @@ class SolveStats(ctypes.Structure):
     _fields_ = [("bricks", c_int64), ("converged", c_int64), ("not_converged", c_int64),
                 ("zero_rhs", c_int64), ("iterations_max", c_int64), ("iterations_sum", c_int64),
                 ("unknowns", c_int64), ("sweeps", c_int32), ("cg_ms", c_float), ("path", c_int32),
-                ("reserved", c_int32)]
+                ("reserved", c_int32), ("unknown_iterations", c_int64)]
 
     def as_dict(self):
         out = {name: int(getattr(self, name)) for name, _ in self._fields_ if name not in ("cg_ms", "reserved")}

@@ -55,6 +55,7 @@ struct Work {
   double* bb;  // [nb]
   int* state;  // [nb]
   int* iters;  // [nb]
+  unsigned* unk;     // [nb] unknowns per brick
   unsigned* ticket;  // [nb]
   float2* part;      // [nb*tiles]
   int* alist;        // [nb] compacted active slots
@@ -365,8 +366,10 @@ __global__ void __launch_bounds__(NTHREADS) setup_system_kernel(Geo g, Work w, c
     __syncthreads();
     if (n_unknown) atomicAdd(&cta_unknown, n_unknown);
     __syncthreads();
-    if (threadIdx.x == 0 && threadIdx.y == 0 && cta_unknown)
+    if (threadIdx.x == 0 && threadIdx.y == 0 && cta_unknown) {
       atomicAdd(w.unknowns, (unsigned long long)cta_unknown);
+      atomicAdd(w.unk + c.slot, cta_unknown);
+    }
   }
   double bb, rr;
   if (brick_reduce(g, w, c.slot, c.tile, acc_bb, acc_rr, &bb, &rr, setup_tiles(g))) {
@@ -739,6 +742,7 @@ __global__ void __launch_bounds__(STH, 2) setup_brick_kernel(const __grid_consta
     const unsigned su = __reduce_add_sync(0xffffffffu, lane < STH / 32 ? sm.red_unk[lane] : 0u);
     if (lane == 0) {
       if (su) atomicAdd(w.unknowns, (unsigned long long)su);
+      w.unk[slot] = su;
       w.bb[slot] = sbb;
       w.rr[slot] = srr;  // parity 0
       int st = ST_ACTIVE;
@@ -1087,14 +1091,15 @@ __global__ void __launch_bounds__(NTHREADS) settled_epilogue_kernel(Geo g, Work 
 }
 
 // stat_i: [0] converged [1] maxiter [2] zero-rhs [3] max iterations [4..5] u64 sum of iterations
+//         [6..7] u64 sum over bricks of unknowns x iterations
 __global__ void __launch_bounds__(1024) stats_kernel(Work w, int nb) {
   __shared__ int sh[4];
-  __shared__ unsigned long long sum;
+  __shared__ unsigned long long sum, usum;
   if (threadIdx.x < 4) sh[threadIdx.x] = 0;
-  if (threadIdx.x == 0) sum = 0;
+  if (threadIdx.x == 0) sum = usum = 0;
   __syncthreads();
   int c1 = 0, c2 = 0, c3 = 0, mx = 0;
-  unsigned long long sm = 0;
+  unsigned long long sm = 0, um = 0;
   for (int s = threadIdx.x; s < nb; s += blockDim.x) {
     int st = w.state[s];
     c1 += st == ST_CONVERGED;
@@ -1103,16 +1108,19 @@ __global__ void __launch_bounds__(1024) stats_kernel(Work w, int nb) {
     int it = st == ST_ZERO ? 0 : w.iters[s];
     mx = max(mx, it);
     sm += (unsigned long long)it;
+    um += (unsigned long long)it * w.unk[s];
   }
   atomicAdd(&sh[0], c1);
   atomicAdd(&sh[1], c2);
   atomicAdd(&sh[2], c3);
   atomicMax(&sh[3], mx);
   atomicAdd(&sum, sm);
+  atomicAdd(&usum, um);
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int i = 0; i < 4; ++i) w.stat_i[i] = sh[i];
     *reinterpret_cast<unsigned long long*>(w.stat_i + 4) = sum;
+    *reinterpret_cast<unsigned long long*>(w.stat_i + 6) = usum;
   }
 }
 
@@ -1153,7 +1161,7 @@ static int make_geo(const rwb_geometry_t* geom, Geo* g) {
 }
 
 
-enum { L_Y, L_R, L_P0, L_P1, L_Q, L_WX, L_WY, L_WZ, L_SC, L_RR, L_PQ, L_BB, L_STATE, L_ITERS, L_TICKET,
+enum { L_Y, L_R, L_P0, L_P1, L_Q, L_WX, L_WY, L_WZ, L_SC, L_RR, L_PQ, L_BB, L_STATE, L_ITERS, L_UNK, L_TICKET,
        L_ALIST, L_PART, L_MISC, L_N };
 
 struct Layout {
@@ -1166,7 +1174,7 @@ static Layout layout(const Geo& g, long long nb) {
   const size_t vox = (size_t)nb * (size_t)g.bvol * sizeof(float);
   const size_t sizes[L_N] = {vox, vox, vox, vox, vox, vox, vox, g.is3d ? vox : 0, vox,
                              2 * nb * sizeof(double), nb * sizeof(double), nb * sizeof(double),
-                             nb * sizeof(int), nb * sizeof(int), nb * sizeof(unsigned), nb * sizeof(int),
+                             nb * sizeof(int), nb * sizeof(int), nb * sizeof(unsigned), nb * sizeof(unsigned), nb * sizeof(int),
                              std::max((size_t)nb * std::max(g.tiles, setup_tiles(g)) * sizeof(float2),
                                       (size_t)2 * kCoopMaxBlocks * sizeof(float)),
                              64};
@@ -1189,6 +1197,7 @@ static Work carve(const Layout& L, char* base, const Geo& g) {
   w.bb = reinterpret_cast<double*>(base + L.off[L_BB]);
   w.state = reinterpret_cast<int*>(base + L.off[L_STATE]);
   w.iters = reinterpret_cast<int*>(base + L.off[L_ITERS]);
+  w.unk = reinterpret_cast<unsigned*>(base + L.off[L_UNK]);
   w.ticket = reinterpret_cast<unsigned*>(base + L.off[L_TICKET]);
   w.alist = reinterpret_cast<int*>(base + L.off[L_ALIST]);
   w.part = reinterpret_cast<float2*>(base + L.off[L_PART]);
@@ -1294,6 +1303,9 @@ static int read_stats(const Work& w, int nb, cudaStream_t st, cudaEvent_t ev0, c
   stats->iterations_sum = (int64_t)s64;
   stats->unknowns = (int64_t)unk;
   stats->sweeps = sweeps ? sweeps : hs[3];
+  unsigned long long ui;
+  std::memcpy(&ui, hs + 6, sizeof(ui));
+  stats->unknown_iterations = (int64_t)ui;
   stats->cg_ms = ms;
   stats->path = path;
   return RWB_OK;

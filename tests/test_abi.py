@@ -40,7 +40,7 @@ def test_library_exports_every_declared_symbol(lib):
 def test_struct_layouts_match_header():
     assert ctypes.sizeof(_native.Geometry) == 8 + 3 * 8 * 3
     assert ctypes.sizeof(_native.SolveParams) == 24
-    assert ctypes.sizeof(_native.SolveStats) == 7 * 8 + 16  # ..., int32 sweeps, float cg_ms
+    assert ctypes.sizeof(_native.SolveStats) == 7 * 8 + 16 + 8  # ..., int32 sweeps, float cg_ms, ..., int64
 
 
 def test_workspace_size_query_needs_no_device(lib):
