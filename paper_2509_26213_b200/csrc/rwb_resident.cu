@@ -203,6 +203,16 @@ __device__ __forceinline__ float sum_parts(const float* red) {
   return s;
 }
 
+// Two fmaf in one FFMA2 (fma.rn.f32x2, sm_100): bit-identical to the scalar pair,
+// half the issue slots.  d = a * b + c elementwise.
+__device__ __forceinline__ void fma2(float& d0, float& d1, float a0, float a1, float b0, float b1, float c0, float c1) {
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+
 __device__ __forceinline__ float rcp_ftz(float x) {
   float y;
   asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -394,9 +404,9 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
       const uint32_t ph = (gk >> 1) & 1;
       if (tid == 0) mbar_expect_tx(&sm.barR[par], tx_faces + 2 * NPART * 4);
       // w = A'r
-      float g4[TZT], d4[TZT];
+      float gp[TZT][2], dp[TZT][2];  // dot partials per plane, per x-pair lane
 #pragma unroll
-      for (int z = 0; z < TZT; ++z) g4[z] = d4[z] = 0.f;
+      for (int z = 0; z < TZT; ++z) gp[z][0] = gp[z][1] = dp[z][0] = dp[z][1] = 0.f;
 #pragma unroll
       for (int z = 0; z < TZT; ++z) {
         const int pz = pz0 + z;
@@ -406,22 +416,32 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
         const float4 rzd = z > 0 ? plane4(r, z - 1) : (pz > 0 ? sm.rp[pz - 1][ly][xq] : rf_dn);
         const float rl = __shfl_up_sync(0xffffffffu, r[z * RQ + RQ - 1], 1);
         const float rr_ = __shfl_down_sync(0xffffffffu, r[z * RQ], 1);
+        // y / z terms on x-pairs (FFMA2), then the x terms per voxel
+        float acc[RQ];
+#pragma unroll
+        for (int i = 0; i < RQ; i += 2) {
+          const int v = z * RQ + i;
+          const float wzl0 = z > 0 ? wzf[v - RQ] : wzb[i], wzl1 = z > 0 ? wzf[v + 1 - RQ] : wzb[i + 1];
+          fma2(acc[i], acc[i + 1], wyf[v], wyf[v + 1], lane_of(ru, i), lane_of(ru, i + 1), 0.f, 0.f);
+          fma2(acc[i], acc[i + 1], wyb[v], wyb[v + 1], lane_of(rd, i), lane_of(rd, i + 1), acc[i], acc[i + 1]);
+          fma2(acc[i], acc[i + 1], wzf[v], wzf[v + 1], lane_of(rzu, i), lane_of(rzu, i + 1), acc[i], acc[i + 1]);
+          fma2(acc[i], acc[i + 1], wzl0, wzl1, lane_of(rzd, i), lane_of(rzd, i + 1), acc[i], acc[i + 1]);
+        }
 #pragma unroll
         for (int i = 0; i < RQ; ++i) {
           const int v = z * RQ + i;
           const float rxl = i > 0 ? r[v - 1] : rl;
           const float rxr = i < RQ - 1 ? r[v + 1] : rr_;
           const float wxl = i > 0 ? wxf[v - 1] : wxb[z];
-          const float wzl = z > 0 ? wzf[v - RQ] : wzb[i];
-          float acc = wxf[v] * rxr;
-          acc = fmaf(wxl, rxl, acc);
-          acc = fmaf(wyf[v], lane_of(ru, i), acc);
-          acc = fmaf(wyb[v], lane_of(rd, i), acc);
-          acc = fmaf(wzf[v], lane_of(rzu, i), acc);
-          acc = fmaf(wzl, lane_of(rzd, i), acc);
-          w[v] = r[v] - acc;
-          g4[z] = fmaf(r[v], r[v], g4[z]);
-          d4[z] = fmaf(w[v], r[v], d4[z]);
+          acc[i] = fmaf(wxf[v], rxr, acc[i]);
+          acc[i] = fmaf(wxl, rxl, acc[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < RQ; i += 2) {
+          const int v = z * RQ + i;
+          fma2(w[v], w[v + 1], -1.f, -1.f, acc[i], acc[i + 1], r[v], r[v + 1]);  // w = r - acc (exact product)
+          fma2(gp[z][0], gp[z][1], r[v], r[v + 1], r[v], r[v + 1], gp[z][0], gp[z][1]);
+          fma2(dp[z][0], dp[z][1], w[v], w[v + 1], r[v], r[v + 1], dp[z][0], dp[z][1]);
         }
       }
       TRACE(1);
@@ -434,8 +454,8 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
         float gs = 0.f, ds = 0.f;
 #pragma unroll
         for (int z = 0; z < TZT; ++z) {
-          gs += g4[z];
-          ds += d4[z];
+          gs += gp[z][0] + gp[z][1];
+          ds += dp[z][0] + dp[z][1];
         }
         // warp sums -> CTA sum (fixed order) -> one st.async pair per CTA into every CTA
         const float gw = warp_sum(gs);
@@ -493,11 +513,11 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
       TRACE(4);
       // update k: p = r + beta p, s = w + beta s, y += alpha p, r -= alpha s (and the neighbour faces)
 #pragma unroll
-      for (int v = 0; v < RV; ++v) {
-        p[v] = fmaf(beta, p[v], r[v]);
-        sv[v] = fmaf(beta, sv[v], w[v]);
-        y[v] = fmaf(alpha, p[v], y[v]);
-        r[v] = fmaf(-alpha, sv[v], r[v]);
+      for (int v = 0; v < RV; v += 2) {  // packed pairs: the same fmaf, two per FFMA2
+        fma2(p[v], p[v + 1], beta, beta, p[v], p[v + 1], r[v], r[v + 1]);
+        fma2(sv[v], sv[v + 1], beta, beta, sv[v], sv[v + 1], w[v], w[v + 1]);
+        fma2(y[v], y[v + 1], alpha, alpha, p[v], p[v + 1], y[v], y[v + 1]);
+        fma2(r[v], r[v + 1], -alpha, -alpha, sv[v], sv[v + 1], r[v], r[v + 1]);
       }
       ++it;
       if (first_zg && below) {
