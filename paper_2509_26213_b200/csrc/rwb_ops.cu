@@ -235,6 +235,69 @@ __global__ void __launch_bounds__(256) upsample_kernel(const float* __restrict__
   }
 }
 
+// Whole-level upsampling, 4 parent x-voxels (8 fine x) per thread: the 9
+// parent rows a thread needs are x-interpolated once and reused by its 2x2
+// fine rows, and every fine row segment is written with two 16 B stores.
+// Same expressions as upsample_kernel, so the results are bit-identical.
+// Requires fine nx == 2 * parent nx, nx % 8 == 0 (16 B aligned row segments).
+constexpr int UQ = 4;  // parent x-voxels per thread
+__global__ void __launch_bounds__(256) upsample4_kernel(const float* __restrict__ parent, Shape3 ps,
+                                                        float* __restrict__ fine, Shape3 fs) {
+  const int jx0 = (blockIdx.x * BX + threadIdx.x) * UQ;
+  const int jy = blockIdx.y * BY + threadIdx.y;
+  const int jz = blockIdx.z;
+  if (jx0 >= ps.nx || jy >= ps.ny) return;
+  const long long psxy = (long long)ps.ny * ps.nx;
+  const int zz[3] = {max(jz - 1, 0), jz, min(jz + 1, ps.nz - 1)};
+  const int yy[3] = {max(jy - 1, 0), jy, min(jy + 1, ps.ny - 1)};
+  int xx[UQ + 2];
+#pragma unroll
+  for (int k = 0; k < UQ + 2; ++k) xx[k] = min(max(jx0 - 1 + k, 0), ps.nx - 1);
+  float lo[3][3][UQ], hi[3][3][UQ];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      const float* row = parent + zz[a] * psxy + (long long)yy[b] * ps.nx;
+      float v[UQ + 2];
+#pragma unroll
+      for (int k = 0; k < UQ + 2; ++k) v[k] = __ldg(row + xx[k]);
+#pragma unroll
+      for (int i = 0; i < UQ; ++i) {
+        lo[a][b][i] = __fmaf_rn(0.25f, v[i], __fmul_rn(0.75f, v[i + 1]));
+        hi[a][b][i] = __fmaf_rn(0.75f, v[i + 1], __fmul_rn(0.25f, v[i + 2]));
+      }
+    }
+  const bool fy2 = fs.ny > 1, fz2 = fs.nz > 1;
+#pragma unroll
+  for (int dz = 0; dz < 2; ++dz) {
+    const int gz = 2 * jz + dz;
+    if (gz >= fs.nz) continue;
+    const int za = dz ? 1 : 0, zb = dz ? 2 : 1;
+    const float wa = fz2 ? (dz ? 0.75f : 0.25f) : 0.f, wb = fz2 ? (dz ? 0.25f : 0.75f) : 1.f;
+#pragma unroll
+    for (int dy = 0; dy < 2; ++dy) {
+      const int gy = 2 * jy + dy;
+      if (gy >= fs.ny) continue;
+      const int ya = dy ? 1 : 0, yb = dy ? 2 : 1;
+      const float va = fy2 ? (dy ? 0.75f : 0.25f) : 0.f, vb = fy2 ? (dy ? 0.25f : 0.75f) : 1.f;
+      float f[2 * UQ];
+#pragma unroll
+      for (int i = 0; i < UQ; ++i)
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx) {
+          const float(*xs)[3][UQ] = dx ? hi : lo;
+          const float ra = __fmaf_rn(va, xs[za][ya][i], __fmul_rn(vb, xs[za][yb][i]));
+          const float rb = __fmaf_rn(va, xs[zb][ya][i], __fmul_rn(vb, xs[zb][yb][i]));
+          f[2 * i + dx] = __fmaf_rn(wa, ra, __fmul_rn(wb, rb));
+        }
+      float4* out = reinterpret_cast<float4*>(fine + ((long long)gz * fs.ny + gy) * fs.nx + 2 * jx0);
+      out[0] = make_float4(f[0], f[1], f[2], f[3]);
+      out[1] = make_float4(f[4], f[5], f[6], f[7]);
+    }
+  }
+}
+
 static void launch_upsample(const float* parent, Shape3 ps, Shape3 po, Shape3 pw, float* fine, Shape3 fs, Shape3 fo,
                             Shape3 fw, cudaStream_t st) {
   // parent voxels whose fine children intersect the window
@@ -414,6 +477,40 @@ extern "C" int rwb_lod_down_f32(int32_t ndim, const int64_t* size, const float* 
   return RWB_OK;
 }
 
+// Seed projection, 8 coarse x-voxels per thread: each fine row segment (16
+// bytes) is one 16 B load, the 8 results one 8 B store.  Requires fine nx a
+// multiple of 16 (coarse nx = fine nx / 2).
+__global__ void __launch_bounds__(256) project_seeds8_kernel(const uint8_t* __restrict__ fine, Shape3 fs,
+                                                             uint8_t* __restrict__ coarse, Shape3 cs) {
+  const int jx0 = (blockIdx.x * BX + threadIdx.x) * 8;
+  const int jy = blockIdx.y * BY + threadIdx.y;
+  const int jz = blockIdx.z;
+  if (jx0 >= cs.nx || jy >= cs.ny) return;
+  unsigned fg = 0, bg = 0;  // bit i: coarse voxel jx0 + i has a fg / bg child
+  for (int z = 2 * jz; z < min(2 * jz + 2, fs.nz); ++z)
+    for (int y = 2 * jy; y < min(2 * jy + 2, fs.ny); ++y) {
+      const uint4 q = *reinterpret_cast<const uint4*>(fine + ((long long)z * fs.ny + y) * fs.nx + 2 * jx0);
+      const unsigned w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const unsigned s = (w[k >> 2] >> (8 * (k & 3))) & 0xffu;
+        fg |= (unsigned)(s == 1) << (k >> 1);
+        bg |= (unsigned)(s == 2) << (k >> 1);
+      }
+    }
+  unsigned lo = 0, hi = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool f = (fg >> i) & 1, b = (bg >> i) & 1;
+    const unsigned v = (f && !b) ? 1u : ((b && !f) ? 2u : 0u);
+    if (i < 4)
+      lo |= v << (8 * i);
+    else
+      hi |= v << (8 * (i - 4));
+  }
+  *reinterpret_cast<uint2*>(coarse + ((long long)jz * cs.ny + jy) * cs.nx + jx0) = make_uint2(lo, hi);
+}
+
 extern "C" int rwb_project_seeds_u8(int32_t ndim, const int64_t* size, const uint8_t* fine, uint8_t* coarse,
                                     void* stream) {
   Shape3 fs, cs;
@@ -423,7 +520,12 @@ extern "C" int rwb_project_seeds_u8(int32_t ndim, const int64_t* size, const uin
   coarse_of(fs, &cs);
   if (ndim < 3) cs.nz = fs.nz;
   if (ndim < 2) cs.ny = fs.ny;
-  project_seeds_kernel<<<grid3(cs), kBlock3, 0, (cudaStream_t)stream>>>(fine, fs, coarse, cs);
+  if (fs.nx % 16 == 0 && cs.nx * 2 == fs.nx && ((uintptr_t)fine & 15) == 0 && ((uintptr_t)coarse & 7) == 0) {
+    dim3 grid((cs.nx / 8 + BX - 1) / BX, (cs.ny + BY - 1) / BY, cs.nz);
+    project_seeds8_kernel<<<grid, kBlock3, 0, (cudaStream_t)stream>>>(fine, fs, coarse, cs);
+  } else {
+    project_seeds_kernel<<<grid3(cs), kBlock3, 0, (cudaStream_t)stream>>>(fine, fs, coarse, cs);
+  }
   RWB_LAUNCH_CHECK("project_seeds_kernel");
   count_launches(1);
   return RWB_OK;
@@ -442,7 +544,12 @@ extern "C" int rwb_upsample_f32(int32_t ndim, const int64_t* parent_size, const 
   if (ndim < 2) chk.ny = fs.ny;
   if (chk.nz != ps.nz || chk.ny != ps.ny || chk.nx != ps.nx)
     return fail(RWB_ERR_INVALID, "fine size is not a 2x refinement of the parent size");
-  launch_upsample(parent, ps, Shape3{0, 0, 0}, ps, fine, fs, Shape3{0, 0, 0}, fs, (cudaStream_t)stream);
+  if (fs.nx == 2 * ps.nx && fs.nx % (2 * UQ) == 0 && ((uintptr_t)fine & 15) == 0) {
+    dim3 grid((ps.nx / UQ + BX - 1) / BX, (ps.ny + BY - 1) / BY, ps.nz);
+    upsample4_kernel<<<grid, kBlock3, 0, (cudaStream_t)stream>>>(parent, ps, fine, fs);
+  } else {
+    launch_upsample(parent, ps, Shape3{0, 0, 0}, ps, fine, fs, Shape3{0, 0, 0}, fs, (cudaStream_t)stream);
+  }
   RWB_LAUNCH_CHECK("upsample_kernel");
   count_launches(1);
   return RWB_OK;

@@ -402,7 +402,11 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
       TRACE(0);
       const int par = gk & 1;
       const uint32_t ph = (gk >> 1) & 1;
+#ifdef RWB_NOFACE  // diagnostics only: time an iteration without the face traffic (wrong results)
+      if (tid == 0) mbar_expect_tx(&sm.barR[par], 2 * NPART * 4);
+#else
       if (tid == 0) mbar_expect_tx(&sm.barR[par], tx_faces + 2 * NPART * 4);
+#endif
       // w = A'r
       float gp[TZT][2], dp[TZT][2];  // dot partials per plane, per x-pair lane
 #pragma unroll
@@ -446,10 +450,12 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
       }
       TRACE(1);
       // push the faces of w, then the dot partials, all onto the peers' barR[par]
+      #ifndef RWB_NOFACE
       if (below && first_zg)
         st_async_v4(par ? face_dn_dst[1] : face_dn_dst[0], plane4(w, 0), par ? bar_dn[1] : bar_dn[0]);
       if (above && last_zg)
         st_async_v4(par ? face_up_dst[1] : face_up_dst[0], plane4(w, TZT - 1), par ? bar_up[1] : bar_up[0]);
+#endif
       {
         float gs = 0.f, ds = 0.f;
 #pragma unroll

@@ -72,14 +72,16 @@ def test_lod_bit_exact_random_shapes(rng):
 
 
 def test_seed_projection_bit_exact(rng):
-    for shape in [(9, 7, 5), (16, 16), (33, 8, 2)]:
+    # (.., 32/48) hit the vectorised 8-per-thread kernel (fine nx % 16 == 0), incl. odd y / z
+    for shape in [(9, 7, 5), (16, 16), (33, 8, 2), (7, 9, 32), (5, 48), (2, 3, 64)]:
         s = rng.integers(0, 3, size=shape, dtype=np.uint8)
         s[rng.random(shape) < 0.7] = 0
         np.testing.assert_array_equal(host(device.project_seeds(cuda(s))), orw.project_seeds(s))
 
 
 def test_upsample_matches_oracle(rng):
-    for fine in [(16, 16, 16), (9, 7, 5), (31, 12), (2, 1, 3)]:
+    # (.., 16/32/24) hit the 4-parents-per-thread kernel (fine nx even, % 8 == 0), incl. odd y / z
+    for fine in [(16, 16, 16), (9, 7, 5), (31, 12), (2, 1, 3), (7, 13, 32), (9, 24), (1, 5, 16)]:
         parent = rng.random(device.coarse_shape(fine), dtype=np.float32)
         np.testing.assert_allclose(host(device.upsample(cuda(parent), fine)), orw.upsample_linear(parent, fine),
                                    rtol=0, atol=2e-7)
@@ -313,7 +315,8 @@ def test_cooperative_whole_level_matches_graph_path():
 
 
 def test_upsample_window_slabs_match_full(rng):
-    for fine in [(33, 20, 18), (40, 16)]:
+    # (33, 20, 32): the full upsample takes the vectorised kernel, the windows the general one
+    for fine in [(33, 20, 18), (40, 16), (33, 20, 32)]:
         parent = cuda(rng.random(device.coarse_shape(fine), dtype=np.float32))
         full = host(device.upsample(parent, fine))
         for z0, z1 in [(0, 5), (7, 8), (13, fine[0]), (0, fine[0])]:
