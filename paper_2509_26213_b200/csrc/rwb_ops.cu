@@ -235,13 +235,13 @@ __global__ void __launch_bounds__(256) upsample_kernel(const float* __restrict__
   }
 }
 
-// Whole-level upsampling, 4 parent x-voxels (8 fine x) per thread: the 9
+// Whole-level upsampling, UQ parent x-voxels (2 UQ fine x) per thread: the 9
 // parent rows a thread needs are x-interpolated once and reused by its 2x2
-// fine rows, and every fine row segment is written with two 16 B stores.
+// fine rows, and every fine row segment is written with 16 B stores.
 // Same expressions as upsample_kernel, so the results are bit-identical.
-// Requires fine nx == 2 * parent nx, nx % 8 == 0 (16 B aligned row segments).
-constexpr int UQ = 4;  // parent x-voxels per thread
-__global__ void __launch_bounds__(256) upsample4_kernel(const float* __restrict__ parent, Shape3 ps,
+// Requires fine nx == 2 * parent nx, nx % (2 UQ) == 0 (16 B aligned row segments).
+constexpr int UQ = 2;  // parent x-voxels per thread
+__global__ void __launch_bounds__(256, 4) upsample4_kernel(const float* __restrict__ parent, Shape3 ps,
                                                         float* __restrict__ fine, Shape3 fs) {
   const int jx0 = (blockIdx.x * BX + threadIdx.x) * UQ;
   const int jy = blockIdx.y * BY + threadIdx.y;
@@ -292,8 +292,8 @@ __global__ void __launch_bounds__(256) upsample4_kernel(const float* __restrict_
           f[2 * i + dx] = __fmaf_rn(wa, ra, __fmul_rn(wb, rb));
         }
       float4* out = reinterpret_cast<float4*>(fine + ((long long)gz * fs.ny + gy) * fs.nx + 2 * jx0);
-      out[0] = make_float4(f[0], f[1], f[2], f[3]);
-      out[1] = make_float4(f[4], f[5], f[6], f[7]);
+#pragma unroll
+      for (int q = 0; q < UQ / 2; ++q) out[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
     }
   }
 }
@@ -398,25 +398,41 @@ __global__ void __launch_bounds__(LTH) lod_down3_kernel(const float* __restrict_
   const int oy = tid / LCX, ox = tid % LCX;
   const int jy = cy0 + oy, jx = cx0 + ox;
   const int zend = min(cz0 + LZC, cs.nz);
-  for (int jz = cz0; jz < zend; ++jz) {
-    // (1) z-conv: fine planes 2jz-1 .. 2jz+2 (clamped); the first two carried from jz-1
+  // fine planes 2jz+1, 2jz+2 of the current coarse plane, loaded one plane ahead
+  float n1[LCPT], n2[LCPT];
+  auto load_next = [&](int jz) {
     const long long z2 = (long long)clampi(2 * jz + 1, 0, fs.nz - 1) * sxy;
     const long long z3 = (long long)clampi(2 * jz + 2, 0, fs.nz - 1) * sxy;
-    const bool first = jz == cz0;
-    const long long z0 = (long long)clampi(2 * jz - 1, 0, fs.nz - 1) * sxy;
-    const long long z1 = (long long)clampi(2 * jz, 0, fs.nz - 1) * sxy;
+#pragma unroll
+    for (int k = 0; k < LCPT; ++k) {
+      n1[k] = colv[k] ? __ldg(src + colo[k] + z2) : 0.f;
+      n2[k] = colv[k] ? __ldg(src + colo[k] + z3) : 0.f;
+    }
+  };
+  {
+    const long long z0 = (long long)clampi(2 * cz0 - 1, 0, fs.nz - 1) * sxy;
+    const long long z1 = (long long)clampi(2 * cz0, 0, fs.nz - 1) * sxy;
+#pragma unroll
+    for (int k = 0; k < LCPT; ++k) {
+      c1[k] = colv[k] ? __ldg(src + colo[k] + z0) : 0.f;
+      c2[k] = colv[k] ? __ldg(src + colo[k] + z1) : 0.f;
+    }
+    load_next(cz0);
+  }
+  for (int jz = cz0; jz < zend; ++jz) {
+    // (1) z-conv: fine planes 2jz-1 .. 2jz+2 (clamped); the first two carried from jz-1
+    float v2[LCPT], v3[LCPT];
+#pragma unroll
+    for (int k = 0; k < LCPT; ++k) v2[k] = n1[k], v3[k] = n2[k];
+    if (jz + 1 < zend) load_next(jz + 1);  // in flight during this plane's convolutions
 #pragma unroll
     for (int k = 0; k < LCPT; ++k) {
       if (!colv[k]) continue;
-      const float* s = src + colo[k];
-      const float v0 = first ? __ldg(s + z0) : c1[k];
-      const float v1 = first ? __ldg(s + z1) : c2[k];
-      const float v2 = __ldg(s + z2), v3 = __ldg(s + z3);
       const int c = tid + k * LTH, ty = c / LFX, tx = c % LFX;
-      A[0][ty][tx] = conv3(v0, v1, v2);
-      A[1][ty][tx] = conv3(v1, v2, v3);
-      c1[k] = v2;
-      c2[k] = v3;
+      A[0][ty][tx] = conv3(c1[k], c2[k], v2[k]);
+      A[1][ty][tx] = conv3(c2[k], v2[k], v3[k]);
+      c1[k] = v2[k];
+      c2[k] = v3[k];
     }
     __syncthreads();
     // (2) y-conv of the 16 child rows of both child planes
