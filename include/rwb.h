@@ -76,7 +76,7 @@ typedef struct {
 
 /* Solver paths (rwb_solve_stats_t.path) */
 #define RWB_PATH_STREAMING 0 /* brick-batched CG, state in HBM, 2 launches per iteration */
-#define RWB_PATH_RESIDENT 1  /* one 32^3 brick per 8-CTA cluster, CG state on chip */
+#define RWB_PATH_RESIDENT 1  /* CG state on chip: one 32^3 brick per 8-CTA cluster (3-D), one 64^2 tile per CTA (2-D) */
 #define RWB_PATH_COOPERATIVE 2 /* single-brick (whole-level) solve: all iterations in one cooperative kernel */
 
 typedef struct {

@@ -48,6 +48,9 @@ struct ResidentArgs {
 };
 
 int resident3d_supported(const Geo& g);
+// 2-D levels with 64^2 bricks: one CTA per tile (rwb_resident2d.cu)
+int resident2d_supported(const Geo& g);
+int launch_resident2d(const ResidentArgs& a, int max_bricks, cudaStream_t st);
 // variant: 8 = 8-CTA clusters (4 planes per CTA), 16 = 16-CTA clusters (2 planes per CTA, 2 CTAs/SM)
 int launch_resident3d(const ResidentArgs& a, int max_bricks, int variant, cudaStream_t st);
 

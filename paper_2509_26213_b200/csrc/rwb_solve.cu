@@ -1331,7 +1331,7 @@ static int coop_grid(int* grid) {
 using namespace rwb;
 
 static bool use_resident(const Geo& g, long long total, int flags) {
-  return !(flags & RWB_SOLVE_STREAMING) && total > 1 && resident3d_supported(g);
+  return !(flags & RWB_SOLVE_STREAMING) && total > 1 && (resident3d_supported(g) || resident2d_supported(g));
 }
 
 extern "C" size_t rwb_solve_workspace_bytes(const rwb_geometry_t* geom, int64_t n_bricks, int32_t flags) {
@@ -1431,7 +1431,11 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
     RWB_CUDA(cudaEventCreate(&ev0));
     RWB_CUDA(cudaEventCreate(&ev1));
     RWB_CUDA(cudaEventRecord(ev0, st));
-    rc = launch_resident3d(ra, nb, (params->flags & RWB_SOLVE_CLUSTER16) ? 16 : ((params->flags & RWB_SOLVE_SPLIT_Z) ? 512 : 8), st);
+    if (g.is3d)
+      rc = launch_resident3d(ra, nb, (params->flags & RWB_SOLVE_CLUSTER16) ? 16 : ((params->flags & RWB_SOLVE_SPLIT_Z) ? 512 : 8),
+                             st);
+    else
+      rc = launch_resident2d(ra, nb, st);
     if (rc) {
       cudaEventDestroy(ev0);
       cudaEventDestroy(ev1);

@@ -327,6 +327,30 @@ def test_upsample_window_slabs_match_full(rng):
             assert np.isnan(got[:z0]).all() and np.isnan(got[z1:]).all()
 
 
+@pytest.mark.parametrize("shape", [(128, 192), (130, 201), (64, 64 * 3)])
+def test_resident2d_tiles_match_oracle(rng, shape):
+    """2-D levels with 64^2 bricks run on the tile-resident engine (one CTA per tile)."""
+    vol, seeds = _random_case(rng, shape)
+    bound = rng.random(shape).astype(np.float32)
+    ref = orw.solve_level(vol, seeds, (64, 64), bound.astype(np.float64), TIGHT).prob
+    out, st = device.solve_level(cuda(vol), cuda(seeds), (64, 64), cuda(bound), GPU_CFG)
+    assert st["path"] == 1 and st["not_converged"] == 0
+    assert_rw_parity(host(out), ref)
+    streaming, ss = device.solve_level(cuda(vol), cuda(seeds), (64, 64), cuda(bound),
+                                       RWConfig(tol=GPU_CFG.tol, max_iter=GPU_CFG.max_iter, resident=False))
+    assert ss["path"] == 0
+    assert np.abs(host(out) - host(streaming)).max() <= 2e-5
+
+
+def test_resident2d_hierarchy_vs_oracle():
+    vol = synthetic.phantom((256, 320))
+    seeds = synthetic.seeds(vol.shape, "S2")
+    res = device.hierarchical_random_walker(cuda(vol), cuda(seeds), (64, 64), 3, GPU_CFG)
+    ref = orw.hierarchical_random_walker(vol, seeds, (64, 64), 3, TIGHT)
+    assert res.stats[0]["path"] == 1 and res.stats[1]["path"] == 1
+    assert_rw_parity(host(res.prob), ref.prob[0], host(res.labels))
+
+
 @pytest.mark.parametrize("cluster", [8, 16, 512])
 def test_resident_cluster_variants(rng, cluster):
     vol = synthetic.phantom((64, 96, 64))
