@@ -758,6 +758,199 @@ __global__ void __launch_bounds__(STH, 2) setup_brick_kernel(const __grid_consta
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused setup for 2-D levels with 64^2 tiles (config 3), one CTA per tile:
+// the tile plus its one-pixel halo of intensity, seeds and bound is read once
+// into shared memory (coalesced rows), each thread builds the system of a 4 x 4
+// pixel block (the mapping of the tile-resident engine), and ||S b||^2, ||r0||^2
+// are reduced in setup_system_kernel's order (per-pixel values, xor tree over
+// the 32 x of a setup tile row, 8 rows in sequence, tiles in float64), so the
+// result is bit-identical to the two-kernel setup.
+constexpr int ST2 = 64, SH2 = ST2 + 2;  // tile edge, with halo
+constexpr int SQ2 = 4, SQN2 = ST2 / SQ2, STH2 = SQN2 * SQN2;
+
+__global__ void __launch_bounds__(STH2) setup_tile2d_kernel(Geo g, Work w, const int* __restrict__ list,
+                                                            const float* __restrict__ I,
+                                                            const uint8_t* __restrict__ S,
+                                                            const float* __restrict__ B, float beta, float wmin,
+                                                            float tol2, int max_iter, int write_p) {
+  __shared__ float sI[SH2][SH2];
+  __shared__ float sDv[SH2][SH2];  // Dirichlet value: seed value, else bound
+  __shared__ unsigned char sS[SH2][SH2];
+  __shared__ float rowpart[2][ST2][2];  // [x tile][row] (bb, rr)
+  __shared__ float2 tpart[16];
+  __shared__ unsigned red_unk[STH2 / 32];
+  const int slot = blockIdx.x;
+  const int brick = list ? list[slot] : slot;
+  const int hx = brick % g.gx, hy = brick / g.gx;
+  const int gy0 = g.oy + hy * ST2, gx0 = g.ox + hx * ST2;
+  const int tid = threadIdx.x;
+  const int xq = tid % SQN2, yq = tid / SQN2;
+  auto wgt = [&](float a, float b) { return edge_weight(a, b, beta, wmin); };
+  // ---- tile + halo into shared memory ----
+  for (int e = tid; e < SH2 * SH2; e += STH2) {
+    const int ty = e / SH2, tx = e % SH2;
+    const int gy = gy0 - 1 + ty, gx = gx0 - 1 + tx;
+    float iv = 0.f, dv = 0.f;
+    unsigned char sv = 0;
+    if (gy >= 0 && gy < g.ny && gx >= 0 && gx < g.nx) {
+      const long long gi = (long long)gy * g.nx + gx;
+      iv = __ldg(I + gi);
+      sv = __ldg(S + gi);
+      dv = sv ? seed_value(sv) : (B ? __ldg(B + gi) : 0.f);
+    }
+    sI[ty][tx] = iv;
+    sS[ty][tx] = sv;
+    sDv[ty][tx] = dv;
+  }
+  __syncthreads();
+  // ---- weights and scales of the thread's 4 x 4 pixels ----
+  float wyb[SQ2][SQ2], wyf[SQ2][SQ2], wxb[SQ2][SQ2], wxf[SQ2][SQ2], sc[SQ2][SQ2];
+  bool in[SQ2][SQ2];
+#pragma unroll
+  for (int i = 0; i < SQ2; ++i)
+#pragma unroll
+    for (int k = 0; k < SQ2; ++k) {
+      const int ly = SQ2 * yq + i, lx = SQ2 * xq + k;
+      const int gy = gy0 + ly, gx = gx0 + lx;
+      const int ty = ly + 1, tx = lx + 1;
+      in[i][k] = ly < g.by && lx < g.bx && gy >= 0 && gy < g.ny && gx >= 0 && gx < g.nx;
+      const float c = sI[ty][tx];
+      wyb[i][k] = in[i][k] && gy > 0 ? wgt(c, sI[ty - 1][tx]) : 0.f;
+      wyf[i][k] = in[i][k] && gy + 1 < g.ny ? wgt(c, sI[ty + 1][tx]) : 0.f;
+      wxb[i][k] = in[i][k] && gx > 0 ? wgt(c, sI[ty][tx - 1]) : 0.f;
+      wxf[i][k] = in[i][k] && gx + 1 < g.nx ? wgt(c, sI[ty][tx + 1]) : 0.f;
+      // the two-kernel order -z, +z, -y, +y, -x, +x (the z terms are absent: adding nothing)
+      const float d = ((wyb[i][k] + wyf[i][k]) + wxb[i][k]) + wxf[i][k];
+      sc[i][k] = (in[i][k] && sS[ty][tx] == 0 && d > 0.f) ? jacobi_scale(d) : 0.f;
+    }
+  // the intensities are consumed: their buffer becomes the scale tile (halo 0: never coupled)
+  float(*sSc)[SH2] = sI;
+  __syncthreads();
+  for (int e = tid; e < SH2 * SH2; e += STH2) {
+    const int ty = e / SH2, tx = e % SH2;
+    if (ty == 0 || tx == 0 || ty == SH2 - 1 || tx == SH2 - 1) sSc[ty][tx] = 0.f;
+  }
+#pragma unroll
+  for (int i = 0; i < SQ2; ++i)
+#pragma unroll
+    for (int k = 0; k < SQ2; ++k) sSc[SQ2 * yq + i + 1][SQ2 * xq + k + 1] = sc[i][k];
+  __syncthreads();
+  // ---- system ----
+  float vbb[SQ2][SQ2], vrr[SQ2][SQ2];
+  unsigned n_unknown = 0;
+#pragma unroll
+  for (int i = 0; i < SQ2; ++i) {
+    const int ly = SQ2 * yq + i;
+    float wfx[SQ2], wfy[SQ2], rr[SQ2], yy[SQ2], ss[SQ2];
+#pragma unroll
+    for (int k = 0; k < SQ2; ++k) {
+      const int lx = SQ2 * xq + k, ty = ly + 1, tx = lx + 1;
+      const float si = sc[i][k];
+      const bool unk = si > 0.f;
+      n_unknown += unk;
+      float diag = 0.f, b = 0.f, acc = 0.f;
+      auto visit = [&](float wt, float sn, float dv) {
+        diag += wt;
+        const bool coupled = sn > 0.f;
+        acc = coupled ? fmaf(wt, dv, acc) : acc;
+        b = coupled ? b : fmaf(wt, dv, b);
+        return coupled ? wt * si * sn : 0.f;
+      };
+      visit(wyb[i][k], sSc[ty - 1][tx], sDv[ty - 1][tx]);
+      const float fy = visit(wyf[i][k], sSc[ty + 1][tx], sDv[ty + 1][tx]);
+      visit(wxb[i][k], sSc[ty][tx - 1], sDv[ty][tx - 1]);
+      const float fx = visit(wxf[i][k], sSc[ty][tx + 1], sDv[ty][tx + 1]);
+      const float x0 = B ? sDv[ty][tx] : 0.f;  // an unknown's bound (its Dirichlet value)
+      const float ri = initial_residual(si, b, acc, diag, x0);
+      const float sb = si * b;
+      wfx[k] = unk ? fx : 0.f;
+      wfy[k] = unk ? fy : 0.f;
+      rr[k] = unk ? ri : 0.f;
+      yy[k] = unk ? initial_y(x0, si, diag) : (in[i][k] ? sDv[ty][tx] : 0.f);
+      ss[k] = in[i][k] ? si : 0.f;
+      vbb[i][k] = unk ? fmaf(sb, sb, 0.f) : 0.f;
+      vrr[i][k] = unk ? fmaf(ri, ri, 0.f) : 0.f;
+    }
+    if (ly < g.by && SQ2 * xq < g.bx) {
+      const long long li = (long long)slot * g.bvol + (long long)ly * g.bx + SQ2 * xq;
+      *reinterpret_cast<float4*>(w.wx + li) = make_float4(wfx[0], wfx[1], wfx[2], wfx[3]);
+      *reinterpret_cast<float4*>(w.wy + li) = make_float4(wfy[0], wfy[1], wfy[2], wfy[3]);
+      *reinterpret_cast<float4*>(w.r + li) = make_float4(rr[0], rr[1], rr[2], rr[3]);
+      *reinterpret_cast<float4*>(w.y + li) = make_float4(yy[0], yy[1], yy[2], yy[3]);
+      *reinterpret_cast<float4*>(w.sc + li) = make_float4(ss[0], ss[1], ss[2], ss[3]);
+      if (write_p) *reinterpret_cast<float4*>(w.p0 + li) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  // ---- ||S b||^2, ||r0||^2 in the two-kernel order ----
+#pragma unroll
+  for (int i = 0; i < SQ2; ++i) {
+    float bq[SQ2], rq[SQ2];
+#pragma unroll
+    for (int k = 0; k < SQ2; ++k) {
+      bq[k] = vbb[i][k];
+      rq[k] = vrr[i][k];
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {  // x ^ 16, 8, 4 = quad ^ 4, 2, 1 (within a 32-pixel setup tile row)
+        bq[k] += __shfl_xor_sync(0xffffffffu, bq[k], o);
+        rq[k] += __shfl_xor_sync(0xffffffffu, rq[k], o);
+      }
+    }
+    if ((xq & 7) == 0) {  // x ^ 2, then x ^ 1, inside the quad
+      rowpart[xq >> 3][SQ2 * yq + i][0] = (bq[0] + bq[2]) + (bq[1] + bq[3]);
+      rowpart[xq >> 3][SQ2 * yq + i][1] = (rq[0] + rq[2]) + (rq[1] + rq[3]);
+    }
+  }
+  const unsigned nu = __reduce_add_sync(0xffffffffu, n_unknown);
+  if ((tid & 31) == 0) red_unk[tid >> 5] = nu;
+  __syncthreads();
+  // setup tiles of 32 x 8 pixels, index tty * 2 + ttx (setup_ctx order)
+  if (tid < 16) {
+    const int tty = tid >> 1, ttx = tid & 1;
+    float2 s = make_float2(0.f, 0.f);
+    for (int r8 = 0; r8 < TY; ++r8) {
+      s.x += rowpart[ttx][tty * TY + r8][0];
+      s.y += rowpart[ttx][tty * TY + r8][1];
+    }
+    tpart[tid] = s;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    const int tiles = ((g.by + TY - 1) / TY) * ((g.bx + TX - 1) / TX);
+    double sbb = 0.0, srr = 0.0;
+    if (tiles == 1) {
+      sbb = (double)tpart[0].x;
+      srr = (double)tpart[0].y;
+    } else {
+      for (int i = tid; i < tiles; i += 32) {
+        sbb += (double)tpart[i].x;
+        srr += (double)tpart[i].y;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sbb += __shfl_xor_sync(0xffffffffu, sbb, o);
+        srr += __shfl_xor_sync(0xffffffffu, srr, o);
+      }
+    }
+    const unsigned su = __reduce_add_sync(0xffffffffu, tid < STH2 / 32 ? red_unk[tid] : 0u);
+    if (tid == 0) {
+      if (su) atomicAdd(w.unknowns, (unsigned long long)su);
+      w.unk[slot] = su;
+      w.bb[slot] = sbb;
+      w.rr[slot] = srr;
+      int st = ST_ACTIVE;
+      if (sbb <= 0.0)
+        st = ST_ZERO;
+      else if (srr <= (double)tol2 * sbb)
+        st = ST_CONVERGED;
+      else if (max_iter <= 0)
+        st = ST_MAXITER;
+      w.state[slot] = st;
+      w.iters[slot] = 0;
+    }
+  }
+}
+
 // Tensor maps for the fused setup; false when the level's layout does not
 // meet TMA's rules (16 B aligned bases, row pitches and box x starts) — the
 // caller then uses the two-kernel setup.
@@ -1383,7 +1576,11 @@ extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensit
   dim3 block(TX, TY);
   const bool resident = use_resident(g, total, params->flags);
   SetupMaps maps;
-  if (!(params->flags & RWB_SOLVE_SETUP2) && make_setup_maps(g, intensity, seeds, bound, &maps)) {
+  if (!(params->flags & RWB_SOLVE_SETUP2) && !g.is3d && g.by == ST2 && g.bx == ST2) {
+    setup_tile2d_kernel<<<nb, STH2, 0, st>>>(g, w, list, intensity, seeds, bound, params->beta, params->min_weight,
+                                             tol2, max_iter, resident ? 0 : 1);
+    RWB_LAUNCH_CHECK("2-D tile setup kernel");
+  } else if (!(params->flags & RWB_SOLVE_SETUP2) && make_setup_maps(g, intensity, seeds, bound, &maps)) {
     static bool smem_set = false;
     if (!smem_set) {
       RWB_CUDA(cudaFuncSetAttribute(setup_brick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -367,7 +367,8 @@ def test_resident_cluster_variants(rng, cluster):
 # two-kernel path in both arms
 @pytest.mark.parametrize("shape,brick", [((70, 40, 48), (32, 32, 32)), ((48, 40, 32), (16, 16, 16)),
                                          ((40, 37, 64), (32, 32, 32)), ((90, 64), (32, 32)),
-                                         ((20, 18, 16), (20, 18, 16)), ((70, 40, 33), (32, 32, 32))])
+                                         ((20, 18, 16), (20, 18, 16)), ((70, 40, 33), (32, 32, 32)),
+                                         ((130, 201), (64, 64)), ((128, 128), (64, 64))])
 def test_fused_setup_matches_two_kernel_setup(rng, shape, brick):
     vol, seeds = _random_case(rng, shape)
     whole = tuple(brick) == tuple(shape)
