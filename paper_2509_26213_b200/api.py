@@ -37,28 +37,19 @@ def segment(volume, seeds, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWCo
     """
     vol = _as_host_tensor(volume, np.float32)
     sd = _as_host_tensor(seeds, np.uint8)
-    on_host = not vol.is_cuda
-    dev = torch.device("cuda", torch.cuda.current_device())
-    if on_host:
-        vol_d = vol.to(dev, non_blocking=vol.is_pinned())
-        sd_d = sd.to(dev, non_blocking=sd.is_pinned())
-    else:
-        vol_d, sd_d = vol, sd
-    res = device.hierarchical_random_walker(vol_d, sd_d, brick, levels, cfg, workspace=workspace)
-    if not on_host:
+    if vol.is_cuda:
+        res = device.hierarchical_random_walker(vol, sd, brick, levels, cfg, workspace=workspace)
         return res.prob, res.labels
     if out_prob is None:
-        out_prob = torch.empty(res.prob.shape, dtype=torch.float32, pin_memory=True)
+        out_prob = torch.empty(tuple(vol.shape), dtype=torch.float32, pin_memory=True)
     if out_labels is None:
-        out_labels = torch.empty(res.labels.shape, dtype=torch.uint8, pin_memory=True)
-    out_prob.copy_(res.prob, non_blocking=out_prob.is_pinned())
-    out_labels.copy_(res.labels, non_blocking=out_labels.is_pinned())
-    torch.cuda.current_stream().synchronize()
-    return out_prob, out_labels
+        out_labels = torch.empty(tuple(vol.shape), dtype=torch.uint8, pin_memory=True)
+    # one volume through the overlapped pipeline: level-0 slabs download while the rest solves
+    return segment_many([(vol, sd)], brick, levels, cfg, outputs=[(out_prob, out_labels)], workspace=workspace)[0]
 
 
 def segment_many(inputs, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConfig(), *, outputs=None,
-                 workspace: device.Workspace | None = None):
+                 workspace: device.Workspace | None = None, level0_chunks: int = 8):
     """Segment a sequence of host volumes with the transfers overlapped.
 
     `inputs`: list of (volume, seeds) host tensors of one shape (pinned for
@@ -67,7 +58,9 @@ def segment_many(inputs, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConf
     uploaded on its own stream while volume k is segmented, and the results
     of volume k are downloaded on a third stream while volume k+1 is
     segmented (device inputs double-buffered), so in steady state a volume
-    costs max(upload, compute, download) instead of their sum.  Returns the
+    costs max(upload, compute, download) instead of their sum; level 0 is
+    solved in `level0_chunks` slabs whose rows download while the next slab
+    solves, so even the last volume's download mostly overlaps its compute.  Returns the
     list of (prob, labels) host tensors, complete when the call returns.
     """
     n = len(inputs)
@@ -105,18 +98,25 @@ def segment_many(inputs, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConf
         if i + 1 < n:
             uploaded.append(upload(i + 1))
         comp.wait_event(uploaded[i])
-        res = device.hierarchical_random_walker(vol_d[i % 2], sd_d[i % 2], brick, levels, cfg,
-                                                workspace=workspace)
+        out_p, out_l = outputs[i % len(outputs)]
+
+        def download(r0, r1, prob, labels, out_p=out_p, out_l=out_l):
+            # level-0 rows [r0, r1) are final at this point of the compute stream:
+            # download them while the remaining slabs solve
+            ev_c = torch.cuda.Event()
+            ev_c.record(comp)
+            with torch.cuda.stream(down):
+                down.wait_event(ev_c)
+                out_p[r0:r1].copy_(prob[r0:r1], non_blocking=True)
+                out_l[r0:r1].copy_(labels[r0:r1], non_blocking=True)
+                prob.record_stream(down)
+                labels.record_stream(down)
+
+        device.hierarchical_random_walker(vol_d[i % 2], sd_d[i % 2], brick, levels, cfg, workspace=workspace,
+                                          level0_chunks=level0_chunks, on_level0_chunk=download)
         ev = torch.cuda.Event()
         ev.record(comp)
         computed.append(ev)
-        out_p, out_l = outputs[i % len(outputs)]
-        with torch.cuda.stream(down):
-            down.wait_event(ev)
-            out_p.copy_(res.prob, non_blocking=True)
-            out_l.copy_(res.labels, non_blocking=True)
-            res.prob.record_stream(down)
-            res.labels.record_stream(down)
         results.append((out_p, out_l))
     comp.wait_stream(down)
     comp.wait_stream(up)

@@ -14,6 +14,7 @@ tensor (`Workspace`), reused across levels.
 from __future__ import annotations
 
 import ctypes
+import math
 from dataclasses import dataclass, field
 
 import torch
@@ -261,6 +262,40 @@ def solve_level(volume: torch.Tensor, seeds: torch.Tensor, brick, bound: torch.T
 # hierarchical driver
 
 
+def _merge_stats(parts):
+    out = dict(parts[0])
+    for s in parts[1:]:
+        for key in ("bricks", "converged", "not_converged", "zero_rhs", "iterations_sum", "unknowns",
+                    "unknown_iterations"):
+            out[key] += s[key]
+        for key in ("iterations_max", "sweeps"):
+            out[key] = max(out[key], s[key])
+        out["cg_ms"] += s["cg_ms"]
+    return out
+
+
+def _solve_level_chunked(volume, seeds, brick, bound, cfg, labels_out, workspace, chunks, on_chunk):
+    """One level solved as `chunks` slabs of whole brick rows along dim 0, in order,
+    all into the same output; `on_chunk(r0, r1, prob, labels)` is called after each slab's
+    launches are queued (its rows [r0, r1) are final once the stream reaches
+    that point), e.g. to queue the slab's download while the next one solves."""
+    grid = brick_grid(volume.shape, brick)
+    per_row = math.prod(grid[1:])
+    rows = grid[0]
+    chunks = max(1, min(chunks, rows))
+    out = torch.empty(volume.shape, dtype=torch.float32, device=volume.device)
+    parts = []
+    for c in range(chunks):
+        h0, h1 = rows * c // chunks, rows * (c + 1) // chunks
+        lst = torch.arange(h0 * per_row, h1 * per_row, dtype=torch.int32, device=volume.device)
+        _, st = solve_level(volume, seeds, brick, bound, cfg, brick_list=lst, out=out, labels_out=labels_out,
+                            workspace=workspace)
+        parts.append(st)
+        if on_chunk is not None:
+            on_chunk(h0 * brick[0], min(h1 * brick[0], volume.shape[0]), out, labels_out)
+    return out, _merge_stats(parts)
+
+
 @dataclass
 class HRWResult:
     prob: torch.Tensor            # level-0 probabilities (f32)
@@ -274,7 +309,8 @@ class HRWResult:
 def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick, levels: int | None = None,
                                cfg: RWConfig = RWConfig(), *, want_labels: bool = True,
                                workspace: Workspace | None = None, brick_lists=None,
-                               exchange=None, upsample_planes=None) -> HRWResult:
+                               exchange=None, upsample_planes=None, level0_chunks: int = 1,
+                               on_level0_chunk=None) -> HRWResult:
     """Coarse-to-fine random walker (oracle/rw.py: hierarchical_random_walker).
 
     The coarsest level is solved whole; each finer level is initialised and
@@ -284,6 +320,10 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
     after level k is solved so the caller can complete the halo of the
     parent level before it is upsampled; `upsample_planes[k]` = (z0, z1)
     limits the prolongation of level k to those planes (see sharding.py).
+    `level0_chunks` > 1 solves level 0 as that many slabs of brick rows (same
+    results: bricks are independent) and calls `on_level0_chunk(r0, r1)` after
+    each with the level's (partially written) prob / labels tensors, so a
+    caller can download finished rows while the rest solves.
     """
     brick = tuple(int(b) for b in brick)
     vols = lod_chain(volume, brick, levels)
@@ -315,8 +355,14 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
         bl = brick_lists[k] if brick_lists is not None else None
         # separate output: the brick-resident solver reads neighbour bounds while
         # other bricks already write their results
-        probs[k], stats[k] = solve_level(vols[k], seed_levels[k], brick, x, cfg, brick_list=bl,
-                                         labels_out=lab_k, workspace=workspace)
+        if k == 0 and level0_chunks > 1 and bl is None:
+            probs[k], stats[k] = _solve_level_chunked(vols[k], seed_levels[k], brick, x, cfg, lab_k, workspace,
+                                                      level0_chunks, on_level0_chunk)
+        else:
+            probs[k], stats[k] = solve_level(vols[k], seed_levels[k], brick, x, cfg, brick_list=bl,
+                                             labels_out=lab_k, workspace=workspace)
+            if k == 0 and on_level0_chunk is not None:
+                on_level0_chunk(0, vols[0].shape[0], probs[0], lab_k)
         del x
         if k == 0:
             lab = lab_k

@@ -53,3 +53,24 @@ def test_segment_many_matches_single_calls(n_out):
         for (p, l), (rp, rl) in zip(got, ref):
             np.testing.assert_array_equal(p.numpy(), rp.numpy())
             np.testing.assert_array_equal(l.numpy(), rl.numpy())
+
+
+@pytest.mark.parametrize("shape,brick,levels", [((96, 64, 64), (32, 32, 32), 2), ((256, 192), (64, 64), 2),
+                                                ((70, 40, 48), (16, 16, 16), 2)])
+def test_level0_chunks_bytes_identical(shape, brick, levels):
+    """Level 0 solved in slabs of brick rows (api.segment_many's download overlap) = one solve."""
+    from paper_2509_26213_b200 import device
+
+    vol = torch.from_numpy(synthetic.phantom(shape)).cuda()
+    sd = torch.from_numpy(synthetic.seeds(shape, "S1")).cuda()
+    cfg = RWConfig(tol=1e-6)
+    a = device.hierarchical_random_walker(vol, sd, brick, levels, cfg)
+    seen = []
+    b = device.hierarchical_random_walker(vol, sd, brick, levels, cfg, level0_chunks=3,
+                                          on_level0_chunk=lambda r0, r1, p, l: seen.append((r0, r1)))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(a.prob.cpu().numpy(), b.prob.cpu().numpy())
+    np.testing.assert_array_equal(a.labels.cpu().numpy(), b.labels.cpu().numpy())
+    assert seen[0][0] == 0 and seen[-1][1] == shape[0] and all(x[1] == y[0] for x, y in zip(seen, seen[1:]))
+    for key in ("bricks", "iterations_sum", "unknowns", "unknown_iterations", "iterations_max"):
+        assert a.stats[0][key] == b.stats[0][key]
