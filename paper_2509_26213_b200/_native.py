@@ -13,7 +13,7 @@ import os
 import threading
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
-LIB_PATH = os.path.join(LIB_DIR, "librwb.so")
+LIB_PATH = os.environ.get("RWB_LIBRARY") or os.path.join(LIB_DIR, "librwb.so")  # RWB_LIBRARY: diagnostics builds
 
 c_int32, c_int64, c_float, c_void_p, c_size_t = (
     ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_void_p, ctypes.c_size_t)

@@ -1090,7 +1090,10 @@ __global__ void __launch_bounds__(NTHREADS) cg_pass2_kernel(Geo g, Work w, int n
 // result is deterministic.  (A single-sweep Chronopoulos-Gear variant needs
 // r, s, w double-buffered — 11 vectors, 92 MB at 128^3 — and fell out of L2:
 // 38 GB of DRAM traffic per solve instead of 0.14 GB; it was slower.)
-constexpr int kCoopTZ = 4;            // z planes per work item of the cooperative sweeps
+#ifndef RWB_COOP_TZ
+#define RWB_COOP_TZ 4
+#endif
+constexpr int kCoopTZ = RWB_COOP_TZ;  // z planes per work item of the cooperative sweeps
 constexpr int kCoopMaxBlocks = 4096;  // partial slots of the cooperative whole-level solve
 
 __device__ __forceinline__ double coop_total(const float* part, int n, double* sh) {
