@@ -45,6 +45,11 @@ WORKLOADS = {
     "c3": dict(shape=(16384, 16384), brick=(64, 64), levels=9,
                desc="config 3: 16384^2 f32 two-blob image + noise, 9-level hierarchy, 64^2 bricks, seeds S1",
                sample=dict(shape=(1024, 1024), levels=5)),
+    "c5": dict(shape=(512, 512, 512), timesteps=16, brick=(32, 32, 32), levels=4,
+               desc="config 5: 4-D series 512^3 x 16 timesteps (blobs shift along axis 1), per-timestep 4-level "
+                    "hierarchy (512/256/128/64), 32^3 bricks, seeds S1; the series lives in pinned host memory "
+                    "and streams through the GPU two timesteps at a time (out-of-HBM by construction)",
+               sample=dict(shape=(128, 128, 128), levels=2)),
     "c1": dict(shape=(64, 64, 64), brick=(32, 32, 32), levels=1,
                desc="config 1: 64^3 f32 two-blob phantom + noise, single level, seeds S1",
                sample=dict(shape=(64, 64, 64), levels=1)),
@@ -165,6 +170,94 @@ def cpu_reference_sample(wl, steps=1, warmup=0):
               f"with {s['levels']} levels ({n} voxels) instead of {'x'.join(map(str, wl['shape']))}; "
               f"float64 numpy oracle, bricks split over {cores} threads")
     return n, times, cores, sample
+
+
+def run_series(args, wl, rank, world):
+    """Config 5: a step = the whole 4-D series through api.segment_series (streamed from host)."""
+    import torch
+
+    import __graft_entry__ as entry
+
+    entry.build()
+    from paper_2509_26213_b200 import _native, api, device, synthetic
+    from paper_2509_26213_b200.config import RWConfig
+
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = _native.lib()
+    cfg = RWConfig(beta=BETA, min_weight=WMIN, tol=TOL, max_iter=10_000, check_every=args.check_every)
+    shape, brick, levels, n_t = wl["shape"], wl["brick"], wl["levels"], wl["timesteps"]
+    full = (n_t,) + tuple(shape)
+    vol_h = torch.empty(full, dtype=torch.float32, pin_memory=True)
+    sd_h = torch.empty(full, dtype=torch.uint8, pin_memory=True)
+    for t in range(n_t):  # generated on the device, kept on the host (untimed)
+        vol_h[t].copy_(synthetic.phantom_device(shape, device=dev, t=t, steps=n_t))
+        sd_h[t].copy_(synthetic.seeds_device(shape, "S1", device=dev, t=t, steps=n_t))
+    outs = (torch.empty(full, dtype=torch.float32, pin_memory=True),
+            torch.empty(full, dtype=torch.uint8, pin_memory=True))
+    ws = device.Workspace(dev)
+    warm = max(1, min(args.warmup, 3))
+    for _ in range(warm):
+        api.segment_many([(vol_h[t], sd_h[t]) for t in range(2)], brick, levels, cfg,
+                         outputs=[(outs[0][t], outs[1][t]) for t in range(2)], workspace=ws)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = lib.rwb_kernel_launches()
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            api.segment_series(vol_h, sd_h, brick, levels, cfg, outputs=outs, workspace=ws)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = lib.rwb_kernel_launches() - launches0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    nvox = math.prod(full)
+    # kernel-level view: one timestep device-resident
+    v0 = vol_h[0].to(dev)
+    s0 = sd_h[0].to(dev)
+    device.hierarchical_random_walker(v0, s0, brick, levels, cfg, workspace=ws)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    res = device.hierarchical_random_walker(v0, s0, brick, levels, cfg, workspace=ws)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t_ms = e0.elapsed_time(e1)
+    peak, peak_src = load_peak()
+    alg_b = ALG_BYTES_PER_UNKNOWN_ITER[3]
+    lv = max((s for s in res.stats if s), key=lambda s: s["cg_ms"])
+    gbs = alg_b * lv["unknown_iterations"] / (lv["cg_ms"] / 1e3) / 1e9
+    cpu = None
+    if not args.no_cpu_baseline:
+        n, times, cores, sample = cpu_reference_sample(wl, steps=1)
+        cpu = {"value": n / times[0], "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": nvox / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": warm, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (device-generated 4-D phantom, torch RNG noise), held in pinned host memory",
+            "config": {"workload": wl["desc"], "size": list(full), "brick": list(brick), "levels": levels,
+                       "beta": BETA, "min_weight": WMIN, "tol": TOL, "parallelism": "1 GPU (timestep stream)",
+                       "l2": "every timestep uploaded from host (512 MiB f32) > 126 MB L2"},
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                         "traffic": None, "peak_source": peak_src,
+                         "kernel": f"level-{res.stats.index(lv)} solve of one timestep (path {lv['path']}), "
+                                   f"{alg_b} B per unknown-iteration (SURVEY.md 8(d))",
+                         "timestep_device_resident_ms": t_ms},
+            "cpu_baseline": cpu,
+            "e2e": {"value": nvox / (ms / 1e3), "unit": UNIT, "ms_per_step": ms,
+                    "h2d_bytes_per_step": vol_h.numel() * 4 + sd_h.numel(),
+                    "d2h_bytes_per_step": outs[0].numel() * 4 + outs[1].numel(),
+                    "api": "paper_2509_26213_b200.api.segment_series (host series streamed through "
+                           "segment_many; the value above is this end-to-end number)"},
+            "clocks": clocks.summary(), "gpu_launches": int(launches),
+            "levels": [dict(st, level=k) for k, st in enumerate(res.stats) if st is not None],
+        }
+        print(json.dumps(line), flush=True)
+    return 0
 
 
 def run_reference(args, wl, rank):
@@ -368,6 +461,8 @@ def main():
     wl = WORKLOADS[args.config]
     if args.impl == "reference":
         return run_reference(args, wl, rank)
+    if "timesteps" in wl:
+        return run_series(args, wl, rank, world)
     if world > 1:
         import torch
         import torch.distributed as dist

@@ -122,3 +122,28 @@ def segment_many(inputs, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConf
     comp.wait_stream(up)
     comp.synchronize()
     return results
+
+
+def segment_series(volume, seeds, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConfig(), *,
+                   outputs=None, workspace: device.Workspace | None = None):
+    """Per-timestep hierarchical random walker of a 4-D (T, Z, Y, X) host series.
+
+    The reference's 4-D → 3-D `slice_node` view (`ops.py:555-586`), one
+    timestep at a time: every timestep is a host view streamed through
+    `segment_many` (upload of t+1 and download of t-1 overlapped with t), so
+    only two timesteps are ever resident on the device — the series may be far
+    larger than HBM.  Returns (prob, labels) host tensors of shape (T, ...);
+    `outputs` = (prob, labels) pinned 4-D buffers to write into.
+    """
+    vol = _as_host_tensor(volume, np.float32)
+    sd = _as_host_tensor(seeds, np.uint8)
+    if vol.dim() < 2 or vol.shape != sd.shape:
+        raise ValueError("volume and seeds must be (T, ...) series of the same shape")
+    if outputs is None:
+        outputs = (torch.empty(tuple(vol.shape), dtype=torch.float32, pin_memory=True),
+                   torch.empty(tuple(vol.shape), dtype=torch.uint8, pin_memory=True))
+    prob, labels = outputs
+    n = vol.shape[0]
+    segment_many([(vol[t], sd[t]) for t in range(n)], brick, levels, cfg,
+                 outputs=[(prob[t], labels[t]) for t in range(n)], workspace=workspace)
+    return prob, labels

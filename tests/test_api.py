@@ -74,3 +74,17 @@ def test_level0_chunks_bytes_identical(shape, brick, levels):
     assert seen[0][0] == 0 and seen[-1][1] == shape[0] and all(x[1] == y[0] for x, y in zip(seen, seen[1:]))
     for key in ("bricks", "iterations_sum", "unknowns", "unknown_iterations", "iterations_max"):
         assert a.stats[0][key] == b.stats[0][key]
+
+
+def test_segment_series_matches_per_timestep_calls():
+    t_steps, shape = 3, (64, 64, 64)
+    vol = torch.stack([torch.from_numpy(synthetic.phantom(shape, t=t, steps=t_steps)) for t in range(t_steps)])
+    sd = torch.stack([torch.from_numpy(synthetic.seeds(shape, "S1", t=t, steps=t_steps)) for t in range(t_steps)])
+    vol, sd = vol.pin_memory(), sd.pin_memory()
+    cfg = RWConfig(tol=1e-6)
+    prob, labels = api.segment_series(vol, sd, (32, 32, 32), 2, cfg)
+    for t in range(t_steps):
+        p, l = api.segment(vol[t].clone(), sd[t].clone(), (32, 32, 32), 2, cfg)
+        np.testing.assert_array_equal(prob[t].numpy(), p.numpy())
+        np.testing.assert_array_equal(labels[t].numpy(), l.numpy())
+    assert not np.array_equal(prob[0].numpy(), prob[-1].numpy())  # the blobs move
