@@ -435,10 +435,18 @@ __global__ void __launch_bounds__(LTH) lod_down3_kernel(const float* __restrict_
       c2[k] = v3[k];
     }
     __syncthreads();
-    // (2) y-conv of the 16 child rows of both child planes
-    for (int e = tid; e < 2 * 2 * LCY * LFX; e += LTH) {
-      const int cz = e / (2 * LCY * LFX), rem = e % (2 * LCY * LFX), r = rem / LFX, tx = rem % LFX;
-      B[cz][r][tx] = conv3(A[cz][r][tx], A[cz][r + 1][tx], A[cz][r + 2][tx]);
+    // (2) y-conv of the 16 child rows of both child planes: one thread per (plane,
+    // column) slides down the 18 A rows, so every A value is read once
+    if (tid < 2 * LFX) {
+      const int cz = tid / LFX, tx = tid % LFX;
+      double a0 = A[cz][0][tx], a1 = A[cz][1][tx];
+#pragma unroll
+      for (int r = 0; r < 2 * LCY; ++r) {
+        const double a2 = A[cz][r + 2][tx];
+        B[cz][r][tx] = conv3(a0, a1, a2);
+        a0 = a1;
+        a1 = a2;
+      }
     }
     __syncthreads();
     // (3) x-conv of this output's 8 children, then the pairwise means (z, y, x)
@@ -447,12 +455,12 @@ __global__ void __launch_bounds__(LTH) lod_down3_kernel(const float* __restrict_
 #pragma unroll
       for (int cz = 0; cz < 2; ++cz)
 #pragma unroll
-        for (int cy = 0; cy < 2; ++cy)
-#pragma unroll
-          for (int cx = 0; cx < 2; ++cx) {
-            const double* b = &B[cz][2 * oy + cy][2 * ox + cx];
-            C[cz][cy][cx] = (float)conv3(b[0], b[1], b[2]);
-          }
+        for (int cy = 0; cy < 2; ++cy) {
+          const double* b = &B[cz][2 * oy + cy][2 * ox];
+          const double b0 = b[0], b1 = b[1], b2 = b[2], b3 = b[3];
+          C[cz][cy][0] = (float)conv3(b0, b1, b2);
+          C[cz][cy][1] = (float)conv3(b1, b2, b3);
+        }
       const int ncz = (2 * jz + 1 < fs.nz) ? 2 : 1;
       const int ncy = (2 * jy + 1 < fs.ny) ? 2 : 1;
       const int ncx = (2 * jx + 1 < fs.nx) ? 2 : 1;
