@@ -27,6 +27,12 @@ int cuda_fail(cudaError_t err, const char* what);
 // RWB_DEBUG_SYNC=1 in the environment: synchronise after every checked launch
 // so an asynchronous fault is reported at the launch that caused it.
 bool debug_sync();
+// for launches that may be captured into a graph: never synchronise
+#define RWB_LAUNCH_CHECK_CAPTURE(what)                   \
+  do {                                                   \
+    cudaError_t err__ = cudaGetLastError();              \
+    if (err__ != cudaSuccess) return ::rwb::cuda_fail(err__, what); \
+  } while (0)
 #define RWB_LAUNCH_CHECK(what)                           \
   do {                                                   \
     cudaError_t err__ = cudaGetLastError();              \

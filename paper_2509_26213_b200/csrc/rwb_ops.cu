@@ -241,60 +241,76 @@ __global__ void __launch_bounds__(256) upsample_kernel(const float* __restrict__
 // Same expressions as upsample_kernel, so the results are bit-identical.
 // Requires fine nx == 2 * parent nx, nx % (2 UQ) == 0 (16 B aligned row segments).
 constexpr int UQ = 2;  // parent x-voxels per thread
+constexpr int UZ = 8;  // parent planes marched per thread
 __global__ void __launch_bounds__(256, 4) upsample4_kernel(const float* __restrict__ parent, Shape3 ps,
                                                         float* __restrict__ fine, Shape3 fs) {
   const int jx0 = (blockIdx.x * BX + threadIdx.x) * UQ;
   const int jy = blockIdx.y * BY + threadIdx.y;
-  const int jz = blockIdx.z;
+  const int jz0 = blockIdx.z * UZ;
   if (jx0 >= ps.nx || jy >= ps.ny) return;
   const long long psxy = (long long)ps.ny * ps.nx;
-  const int zz[3] = {max(jz - 1, 0), jz, min(jz + 1, ps.nz - 1)};
   const int yy[3] = {max(jy - 1, 0), jy, min(jy + 1, ps.ny - 1)};
   int xx[UQ + 2];
 #pragma unroll
   for (int k = 0; k < UQ + 2; ++k) xx[k] = min(max(jx0 - 1 + k, 0), ps.nx - 1);
+  // x-interpolated rows of the parent planes jz-1, jz, jz+1 (clamped): a window slid along z
   float lo[3][3][UQ], hi[3][3][UQ];
-#pragma unroll
-  for (int a = 0; a < 3; ++a)
+  auto load_plane = [&](int pz, float (&l)[3][UQ], float (&h)[3][UQ]) {
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      const float* row = parent + zz[a] * psxy + (long long)yy[b] * ps.nx;
+      const float* row = parent + pz * psxy + (long long)yy[b] * ps.nx;
       float v[UQ + 2];
 #pragma unroll
       for (int k = 0; k < UQ + 2; ++k) v[k] = __ldg(row + xx[k]);
 #pragma unroll
       for (int i = 0; i < UQ; ++i) {
-        lo[a][b][i] = __fmaf_rn(0.25f, v[i], __fmul_rn(0.75f, v[i + 1]));
-        hi[a][b][i] = __fmaf_rn(0.75f, v[i + 1], __fmul_rn(0.25f, v[i + 2]));
+        l[b][i] = __fmaf_rn(0.25f, v[i], __fmul_rn(0.75f, v[i + 1]));
+        h[b][i] = __fmaf_rn(0.75f, v[i + 1], __fmul_rn(0.25f, v[i + 2]));
       }
     }
+  };
+  load_plane(max(jz0 - 1, 0), lo[0], hi[0]);
+  load_plane(min(jz0, ps.nz - 1), lo[1], hi[1]);
   const bool fy2 = fs.ny > 1, fz2 = fs.nz > 1;
 #pragma unroll
-  for (int dz = 0; dz < 2; ++dz) {
-    const int gz = 2 * jz + dz;
-    if (gz >= fs.nz) continue;
-    const int za = dz ? 1 : 0, zb = dz ? 2 : 1;
-    const float wa = fz2 ? (dz ? 0.75f : 0.25f) : 0.f, wb = fz2 ? (dz ? 0.25f : 0.75f) : 1.f;
+  for (int s = 0; s < UZ; ++s) {
+    const int jz = jz0 + s;
+    if (jz >= ps.nz) break;
+    load_plane(min(jz + 1, ps.nz - 1), lo[2], hi[2]);
 #pragma unroll
-    for (int dy = 0; dy < 2; ++dy) {
-      const int gy = 2 * jy + dy;
-      if (gy >= fs.ny) continue;
-      const int ya = dy ? 1 : 0, yb = dy ? 2 : 1;
-      const float va = fy2 ? (dy ? 0.75f : 0.25f) : 0.f, vb = fy2 ? (dy ? 0.25f : 0.75f) : 1.f;
-      float f[2 * UQ];
+    for (int dz = 0; dz < 2; ++dz) {
+      const int gz = 2 * jz + dz;
+      if (gz >= fs.nz) continue;
+      const int za = dz ? 1 : 0, zb = dz ? 2 : 1;
+      const float wa = fz2 ? (dz ? 0.75f : 0.25f) : 0.f, wb = fz2 ? (dz ? 0.25f : 0.75f) : 1.f;
 #pragma unroll
-      for (int i = 0; i < UQ; ++i)
+      for (int dy = 0; dy < 2; ++dy) {
+        const int gy = 2 * jy + dy;
+        if (gy >= fs.ny) continue;
+        const int ya = dy ? 1 : 0, yb = dy ? 2 : 1;
+        const float va = fy2 ? (dy ? 0.75f : 0.25f) : 0.f, vb = fy2 ? (dy ? 0.25f : 0.75f) : 1.f;
+        float f[2 * UQ];
 #pragma unroll
-        for (int dx = 0; dx < 2; ++dx) {
-          const float(*xs)[3][UQ] = dx ? hi : lo;
-          const float ra = __fmaf_rn(va, xs[za][ya][i], __fmul_rn(vb, xs[za][yb][i]));
-          const float rb = __fmaf_rn(va, xs[zb][ya][i], __fmul_rn(vb, xs[zb][yb][i]));
-          f[2 * i + dx] = __fmaf_rn(wa, ra, __fmul_rn(wb, rb));
-        }
-      float4* out = reinterpret_cast<float4*>(fine + ((long long)gz * fs.ny + gy) * fs.nx + 2 * jx0);
+        for (int i = 0; i < UQ; ++i)
 #pragma unroll
-      for (int q = 0; q < UQ / 2; ++q) out[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+          for (int dx = 0; dx < 2; ++dx) {
+            const float(*xs)[3][UQ] = dx ? hi : lo;
+            const float ra = __fmaf_rn(va, xs[za][ya][i], __fmul_rn(vb, xs[za][yb][i]));
+            const float rb = __fmaf_rn(va, xs[zb][ya][i], __fmul_rn(vb, xs[zb][yb][i]));
+            f[2 * i + dx] = __fmaf_rn(wa, ra, __fmul_rn(wb, rb));
+          }
+        float4* out = reinterpret_cast<float4*>(fine + ((long long)gz * fs.ny + gy) * fs.nx + 2 * jx0);
+#pragma unroll
+        for (int q = 0; q < UQ / 2; ++q) out[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
+      }
     }
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+      for (int i = 0; i < UQ; ++i) {
+        lo[0][b][i] = lo[1][b][i], hi[0][b][i] = hi[1][b][i];
+        lo[1][b][i] = lo[2][b][i], hi[1][b][i] = hi[2][b][i];
+      }
   }
 }
 
@@ -569,7 +585,7 @@ extern "C" int rwb_upsample_f32(int32_t ndim, const int64_t* parent_size, const 
   if (chk.nz != ps.nz || chk.ny != ps.ny || chk.nx != ps.nx)
     return fail(RWB_ERR_INVALID, "fine size is not a 2x refinement of the parent size");
   if (fs.nx == 2 * ps.nx && fs.nx % (2 * UQ) == 0 && ((uintptr_t)fine & 15) == 0) {
-    dim3 grid((ps.nx / UQ + BX - 1) / BX, (ps.ny + BY - 1) / BY, ps.nz);
+    dim3 grid((ps.nx / UQ + BX - 1) / BX, (ps.ny + BY - 1) / BY, (ps.nz + UZ - 1) / UZ);
     upsample4_kernel<<<grid, kBlock3, 0, (cudaStream_t)stream>>>(parent, ps, fine, fs);
   } else {
     launch_upsample(parent, ps, Shape3{0, 0, 0}, ps, fine, fs, Shape3{0, 0, 0}, fs, (cudaStream_t)stream);

@@ -33,6 +33,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include "rwb_common.cuh"
@@ -1467,7 +1468,7 @@ static int launch_chunk(const Geo& g, const Work& w, int nb, const int* list, in
     cg_pass2_kernel<<<grid, block, 0, st>>>(g, w, nb, list, j, tol2, max_iter);
   }
   advance_kernel<<<1, 1024, 0, st>>>(w, nb, k);
-  RWB_LAUNCH_CHECK("cg iteration kernels");
+  RWB_LAUNCH_CHECK_CAPTURE("cg iteration kernels");
   return RWB_OK;
 }
 
@@ -1539,10 +1540,31 @@ extern "C" size_t rwb_solve_workspace_bytes(const rwb_geometry_t* geom, int64_t 
   return layout(g, nb).total;
 }
 
+static int solve_level_impl(const rwb_geometry_t* geom, const float* intensity, const uint8_t* seeds,
+                            const float* bound, const int32_t* brick_list, int64_t n_bricks,
+                            const rwb_solve_params_t* params, float* prob, uint8_t* labels, void* workspace,
+                            size_t workspace_bytes, rwb_solve_stats_t* stats, void* stream);
+
+// Host calls are serialised per process: a solve captures CUDA graphs and
+// synchronises its stream for its polls and stats, and concurrent callers
+// (the reference Engine runs kernels on a thread pool) must not interleave
+// those with another thread's capture.  The device work of different calls is
+// stream-ordered anyway.
+static std::mutex g_solve_mutex;
+
 extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensity, const uint8_t* seeds,
                                const float* bound, const int32_t* brick_list, int64_t n_bricks,
                                const rwb_solve_params_t* params, float* prob, uint8_t* labels, void* workspace,
                                size_t workspace_bytes, rwb_solve_stats_t* stats, void* stream) {
+  std::lock_guard<std::mutex> lock(g_solve_mutex);
+  return solve_level_impl(geom, intensity, seeds, bound, brick_list, n_bricks, params, prob, labels, workspace,
+                          workspace_bytes, stats, stream);
+}
+
+static int solve_level_impl(const rwb_geometry_t* geom, const float* intensity, const uint8_t* seeds,
+                            const float* bound, const int32_t* brick_list, int64_t n_bricks,
+                            const rwb_solve_params_t* params, float* prob, uint8_t* labels, void* workspace,
+                            size_t workspace_bytes, rwb_solve_stats_t* stats, void* stream) {
   Geo g;
   int rc = make_geo(geom, &g);
   if (rc) return rc;
