@@ -112,11 +112,38 @@ def make_rw(manifest):
         print(name, manifest["rw"][name]["iterations_max"], flush=True)
 
 
+C2_SUB = 4  # config-2 fixture: every 4th voxel per axis of the level-0 probabilities
+
+
+def make_c2(manifest):
+    """Config 2 at full size (256^3, 2 levels, 32^3 bricks, seeds S1), oracle at tol 1e-9 on 8
+    threads (~3 min); the fixture keeps a strided subsample (64^3 points, ~1 MB)."""
+    params = rw.RWParams(beta=100.0, min_weight=1e-6, tol=1e-9, max_iter=50000)
+    shape = (256, 256, 256)
+    vol = syn.phantom(shape)
+    seeds = syn.seeds(shape, "S1")
+    res = rw.hierarchical_random_walker(vol, seeds, (32, 32, 32), 2, params, threads=8)
+    sub = tuple(slice(None, None, C2_SUB) for _ in shape)
+    p = res.prob[0][sub].astype(np.float32)
+    np.savez_compressed(os.path.join(HERE, "rw_c2_sub4.npz"), prob0=p)
+    manifest["rw_c2_sub4"] = {"shape": list(shape), "seeds": "S1", "brick": [32, 32, 32], "levels": 2,
+                              "tol": params.tol, "stride": C2_SUB, "input_sha256": sha(vol),
+                              "seeds_sha256": sha(seeds), "prob0_sub_sha256": sha(p)}
+
+
 def main():
     manifest = {"lod": {}, "rw": {}}
-    make_lod(manifest)
-    make_rw(manifest)
-    with open(os.path.join(HERE, "MANIFEST.json"), "w") as f:
+    path = os.path.join(HERE, "MANIFEST.json")
+    if "--c2-only" in sys.argv:  # the heavy fixture alone, merged into the existing manifest
+        with open(path) as f:
+            manifest = json.load(f)
+        make_c2(manifest)
+    else:
+        make_lod(manifest)
+        make_rw(manifest)
+        if "--c2" in sys.argv:
+            make_c2(manifest)
+    with open(path, "w") as f:
         json.dump(manifest, f, indent=1, sort_keys=True)
 
 

@@ -327,6 +327,23 @@ def test_upsample_window_slabs_match_full(rng):
             assert np.isnan(got[:z0]).all() and np.isnan(got[z1:]).all()
 
 
+def test_config2_full_size_vs_oracle():
+    """Config 2 at its full size (256^3, 2 levels, 32^3 bricks): the level-0 probabilities and
+    labels of the brick-resident hierarchy against the float64 oracle (tol 1e-9), on a strided
+    subsample (every 4th voxel per axis; fixture made by tests/golden/make_golden.py --c2-only)."""
+    import hashlib
+
+    meta = MANIFEST["rw_c2_sub4"]
+    vol = synthetic.phantom(tuple(meta["shape"]))
+    seeds = synthetic.seeds(vol.shape, meta["seeds"])
+    assert hashlib.sha256(np.ascontiguousarray(vol).tobytes()).hexdigest() == meta["input_sha256"]
+    res = device.hierarchical_random_walker(cuda(vol), cuda(seeds), tuple(meta["brick"]), meta["levels"], GPU_CFG)
+    assert res.stats[0]["path"] == 1 and res.stats[1]["path"] == 2
+    s = meta["stride"]
+    ref = load_golden("rw_c2_sub4.npz")["prob0"].astype(np.float64)
+    assert_rw_parity(host(res.prob)[::s, ::s, ::s], ref, host(res.labels)[::s, ::s, ::s])
+
+
 @pytest.mark.parametrize("shape", [(128, 192), (130, 201), (64, 64 * 3)])
 def test_resident2d_tiles_match_oracle(rng, shape):
     """2-D levels with 64^2 bricks run on the tile-resident engine (one CTA per tile)."""
