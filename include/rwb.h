@@ -73,6 +73,12 @@ typedef struct {
 #define RWB_SOLVE_CLUSTER16 8 /* brick-resident solver: 16-CTA clusters, 2 CTAs/SM (default 8-CTA, 1 CTA/SM) */
 #define RWB_SOLVE_SPLIT_Z 16  /* brick-resident solver: 8-CTA clusters with 512 threads x 8 voxels per CTA */
 #define RWB_SOLVE_SETUP2 32   /* build the system with the two-kernel setup instead of the fused per-brick one */
+/* Two-phase use of the brick-resident engine (resident path only): SETUP_ONLY builds the level's
+   system in `workspace` (and finishes the bricks the setup settles); a later call with the SAME
+   arguments and NO_SETUP solves it.  Lets a caller build slab k+1's system on one stream while
+   slab k solves on another (device.hierarchical_random_walker, level0_chunks). */
+#define RWB_SOLVE_SETUP_ONLY 128
+#define RWB_SOLVE_NO_SETUP 256
 
 /* Solver paths (rwb_solve_stats_t.path) */
 #define RWB_PATH_STREAMING 0 /* brick-batched CG, state in HBM, 2 launches per iteration */

@@ -25,6 +25,8 @@ SOLVE_NO_COOP = 4
 SOLVE_CLUSTER16 = 8
 SOLVE_SPLIT_Z = 16
 SOLVE_SETUP2 = 32
+SOLVE_SETUP_ONLY = 128
+SOLVE_NO_SETUP = 256
 PATH_STREAMING, PATH_RESIDENT, PATH_COOPERATIVE = 0, 1, 2
 
 # every symbol include/rwb.h declares, with (restype, argtypes)

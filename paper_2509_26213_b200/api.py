@@ -104,7 +104,7 @@ def segment_many(inputs, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConf
             # level-0 rows [r0, r1) are final at this point of the compute stream:
             # download them while the remaining slabs solve
             ev_c = torch.cuda.Event()
-            ev_c.record(comp)
+            ev_c.record(torch.cuda.current_stream())  # the stream that produced the rows
             with torch.cuda.stream(down):
                 down.wait_event(ev_c)
                 out_p[r0:r1].copy_(prob[r0:r1], non_blocking=True)

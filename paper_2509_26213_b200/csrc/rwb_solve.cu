@@ -1594,13 +1594,19 @@ static int solve_level_impl(const rwb_geometry_t* geom, const float* intensity, 
   rc = persistent_grid(&grid);
   if (rc) return rc;
 
-  // zero the scalar region (rr .. misc) in one memset
-  RWB_CUDA(cudaMemsetAsync((char*)workspace + L.off[L_RR], 0, L.total - L.off[L_RR], st));
   const unsigned sgrid = (unsigned)((long long)nb * g.tiles);
   const unsigned setup_grid = (unsigned)((long long)nb * setup_tiles(g));
   dim3 block(TX, TY);
   const bool resident = use_resident(g, total, params->flags);
+  const bool setup_only = params->flags & RWB_SOLVE_SETUP_ONLY, no_setup = params->flags & RWB_SOLVE_NO_SETUP;
+  if ((setup_only || no_setup) && (!resident || (setup_only && no_setup)))
+    return fail(RWB_ERR_INVALID, "SETUP_ONLY / NO_SETUP: one of them, and only where the brick-resident engine runs");
   SetupMaps maps;
+  if (no_setup) {
+    // the workspace already holds this level's system (an earlier SETUP_ONLY call, same arguments)
+  } else {
+  // zero the scalar region (rr .. misc) in one memset
+  RWB_CUDA(cudaMemsetAsync((char*)workspace + L.off[L_RR], 0, L.total - L.off[L_RR], st));
   if (!(params->flags & RWB_SOLVE_SETUP2) && !g.is3d && g.by == ST2 && g.bx == ST2) {
     setup_tile2d_kernel<<<nb, STH2, 0, st>>>(g, w, list, intensity, seeds, bound, params->beta, params->min_weight,
                                              tol2, max_iter, resident ? 0 : 1);
@@ -1624,6 +1630,14 @@ static int solve_level_impl(const rwb_geometry_t* geom, const float* intensity, 
   advance_kernel<<<1, 1024, 0, st>>>(w, nb, 0);
   RWB_LAUNCH_CHECK("setup kernels");
   count_launches(3);
+  if (resident) {
+    // bricks the setup settled are finished here; the engine writes its own bricks' results
+    settled_epilogue_kernel<<<grid, block, 0, st>>>(g, w, list, nb, prob, labels);
+    RWB_LAUNCH_CHECK("settled epilogue");
+    count_launches(1);
+  }
+  }
+  if (setup_only) return RWB_OK;
 
   if (resident) {
     // every CG iteration of a brick on chip: one 8-CTA cluster per 32^3 brick
@@ -1647,8 +1661,6 @@ static int solve_level_impl(const rwb_geometry_t* geom, const float* intensity, 
     ra.nz = g.nz, ra.ny = g.ny, ra.nx = g.nx;
     ra.oz = g.oz, ra.oy = g.oy, ra.ox = g.ox;
     ra.gy = g.gy, ra.gx = g.gx;
-    // bricks the setup settled are finished here; the engine writes its own bricks' results
-    settled_epilogue_kernel<<<grid, block, 0, st>>>(g, w, list, nb, prob, labels);
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     RWB_CUDA(cudaEventCreate(&ev0));
     RWB_CUDA(cudaEventCreate(&ev1));

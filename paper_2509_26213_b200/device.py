@@ -213,12 +213,15 @@ def workspace_bytes(shape, brick, n_bricks=-1, origin=None, cfg: RWConfig = RWCo
 def solve_level(volume: torch.Tensor, seeds: torch.Tensor, brick, bound: torch.Tensor | None = None,
                 cfg: RWConfig = RWConfig(), *, brick_list: torch.Tensor | None = None, out: torch.Tensor | None = None,
                 labels_out: torch.Tensor | None = None, workspace: Workspace | None = None,
-                origin=None) -> tuple:
+                origin=None, phase: str | None = None) -> tuple:
     """Random-walker solve of (the listed bricks of) one level.
 
     `bound` = upsampled parent probabilities (Dirichlet values outside each
     brick and initial guess); None only when `brick` covers the level.
     `out` may be `bound` itself (in-place).  Returns (prob, stats dict).
+    `phase` ("setup" / "solve", brick-resident levels only) splits the call in two:
+    "setup" builds the system in the workspace, a later "solve" with the same
+    arguments and workspace solves it (stats only from "solve").
     """
     _check_tensor(volume, torch.float32, "volume", (2, 3))
     _check_tensor(seeds, torch.uint8, "seeds")
@@ -249,13 +252,13 @@ def solve_level(volume: torch.Tensor, seeds: torch.Tensor, brick, bound: torch.T
     p = _native.SolveParams()
     p.beta, p.min_weight, p.tol = float(cfg.beta), float(cfg.min_weight), float(cfg.tol)
     p.max_iter, p.check_every = int(cfg.max_iter), int(cfg.check_every)
-    p.flags = _flags(cfg)
+    p.flags = _flags(cfg) | {None: 0, "setup": _native.SOLVE_SETUP_ONLY, "solve": _native.SOLVE_NO_SETUP}[phase]
     stats = _native.SolveStats()
     _native.check(lib.rwb_solve_level(
         ctypes.byref(g), _ptr(volume), _ptr(seeds), _ptr(bound), _ptr(brick_list), int(max(n_list, 0)),
         ctypes.byref(p), _ptr(out), _ptr(labels_out), _ptr(ws), ctypes.c_size_t(ws.numel()),
-        ctypes.byref(stats), _stream_handle()))
-    return out, stats.as_dict()
+        ctypes.byref(stats) if phase != "setup" else None, _stream_handle()))
+    return out, (stats.as_dict() if phase != "setup" else None)
 
 
 # ---------------------------------------------------------------------------
@@ -285,15 +288,72 @@ def _solve_level_chunked(volume, seeds, brick, bound, cfg, labels_out, workspace
     chunks = max(1, min(chunks, rows))
     out = torch.empty(volume.shape, dtype=torch.float32, device=volume.device)
     parts = []
+    bounds = [(rows * c // chunks, rows * (c + 1) // chunks) for c in range(chunks)]
+    lists = [torch.arange(h0 * per_row, h1 * per_row, dtype=torch.int32, device=volume.device) for h0, h1 in bounds]
+    rows_of = [(h0 * brick[0], min(h1 * brick[0], volume.shape[0])) for h0, h1 in bounds]
+    if not (cfg.resident and _resident_geometry(volume.shape, brick)):
+        for c in range(chunks):
+            _, st = solve_level(volume, seeds, brick, bound, cfg, brick_list=lists[c], out=out, labels_out=labels_out,
+                                workspace=workspace)
+            parts.append(st)
+            if on_chunk is not None:
+                on_chunk(*rows_of[c], out, labels_out)
+        return out, _merge_stats(parts)
+    # Brick-resident slabs, two-phase: slab c+1's system is built on a setup stream while slab
+    # c solves on a high-priority stream (the engine's clusters leave SMs free for the setup
+    # CTAs; priority hands SMs back to the engine first).  Two workspaces alternate.
+    comp = torch.cuda.current_stream()
+    solver = torch.cuda.Stream(priority=-1)
+    setup = torch.cuda.Stream()
+    solver.wait_stream(comp)
+    setup.wait_stream(comp)
+    spaces = [workspace, _twin(workspace)]
+    done = [None, None]  # event after the last solve that used each workspace
+
+    def build(c):
+        with torch.cuda.stream(setup):
+            if done[c % 2] is not None:
+                setup.wait_event(done[c % 2])
+            solve_level(volume, seeds, brick, bound, cfg, brick_list=lists[c], out=out, labels_out=labels_out,
+                        workspace=spaces[c % 2], phase="setup")
+            ev = torch.cuda.Event()
+            ev.record(setup)
+        return ev
+
+    built = build(0)
     for c in range(chunks):
-        h0, h1 = rows * c // chunks, rows * (c + 1) // chunks
-        lst = torch.arange(h0 * per_row, h1 * per_row, dtype=torch.int32, device=volume.device)
-        _, st = solve_level(volume, seeds, brick, bound, cfg, brick_list=lst, out=out, labels_out=labels_out,
-                            workspace=workspace)
-        parts.append(st)
-        if on_chunk is not None:
-            on_chunk(h0 * brick[0], min(h1 * brick[0], volume.shape[0]), out, labels_out)
+        nxt = build(c + 1) if c + 1 < chunks else None
+        with torch.cuda.stream(solver):
+            solver.wait_event(built)
+            _, st = solve_level(volume, seeds, brick, bound, cfg, brick_list=lists[c], out=out, labels_out=labels_out,
+                                workspace=spaces[c % 2], phase="solve")
+            ev = torch.cuda.Event()
+            ev.record(solver)
+            done[c % 2] = ev
+            parts.append(st)
+            if on_chunk is not None:
+                on_chunk(*rows_of[c], out, labels_out)
+        built = nxt
+    comp.wait_stream(solver)
+    comp.wait_stream(setup)
+    out.record_stream(solver)
+    if labels_out is not None:
+        labels_out.record_stream(solver)
     return out, _merge_stats(parts)
+
+
+def _resident_geometry(shape, brick) -> bool:
+    """Levels the brick-resident engines take (rwb_solve.cu use_resident)."""
+    return (len(shape) == 3 and tuple(brick) == (32, 32, 32)) or (len(shape) == 2 and tuple(brick) == (64, 64))
+
+
+def _twin(workspace):
+    """A second workspace paired with `workspace` (kept on it, grown on demand)."""
+    twin = getattr(workspace, "_twin", None)
+    if twin is None:
+        twin = Workspace(workspace.device)
+        workspace._twin = twin
+    return twin
 
 
 @dataclass
@@ -309,7 +369,7 @@ class HRWResult:
 def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick, levels: int | None = None,
                                cfg: RWConfig = RWConfig(), *, want_labels: bool = True,
                                workspace: Workspace | None = None, brick_lists=None,
-                               exchange=None, upsample_planes=None, level0_chunks: int = 1,
+                               exchange=None, upsample_planes=None, level0_chunks: int | None = None,
                                on_level0_chunk=None) -> HRWResult:
     """Coarse-to-fine random walker (oracle/rw.py: hierarchical_random_walker).
 
@@ -321,7 +381,9 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
     parent level before it is upsampled; `upsample_planes[k]` = (z0, z1)
     limits the prolongation of level k to those planes (see sharding.py).
     `level0_chunks` > 1 solves level 0 as that many slabs of brick rows (same
-    results: bricks are independent) and calls `on_level0_chunk(r0, r1)` after
+    results: bricks are independent; on brick-resident levels slab c+1's system
+    is built while slab c solves; default: 8 slabs for levels of >= 4096 bricks,
+    else 1) and calls `on_level0_chunk(r0, r1)` after
     each with the level's (partially written) prob / labels tensors, so a
     caller can download finished rows while the rest solves.
     """
@@ -355,6 +417,8 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
         bl = brick_lists[k] if brick_lists is not None else None
         # separate output: the brick-resident solver reads neighbour bounds while
         # other bricks already write their results
+        if k == 0 and level0_chunks is None:
+            level0_chunks = 8 if math.prod(brick_grid(vols[0].shape, brick)) >= 4096 else 1
         if k == 0 and level0_chunks > 1 and bl is None:
             probs[k], stats[k] = _solve_level_chunked(vols[k], seed_levels[k], brick, x, cfg, lab_k, workspace,
                                                       level0_chunks, on_level0_chunk)
