@@ -277,11 +277,13 @@ def _merge_stats(parts):
     return out
 
 
-def _solve_level_chunked(volume, seeds, brick, bound, cfg, labels_out, workspace, chunks, on_chunk):
+def _solve_level_chunked(volume, seeds, brick, parent, cfg, labels_out, workspace, chunks, on_chunk):
     """One level solved as `chunks` slabs of whole brick rows along dim 0, in order,
     all into the same output; `on_chunk(r0, r1, prob, labels)` is called after each slab's
     launches are queued (its rows [r0, r1) are final once the stream reaches
-    that point), e.g. to queue the slab's download while the next one solves."""
+    that point), e.g. to queue the slab's download while the next one solves.  The
+    bound (the upsampled `parent` level) is produced slab by slab (the slab's planes
+    plus their one-plane halo), just before the slab's setup."""
     grid = brick_grid(volume.shape, brick)
     per_row = math.prod(grid[1:])
     rows = grid[0]
@@ -291,8 +293,15 @@ def _solve_level_chunked(volume, seeds, brick, bound, cfg, labels_out, workspace
     bounds = [(rows * c // chunks, rows * (c + 1) // chunks) for c in range(chunks)]
     lists = [torch.arange(h0 * per_row, h1 * per_row, dtype=torch.int32, device=volume.device) for h0, h1 in bounds]
     rows_of = [(h0 * brick[0], min(h1 * brick[0], volume.shape[0])) for h0, h1 in bounds]
+    bound = torch.empty(volume.shape, dtype=torch.float32, device=volume.device)
+
+    def upsample_slab(c):  # the slab's planes + one-plane halo (identical bytes where slabs overlap)
+        r0, r1 = rows_of[c]
+        upsample_window(parent, volume.shape, max(r0 - 1, 0), min(r1 + 1, volume.shape[0]), bound)
+
     if not (cfg.resident and _resident_geometry(volume.shape, brick)):
         for c in range(chunks):
+            upsample_slab(c)
             _, st = solve_level(volume, seeds, brick, bound, cfg, brick_list=lists[c], out=out, labels_out=labels_out,
                                 workspace=workspace)
             parts.append(st)
@@ -312,6 +321,7 @@ def _solve_level_chunked(volume, seeds, brick, bound, cfg, labels_out, workspace
 
     def build(c):
         with torch.cuda.stream(setup):
+            upsample_slab(c)
             if done[c % 2] is not None:
                 setup.wait_event(done[c % 2])
             solve_level(volume, seeds, brick, bound, cfg, brick_list=lists[c], out=out, labels_out=labels_out,
@@ -336,6 +346,7 @@ def _solve_level_chunked(volume, seeds, brick, bound, cfg, labels_out, workspace
         built = nxt
     comp.wait_stream(solver)
     comp.wait_stream(setup)
+    bound.record_stream(setup)
     out.record_stream(solver)
     if labels_out is not None:
         labels_out.record_stream(solver)
@@ -407,7 +418,12 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
         if exchange is not None:
             exchange(k + 1, probs[k + 1])
         win = upsample_planes[k] if upsample_planes is not None else None
-        if win is None:
+        if k == 0 and level0_chunks is None:
+            level0_chunks = 8 if math.prod(brick_grid(vols[0].shape, brick)) >= 4096 else 1
+        slabbed = k == 0 and level0_chunks > 1 and win is None and brick_lists is None
+        if slabbed:
+            x = None  # upsampled slab by slab inside the chunked solve
+        elif win is None:
             x = upsample(probs[k + 1], vols[k].shape)
         else:  # sharded: only the planes this rank's bricks (+ halo) read
             x = upsample_window(probs[k + 1], vols[k].shape, win[0], win[1],
@@ -417,11 +433,9 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
         bl = brick_lists[k] if brick_lists is not None else None
         # separate output: the brick-resident solver reads neighbour bounds while
         # other bricks already write their results
-        if k == 0 and level0_chunks is None:
-            level0_chunks = 8 if math.prod(brick_grid(vols[0].shape, brick)) >= 4096 else 1
-        if k == 0 and level0_chunks > 1 and bl is None:
-            probs[k], stats[k] = _solve_level_chunked(vols[k], seed_levels[k], brick, x, cfg, lab_k, workspace,
-                                                      level0_chunks, on_level0_chunk)
+        if slabbed:
+            probs[k], stats[k] = _solve_level_chunked(vols[k], seed_levels[k], brick, probs[k + 1], cfg, lab_k,
+                                                      workspace, level0_chunks, on_level0_chunk)
         else:
             probs[k], stats[k] = solve_level(vols[k], seed_levels[k], brick, x, cfg, brick_list=bl,
                                              labels_out=lab_k, workspace=workspace)
