@@ -9,8 +9,7 @@ from paper_2509_26213_b200 import device, synthetic
 from paper_2509_26213_b200.config import RWConfig
 shape = (256, 256, 256)
 vol = synthetic.phantom_device(shape); sd = synthetic.seeds_device(shape, "S1")
-PIPE = False
-res = device.hierarchical_random_walker(vol, sd, (32, 32, 32), 2, RWConfig())
+res = device.hierarchical_random_walker(vol, sd, (32, 32, 32), 2, RWConfig(), level0_chunks=1)
 torch.cuda.synchronize()
 print(res.stats[0])
 buf = (ctypes.c_longlong * (8 * 64 * 8))()
@@ -20,9 +19,6 @@ print("rc", lib.rwb_trace_dump(buf))
 t = np.frombuffer(buf, dtype=np.int64).reshape(8, 64, 8)
 names = ["spmv", "warp_sums+push", "wait", "scalars", "update+publish", "-"]
 ncol = 7
-if PIPE:
-    names = ["push_partials", "spmv+push_faces", "wait", "scalars", "update+faces+sync"]
-    ncol = 6
 for rank in (0, 3, 7):
     d = np.diff(t[rank][:, :ncol], axis=1)[5:40]
     tot = (t[rank, 6:41, 0] - t[rank, 5:40, 0])
