@@ -131,13 +131,31 @@ def make_c2(manifest):
                               "seeds_sha256": sha(seeds), "prob0_sub_sha256": sha(p)}
 
 
+def make_c3like(manifest):
+    """Config-3 structure at 2048^2 (64^2 tiles, all 6 levels down to a 64^2 whole level), oracle
+    at tol 1e-9; the fixture keeps every 4th pixel per axis of level 0 (512^2 points)."""
+    params = rw.RWParams(beta=100.0, min_weight=1e-6, tol=1e-9, max_iter=50000)
+    shape = (2048, 2048)
+    vol = syn.phantom(shape)
+    seeds = syn.seeds(shape, "S1")
+    res = rw.hierarchical_random_walker(vol, seeds, (64, 64), 6, params, threads=8)
+    p = res.prob[0][::4, ::4].astype(np.float32)
+    np.savez_compressed(os.path.join(HERE, "rw_c3like_sub4.npz"), prob0=p)
+    manifest["rw_c3like_sub4"] = {"shape": list(shape), "seeds": "S1", "brick": [64, 64], "levels": 6,
+                                  "tol": params.tol, "stride": 4, "input_sha256": sha(vol),
+                                  "seeds_sha256": sha(seeds), "prob0_sub_sha256": sha(p)}
+
+
 def main():
     manifest = {"lod": {}, "rw": {}}
     path = os.path.join(HERE, "MANIFEST.json")
-    if "--c2-only" in sys.argv:  # the heavy fixture alone, merged into the existing manifest
+    if "--c2-only" in sys.argv or "--c3like-only" in sys.argv:  # heavy fixtures, merged into the manifest
         with open(path) as f:
             manifest = json.load(f)
-        make_c2(manifest)
+        if "--c2-only" in sys.argv:
+            make_c2(manifest)
+        if "--c3like-only" in sys.argv:
+            make_c3like(manifest)
     else:
         make_lod(manifest)
         make_rw(manifest)

@@ -344,6 +344,22 @@ def test_config2_full_size_vs_oracle():
     assert_rw_parity(host(res.prob)[::s, ::s, ::s], ref, host(res.labels)[::s, ::s, ::s])
 
 
+def test_config3_structure_2048_vs_oracle():
+    """Config 3's structure at 2048^2 (64^2 tiles, all 6 levels: tile-resident levels down to a
+    64^2 whole-level solve) against the float64 oracle (tol 1e-9), every 4th pixel per axis."""
+    import hashlib
+
+    meta = MANIFEST["rw_c3like_sub4"]
+    vol = synthetic.phantom(tuple(meta["shape"]))
+    seeds = synthetic.seeds(vol.shape, meta["seeds"])
+    assert hashlib.sha256(np.ascontiguousarray(vol).tobytes()).hexdigest() == meta["input_sha256"]
+    res = device.hierarchical_random_walker(cuda(vol), cuda(seeds), tuple(meta["brick"]), meta["levels"], GPU_CFG)
+    assert res.stats[0]["path"] == 1 and res.stats[-1]["path"] == 2
+    s = meta["stride"]
+    ref = load_golden("rw_c3like_sub4.npz")["prob0"].astype(np.float64)
+    assert_rw_parity(host(res.prob)[::s, ::s], ref, host(res.labels)[::s, ::s])
+
+
 @pytest.mark.parametrize("shape", [(128, 192), (130, 201), (64, 64 * 3)])
 def test_resident2d_tiles_match_oracle(rng, shape):
     """2-D levels with 64^2 bricks run on the tile-resident engine (one CTA per tile)."""
