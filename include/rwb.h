@@ -79,6 +79,10 @@ typedef struct {
    slab k solves on another (device.hierarchical_random_walker, level0_chunks). */
 #define RWB_SOLVE_SETUP_ONLY 128
 #define RWB_SOLVE_NO_SETUP 256
+/* `stats` points to device-accessible memory (device or mapped pinned host memory), filled
+   by a kernel on `stream` with no host synchronisation (brick-resident / cooperative paths never
+   block the host then; cg_ms from %globaltimer around the solve launches). */
+#define RWB_SOLVE_STATS_DEVICE 512
 
 /* Solver paths (rwb_solve_stats_t.path) */
 #define RWB_PATH_STREAMING 0 /* brick-batched CG, state in HBM, 2 launches per iteration */

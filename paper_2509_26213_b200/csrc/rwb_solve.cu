@@ -64,6 +64,7 @@ struct Work {
   int* n_active;     // [1]
   unsigned long long* unknowns;  // [1]
   int* stat_i;       // [8] device stats scratch
+  unsigned long long* stamp;  // [2] %globaltimer (ns) around the solve launches
 };
 
 // ---------------------------------------------------------------------------
@@ -1403,6 +1404,7 @@ static Work carve(const Layout& L, char* base, const Geo& g) {
   w.n_active = reinterpret_cast<int*>(misc + 4);
   w.unknowns = reinterpret_cast<unsigned long long*>(misc + 8);
   w.stat_i = reinterpret_cast<int*>(misc + 16);
+  w.stamp = reinterpret_cast<unsigned long long*>(misc + 48);
   return w;
 }
 
@@ -1477,8 +1479,44 @@ static int launch_chunk(const Geo& g, const Work& w, int nb, const int* list, in
 // land in PINNED scratch: a copy into pageable memory is staged by the driver
 // and can queue behind unrelated bulk copies on other streams (e.g. the
 // overlapped downloads of api.segment_many), stalling this stream for them.
+__global__ void stamp_kernel(unsigned long long* dst) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *dst = t;
+}
+
+// RWB_SOLVE_STATS_DEVICE: `stats` is device-accessible memory (device memory or
+// mapped pinned host memory); one thread fills it after the level's stats
+// kernel, with no host synchronisation.  cg_ms = `host_ms` when given (>= 0),
+// else the %globaltimer span around the solve launches.
+__global__ void stats_to_struct_kernel(Work w, int nb, int sweeps, int path, float host_ms,
+                                       rwb_solve_stats_t* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  const int* hs = w.stat_i;
+  rwb_solve_stats_t s;
+  s.bricks = nb;
+  s.converged = hs[0];
+  s.not_converged = hs[1];
+  s.zero_rhs = hs[2];
+  s.iterations_max = hs[3];
+  s.iterations_sum = (int64_t)*reinterpret_cast<const unsigned long long*>(hs + 4);
+  s.unknowns = (int64_t)*w.unknowns;
+  s.sweeps = sweeps ? sweeps : hs[3];
+  s.cg_ms = host_ms >= 0.f ? host_ms : (float)((double)(w.stamp[1] - w.stamp[0]) * 1e-6);
+  s.path = path;
+  s.reserved = 0;
+  s.unknown_iterations = (int64_t)*reinterpret_cast<const unsigned long long*>(hs + 6);
+  *out = s;
+}
+
 static int read_stats(const Work& w, int nb, cudaStream_t st, cudaEvent_t ev0, cudaEvent_t ev1, int sweeps, int path,
-                      rwb_solve_stats_t* stats, float cg_ms = -1.f) {
+                      rwb_solve_stats_t* stats, float cg_ms = -1.f, bool on_device = false) {
+  if (on_device) {
+    stats_to_struct_kernel<<<1, 32, 0, st>>>(w, nb, sweeps, path, cg_ms, stats);
+    RWB_LAUNCH_CHECK("stats_to_struct_kernel");
+    count_launches(1);
+    return RWB_OK;
+  }
   int* host = nullptr;
   int rc = pinned(&host);
   if (rc) return rc;
@@ -1580,7 +1618,9 @@ static int solve_level_impl(const rwb_geometry_t* geom, const float* intensity, 
   const Layout L = layout(g, nbl);
   if (workspace_bytes < L.total)
     return fail(RWB_ERR_WORKSPACE, "workspace too small: need " + std::to_string(L.total) + " bytes");
-  if (stats) std::memset(stats, 0, sizeof(*stats));
+  const bool dev_stats = params->flags & RWB_SOLVE_STATS_DEVICE;
+  if (stats && !dev_stats) std::memset(stats, 0, sizeof(*stats));
+  if (stats && dev_stats) RWB_CUDA(cudaMemsetAsync(stats, 0, sizeof(*stats), (cudaStream_t)stream));
   if (nbl == 0) return RWB_OK;
   const int nb = (int)nbl;
   cudaStream_t st = (cudaStream_t)stream;
@@ -1665,6 +1705,7 @@ static int solve_level_impl(const rwb_geometry_t* geom, const float* intensity, 
     RWB_CUDA(cudaEventCreate(&ev0));
     RWB_CUDA(cudaEventCreate(&ev1));
     RWB_CUDA(cudaEventRecord(ev0, st));
+    stamp_kernel<<<1, 1, 0, st>>>(w.stamp);
     if (g.is3d)
       rc = launch_resident3d(ra, nb, (params->flags & RWB_SOLVE_CLUSTER16) ? 16 : ((params->flags & RWB_SOLVE_SPLIT_Z) ? 512 : 8),
                              st);
@@ -1675,12 +1716,14 @@ static int solve_level_impl(const rwb_geometry_t* geom, const float* intensity, 
       cudaEventDestroy(ev1);
       return rc;
     }
+    stamp_kernel<<<1, 1, 0, st>>>(w.stamp + 1);
+    count_launches(2);
     RWB_CUDA(cudaEventRecord(ev1, st));
     stats_kernel<<<1, 1024, 0, st>>>(w, nb);
     RWB_LAUNCH_CHECK("resident solve epilogue");
     count_launches(2);
     if (stats) {
-      rc = read_stats(w, nb, st, ev0, ev1, 0, RWB_PATH_RESIDENT, stats);
+      rc = read_stats(w, nb, st, ev0, ev1, 0, RWB_PATH_RESIDENT, stats, -1.f, dev_stats);
       if (rc) return rc;
     }
     cudaEventDestroy(ev0);
@@ -1706,14 +1749,17 @@ static int solve_level_impl(const rwb_geometry_t* geom, const float* intensity, 
     RWB_CUDA(cudaEventCreate(&ev0));
     RWB_CUDA(cudaEventCreate(&ev1));
     RWB_CUDA(cudaEventRecord(ev0, st));
+    stamp_kernel<<<1, 1, 0, st>>>(w.stamp);
     RWB_CUDA(cudaLaunchCooperativeKernel((const void*)coop_cg_kernel, dim3(cgrid), block, args, 0, st));
+    stamp_kernel<<<1, 1, 0, st>>>(w.stamp + 1);
+    count_launches(2);
     RWB_CUDA(cudaEventRecord(ev1, st));
     epilogue_kernel<<<sgrid, block, 0, st>>>(g, w, list, prob, labels);
     stats_kernel<<<1, 1024, 0, st>>>(w, nb);
     RWB_LAUNCH_CHECK("cooperative solve");
     count_launches(3);
     if (stats) {
-      rc = read_stats(w, nb, st, ev0, ev1, 0, RWB_PATH_COOPERATIVE, stats);
+      rc = read_stats(w, nb, st, ev0, ev1, 0, RWB_PATH_COOPERATIVE, stats, -1.f, dev_stats);
       if (rc) return rc;
     }
     cudaEventDestroy(ev0);
@@ -1793,7 +1839,7 @@ static int solve_level_impl(const rwb_geometry_t* geom, const float* intensity, 
   RWB_LAUNCH_CHECK("epilogue kernels");
   count_launches(3);
   if (stats) {
-    rc = read_stats(w, nb, st, nullptr, nullptr, sweeps, RWB_PATH_STREAMING, stats, cg_ms);
+    rc = read_stats(w, nb, st, nullptr, nullptr, sweeps, RWB_PATH_STREAMING, stats, cg_ms, dev_stats);
     if (rc) return rc;
   }
   return RWB_OK;

@@ -213,7 +213,7 @@ def workspace_bytes(shape, brick, n_bricks=-1, origin=None, cfg: RWConfig = RWCo
 def solve_level(volume: torch.Tensor, seeds: torch.Tensor, brick, bound: torch.Tensor | None = None,
                 cfg: RWConfig = RWConfig(), *, brick_list: torch.Tensor | None = None, out: torch.Tensor | None = None,
                 labels_out: torch.Tensor | None = None, workspace: Workspace | None = None,
-                origin=None, phase: str | None = None) -> tuple:
+                origin=None, phase: str | None = None, stats_on_device: bool = False) -> tuple:
     """Random-walker solve of (the listed bricks of) one level.
 
     `bound` = upsampled parent probabilities (Dirichlet values outside each
@@ -222,6 +222,9 @@ def solve_level(volume: torch.Tensor, seeds: torch.Tensor, brick, bound: torch.T
     `phase` ("setup" / "solve", brick-resident levels only) splits the call in two:
     "setup" builds the system in the workspace, a later "solve" with the same
     arguments and workspace solves it (stats only from "solve").
+    `stats_on_device`: the stats are written by the device into pinned host memory
+    without a host synchronisation; the returned `DeviceStats` resolves to the dict
+    once the stream has passed the solve (`.resolve()`).
     """
     _check_tensor(volume, torch.float32, "volume", (2, 3))
     _check_tensor(seeds, torch.uint8, "seeds")
@@ -253,6 +256,14 @@ def solve_level(volume: torch.Tensor, seeds: torch.Tensor, brick, bound: torch.T
     p.beta, p.min_weight, p.tol = float(cfg.beta), float(cfg.min_weight), float(cfg.tol)
     p.max_iter, p.check_every = int(cfg.max_iter), int(cfg.check_every)
     p.flags = _flags(cfg) | {None: 0, "setup": _native.SOLVE_SETUP_ONLY, "solve": _native.SOLVE_NO_SETUP}[phase]
+    if stats_on_device and phase != "setup":
+        p.flags |= _native.SOLVE_STATS_DEVICE
+        dstats = DeviceStats()
+        _native.check(lib.rwb_solve_level(
+            ctypes.byref(g), _ptr(volume), _ptr(seeds), _ptr(bound), _ptr(brick_list), int(max(n_list, 0)),
+            ctypes.byref(p), _ptr(out), _ptr(labels_out), _ptr(ws), ctypes.c_size_t(ws.numel()),
+            ctypes.c_void_p(dstats.buffer.data_ptr()), _stream_handle()))
+        return out, dstats
     stats = _native.SolveStats()
     _native.check(lib.rwb_solve_level(
         ctypes.byref(g), _ptr(volume), _ptr(seeds), _ptr(bound), _ptr(brick_list), int(max(n_list, 0)),
@@ -261,11 +272,27 @@ def solve_level(volume: torch.Tensor, seeds: torch.Tensor, brick, bound: torch.T
     return out, (stats.as_dict() if phase != "setup" else None)
 
 
+class DeviceStats:
+    """Solver stats written by the device into pinned (device-mapped) host memory."""
+
+    def __init__(self):
+        self.buffer = torch.zeros(ctypes.sizeof(_native.SolveStats), dtype=torch.uint8, pin_memory=True)
+
+    def resolve(self) -> dict:
+        """The stats dict; the caller must have synchronised past the solve."""
+        return _native.SolveStats.from_buffer_copy(self.buffer.numpy().tobytes()).as_dict()
+
+
+def _resolve(st):
+    return st.resolve() if isinstance(st, DeviceStats) else st
+
+
 # ---------------------------------------------------------------------------
 # hierarchical driver
 
 
 def _merge_stats(parts):
+    parts = [_resolve(s) for s in parts]
     out = dict(parts[0])
     for s in parts[1:]:
         for key in ("bricks", "converged", "not_converged", "zero_rhs", "iterations_sum", "unknowns",
@@ -303,11 +330,11 @@ def _solve_level_chunked(volume, seeds, brick, parent, cfg, labels_out, workspac
         for c in range(chunks):
             upsample_slab(c)
             _, st = solve_level(volume, seeds, brick, bound, cfg, brick_list=lists[c], out=out, labels_out=labels_out,
-                                workspace=workspace)
+                                workspace=workspace, stats_on_device=True)
             parts.append(st)
             if on_chunk is not None:
                 on_chunk(*rows_of[c], out, labels_out)
-        return out, _merge_stats(parts)
+        return out, parts
     # Brick-resident slabs, two-phase: slab c+1's system is built on a setup stream while slab
     # c solves on a high-priority stream (the engine's clusters leave SMs free for the setup
     # CTAs; priority hands SMs back to the engine first).  Two workspaces alternate.
@@ -336,7 +363,7 @@ def _solve_level_chunked(volume, seeds, brick, parent, cfg, labels_out, workspac
         with torch.cuda.stream(solver):
             solver.wait_event(built)
             _, st = solve_level(volume, seeds, brick, bound, cfg, brick_list=lists[c], out=out, labels_out=labels_out,
-                                workspace=spaces[c % 2], phase="solve")
+                                workspace=spaces[c % 2], phase="solve", stats_on_device=True)
             ev = torch.cuda.Event()
             ev.record(solver)
             done[c % 2] = ev
@@ -350,7 +377,7 @@ def _solve_level_chunked(volume, seeds, brick, parent, cfg, labels_out, workspac
     out.record_stream(solver)
     if labels_out is not None:
         labels_out.record_stream(solver)
-    return out, _merge_stats(parts)
+    return out, parts
 
 
 def _resident_geometry(shape, brick) -> bool:
@@ -411,8 +438,10 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
     lab = None
     top_labels = torch.empty(vols[top].shape, dtype=torch.uint8, device=volume.device) \
         if (want_labels and top == 0) else None
+    # stats land in pinned host memory without host synchronisation: the whole hierarchy is
+    # queued back to back, and the stats are read once at the end
     probs[top], stats[top] = solve_level(vols[top], seed_levels[top], tuple(vols[top].shape), None, cfg,
-                                         labels_out=top_labels, workspace=workspace)
+                                         labels_out=top_labels, workspace=workspace, stats_on_device=True)
     lab = top_labels
     for k in range(top - 1, -1, -1):
         if exchange is not None:
@@ -438,10 +467,13 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
                                                       workspace, level0_chunks, on_level0_chunk)
         else:
             probs[k], stats[k] = solve_level(vols[k], seed_levels[k], brick, x, cfg, brick_list=bl,
-                                             labels_out=lab_k, workspace=workspace)
+                                             labels_out=lab_k, workspace=workspace, stats_on_device=True)
             if k == 0 and on_level0_chunk is not None:
                 on_level0_chunk(0, vols[0].shape[0], probs[0], lab_k)
         del x
         if k == 0:
             lab = lab_k
+    if volume.is_cuda:
+        torch.cuda.current_stream().synchronize()
+    stats = [_merge_stats(s) if isinstance(s, list) else _resolve(s) for s in stats]
     return HRWResult(probs[0], lab, probs, vols, seed_levels, stats)

@@ -141,7 +141,7 @@ def _install_oracle_backend():
         return torch.from_numpy(orw.upsample_linear(parent.numpy(), tuple(fine_shape)).astype(np.float32))
 
     def solve_level(vol, seeds, brick, bound, cfg, *, brick_list=None, out=None, labels_out=None,
-                    workspace=None, origin=None):
+                    workspace=None, origin=None, **_unused):
         params = orw.RWParams(beta=cfg.beta, min_weight=cfg.min_weight, tol=1e-10)
         b = None if bound is None else bound.numpy().astype(np.float64)
         res = orw.solve_level(vol.numpy(), seeds.numpy(), brick, b, params).prob.astype(np.float32)
