@@ -31,6 +31,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <mutex>
@@ -1555,6 +1556,8 @@ static int coop_grid(int* grid) {
     if (!coop) return fail(RWB_ERR_UNSUPPORTED, "device does not support cooperative launches");
     RWB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, coop_cg_kernel, NTHREADS, 0));
+    if (const char* e = std::getenv("RWB_COOP_BLOCKS_PER_SM"))  // diagnostics: fewer, fatter blocks
+      per = std::max(1, std::min(per, std::atoi(e)));
     cached = std::min(sms * std::max(per, 1), kCoopMaxBlocks);
   }
   *grid = cached;
