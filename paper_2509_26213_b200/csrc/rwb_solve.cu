@@ -1292,6 +1292,7 @@ __global__ void __launch_bounds__(NTHREADS) settled_epilogue_kernel(Geo g, Work 
 // stat_i: [0] converged [1] maxiter [2] zero-rhs [3] max iterations [4..5] u64 sum of iterations
 //         [6..7] u64 sum over bricks of unknowns x iterations
 __global__ void __launch_bounds__(1024) stats_kernel(Work w, int nb) {
+  // integer sums: order-free, so warp reductions and one shared atomic per warp
   __shared__ int sh[4];
   __shared__ unsigned long long sum, usum;
   if (threadIdx.x < 4) sh[threadIdx.x] = 0;
@@ -1300,21 +1301,32 @@ __global__ void __launch_bounds__(1024) stats_kernel(Work w, int nb) {
   int c1 = 0, c2 = 0, c3 = 0, mx = 0;
   unsigned long long sm = 0, um = 0;
   for (int s = threadIdx.x; s < nb; s += blockDim.x) {
-    int st = w.state[s];
+    const int st = w.state[s];
     c1 += st == ST_CONVERGED;
     c2 += st == ST_MAXITER;
     c3 += st == ST_ZERO;
-    int it = st == ST_ZERO ? 0 : w.iters[s];
+    const int it = st == ST_ZERO ? 0 : w.iters[s];
     mx = max(mx, it);
     sm += (unsigned long long)it;
     um += (unsigned long long)it * w.unk[s];
   }
-  atomicAdd(&sh[0], c1);
-  atomicAdd(&sh[1], c2);
-  atomicAdd(&sh[2], c3);
-  atomicMax(&sh[3], mx);
-  atomicAdd(&sum, sm);
-  atomicAdd(&usum, um);
+  c1 = __reduce_add_sync(0xffffffffu, c1);
+  c2 = __reduce_add_sync(0xffffffffu, c2);
+  c3 = __reduce_add_sync(0xffffffffu, c3);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    sm += __shfl_xor_sync(0xffffffffu, sm, o);
+    um += __shfl_xor_sync(0xffffffffu, um, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&sh[0], c1);
+    atomicAdd(&sh[1], c2);
+    atomicAdd(&sh[2], c3);
+    atomicMax(&sh[3], mx);
+    atomicAdd(&sum, sm);
+    atomicAdd(&usum, um);
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int i = 0; i < 4; ++i) w.stat_i[i] = sh[i];
