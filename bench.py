@@ -420,7 +420,7 @@ def run_ours(args, wl, rank, world):
     traffic = load_traffic(args.config, dom)
     roofline = {"bound": "hbm", "achieved": dk["achieved_gbs"], "peak": peak, "unit": "GB/s", "frac": dk["frac"],
                 "traffic": traffic,
-                "kernel": f"{dk['kernel']} ({dom}, the step's largest launch)",
+                "kernel": f"{dk['kernel']} ({dom}: the level with the largest solve time; its launches)",
                 "algorithmic_bytes": f"{alg_b} B per unknown voxel per PCG iteration (SURVEY.md 8(d)) x "
                                      f"{dk['unknown_iterations_per_step']} unknown-iterations per launch",
                 "peak_source": peak_src,
