@@ -83,3 +83,15 @@ def test_device_path_fails_loudly_without_gpu():
 
     with pytest.raises((_native.NativeUnavailable, ValueError)):
         device.lod_down(torch.zeros(4, 4))
+
+
+def test_solve_flags_match_header():
+    """Every RWB_SOLVE_* flag of the header has the same value in the Python binding."""
+    text = open(HEADER).read()
+    flags = dict(re.findall(r"#define RWB_SOLVE_(\w+)\s+(\d+)", text))
+    assert {"NO_GRAPH", "STREAMING", "NO_COOP", "CLUSTER16", "SPLIT_Z", "SETUP2", "SETUP_ONLY", "NO_SETUP",
+            "STATS_DEVICE"} <= set(flags)
+    for name, value in flags.items():
+        assert getattr(_native, f"SOLVE_{name}") == int(value), name
+    values = [int(v) for v in flags.values()]
+    assert len(set(values)) == len(values) and all(v & (v - 1) == 0 for v in values)  # distinct bits

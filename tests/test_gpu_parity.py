@@ -412,3 +412,35 @@ def test_fused_setup_matches_two_kernel_setup(rng, shape, brick):
     # same arithmetic in the same order: the systems, hence the solves, are bit-identical
     np.testing.assert_array_equal(host(a), host(b))
     assert sa["unknowns"] == sb["unknowns"]
+
+
+@pytest.mark.parametrize("shape,brick", [((64, 96, 64), (32, 32, 32)), ((130, 201), (64, 64))])
+def test_two_phase_and_device_stats_match_one_call(rng, shape, brick):
+    """RWB_SOLVE_SETUP_ONLY + RWB_SOLVE_NO_SETUP (same arguments) and device-written stats give
+    the bytes and the stats of one ordinary call."""
+    vol, seeds = _random_case(rng, shape)
+    bound = cuda(rng.random(shape).astype(np.float32))
+    a, sa = device.solve_level(cuda(vol), cuda(seeds), brick, bound, GPU_CFG)
+    ws = device.Workspace()
+    out = torch.empty(shape, dtype=torch.float32, device="cuda")
+    lab = torch.empty(shape, dtype=torch.uint8, device="cuda")
+    _, none = device.solve_level(cuda(vol), cuda(seeds), brick, bound, GPU_CFG, out=out, labels_out=lab,
+                                 workspace=ws, phase="setup")
+    assert none is None
+    b, sb = device.solve_level(cuda(vol), cuda(seeds), brick, bound, GPU_CFG, out=out, labels_out=lab,
+                               workspace=ws, phase="solve", stats_on_device=True)
+    torch.cuda.synchronize()
+    sb = sb.resolve()
+    np.testing.assert_array_equal(host(a), host(b))
+    np.testing.assert_array_equal(host(lab), (host(b) > 0.5).astype(np.uint8))
+    for key in ("bricks", "converged", "not_converged", "zero_rhs", "iterations_max", "iterations_sum",
+                "unknowns", "unknown_iterations", "path"):
+        assert sa[key] == sb[key], key
+    assert sb["cg_ms"] > 0
+
+
+def test_two_phase_rejected_off_the_resident_path(rng):
+    vol, seeds = _random_case(rng, (40, 40, 40))
+    bound = cuda(rng.random(vol.shape).astype(np.float32))
+    with pytest.raises(ValueError):  # 16^3 bricks: streaming path, no split
+        device.solve_level(cuda(vol), cuda(seeds), (16, 16, 16), bound, GPU_CFG, phase="setup")
