@@ -242,11 +242,12 @@ __global__ void __launch_bounds__(256) upsample_kernel(const float* __restrict__
 // Requires fine nx == 2 * parent nx, nx % (2 UQ) == 0 (16 B aligned row segments).
 constexpr int UQ = 2;  // parent x-voxels per thread
 constexpr int UZ = 8;  // parent planes marched per thread
+// `fine` = fine plane fz0 (a z-window [fz0, fz1) of the level, full in y and x).
 __global__ void __launch_bounds__(256, 4) upsample4_kernel(const float* __restrict__ parent, Shape3 ps,
-                                                        float* __restrict__ fine, Shape3 fs) {
+                                                        float* __restrict__ fine, Shape3 fs, int fz0, int fz1) {
   const int jx0 = (blockIdx.x * BX + threadIdx.x) * UQ;
   const int jy = blockIdx.y * BY + threadIdx.y;
-  const int jz0 = blockIdx.z * UZ;
+  const int jz0 = (fz0 >> 1) + blockIdx.z * UZ;
   if (jx0 >= ps.nx || jy >= ps.ny) return;
   const long long psxy = (long long)ps.ny * ps.nx;
   const int yy[3] = {max(jy - 1, 0), jy, min(jy + 1, ps.ny - 1)};
@@ -275,12 +276,12 @@ __global__ void __launch_bounds__(256, 4) upsample4_kernel(const float* __restri
 #pragma unroll
   for (int s = 0; s < UZ; ++s) {
     const int jz = jz0 + s;
-    if (jz >= ps.nz) break;
+    if (jz >= ps.nz || 2 * jz >= fz1) break;
     load_plane(min(jz + 1, ps.nz - 1), lo[2], hi[2]);
 #pragma unroll
     for (int dz = 0; dz < 2; ++dz) {
       const int gz = 2 * jz + dz;
-      if (gz >= fs.nz) continue;
+      if (gz >= fs.nz || gz < fz0 || gz >= fz1) continue;
       const int za = dz ? 1 : 0, zb = dz ? 2 : 1;
       const float wa = fz2 ? (dz ? 0.75f : 0.25f) : 0.f, wb = fz2 ? (dz ? 0.25f : 0.75f) : 1.f;
 #pragma unroll
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(256, 4) upsample4_kernel(const float* __restri
             const float rb = __fmaf_rn(va, xs[zb][ya][i], __fmul_rn(vb, xs[zb][yb][i]));
             f[2 * i + dx] = __fmaf_rn(wa, ra, __fmul_rn(wb, rb));
           }
-        float4* out = reinterpret_cast<float4*>(fine + ((long long)gz * fs.ny + gy) * fs.nx + 2 * jx0);
+        float4* out = reinterpret_cast<float4*>(fine + ((long long)(gz - fz0) * fs.ny + gy) * fs.nx + 2 * jx0);
 #pragma unroll
         for (int q = 0; q < UQ / 2; ++q) out[q] = make_float4(f[4 * q], f[4 * q + 1], f[4 * q + 2], f[4 * q + 3]);
       }
@@ -586,7 +587,7 @@ extern "C" int rwb_upsample_f32(int32_t ndim, const int64_t* parent_size, const 
     return fail(RWB_ERR_INVALID, "fine size is not a 2x refinement of the parent size");
   if (fs.nx == 2 * ps.nx && fs.nx % (2 * UQ) == 0 && ((uintptr_t)fine & 15) == 0) {
     dim3 grid((ps.nx / UQ + BX - 1) / BX, (ps.ny + BY - 1) / BY, (ps.nz + UZ - 1) / UZ);
-    upsample4_kernel<<<grid, kBlock3, 0, (cudaStream_t)stream>>>(parent, ps, fine, fs);
+    upsample4_kernel<<<grid, kBlock3, 0, (cudaStream_t)stream>>>(parent, ps, fine, fs, 0, fs.nz);
   } else {
     launch_upsample(parent, ps, Shape3{0, 0, 0}, ps, fine, fs, Shape3{0, 0, 0}, fs, (cudaStream_t)stream);
   }
@@ -636,7 +637,15 @@ extern "C" int rwb_upsample_window_f32(int32_t ndim, const int64_t* parent_size,
     if (fd[d] == 1) lo = hi = 0;
     if (lo < pod[d] || hi >= pod[d] + pwd[d]) return fail(RWB_ERR_INVALID, "parent window does not cover the taps");
   }
-  launch_upsample(parent, ps, po, pw, fine, fs, fo, fw, (cudaStream_t)stream);
+  const bool whole_parent = po.nz == 0 && po.ny == 0 && po.nx == 0 && pw.nz == ps.nz && pw.ny == ps.ny && pw.nx == ps.nx;
+  const bool z_slab = fo.ny == 0 && fo.nx == 0 && fw.ny == fs.ny && fw.nx == fs.nx;
+  if (whole_parent && z_slab && fs.nx == 2 * ps.nx && fs.nx % (2 * UQ) == 0 && ((uintptr_t)fine & 15) == 0) {
+    const int pz0 = fo.nz >> 1, pz1 = (fo.nz + fw.nz + 1) >> 1;
+    dim3 grid((ps.nx / UQ + BX - 1) / BX, (ps.ny + BY - 1) / BY, (pz1 - pz0 + UZ - 1) / UZ);
+    upsample4_kernel<<<grid, kBlock3, 0, (cudaStream_t)stream>>>(parent, ps, fine, fs, fo.nz, fo.nz + fw.nz);
+  } else {
+    launch_upsample(parent, ps, po, pw, fine, fs, fo, fw, (cudaStream_t)stream);
+  }
   RWB_LAUNCH_CHECK("upsample_kernel (window)");
   count_launches(1);
   return RWB_OK;
