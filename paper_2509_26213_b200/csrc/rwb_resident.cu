@@ -86,6 +86,7 @@ struct RCfg {
 // phase timestamps of cluster 0 (diagnostics build only)
 __device__ long long g_rwb_trace[8][64][8];
 __device__ long long g_rwb_btrace[8][16][10];
+__device__ unsigned long long g_rwb_end[64];  // %globaltimer at each cluster's last brick (launch 0 only)
 #define TRACE(k)                                                                                      \
   do {                                                                                                \
     if (tid == 0 && blockIdx.x < 8 && rank < 8 && trace_it < 64) g_rwb_trace[rank][trace_it][k] = clock64(); \
@@ -121,6 +122,8 @@ struct ResidentSmem {
   unsigned long long barR[2];            // mbarriers: dot-product partials, per parity
   unsigned long long barL[2];            // mbarriers: bulk staging, per buffer
   unsigned long long barS[2];            // mbarriers: Jacobi scales staged into sr[] for the epilogue
+  unsigned long long barJ[2];            // mbarriers: the cluster's next brick index, per parity
+  int jn[2];                             // ... pushed by rank 0 into every CTA
 };
 
 // ---- PTX helpers ----------------------------------------------------------------
@@ -267,6 +270,7 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
       mbar_init(&sm.barR[i], 1);
       mbar_init(&sm.barL[i], 1);
       mbar_init(&sm.barS[i], 1);
+      mbar_init(&sm.barJ[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -300,12 +304,26 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
   int btrace_n = 0;
 #endif
 
+  // Bricks are handed out dynamically: a cluster's first two bricks are static (cid, cid + ncl),
+  // every further one comes from a global counter.  Rank 0 draws the brick after next at the start
+  // of a brick, pushes the index into the cluster's CTAs once the brick's registers are loaded
+  // (the atomic's latency is hidden behind the slab wait), and every CTA picks it up at the end of
+  // the brick, so the next brick's slab is always staged while this one iterates.  The end of a
+  // launch then idles at most about one brick's time instead of the spread of static shares.
+  unsigned uJ = 0;
   int buf = 0;
   if (cid < n_act && tid == 0) stage_slab<RPZ, TZT>(a, sm, 0, a.alist[cid], rank);
-  for (int j = cid; j < n_act; j += ncl, buf ^= (NBUF - 1)) {
+  for (int j = cid, jn = cid + ncl, jnn; j < n_act; j = jn, jn = jnn, buf ^= (NBUF - 1)) {
     BTRACE(0);
     const int slot = a.alist[j];
-    if (NBUF == 2 && j + ncl < n_act && tid == 0) stage_slab<RPZ, TZT>(a, sm, buf ^ 1, a.alist[j + ncl], rank);
+    const bool draw = jn < n_act;  // cluster-uniform: once past the end, every later draw is too
+    const int parJ = uJ & 1;
+    int jd = 0;
+    if (draw && tid == 0) {
+      mbar_expect_tx(&sm.barJ[parJ], 4);
+      if (rank == 0) jd = 2 * ncl + atomicAdd(a.next, 1);
+    }
+    if (NBUF == 2 && draw && tid == 0) stage_slab<RPZ, TZT>(a, sm, buf ^ 1, a.alist[jn], rank);
     if (buf) {
       mbar_wait(&sm.barL[1], uses1 & 1);
       ++uses1;
@@ -349,6 +367,11 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
       }
     }
     const float thresh = (float)((double)a.tol2 * a.bb[slot]);
+    if (draw && rank == 0 && tid == 0) {
+#pragma unroll 1
+      for (int c = 0; c < RCL; ++c)
+        st_async_f32(mapa_u32(smem_u32(&sm.jn[parJ]), c), __int_as_float(jd), mapa_u32(smem_u32(&sm.barJ[parJ]), c));
+    }
     BTRACE(2);
 
     // ---------------- CG (Chronopoulos-Gear) ----------------
@@ -598,18 +621,34 @@ __global__ void __launch_bounds__(RCfg<RPZ, TZT>::RTT, RCfg<RPZ, TZT>::MINB) res
     // the staging buffer just read is refilled for a later brick: every thread
     // must be past its register loads first
     __syncthreads();
-    if (NBUF == 1 && j + ncl < n_act && tid == 0) stage_slab<RPZ, TZT>(a, sm, 0, a.alist[j + ncl], rank);
+    if (NBUF == 1 && draw && tid == 0) stage_slab<RPZ, TZT>(a, sm, 0, a.alist[jn], rank);
+    jnn = n_act;
+    if (draw) {
+      mbar_wait(&sm.barJ[parJ], (uJ >> 1) & 1);
+      jnn = sm.jn[parJ];
+      ++uJ;
+    }
     BTRACE(7);
     BTRACE(8);
 #ifdef RWB_TRACE
     ++btrace_n;
 #endif
   }
+#ifdef RWB_TRACE
+  if (rank == 0 && tid == 0 && cid < 64) {
+    unsigned long long tnow;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+    g_rwb_end[cid] = tnow;
+  }
+#endif
 }
 
 #ifdef RWB_TRACE
 extern "C" int rwb_trace_dump(long long* out) {  // 8*64*8 int64
   return (int)cudaMemcpyFromSymbol(out, g_rwb_trace, sizeof(g_rwb_trace));
+}
+extern "C" int rwb_end_dump(unsigned long long* out) {  // 64 uint64
+  return (int)cudaMemcpyFromSymbol(out, g_rwb_end, sizeof(g_rwb_end));
 }
 extern "C" int rwb_btrace_dump(long long* out) {  // 8*16*10 int64
   return (int)cudaMemcpyFromSymbol(out, g_rwb_btrace, sizeof(g_rwb_btrace));

@@ -36,6 +36,7 @@ struct ResidentArgs {
   const int* n_active;
   int* state;             // per slot
   int* iters;             // per slot
+  int* next;              // dynamic brick counter (zero at launch)
   float tol2;
   int max_iter;
   // results straight into the level: prob = s y (unknowns) or y, labels = prob > 0.5

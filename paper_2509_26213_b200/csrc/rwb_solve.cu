@@ -66,6 +66,7 @@ struct Work {
   unsigned long long* unknowns;  // [1]
   int* stat_i;       // [8] device stats scratch
   unsigned long long* stamp;  // [2] %globaltimer (ns) around the solve launches
+  int* next;                  // [1] dynamic brick counter of the resident 3-D engine
 };
 
 // ---------------------------------------------------------------------------
@@ -1388,7 +1389,7 @@ static Layout layout(const Geo& g, long long nb) {
                              nb * sizeof(int), nb * sizeof(int), nb * sizeof(unsigned), nb * sizeof(unsigned), nb * sizeof(int),
                              std::max((size_t)nb * std::max(g.tiles, setup_tiles(g)) * sizeof(float2),
                                       (size_t)2 * kCoopMaxBlocks * sizeof(float)),
-                             64};
+                             128};
   size_t o = 0;
   for (int i = 0; i < L_N; ++i) {
     L.off[i] = o;
@@ -1418,6 +1419,7 @@ static Work carve(const Layout& L, char* base, const Geo& g) {
   w.unknowns = reinterpret_cast<unsigned long long*>(misc + 8);
   w.stat_i = reinterpret_cast<int*>(misc + 16);
   w.stamp = reinterpret_cast<unsigned long long*>(misc + 48);
+  w.next = reinterpret_cast<int*>(misc + 64);
   return w;
 }
 
@@ -1492,10 +1494,11 @@ static int launch_chunk(const Geo& g, const Work& w, int nb, const int* list, in
 // land in PINNED scratch: a copy into pageable memory is staged by the driver
 // and can queue behind unrelated bulk copies on other streams (e.g. the
 // overlapped downloads of api.segment_many), stalling this stream for them.
-__global__ void stamp_kernel(unsigned long long* dst) {
+__global__ void stamp_kernel(unsigned long long* dst, int* zero = nullptr) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   *dst = t;
+  if (zero) *zero = 0;
 }
 
 // RWB_SOLVE_STATS_DEVICE: `stats` is device-accessible memory (device memory or
@@ -1707,6 +1710,7 @@ static int solve_level_impl(const rwb_geometry_t* geom, const float* intensity, 
     ra.n_active = w.n_active;
     ra.state = w.state;
     ra.iters = w.iters;
+    ra.next = w.next;
     ra.tol2 = tol2;
     ra.max_iter = max_iter;
     ra.sc = w.sc;
@@ -1720,7 +1724,7 @@ static int solve_level_impl(const rwb_geometry_t* geom, const float* intensity, 
     RWB_CUDA(cudaEventCreate(&ev0));
     RWB_CUDA(cudaEventCreate(&ev1));
     RWB_CUDA(cudaEventRecord(ev0, st));
-    stamp_kernel<<<1, 1, 0, st>>>(w.stamp);
+    stamp_kernel<<<1, 1, 0, st>>>(w.stamp, w.next);  // also re-arms the brick counter
     if (g.is3d)
       rc = launch_resident3d(ra, nb, (params->flags & RWB_SOLVE_CLUSTER16) ? 16 : ((params->flags & RWB_SOLVE_SPLIT_Z) ? 512 : 8),
                              st);
