@@ -98,10 +98,13 @@ class ClockSampler:
         self.lines = []
 
     def __enter__(self):
+        period = int(os.environ.get("RWB_BENCH_CLOCK_MS", "200"))  # diagnostics: 0 = no sampling
+        if period <= 0:
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", str(period)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
         except OSError:
@@ -401,7 +404,8 @@ def run_ours(args, wl, rank, world):
         del vol_h, seeds_h, outs
 
     peak, peak_src = load_peak()
-    path_name = {0: "streaming cg_pass1/cg_pass2", 1: "resident3d_kernel", 2: "coop_cg_kernel"}
+    path_name = {0: "streaming cg_pass1/cg_pass2", 1: "resident3d_q4_kernel" if len(wl["shape"]) == 3 else
+                 "resident2d_kernel", 2: "coop_cg_kernel"}
     kernels = {}
     for k, a in sorted(acc.items()):
         if a["ms"] <= 0:
@@ -424,8 +428,8 @@ def run_ours(args, wl, rank, world):
                 "algorithmic_bytes": f"{alg_b} B per unknown voxel per PCG iteration (SURVEY.md 8(d)) x "
                                      f"{dk['unknown_iterations_per_step']} unknown-iterations per launch",
                 "peak_source": peak_src,
-                "note": ("frac > 1: the brick-resident engine keeps every CG vector of a brick in registers/SMEM "
-                         "of an 8-CTA cluster, so per-iteration traffic never reaches HBM; the HBM roofline of "
+                "note": ("frac > 1: the brick-resident engine keeps every CG vector of a brick on chip (registers, "
+                         "TMEM and SMEM of a 4-CTA cluster), so per-iteration traffic never reaches HBM; the HBM roofline of "
                          "the streaming algorithm (the 8(d) bytes) is beaten, and the kernel is bound by the "
                          "latency of its per-iteration cluster reduction instead. traffic = ncu DRAM bytes of "
                          "this launch (profiles/)"),

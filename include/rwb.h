@@ -83,6 +83,8 @@ typedef struct {
    by a kernel on `stream` with no host synchronisation (brick-resident / cooperative paths never
    block the host then; cg_ms from %globaltimer around the solve launches). */
 #define RWB_SOLVE_STATS_DEVICE 512
+/* brick-resident solver: 4-CTA clusters (8 planes x 8192 voxels per CTA, weights in shared memory) */
+#define RWB_SOLVE_CLUSTER4 1024
 
 /* Solver paths (rwb_solve_stats_t.path) */
 #define RWB_PATH_STREAMING 0 /* brick-batched CG, state in HBM, 2 launches per iteration */

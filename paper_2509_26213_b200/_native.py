@@ -28,6 +28,7 @@ SOLVE_SETUP2 = 32
 SOLVE_SETUP_ONLY = 128
 SOLVE_NO_SETUP = 256
 SOLVE_STATS_DEVICE = 512
+SOLVE_CLUSTER4 = 1024
 PATH_STREAMING, PATH_RESIDENT, PATH_COOPERATIVE = 0, 1, 2
 
 # every symbol include/rwb.h declares, with (restype, argtypes)

@@ -21,7 +21,8 @@ class RWConfig:
     resident: bool = True      # 32^3 bricks: solve each brick on chip (8-CTA cluster) instead of streaming
     cooperative: bool = True   # whole-level solves: one cooperative kernel for all iterations
     fused_setup: bool = True   # build the brick system with the fused per-brick setup kernel
-    cluster: int = 8           # resident solver: CTAs per brick cluster (8: 1 CTA/SM; 16: 2 CTAs/SM, measured 1.7x slower)
+    cluster: int = 4           # resident solver: CTAs per brick cluster (4: weights in TMEM, default; 8: all in registers;
+                               # 16: 2 CTAs/SM; 512: 8-CTA with 512 threads) — 4 is 1.4x faster than 8 on config 4
 
     def params(self) -> dict:
         d = asdict(self)

@@ -47,6 +47,7 @@
 
 #include "rwb_common.cuh"
 #include "rwb_resident.cuh"
+#include "rwb_ptx.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -125,102 +126,6 @@ struct ResidentSmem {
   unsigned long long barJ[2];            // mbarriers: the cluster's next brick index, per parity
   int jn[2];                             // ... pushed by rank 0 into every CTA
 };
-
-// ---- PTX helpers ----------------------------------------------------------------
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
-  uint32_t out;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(addr), "r"(rank));
-  return out;
-}
-
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t phase) {
-  const uint32_t a = smem_u32(bar);
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra.uni WAIT_%=;\n\t}" ::"r"(a),
-      "r"(phase)
-      : "memory");
-}
-
-__device__ __forceinline__ void st_async_f32(uint32_t remote, float v, uint32_t remote_bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(remote),
-               "r"(__float_as_uint(v)), "r"(remote_bar)
-               : "memory");
-}
-
-__device__ __forceinline__ void st_async_v4(uint32_t remote, float4 v, uint32_t remote_bar) {
-  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
-                   remote),
-               "r"(__float_as_uint(v.x)), "r"(__float_as_uint(v.y)), "r"(__float_as_uint(v.z)),
-               "r"(__float_as_uint(v.w)), "r"(remote_bar)
-               : "memory");
-}
-
-// 1-D bulk copy global -> own shared memory, completing on an mbarrier (16 B aligned, size % 16 == 0)
-__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, uint32_t bytes, unsigned long long* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(smem)),
-               "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ float lane_of(const float4& v, int i) {
-  return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
-}
-
-__device__ __forceinline__ float4 f4(float a, float b, float c, float d) { return make_float4(a, b, c, d); }
-
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// Sum of the N pushed per-CTA partials (N = 8 or 16): every thread loads all
-// of them (broadcast LDS.128) and adds them in the same fixed tree, so every
-// warp of every CTA gets the bit-identical total.
-template <int N>
-__device__ __forceinline__ float sum_parts(const float* red) {
-  static_assert(N == 8 || N == 16, "partial count");
-  const float4* v = reinterpret_cast<const float4*>(red);
-  const float4 a = v[0], b = v[1];
-  float s = ((a.x + a.y) + (a.z + a.w)) + ((b.x + b.y) + (b.z + b.w));
-  if constexpr (N == 16) {
-    const float4 c = v[2], d = v[3];
-    s += ((c.x + c.y) + (c.z + c.w)) + ((d.x + d.y) + (d.z + d.w));
-  }
-  return s;
-}
-
-// Two fmaf in one FFMA2 (fma.rn.f32x2, sm_100): bit-identical to the scalar pair,
-// half the issue slots.  d = a * b + c elementwise.
-__device__ __forceinline__ void fma2(float& d0, float& d1, float a0, float a1, float b0, float b1, float c0, float c1) {
-  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
-      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
-      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
-      : "=f"(d0), "=f"(d1)
-      : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
-}
-
-__device__ __forceinline__ float rcp_ftz(float x) {
-  float y;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
 
 // Stage the slab of `slot` into buffer `buf` (one thread issues; completes on barL[buf]).
 template <int RPZ, int TZT>
@@ -693,6 +598,7 @@ static int launch_resident(const ResidentArgs& a, int max_bricks, cudaStream_t s
 
 int launch_resident3d(const ResidentArgs& a, int max_bricks, int variant, cudaStream_t st) {
   switch (variant) {
+    case 4: return launch_resident3d_q4(a, max_bricks, st);
     case 16: return launch_resident<2, 2>(a, max_bricks, st);
     case 512: return launch_resident<4, 2>(a, max_bricks, st);
     default: return launch_resident<4, 4>(a, max_bricks, st);

@@ -54,5 +54,7 @@ int resident2d_supported(const Geo& g);
 int launch_resident2d(const ResidentArgs& a, int max_bricks, cudaStream_t st);
 // variant: 8 = 8-CTA clusters (4 planes per CTA), 16 = 16-CTA clusters (2 planes per CTA, 2 CTAs/SM)
 int launch_resident3d(const ResidentArgs& a, int max_bricks, int variant, cudaStream_t st);
+// 4-CTA clusters, 8 planes per CTA, weights in shared memory (rwb_resident4.cu)
+int launch_resident3d_q4(const ResidentArgs& a, int max_bricks, cudaStream_t st);
 
 }  // namespace rwb

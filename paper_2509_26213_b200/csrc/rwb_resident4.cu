@@ -1,0 +1,469 @@
+// Brick-resident Jacobi-PCG engine, 4-CTA variant: one 32^3 brick per 4-CTA
+// cluster, each CTA a slab of 8 z-planes (8192 voxels), every CG iteration on chip.
+//
+// Why a second engine (rwb_resident.cu holds the 8-CTA one): an 8-CTA brick
+// iteration takes ~1950 cycles of which only ~650 are instruction issue; the
+// rest is the latency chain of the iteration (SpMV -> warp sums -> DSMEM push
+// -> wait -> scalars -> update), which does not grow with the voxels per SM.
+// Giving each SM twice the voxels amortises that chain over twice the work,
+// and 4-CTA clusters also place better (33 clusters = 132 SMs, against 15 x 8
+// = 120 SMs for 8-CTA clusters).  The register file cannot hold 8192 voxels'
+// vectors AND weights, so the split is:
+//   registers:     y, r, p, s, w of the thread's 4(x) x 8(z) voxels (160 floats)
+//   shared memory: the scaled weights w'x, w'y, w'z of the slab (+ the w'z plane
+//                  below it), read by the SpMV every iteration, and the r planes
+//                  (y neighbours), as in the 8-CTA engine.
+// The iteration, exchange protocol, reduction order and scalar recurrences are
+// those of the 8-CTA engine (see there), with 4 partials per reduction.  Each
+// CTA keeps ONE staging buffer (the weights are live for the whole brick): the
+// next brick's slab is prefetched into L2 (cp.async.bulk.prefetch) when a brick
+// starts and bulk-copied into shared memory when it ends.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "rwb_common.cuh"
+#include "rwb_ptx.cuh"
+#include "rwb_resident.cuh"
+
+namespace cg = cooperative_groups;
+
+#ifdef RWB_TRACE
+__device__ long long g_q4_trace[4][64][8];  // phase clocks of cluster 0 (diagnostics build only)
+#define Q4TRACE(k)                                                                          \
+  do {                                                                                      \
+    if (tid == 0 && blockIdx.x < 4 && trace_it < 64) g_q4_trace[rank][trace_it][k] = clock64(); \
+  } while (0)
+extern "C" int rwb_q4_trace_dump(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_q4_trace, sizeof(g_q4_trace));
+}
+#else
+#define Q4TRACE(k) \
+  do {             \
+  } while (0)
+#endif
+
+namespace rwb {
+namespace q4 {
+constexpr int RB = 32;                 // brick edge
+constexpr int RQ = 4;                  // x voxels per thread
+constexpr int RQN = RB / RQ;           // quads per row
+constexpr int PLANE = RB * RB;
+constexpr int RPZ = 8;                 // z planes per CTA (= per thread)
+constexpr int RCL = RB / RPZ;          // CTAs per cluster (4)
+constexpr int RTT = RQN * RB;          // threads per CTA (256)
+constexpr int RW = RTT / 32;           // warps
+constexpr int RV = RQ * RPZ;           // voxels per thread (32)
+constexpr int SLAB = RPZ * PLANE;      // voxels per CTA (8192)
+constexpr int NPART = RCL;
+}  // namespace q4
+
+struct Q4Smem {
+  float sx[q4::SLAB];                       // scaled weights of the slab
+  float sy[q4::SLAB];
+  float sz[q4::PLANE + q4::SLAB];           // w'z incl. the plane below the slab
+  float sr[q4::SLAB];                       // staged r0; then the Jacobi scales for the epilogue
+  float sv[q4::SLAB];                       // staged y0
+  float4 rp[q4::RPZ][q4::RB][q4::RQN];      // r planes (y neighbours of the SpMV)
+  float4 rface[2][2][q4::RB][q4::RQN];      // received faces [parity][0 = from below, 1 = from above]
+  __align__(16) float red[2][2][q4::NPART]; // pushed partials [parity][gamma, delta][rank]
+  float2 wpart[q4::RW];
+  unsigned long long barR[2];               // faces + partials, per parity
+  unsigned long long barL;                  // slab staging
+  uint32_t tmem;                            // TMEM base address (512 columns)
+  unsigned long long barJ[2];               // next brick index, per parity
+  int jn[2];
+};
+
+// Bulk-copy `slot`'s slab of this CTA into shared memory (one thread; completes on barL).
+__device__ __forceinline__ void q4_stage(const ResidentArgs& a, Q4Smem& sm, int slot, int rank) {
+  using namespace q4;
+  const long long base = (long long)slot * (RB * RB * RB) + (long long)rank * SLAB;
+  const uint32_t slab_bytes = SLAB * 4;
+  const uint32_t zbytes = rank > 0 ? slab_bytes + PLANE * 4 : slab_bytes;
+  mbar_expect_tx(&sm.barL, 4 * slab_bytes + zbytes);
+  bulk_g2s(sm.sx, a.wx + base, slab_bytes, &sm.barL);
+  bulk_g2s(sm.sy, a.wy + base, slab_bytes, &sm.barL);
+  if (rank > 0)
+    bulk_g2s(sm.sz, a.wz + base - PLANE, zbytes, &sm.barL);
+  else
+    bulk_g2s(sm.sz + PLANE, a.wz + base, zbytes, &sm.barL);
+  bulk_g2s(sm.sr, a.r0 + base, slab_bytes, &sm.barL);
+  bulk_g2s(sm.sv, a.y + base, slab_bytes, &sm.barL);
+}
+
+__device__ __forceinline__ void q4_prefetch(const ResidentArgs& a, int slot, int rank) {
+  using namespace q4;
+  const long long base = (long long)slot * (RB * RB * RB) + (long long)rank * SLAB;
+  prefetch_l2(a.sc + base, SLAB * 4);
+}
+
+__global__ void __launch_bounds__(q4::RTT, 1) resident3d_q4_kernel(ResidentArgs a) {
+  using namespace q4;
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Q4Smem& sm = *reinterpret_cast<Q4Smem*>(smem_raw);
+  const int rank = (int)cluster.block_rank();
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int ly = tid / RQN;  // row
+  const int xq = tid % RQN;  // quad within the row
+  const bool below = rank > 0, above = rank < RCL - 1;
+  const int nfaces = (int)below + (int)above;
+  const uint32_t tx_faces = nfaces * (uint32_t)(RB * RQN * sizeof(float4));
+  const int cid = blockIdx.x / RCL, ncl = gridDim.x / RCL;
+  const int n_act = *a.n_active;
+
+  if (tid == 0) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&sm.barR[i], 1);
+      mbar_init(&sm.barJ[i], 1);
+    }
+    mbar_init(&sm.barL, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (rank == 0)  // the CTA holding plane 0 has no plane below
+    for (int i = tid; i < PLANE; i += RTT) sm.sz[i] = 0.f;
+  // pushes (remote addresses formed where used: registers are the scarce resource here):
+  // plane 0 goes to the CTA below as its "from above" face, plane 7 to the CTA above as its
+  // "from below" face, lane t of warp 0 delivers the CTA's partials to CTA t
+  auto push_dn = [&](int par, float4 v) {
+    st_async_v4(mapa_u32(smem_u32(&sm.rface[par][1][ly][xq]), rank - 1), v, mapa_u32(smem_u32(&sm.barR[par]), rank - 1));
+  };
+  auto push_up = [&](int par, float4 v) {
+    st_async_v4(mapa_u32(smem_u32(&sm.rface[par][0][ly][xq]), rank + 1), v, mapa_u32(smem_u32(&sm.barR[par]), rank + 1));
+  };
+  auto push_parts = [&](int par, float g, float d) {
+    const uint32_t dst = mapa_u32(smem_u32(&sm.red[par][0][rank]), lane), bar = mapa_u32(smem_u32(&sm.barR[par]), lane);
+    st_async_f32(dst, g, bar);
+    st_async_f32(dst + NPART * 4, d, bar);
+  };
+  if (warp == 0) tmem_alloc(&sm.tmem, 512);
+  tmem_fence_before();
+  cluster.sync();
+  tmem_fence_after();
+  // this thread's TMEM row: lane quarter of its warp, column half by warp / 4
+  const uint32_t tb = sm.tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 256);
+  unsigned gk = 0, usesL = 0, uJ = 0;
+
+  // dynamic brick scheduling as in the 8-CTA engine: bricks cid and cid + ncl static, then a
+  // global counter drawn one brick ahead by rank 0 and pushed into the cluster's CTAs
+  if (cid < n_act && tid == 0) q4_stage(a, sm, a.alist[cid], rank);
+  for (int j = cid, jn = cid + ncl, jnn; j < n_act; j = jn, jn = jnn) {
+    const int slot = a.alist[j];
+    const bool draw = jn < n_act;
+    const int parJ = uJ & 1;
+    int jd = 0;
+    if (draw && tid == 0) {
+      mbar_expect_tx(&sm.barJ[parJ], 4);
+      if (rank == 0) jd = 2 * ncl + atomicAdd(a.next, 1);
+    }
+    if (tid == 0) q4_prefetch(a, slot, rank);  // scales of this brick, for the epilogue
+    mbar_wait(&sm.barL, usesL & 1);
+    ++usesL;
+
+    // the slab's weights into this thread's TMEM row: per plane z, columns 16z.. hold w'y of
+    // the quad, w'y of the row below, w'z and w'x of the quad; columns 128.. the w'x left of the
+    // quad for each plane, 136.. the w'z plane below the thread's first plane
+    {
+      float tt[16];
+#pragma unroll
+      for (int z = 0; z < RPZ; ++z) {
+        const int o = z * PLANE + ly * RB + xq * RQ;
+        const float4 wx4 = *reinterpret_cast<const float4*>(&sm.sx[o]);
+        const float4 wy4 = *reinterpret_cast<const float4*>(&sm.sy[o]);
+        const float4 wz4 = *reinterpret_cast<const float4*>(&sm.sz[PLANE + o]);
+        const float4 wyb4 = ly > 0 ? *reinterpret_cast<const float4*>(&sm.sy[o - RB]) : f4(0, 0, 0, 0);
+        const float v[16] = {wy4.x, wy4.y, wy4.z, wy4.w, wyb4.x, wyb4.y, wyb4.z, wyb4.w,
+                             wz4.x, wz4.y, wz4.z, wz4.w, wx4.x, wx4.y, wx4.z, wx4.w};
+        tmem_st16(tb + 16 * z, v);
+        tt[z] = xq > 0 ? sm.sx[o - 1] : 0.f;
+      }
+      const float4 wzb4 = *reinterpret_cast<const float4*>(&sm.sz[ly * RB + xq * RQ]);
+      tt[8] = wzb4.x, tt[9] = wzb4.y, tt[10] = wzb4.z, tt[11] = wzb4.w;
+      tt[12] = tt[13] = tt[14] = tt[15] = 0.f;
+      tmem_st16(tb + 128, tt);
+    }
+    float y[RV], r[RV], p[RV], sv[RV], w[RV];
+#pragma unroll
+    for (int z = 0; z < RPZ; ++z) {
+      const int o = z * PLANE + ly * RB + xq * RQ;
+      const float4 fr = *reinterpret_cast<const float4*>(&sm.sr[o]);
+      const float4 fv = *reinterpret_cast<const float4*>(&sm.sv[o]);
+#pragma unroll
+      for (int i = 0; i < RQ; ++i) {
+        const int v = z * RQ + i;
+        r[v] = lane_of(fr, i);
+        y[v] = lane_of(fv, i);
+        p[v] = sv[v] = w[v] = 0.f;
+      }
+    }
+    const float thresh = (float)((double)a.tol2 * a.bb[slot]);
+    if (draw && rank == 0 && tid == 0) {
+#pragma unroll 1
+      for (int c = 0; c < RCL; ++c)
+        st_async_f32(mapa_u32(smem_u32(&sm.jn[parJ]), c), __int_as_float(jd), mapa_u32(smem_u32(&sm.barJ[parJ]), c));
+    }
+
+    float gamma = 0.f, alpha = 0.f, rgamma = 0.f, ralpha = 0.f;
+    int state = ST_ACTIVE, it = 0;
+    float4 rf_dn = f4(0, 0, 0, 0), rf_up = f4(0, 0, 0, 0);
+    float4 sf_dn = f4(0, 0, 0, 0), sf_up = f4(0, 0, 0, 0);
+    const float4 z4 = f4(0, 0, 0, 0);
+    auto plane4 = [&](const float* v, int z) { return f4(v[z * RQ], v[z * RQ + 1], v[z * RQ + 2], v[z * RQ + 3]); };
+#pragma unroll
+    for (int z = 0; z < RPZ; ++z) sm.rp[z][ly][xq] = plane4(r, z);
+    {
+      const int par = gk & 1;
+      const uint32_t ph = (gk >> 1) & 1;
+      if (tid == 0) mbar_expect_tx(&sm.barR[par], tx_faces + 2 * NPART * 4);
+      if (below) push_dn(par, plane4(r, 0));
+      if (above) push_up(par, plane4(r, RPZ - 1));
+      if (warp == 0 && lane < RCL) push_parts(par, 0.f, 0.f);
+      mbar_wait(&sm.barR[par], ph);
+      ++gk;
+      if (below) rf_dn = sm.rface[par][0][ly][xq];
+      if (above) rf_up = sm.rface[par][1][ly][xq];
+      tmem_wait_st();
+      __syncthreads();  // r planes published; every thread has left the staged slab
+    }
+    // the staging buffer is free: bring in the next brick's slab while this one iterates
+    if (draw && tid == 0) q4_stage(a, sm, a.alist[jn], rank);
+
+#ifdef RWB_TRACE
+    int trace_it = (int)gk;
+#endif
+    for (int pass = 0;; ++pass) {
+      Q4TRACE(0);
+      const int par = gk & 1;
+      const uint32_t ph = (gk >> 1) & 1;
+      if (tid == 0) mbar_expect_tx(&sm.barR[par], tx_faces + 2 * NPART * 4);
+      // w = A'r with the weights from shared memory
+      float gp[2] = {0.f, 0.f}, dp[2] = {0.f, 0.f};
+      float4 wzl4;  // w'z of the plane below the slab
+      {
+        float t4[4];
+        tmem_ld4(tb + 136, t4);
+        tmem_wait_ld4(t4);
+        wzl4 = f4(t4[0], t4[1], t4[2], t4[3]);
+      }
+#pragma unroll
+      for (int z = 0; z < RPZ; ++z) {
+        // plane z's weights, loaded once plane z-1 is done (the empty asm ties the address to its
+        // result, so the compiler cannot hoist all eight loads up front and run out of registers)
+        float ta[12];
+        uint32_t ad = tb + 16 * z;
+        if (z > 0) asm volatile("" : "+r"(ad) : "f"(w[z * RQ - 1]));
+        tmem_ld8(ad, ta);
+        tmem_ld4p(ad + 8, ta + 8);
+        tmem_wait_ld12(ta);
+        const float4 wy4 = f4(ta[0], ta[1], ta[2], ta[3]);
+        const float4 wyb4 = f4(ta[4], ta[5], ta[6], ta[7]);
+        const float4 wz4 = f4(ta[8], ta[9], ta[10], ta[11]);
+        const float4 ru = ly + 1 < RB ? sm.rp[z][ly + 1][xq] : z4;
+        const float4 rd = ly > 0 ? sm.rp[z][ly - 1][xq] : z4;
+        const float4 rzu = z + 1 < RPZ ? plane4(r, z + 1) : rf_up;
+        const float4 rzd = z > 0 ? plane4(r, z - 1) : rf_dn;
+        const float rl = __shfl_up_sync(0xffffffffu, r[z * RQ + RQ - 1], 1);
+        const float rr_ = __shfl_down_sync(0xffffffffu, r[z * RQ], 1);
+        float acc[RQ];
+#pragma unroll
+        for (int i = 0; i < RQ; i += 2) {
+          fma2(acc[i], acc[i + 1], lane_of(wy4, i), lane_of(wy4, i + 1), lane_of(ru, i), lane_of(ru, i + 1), 0.f, 0.f);
+          fma2(acc[i], acc[i + 1], lane_of(wyb4, i), lane_of(wyb4, i + 1), lane_of(rd, i), lane_of(rd, i + 1), acc[i],
+               acc[i + 1]);
+          fma2(acc[i], acc[i + 1], lane_of(wz4, i), lane_of(wz4, i + 1), lane_of(rzu, i), lane_of(rzu, i + 1), acc[i],
+               acc[i + 1]);
+          fma2(acc[i], acc[i + 1], lane_of(wzl4, i), lane_of(wzl4, i + 1), lane_of(rzd, i), lane_of(rzd, i + 1), acc[i],
+               acc[i + 1]);
+        }
+        float tx[5];  // w'x of the quad and the one left of it, once the y / z terms are done
+        uint32_t adx = tb + 16 * z + 12, adl = tb + 128 + z;
+        asm volatile("" : "+r"(adx), "+r"(adl) : "f"(acc[0]), "f"(acc[2]));
+        tmem_ld4p(adx, tx);
+        tmem_ld1(adl, tx[4]);
+        tmem_wait_ld5(tx);
+        const float4 wx4 = f4(tx[0], tx[1], tx[2], tx[3]);
+        const float wxl0 = tx[4];
+#pragma unroll
+        for (int i = 0; i < RQ; ++i) {
+          const int v = z * RQ + i;
+          const float rxl = i > 0 ? r[v - 1] : rl;
+          const float rxr = i < RQ - 1 ? r[v + 1] : rr_;
+          const float wxl = i > 0 ? lane_of(wx4, i - 1) : wxl0;
+          acc[i] = fmaf(lane_of(wx4, i), rxr, acc[i]);
+          acc[i] = fmaf(wxl, rxl, acc[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < RQ; i += 2) {
+          const int v = z * RQ + i;
+          fma2(w[v], w[v + 1], -1.f, -1.f, acc[i], acc[i + 1], r[v], r[v + 1]);
+          fma2(gp[0], gp[1], r[v], r[v + 1], r[v], r[v + 1], gp[0], gp[1]);
+          fma2(dp[0], dp[1], w[v], w[v + 1], r[v], r[v + 1], dp[0], dp[1]);
+        }
+        wzl4 = wz4;
+      }
+      Q4TRACE(1);
+      if (below) push_dn(par, plane4(w, 0));
+      if (above) push_up(par, plane4(w, RPZ - 1));
+      {
+        const float gs = gp[0] + gp[1];
+        const float ds = dp[0] + dp[1];
+        const float gw = warp_sum(gs);
+        const float dw = warp_sum(ds);
+        if (lane == 0) sm.wpart[warp] = make_float2(gw, dw);
+        asm volatile("bar.sync 1, %0;" ::"n"(RTT) : "memory");
+        if (warp == 0) {
+          float gc = 0.f, dc = 0.f;
+#pragma unroll
+          for (int wv = 0; wv < RW; ++wv) {
+            const float2 v = sm.wpart[wv];
+            gc += v.x;
+            dc += v.y;
+          }
+          if (lane < RCL) push_parts(par, gc, dc);
+        }
+      }
+      Q4TRACE(2);
+      mbar_wait(&sm.barR[par], ph);
+      Q4TRACE(3);
+      ++gk;
+      const float g_new = sum_parts<NPART>(sm.red[par][0]);
+      const float delta = sum_parts<NPART>(sm.red[par][1]);
+      float beta;
+      if (pass == 0) {
+        beta = 0.f;
+        alpha = delta != 0.f ? g_new * rcp_ftz(delta) : 0.f;
+        if (a.max_iter <= 0) {
+          state = ST_MAXITER;
+          break;
+        }
+      } else {
+        if (g_new <= thresh) {
+          state = ST_CONVERGED;
+          break;
+        }
+        if (it >= a.max_iter) {
+          state = ST_MAXITER;
+          break;
+        }
+        beta = g_new * rgamma;
+        const float den = delta - beta * (g_new * ralpha);
+        alpha = den != 0.f ? g_new * rcp_ftz(den) : 0.f;
+      }
+      gamma = g_new;
+      rgamma = rcp_ftz(g_new);
+      ralpha = rcp_ftz(alpha);
+      Q4TRACE(4);
+#pragma unroll
+      for (int v = 0; v < RV; v += 2) {
+        fma2(p[v], p[v + 1], beta, beta, p[v], p[v + 1], r[v], r[v + 1]);
+        fma2(sv[v], sv[v + 1], beta, beta, sv[v], sv[v + 1], w[v], w[v + 1]);
+        fma2(y[v], y[v + 1], alpha, alpha, p[v], p[v + 1], y[v], y[v + 1]);
+        fma2(r[v], r[v + 1], -alpha, -alpha, sv[v], sv[v + 1], r[v], r[v + 1]);
+      }
+      ++it;
+      if (below) {
+        const float4 wn = sm.rface[par][0][ly][xq];
+        sf_dn = f4(fmaf(beta, sf_dn.x, wn.x), fmaf(beta, sf_dn.y, wn.y), fmaf(beta, sf_dn.z, wn.z), fmaf(beta, sf_dn.w, wn.w));
+        rf_dn = f4(fmaf(-alpha, sf_dn.x, rf_dn.x), fmaf(-alpha, sf_dn.y, rf_dn.y), fmaf(-alpha, sf_dn.z, rf_dn.z),
+                   fmaf(-alpha, sf_dn.w, rf_dn.w));
+      }
+      if (above) {
+        const float4 wn = sm.rface[par][1][ly][xq];
+        sf_up = f4(fmaf(beta, sf_up.x, wn.x), fmaf(beta, sf_up.y, wn.y), fmaf(beta, sf_up.z, wn.z), fmaf(beta, sf_up.w, wn.w));
+        rf_up = f4(fmaf(-alpha, sf_up.x, rf_up.x), fmaf(-alpha, sf_up.y, rf_up.y), fmaf(-alpha, sf_up.z, rf_up.z),
+                   fmaf(-alpha, sf_up.w, rf_up.w));
+      }
+#pragma unroll
+      for (int z = 0; z < RPZ; ++z) sm.rp[z][ly][xq] = plane4(r, z);
+      Q4TRACE(5);
+      __syncthreads();
+      Q4TRACE(6);
+#ifdef RWB_TRACE
+      ++trace_it;
+#endif
+    }
+    (void)gamma;
+    // epilogue: probabilities and labels straight into the level
+    {
+      const long long sbase = (long long)slot * (RB * RB * RB) + (long long)rank * SLAB;
+      const int brick = a.list ? a.list[slot] : slot;
+      const int hx = brick % a.gx, hy = (brick / a.gx) % a.gy, hz = brick / (a.gx * a.gy);
+      const int gy = a.oy + hy * RB + ly, gx0 = a.ox + hx * RB + xq * RQ;
+      const bool row_in = gy >= 0 && gy < a.ny;
+      const bool quad_in = gx0 >= 0 && gx0 + RQ <= a.nx;
+#pragma unroll
+      for (int z = 0; z < RPZ; ++z) {
+        const int gz = a.oz + hz * RB + rank * RPZ + z;
+        if (!row_in || gz < 0 || gz >= a.nz) continue;
+        const float4 s4 = __ldg(reinterpret_cast<const float4*>(a.sc + sbase + z * PLANE + ly * RB + xq * RQ));
+        float pv[RQ];
+#pragma unroll
+        for (int i = 0; i < RQ; ++i) {
+          const float s = lane_of(s4, i), yv = y[z * RQ + i];
+          pv[i] = s > 0.f ? s * yv : yv;
+        }
+        const long long gi = ((long long)gz * a.ny + gy) * a.nx + gx0;
+        if (quad_in && (gi & 3) == 0) {
+          *reinterpret_cast<float4*>(a.prob + gi) = f4(pv[0], pv[1], pv[2], pv[3]);
+          if (a.labels)
+            *reinterpret_cast<uchar4*>(a.labels + gi) = make_uchar4(pv[0] > 0.5f, pv[1] > 0.5f, pv[2] > 0.5f, pv[3] > 0.5f);
+        } else {
+#pragma unroll
+          for (int i = 0; i < RQ; ++i) {
+            if (gx0 + i < 0 || gx0 + i >= a.nx) continue;
+            a.prob[gi + i] = pv[i];
+            if (a.labels) a.labels[gi + i] = pv[i] > 0.5f ? 1 : 0;
+          }
+        }
+      }
+    }
+    if (rank == 0 && tid == 0) {
+      a.state[slot] = state;
+      a.iters[slot] = it;
+    }
+    jnn = n_act;
+    if (draw) {
+      mbar_wait(&sm.barJ[parJ], (uJ >> 1) & 1);
+      jnn = sm.jn[parJ];
+      ++uJ;
+    }
+  }
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(sm.tmem, 512);
+}
+
+int launch_resident3d_q4(const ResidentArgs& a, int max_bricks, cudaStream_t st) {
+  using namespace q4;
+  static thread_local int clusters = 0;
+  const int smem = (int)sizeof(Q4Smem);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = RCL;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.blockDim = dim3(RTT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  if (!clusters) {
+    RWB_CUDA(cudaFuncSetAttribute(resident3d_q4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    cfg.gridDim = dim3(RCL * 1024, 1, 1);
+    int n = 0;
+    RWB_CUDA(cudaOccupancyMaxActiveClusters(&n, resident3d_q4_kernel, &cfg));
+    if (n <= 0) return fail(RWB_ERR_UNSUPPORTED, "no 4-CTA brick cluster fits on this device");
+    clusters = n;
+  }
+  const int grid_clusters = clusters < max_bricks ? clusters : max_bricks;
+  if (grid_clusters <= 0) return RWB_OK;
+  cfg.gridDim = dim3(grid_clusters * RCL, 1, 1);
+  RWB_CUDA(cudaLaunchKernelEx(&cfg, resident3d_q4_kernel, a));
+  count_launches(1);
+  return RWB_OK;
+}
+
+}  // namespace rwb

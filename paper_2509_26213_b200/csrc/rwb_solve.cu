@@ -1726,7 +1726,7 @@ static int solve_level_impl(const rwb_geometry_t* geom, const float* intensity, 
     RWB_CUDA(cudaEventRecord(ev0, st));
     stamp_kernel<<<1, 1, 0, st>>>(w.stamp, w.next);  // also re-arms the brick counter
     if (g.is3d)
-      rc = launch_resident3d(ra, nb, (params->flags & RWB_SOLVE_CLUSTER16) ? 16 : ((params->flags & RWB_SOLVE_SPLIT_Z) ? 512 : 8),
+      rc = launch_resident3d(ra, nb, (params->flags & RWB_SOLVE_CLUSTER4) ? 4 : (params->flags & RWB_SOLVE_CLUSTER16) ? 16 : ((params->flags & RWB_SOLVE_SPLIT_Z) ? 512 : 8),
                              st);
     else
       rc = launch_resident2d(ra, nb, st);

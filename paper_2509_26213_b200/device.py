@@ -196,12 +196,14 @@ def _flags(cfg: RWConfig) -> int:
         f |= _native.SOLVE_NO_COOP
     if not cfg.fused_setup:
         f |= _native.SOLVE_SETUP2
-    if cfg.cluster == 16:
+    if cfg.cluster == 4:  # 4-CTA clusters, weights in shared memory
+        f |= _native.SOLVE_CLUSTER4
+    elif cfg.cluster == 16:
         f |= _native.SOLVE_CLUSTER16
     elif cfg.cluster == 512:  # 8-CTA clusters, 512 threads per CTA
         f |= _native.SOLVE_SPLIT_Z
     elif cfg.cluster != 8:
-        raise ValueError("cluster must be 8, 16 or 512")
+        raise ValueError("cluster must be 4, 8, 16 or 512")
     return f
 
 

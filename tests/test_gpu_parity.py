@@ -384,7 +384,7 @@ def test_resident2d_hierarchy_vs_oracle():
     assert_rw_parity(host(res.prob), ref.prob[0], host(res.labels))
 
 
-@pytest.mark.parametrize("cluster", [8, 16, 512])
+@pytest.mark.parametrize("cluster", [4, 8, 16, 512])
 def test_resident_cluster_variants(rng, cluster):
     vol = synthetic.phantom((64, 96, 64))
     seeds = synthetic.seeds(vol.shape, "S1")

@@ -13,7 +13,7 @@ lib.rwb_end_dump.argtypes = [ctypes.c_void_p]
 n = int(os.environ.get("TAIL_N", "512"))
 shape = (n,) * 3
 vol = synthetic.phantom_device(shape); sd = synthetic.seeds_device(shape, "S1")
-res = device.hierarchical_random_walker(vol, sd, (32, 32, 32), 2, RWConfig(), level0_chunks=1)
+res = device.hierarchical_random_walker(vol, sd, (32, 32, 32), 2, RWConfig(cluster=8), level0_chunks=1)
 torch.cuda.synchronize()
 buf = (ctypes.c_ulonglong * 64)()
 lib.rwb_end_dump(buf)

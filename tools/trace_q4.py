@@ -1,0 +1,24 @@
+"""Phase timing of the 4-CTA brick-resident CG loop (diagnostics; needs librwb_trace.so, tools/build_trace.sh)."""
+import ctypes, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np, torch
+from paper_2509_26213_b200 import _native
+_native.load_library(os.path.join(_native.LIB_DIR, "librwb_trace.so"))
+from paper_2509_26213_b200 import device, synthetic
+from paper_2509_26213_b200.config import RWConfig
+shape = (256, 256, 256)
+vol = synthetic.phantom_device(shape); sd = synthetic.seeds_device(shape, "S1")
+res = device.hierarchical_random_walker(vol, sd, (32, 32, 32), 2, RWConfig(cluster=4), level0_chunks=1)
+torch.cuda.synchronize()
+print(res.stats[0])
+buf = (ctypes.c_longlong * (4 * 64 * 8))()
+lib = _native.load_library()
+lib.rwb_q4_trace_dump.argtypes = [ctypes.c_void_p]
+print("rc", lib.rwb_q4_trace_dump(buf))
+t = np.frombuffer(buf, dtype=np.int64).reshape(4, 64, 8)
+names = ["spmv", "warp_sums+push", "wait", "scalars", "update+publish", "syncthreads"]
+for rank in range(4):
+    d = np.diff(t[rank][:, :7], axis=1)[5:40]
+    tot = (t[rank, 6:41, 0] - t[rank, 5:40, 0])
+    print("rank", rank, "median cycles per phase", dict(zip(names, np.median(d, axis=0).astype(int))), "iter", int(np.median(tot)))

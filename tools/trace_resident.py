@@ -9,7 +9,7 @@ from paper_2509_26213_b200 import device, synthetic
 from paper_2509_26213_b200.config import RWConfig
 shape = (256, 256, 256)
 vol = synthetic.phantom_device(shape); sd = synthetic.seeds_device(shape, "S1")
-res = device.hierarchical_random_walker(vol, sd, (32, 32, 32), 2, RWConfig(), level0_chunks=1)
+res = device.hierarchical_random_walker(vol, sd, (32, 32, 32), 2, RWConfig(cluster=8), level0_chunks=1)
 torch.cuda.synchronize()
 print(res.stats[0])
 buf = (ctypes.c_longlong * (8 * 64 * 8))()
