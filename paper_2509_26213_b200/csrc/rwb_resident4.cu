@@ -19,6 +19,7 @@
 // next brick's slab is prefetched into L2 (cp.async.bulk.prefetch) when a brick
 // starts and bulk-copied into shared memory when it ends.
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "rwb_common.cuh"
@@ -48,13 +49,24 @@ constexpr int RB = 32;                 // brick edge
 constexpr int RQ = 4;                  // x voxels per thread
 constexpr int RQN = RB / RQ;           // quads per row
 constexpr int PLANE = RB * RB;
-constexpr int RPZ = 8;                 // z planes per CTA (= per thread)
+constexpr int RPZ = 8;                 // z planes per CTA
 constexpr int RCL = RB / RPZ;          // CTAs per cluster (4)
-constexpr int RTT = RQN * RB;          // threads per CTA (256)
-constexpr int RW = RTT / 32;           // warps
-constexpr int RV = RQ * RPZ;           // voxels per thread (32)
+constexpr int RT = RQN * RB;           // threads per z-group (one per row quad)
 constexpr int SLAB = RPZ * PLANE;      // voxels per CTA (8192)
 constexpr int NPART = RCL;
+constexpr int MAXW = 16;               // warps per CTA at most
+// TZT z planes per thread: 8 -> 256 threads x 32 voxels, 4 -> 512 threads x 16 voxels
+template <int TZT>
+struct Cfg {
+  static constexpr int NZG = RPZ / TZT;             // thread z-groups
+  static constexpr int RTT = RT * NZG;              // threads per CTA
+  static constexpr int RW = RTT / 32;               // warps
+  static constexpr int RV = RQ * TZT;               // voxels per thread
+  static constexpr int COLS = 512 / (RW / 4);       // TMEM columns per thread (warps sharing a lane quarter)
+  static constexpr int TAIL = 16 * TZT;             // column of the per-plane left w'x values
+  static constexpr int WZB = TAIL + 8;              // column of the w'z plane below the thread's first plane
+  static_assert(WZB + 4 <= COLS, "TMEM row");
+};
 }  // namespace q4
 
 struct Q4Smem {
@@ -66,7 +78,7 @@ struct Q4Smem {
   float4 rp[q4::RPZ][q4::RB][q4::RQN];      // r planes (y neighbours of the SpMV)
   float4 rface[2][2][q4::RB][q4::RQN];      // received faces [parity][0 = from below, 1 = from above]
   __align__(16) float red[2][2][q4::NPART]; // pushed partials [parity][gamma, delta][rank]
-  float2 wpart[q4::RW];
+  float2 wpart[q4::MAXW];
   unsigned long long barR[2];               // faces + partials, per parity
   unsigned long long barL;                  // slab staging
   uint32_t tmem;                            // TMEM base address (512 columns)
@@ -97,17 +109,23 @@ __device__ __forceinline__ void q4_prefetch(const ResidentArgs& a, int slot, int
   prefetch_l2(a.sc + base, SLAB * 4);
 }
 
-__global__ void __launch_bounds__(q4::RTT, 1) resident3d_q4_kernel(ResidentArgs a) {
+template <int TZT>
+__global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(ResidentArgs a) {
   using namespace q4;
+  using C = Cfg<TZT>;
+  constexpr int NZG = C::NZG, RTT = C::RTT, RW = C::RW, RV = C::RV;
   cg::cluster_group cluster = cg::this_cluster();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Q4Smem& sm = *reinterpret_cast<Q4Smem*>(smem_raw);
   const int rank = (int)cluster.block_rank();
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int ly = tid / RQN;  // row
-  const int xq = tid % RQN;  // quad within the row
+  const int zg = tid / RT;          // z-group: planes [pz0, pz0 + TZT) of the slab
+  const int ly = (tid % RT) / RQN;  // row
+  const int xq = tid % RQN;         // quad within the row
+  const int pz0 = zg * TZT;
   const bool below = rank > 0, above = rank < RCL - 1;
+  const bool first_zg = zg == 0, last_zg = zg == NZG - 1;
   const int nfaces = (int)below + (int)above;
   const uint32_t tx_faces = nfaces * (uint32_t)(RB * RQN * sizeof(float4));
   const int cid = blockIdx.x / RCL, ncl = gridDim.x / RCL;
@@ -142,8 +160,8 @@ __global__ void __launch_bounds__(q4::RTT, 1) resident3d_q4_kernel(ResidentArgs 
   tmem_fence_before();
   cluster.sync();
   tmem_fence_after();
-  // this thread's TMEM row: lane quarter of its warp, column half by warp / 4
-  const uint32_t tb = sm.tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 256);
+  // this thread's TMEM row: lane quarter of its warp, column block by warp / 4
+  const uint32_t tb = sm.tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * C::COLS);
   unsigned gk = 0, usesL = 0, uJ = 0;
 
   // dynamic brick scheduling as in the 8-CTA engine: bricks cid and cid + ncl static, then a
@@ -163,13 +181,13 @@ __global__ void __launch_bounds__(q4::RTT, 1) resident3d_q4_kernel(ResidentArgs 
     ++usesL;
 
     // the slab's weights into this thread's TMEM row: per plane z, columns 16z.. hold w'y of
-    // the quad, w'y of the row below, w'z and w'x of the quad; columns 128.. the w'x left of the
-    // quad for each plane, 136.. the w'z plane below the thread's first plane
+    // the quad, w'y of the row below, w'z and w'x of the quad; columns TAIL.. the w'x left of
+    // the quad for each plane, WZB.. the w'z plane below the thread's first plane
     {
       float tt[16];
 #pragma unroll
-      for (int z = 0; z < RPZ; ++z) {
-        const int o = z * PLANE + ly * RB + xq * RQ;
+      for (int z = 0; z < TZT; ++z) {
+        const int o = (pz0 + z) * PLANE + ly * RB + xq * RQ;
         const float4 wx4 = *reinterpret_cast<const float4*>(&sm.sx[o]);
         const float4 wy4 = *reinterpret_cast<const float4*>(&sm.sy[o]);
         const float4 wz4 = *reinterpret_cast<const float4*>(&sm.sz[PLANE + o]);
@@ -179,15 +197,17 @@ __global__ void __launch_bounds__(q4::RTT, 1) resident3d_q4_kernel(ResidentArgs 
         tmem_st16(tb + 16 * z, v);
         tt[z] = xq > 0 ? sm.sx[o - 1] : 0.f;
       }
-      const float4 wzb4 = *reinterpret_cast<const float4*>(&sm.sz[ly * RB + xq * RQ]);
+#pragma unroll
+      for (int z = TZT; z < 8; ++z) tt[z] = 0.f;
+      const float4 wzb4 = *reinterpret_cast<const float4*>(&sm.sz[pz0 * PLANE + ly * RB + xq * RQ]);
       tt[8] = wzb4.x, tt[9] = wzb4.y, tt[10] = wzb4.z, tt[11] = wzb4.w;
       tt[12] = tt[13] = tt[14] = tt[15] = 0.f;
-      tmem_st16(tb + 128, tt);
+      tmem_st16(tb + C::TAIL, tt);
     }
     float y[RV], r[RV], p[RV], sv[RV], w[RV];
 #pragma unroll
-    for (int z = 0; z < RPZ; ++z) {
-      const int o = z * PLANE + ly * RB + xq * RQ;
+    for (int z = 0; z < TZT; ++z) {
+      const int o = (pz0 + z) * PLANE + ly * RB + xq * RQ;
       const float4 fr = *reinterpret_cast<const float4*>(&sm.sr[o]);
       const float4 fv = *reinterpret_cast<const float4*>(&sm.sv[o]);
 #pragma unroll
@@ -212,18 +232,18 @@ __global__ void __launch_bounds__(q4::RTT, 1) resident3d_q4_kernel(ResidentArgs 
     const float4 z4 = f4(0, 0, 0, 0);
     auto plane4 = [&](const float* v, int z) { return f4(v[z * RQ], v[z * RQ + 1], v[z * RQ + 2], v[z * RQ + 3]); };
 #pragma unroll
-    for (int z = 0; z < RPZ; ++z) sm.rp[z][ly][xq] = plane4(r, z);
+    for (int z = 0; z < TZT; ++z) sm.rp[pz0 + z][ly][xq] = plane4(r, z);
     {
       const int par = gk & 1;
       const uint32_t ph = (gk >> 1) & 1;
       if (tid == 0) mbar_expect_tx(&sm.barR[par], tx_faces + 2 * NPART * 4);
-      if (below) push_dn(par, plane4(r, 0));
-      if (above) push_up(par, plane4(r, RPZ - 1));
+      if (below && first_zg) push_dn(par, plane4(r, 0));
+      if (above && last_zg) push_up(par, plane4(r, TZT - 1));
       if (warp == 0 && lane < RCL) push_parts(par, 0.f, 0.f);
       mbar_wait(&sm.barR[par], ph);
       ++gk;
-      if (below) rf_dn = sm.rface[par][0][ly][xq];
-      if (above) rf_up = sm.rface[par][1][ly][xq];
+      if (below && first_zg) rf_dn = sm.rface[par][0][ly][xq];
+      if (above && last_zg) rf_up = sm.rface[par][1][ly][xq];
       tmem_wait_st();
       __syncthreads();  // r planes published; every thread has left the staged slab
     }
@@ -243,12 +263,13 @@ __global__ void __launch_bounds__(q4::RTT, 1) resident3d_q4_kernel(ResidentArgs 
       float4 wzl4;  // w'z of the plane below the slab
       {
         float t4[4];
-        tmem_ld4(tb + 136, t4);
+        tmem_ld4(tb + C::WZB, t4);
         tmem_wait_ld4(t4);
         wzl4 = f4(t4[0], t4[1], t4[2], t4[3]);
       }
 #pragma unroll
-      for (int z = 0; z < RPZ; ++z) {
+      for (int z = 0; z < TZT; ++z) {
+        const int pz = pz0 + z;
         // plane z's weights, loaded once plane z-1 is done (the empty asm ties the address to its
         // result, so the compiler cannot hoist all eight loads up front and run out of registers)
         float ta[12];
@@ -260,10 +281,10 @@ __global__ void __launch_bounds__(q4::RTT, 1) resident3d_q4_kernel(ResidentArgs 
         const float4 wy4 = f4(ta[0], ta[1], ta[2], ta[3]);
         const float4 wyb4 = f4(ta[4], ta[5], ta[6], ta[7]);
         const float4 wz4 = f4(ta[8], ta[9], ta[10], ta[11]);
-        const float4 ru = ly + 1 < RB ? sm.rp[z][ly + 1][xq] : z4;
-        const float4 rd = ly > 0 ? sm.rp[z][ly - 1][xq] : z4;
-        const float4 rzu = z + 1 < RPZ ? plane4(r, z + 1) : rf_up;
-        const float4 rzd = z > 0 ? plane4(r, z - 1) : rf_dn;
+        const float4 ru = ly + 1 < RB ? sm.rp[pz][ly + 1][xq] : z4;
+        const float4 rd = ly > 0 ? sm.rp[pz][ly - 1][xq] : z4;
+        const float4 rzu = z + 1 < TZT ? plane4(r, z + 1) : (pz + 1 < RPZ ? sm.rp[pz + 1][ly][xq] : rf_up);
+        const float4 rzd = z > 0 ? plane4(r, z - 1) : (pz > 0 ? sm.rp[pz - 1][ly][xq] : rf_dn);
         const float rl = __shfl_up_sync(0xffffffffu, r[z * RQ + RQ - 1], 1);
         const float rr_ = __shfl_down_sync(0xffffffffu, r[z * RQ], 1);
         float acc[RQ];
@@ -278,7 +299,7 @@ __global__ void __launch_bounds__(q4::RTT, 1) resident3d_q4_kernel(ResidentArgs 
                acc[i + 1]);
         }
         float tx[5];  // w'x of the quad and the one left of it, once the y / z terms are done
-        uint32_t adx = tb + 16 * z + 12, adl = tb + 128 + z;
+        uint32_t adx = tb + 16 * z + 12, adl = tb + C::TAIL + z;
         asm volatile("" : "+r"(adx), "+r"(adl) : "f"(acc[0]), "f"(acc[2]));
         tmem_ld4p(adx, tx);
         tmem_ld1(adl, tx[4]);
@@ -304,8 +325,8 @@ __global__ void __launch_bounds__(q4::RTT, 1) resident3d_q4_kernel(ResidentArgs 
         wzl4 = wz4;
       }
       Q4TRACE(1);
-      if (below) push_dn(par, plane4(w, 0));
-      if (above) push_up(par, plane4(w, RPZ - 1));
+      if (below && first_zg) push_dn(par, plane4(w, 0));
+      if (above && last_zg) push_up(par, plane4(w, TZT - 1));
       {
         const float gs = gp[0] + gp[1];
         const float ds = dp[0] + dp[1];
@@ -363,20 +384,20 @@ __global__ void __launch_bounds__(q4::RTT, 1) resident3d_q4_kernel(ResidentArgs 
         fma2(r[v], r[v + 1], -alpha, -alpha, sv[v], sv[v + 1], r[v], r[v + 1]);
       }
       ++it;
-      if (below) {
+      if (below && first_zg) {
         const float4 wn = sm.rface[par][0][ly][xq];
         sf_dn = f4(fmaf(beta, sf_dn.x, wn.x), fmaf(beta, sf_dn.y, wn.y), fmaf(beta, sf_dn.z, wn.z), fmaf(beta, sf_dn.w, wn.w));
         rf_dn = f4(fmaf(-alpha, sf_dn.x, rf_dn.x), fmaf(-alpha, sf_dn.y, rf_dn.y), fmaf(-alpha, sf_dn.z, rf_dn.z),
                    fmaf(-alpha, sf_dn.w, rf_dn.w));
       }
-      if (above) {
+      if (above && last_zg) {
         const float4 wn = sm.rface[par][1][ly][xq];
         sf_up = f4(fmaf(beta, sf_up.x, wn.x), fmaf(beta, sf_up.y, wn.y), fmaf(beta, sf_up.z, wn.z), fmaf(beta, sf_up.w, wn.w));
         rf_up = f4(fmaf(-alpha, sf_up.x, rf_up.x), fmaf(-alpha, sf_up.y, rf_up.y), fmaf(-alpha, sf_up.z, rf_up.z),
                    fmaf(-alpha, sf_up.w, rf_up.w));
       }
 #pragma unroll
-      for (int z = 0; z < RPZ; ++z) sm.rp[z][ly][xq] = plane4(r, z);
+      for (int z = 0; z < TZT; ++z) sm.rp[pz0 + z][ly][xq] = plane4(r, z);
       Q4TRACE(5);
       __syncthreads();
       Q4TRACE(6);
@@ -394,10 +415,10 @@ __global__ void __launch_bounds__(q4::RTT, 1) resident3d_q4_kernel(ResidentArgs 
       const bool row_in = gy >= 0 && gy < a.ny;
       const bool quad_in = gx0 >= 0 && gx0 + RQ <= a.nx;
 #pragma unroll
-      for (int z = 0; z < RPZ; ++z) {
-        const int gz = a.oz + hz * RB + rank * RPZ + z;
+      for (int z = 0; z < TZT; ++z) {
+        const int gz = a.oz + hz * RB + rank * RPZ + pz0 + z;
         if (!row_in || gz < 0 || gz >= a.nz) continue;
-        const float4 s4 = __ldg(reinterpret_cast<const float4*>(a.sc + sbase + z * PLANE + ly * RB + xq * RQ));
+        const float4 s4 = __ldg(reinterpret_cast<const float4*>(a.sc + sbase + (pz0 + z) * PLANE + ly * RB + xq * RQ));
         float pv[RQ];
 #pragma unroll
         for (int i = 0; i < RQ; ++i) {
@@ -435,8 +456,11 @@ __global__ void __launch_bounds__(q4::RTT, 1) resident3d_q4_kernel(ResidentArgs 
   if (warp == 0) tmem_dealloc(sm.tmem, 512);
 }
 
-int launch_resident3d_q4(const ResidentArgs& a, int max_bricks, cudaStream_t st) {
+template <int TZT>
+static int launch_q4(const ResidentArgs& a, int max_bricks, cudaStream_t st) {
   using namespace q4;
+  constexpr int RTT = Cfg<TZT>::RTT;
+  auto kern = resident3d_q4_kernel<TZT>;
   static thread_local int clusters = 0;
   const int smem = (int)sizeof(Q4Smem);
   cudaLaunchConfig_t cfg = {};
@@ -451,19 +475,27 @@ int launch_resident3d_q4(const ResidentArgs& a, int max_bricks, cudaStream_t st)
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
   if (!clusters) {
-    RWB_CUDA(cudaFuncSetAttribute(resident3d_q4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    RWB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     cfg.gridDim = dim3(RCL * 1024, 1, 1);
     int n = 0;
-    RWB_CUDA(cudaOccupancyMaxActiveClusters(&n, resident3d_q4_kernel, &cfg));
+    RWB_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
     if (n <= 0) return fail(RWB_ERR_UNSUPPORTED, "no 4-CTA brick cluster fits on this device");
     clusters = n;
   }
   const int grid_clusters = clusters < max_bricks ? clusters : max_bricks;
   if (grid_clusters <= 0) return RWB_OK;
   cfg.gridDim = dim3(grid_clusters * RCL, 1, 1);
-  RWB_CUDA(cudaLaunchKernelEx(&cfg, resident3d_q4_kernel, a));
+  RWB_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   count_launches(1);
   return RWB_OK;
+}
+
+int launch_resident3d_q4(const ResidentArgs& a, int max_bricks, cudaStream_t st) {
+  static const int threads = [] {  // diagnostics: RWB_Q4_THREADS=512 (4 planes per thread)
+    const char* e = getenv("RWB_Q4_THREADS");
+    return e ? atoi(e) : 256;
+  }();
+  return threads == 512 ? launch_q4<4>(a, max_bricks, st) : launch_q4<8>(a, max_bricks, st);
 }
 
 }  // namespace rwb
