@@ -156,6 +156,32 @@ int rwb_edge_weights_f32(int32_t ndim, const int64_t* size, const float* volume,
 /* labels[i] = prob[i] > 0.5 (cast_array semantics of a boolean, ops.py:44-52). */
 int rwb_labels_u8(int64_t n, const float* prob, uint8_t* labels, void* stream);
 
+/* Factor-2 mean downsampling alone (build_lod(smooth=False), downsample_mean,
+ * ops.py:611-676): per coarse element, float64 pairwise means along dimension
+ * 0, then 1, then 2 of its 2^d block (a trailing odd element passing through),
+ * rounded to f32.
+ * dst has size ceil(size/2); ndim 1..3. */
+int rwb_downsample_mean_f32(int32_t ndim, const int64_t* size, const float* src, float* dst, void* stream);
+
+/* Chunk payloads <-> dense tensor, for chunked tensor files (PLCT,
+ * tensorfile.py:1-13).  A payload is the full chunk box (chunk[0..ndim)),
+ * row-major, last dimension fastest, `elem_bytes` per element (scalar width x
+ * lanes, lanes innermost: ElementType.payload_shape, model.py:78-80).  Border
+ * chunks are clipped to `size` (chunk_logical_region, model.py:158-170).
+ * Payload i of the batch belongs to chunk chunk_ids[i] (device int64,
+ * row-major chunk index, model.py:138-146), or to chunk first + i when
+ * chunk_ids is NULL.  ndim 1..4.
+ *  scatter: the clipped part of each payload -> its region of `dense`
+ *           (open_chunked's kernel, tensorfile.py:186-195, for a batch)
+ *  gather : each chunk's region of `dense` -> its payload, zero outside the
+ *           tensor (the payloads _ChunkWriter.write_chunk writes, :126-138) */
+int rwb_chunks_scatter(int32_t ndim, const int64_t* size, const int64_t* chunk, int32_t elem_bytes,
+                       const void* payloads, const int64_t* chunk_ids, int64_t first, int64_t n, void* dense,
+                       void* stream);
+int rwb_chunks_gather(int32_t ndim, const int64_t* size, const int64_t* chunk, int32_t elem_bytes,
+                      const void* dense, const int64_t* chunk_ids, int64_t first, int64_t n, void* payloads,
+                      void* stream);
+
 /* Bytes of solver workspace for n_bricks bricks of `geom` (n_bricks < 0: all)
  * with the given RWB_SOLVE_* flags (the brick-resident path needs almost none). */
 size_t rwb_solve_workspace_bytes(const rwb_geometry_t* geom, int64_t n_bricks, int32_t flags);

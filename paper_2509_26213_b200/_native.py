@@ -46,6 +46,11 @@ SIGNATURES = {
     "rwb_edge_weights_f32": (c_int32, [c_int32, ctypes.POINTER(c_int64), c_void_p, c_float, c_float,
                                        c_void_p, c_void_p]),
     "rwb_labels_u8": (c_int32, [c_int64, c_void_p, c_void_p, c_void_p]),
+    "rwb_downsample_mean_f32": (c_int32, [c_int32, ctypes.POINTER(c_int64), c_void_p, c_void_p, c_void_p]),
+    "rwb_chunks_scatter": (c_int32, [c_int32, ctypes.POINTER(c_int64), ctypes.POINTER(c_int64), c_int32, c_void_p,
+                                     c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
+    "rwb_chunks_gather": (c_int32, [c_int32, ctypes.POINTER(c_int64), ctypes.POINTER(c_int64), c_int32, c_void_p,
+                                    c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "rwb_solve_workspace_bytes": (c_size_t, [c_void_p, c_int64, c_int32]),
     "rwb_solve_level": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_void_p,
                                   c_void_p, c_void_p, c_void_p, c_size_t, c_void_p, c_void_p]),

@@ -1,0 +1,183 @@
+// Chunk payloads <-> dense level tensors, for streaming chunked tensor files
+// (the reference's PLCT format, pkg/src/chunkcast/tensorfile.py:1-13) through
+// the GPU, and the plain factor-2 mean downsampling of build_lod(smooth=False).
+//
+// A chunk payload is the full chunk box, row-major, last dimension fastest,
+// lanes innermost (ElementType.payload_shape, model.py:78-80); border chunks
+// are clipped to the tensor and zero-padded (chunk_logical_region,
+// model.py:158-170; _ChunkWriter / import_raw, tensorfile.py:108-165).
+//   scatter: payloads of a batch of chunks -> their clipped regions of the dense tensor
+//   gather:  dense tensor -> payloads (zero padding outside the tensor)
+// Elements are opaque `elem_bytes`-byte items (scalar width x lanes), so one
+// kernel serves every element type.  These sit on the PCIe / disk path
+// (~50 GB/s), two orders below HBM; one element per thread is plenty.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rwb.h"
+#include "rwb_common.cuh"
+
+namespace rwb {
+namespace {
+
+struct ChunkGeo {
+  int nd;                 // padded to 4 dims (leading 1s)
+  long long size[4];
+  long long chunk[4];
+  long long grid[4];      // chunks per dimension
+  long long box;          // elements per chunk
+};
+
+int make_chunk_geo(int32_t ndim, const int64_t* size, const int64_t* chunk, ChunkGeo* g) {
+  if (ndim < 1 || ndim > 4 || !size || !chunk) return fail(RWB_ERR_INVALID, "chunks: ndim must be 1..4");
+  g->nd = 4;
+  g->box = 1;
+  for (int d = 0; d < 4; ++d) {
+    const int s = d - (4 - ndim);
+    g->size[d] = s >= 0 ? size[s] : 1;
+    g->chunk[d] = s >= 0 ? chunk[s] : 1;
+    if (g->size[d] < 1 || g->chunk[d] < 1) return fail(RWB_ERR_INVALID, "chunks: sizes must be positive");
+    g->grid[d] = (g->size[d] + g->chunk[d] - 1) / g->chunk[d];
+    g->box *= g->chunk[d];
+  }
+  return RWB_OK;
+}
+
+template <typename T>
+__device__ __forceinline__ void copy_elem(unsigned char* dst, const unsigned char* src, int eb) {
+  const int n = eb / (int)sizeof(T);
+  for (int i = 0; i < n; ++i) reinterpret_cast<T*>(dst)[i] = reinterpret_cast<const T*>(src)[i];
+}
+
+__device__ __forceinline__ void move_elem(unsigned char* dst, const unsigned char* src, int eb) {
+  if ((eb & 7) == 0)
+    copy_elem<unsigned long long>(dst, src, eb);
+  else if ((eb & 3) == 0)
+    copy_elem<unsigned int>(dst, src, eb);
+  else if ((eb & 1) == 0)
+    copy_elem<unsigned short>(dst, src, eb);
+  else
+    copy_elem<unsigned char>(dst, src, eb);
+}
+
+__device__ __forceinline__ void zero_elem(unsigned char* dst, int eb) {
+  for (int i = 0; i < eb; ++i) dst[i] = 0;
+}
+
+// blockIdx.y: chunk of the batch; x-blocks stride over the chunk box
+template <bool GATHER>
+__global__ void __launch_bounds__(256) chunks_kernel(ChunkGeo g, int eb, unsigned char* __restrict__ payloads,
+                                                     unsigned char* __restrict__ dense,
+                                                     const long long* __restrict__ ids, long long first,
+                                                     long long n) {
+  const long long c = (long long)blockIdx.y + (long long)blockIdx.z * gridDim.y;
+  if (c >= n) return;
+  long long id = ids ? ids[c] : first + c;
+  long long org[4];
+  for (int d = 3; d >= 0; --d) {
+    org[d] = (id % g.grid[d]) * g.chunk[d];
+    id /= g.grid[d];
+  }
+  unsigned char* pay = payloads + c * g.box * eb;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < g.box; e += (long long)gridDim.x * blockDim.x) {
+    long long r = e, gi = 0;
+    bool in = true;
+    long long coord[4];
+    for (int d = 3; d >= 0; --d) {
+      coord[d] = org[d] + r % g.chunk[d];
+      r /= g.chunk[d];
+      in = in && coord[d] < g.size[d];
+    }
+    for (int d = 0; d < 4; ++d) gi = gi * g.size[d] + coord[d];
+    if (GATHER) {
+      if (in)
+        move_elem(pay + e * eb, dense + gi * eb, eb);
+      else
+        zero_elem(pay + e * eb, eb);
+    } else if (in) {
+      move_elem(dense + gi * eb, pay + e * eb, eb);
+    }
+  }
+}
+
+template <bool GATHER>
+int run_chunks(int32_t ndim, const int64_t* size, const int64_t* chunk, int32_t elem_bytes, void* payloads,
+               const int64_t* chunk_ids, int64_t first, int64_t n, void* dense, void* stream) {
+  ChunkGeo g;
+  int rc = make_chunk_geo(ndim, size, chunk, &g);
+  if (rc) return rc;
+  if (elem_bytes < 1 || elem_bytes > 64) return fail(RWB_ERR_INVALID, "chunks: elem_bytes must be 1..64");
+  if (n < 0) return fail(RWB_ERR_INVALID, "chunks: negative chunk count");
+  if (n == 0) return RWB_OK;
+  if (!payloads || !dense) return fail(RWB_ERR_INVALID, "chunks: null pointer");
+  const long long total = g.grid[0] * g.grid[1] * g.grid[2] * g.grid[3];
+  if (!chunk_ids && (first < 0 || first + n > total)) return fail(RWB_ERR_INVALID, "chunks: chunk range outside the grid");
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long bx = (g.box + 255) / 256;
+  const unsigned gx = (unsigned)(bx < 64 ? bx : 64);
+  const long long ny = n < 65535 ? n : 65535;
+  const long long nz = (n + ny - 1) / ny;
+  chunks_kernel<GATHER><<<dim3(gx, (unsigned)ny, (unsigned)nz), 256, 0, st>>>(
+      g, elem_bytes, (unsigned char*)payloads, (unsigned char*)dense, (const long long*)chunk_ids, first, n);
+  RWB_LAUNCH_CHECK(GATHER ? "chunks_gather" : "chunks_scatter");
+  count_launches(1);
+  return RWB_OK;
+}
+
+// f32(pairwise means along z, then y, then x) of each 2^d block, a trailing odd
+// element passing through (downsample_mean / _pairwise_mean, ops.py:611-676;
+// float64 arithmetic: assemble_region hands the means float64 blocks, ops.py:426-464)
+__global__ void __launch_bounds__(256) downsample_mean_kernel(const float* __restrict__ src, long long fz, long long fy,
+                                                              long long fx, float* __restrict__ dst, long long cz,
+                                                              long long cy, long long cx) {
+  const long long n = cz * cy * cx;
+  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < n; o += (long long)gridDim.x * blockDim.x) {
+    const long long jx = o % cx, jy = (o / cx) % cy, jz = o / (cx * cy);
+    const int nz = (2 * jz + 1 < fz) ? 2 : 1, ny = (2 * jy + 1 < fy) ? 2 : 1, nx = (2 * jx + 1 < fx) ? 2 : 1;
+    double v[2][2][2];
+    for (int a = 0; a < nz; ++a)
+      for (int b = 0; b < ny; ++b)
+        for (int c = 0; c < nx; ++c) v[a][b][c] = src[((2 * jz + a) * fy + (2 * jy + b)) * fx + (2 * jx + c)];
+    double m1[2][2], m2[2];
+    for (int b = 0; b < ny; ++b)
+      for (int c = 0; c < nx; ++c) m1[b][c] = nz == 2 ? __dmul_rn(__dadd_rn(v[0][b][c], v[1][b][c]), 0.5) : v[0][b][c];
+    for (int c = 0; c < nx; ++c) m2[c] = ny == 2 ? __dmul_rn(__dadd_rn(m1[0][c], m1[1][c]), 0.5) : m1[0][c];
+    dst[o] = (float)(nx == 2 ? __dmul_rn(__dadd_rn(m2[0], m2[1]), 0.5) : m2[0]);
+  }
+}
+
+}  // namespace
+}  // namespace rwb
+
+extern "C" int rwb_chunks_scatter(int32_t ndim, const int64_t* size, const int64_t* chunk, int32_t elem_bytes,
+                                  const void* payloads, const int64_t* chunk_ids, int64_t first, int64_t n,
+                                  void* dense, void* stream) {
+  return rwb::run_chunks<false>(ndim, size, chunk, elem_bytes, const_cast<void*>(payloads), chunk_ids, first, n,
+                                dense, stream);
+}
+
+extern "C" int rwb_chunks_gather(int32_t ndim, const int64_t* size, const int64_t* chunk, int32_t elem_bytes,
+                                 const void* dense, const int64_t* chunk_ids, int64_t first, int64_t n,
+                                 void* payloads, void* stream) {
+  return rwb::run_chunks<true>(ndim, size, chunk, elem_bytes, payloads, chunk_ids, first, n,
+                               const_cast<void*>(dense), stream);
+}
+
+extern "C" int rwb_downsample_mean_f32(int32_t ndim, const int64_t* size, const float* src, float* dst,
+                                       void* stream) {
+  if (ndim < 1 || ndim > 3 || !size || !src || !dst) return rwb::fail(RWB_ERR_INVALID, "downsample_mean: bad arguments");
+  long long f[3] = {1, 1, 1};
+  for (int d = 0; d < ndim; ++d) {
+    if (size[d] < 1) return rwb::fail(RWB_ERR_INVALID, "downsample_mean: sizes must be positive");
+    f[3 - ndim + d] = size[d];
+  }
+  // unit leading dims stay 1 (ceil(1/2) = 1), matching a (ndim)-dim downsample_mean
+  const long long c[3] = {(f[0] + 1) / 2, (f[1] + 1) / 2, (f[2] + 1) / 2};
+  const long long n = c[0] * c[1] * c[2];
+  const long long blocks = (n + 255) / 256;
+  rwb::downsample_mean_kernel<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, (cudaStream_t)stream>>>(
+      src, f[0], f[1], f[2], dst, c[0], c[1], c[2]);
+  RWB_LAUNCH_CHECK("downsample_mean_kernel");
+  rwb::count_launches(1);
+  return RWB_OK;
+}

@@ -62,6 +62,17 @@ def lod_down(level: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def downsample_mean(level: torch.Tensor) -> torch.Tensor:
+    """Factor-2 mean downsampling alone (the reference's build_lod(smooth=False) step,
+    `downsample_mean`, ops.py:611-676; float64 pairwise means rounded to f32, bit-identical)."""
+    _check_tensor(level, torch.float32, "level", (1, 2, 3))
+    lib = _native.lib()
+    out = torch.empty(coarse_shape(level.shape), dtype=torch.float32, device=level.device)
+    _native.check(lib.rwb_downsample_mean_f32(level.dim(), _native.int64_array(level.shape), _ptr(level), _ptr(out),
+                                              _stream_handle()))
+    return out
+
+
 def num_lod_levels(shape, chunk) -> int:
     """Level count of the reference's `build_lod` stop rule (ops.py:720)."""
     shape = [int(s) for s in shape]

@@ -6,6 +6,9 @@
   `chunkcast.ops.build_lod(source_from_array(x, chunk))` resolved through
   `chunkcast.Engine` (`pkg/src/chunkcast/ops.py:714-727`, `engine.py:423-448`).
   These pin `oracle.lod` (bit-exact) and the CUDA LOD kernel.
+* `plct/` — chunked tensor files written by the reference's `tensorfile` module
+  (`import_raw`, `_ChunkWriter`, `build_lod_offline`; `tensorfile.py:149-165, 108-146, 307-341`),
+  with the arrays they hold (`*.npy`).
 * `rw_*.npz` — random-walker outputs of the float64 oracle (`oracle.rw`,
   tol 1e-10) on the synthetic configs.  The reference has no random walker,
   so these are oracle outputs, not reference outputs (parity unpinned).
@@ -146,8 +149,71 @@ def make_c3like(manifest):
                                   "seeds_sha256": sha(seeds), "prob0_sub_sha256": sha(p)}
 
 
+PLCT_DIR = os.path.join(HERE, "plct")
+
+
+def make_plct(manifest):
+    """Chunked tensor files written by the REFERENCE (`chunkcast.tensorfile`): `import_raw` of
+    f32 / u8 / u16x2 tensors, a hand-ordered file with absent chunks (`_ChunkWriter`), and the
+    pyramids `build_lod_offline` materialises (smooth and plain).  They pin `plct.py` (reader,
+    byte-identical writer) and the GPU `build_lod_offline` (byte-identical level files)."""
+    from chunkcast import tensorfile as tf
+    from chunkcast.engine import Engine, EngineConfig
+    from chunkcast.model import ElementType, EmbeddingData, Scalar, TensorMetaData
+    from chunkcast.store import StoreConfig
+
+    os.makedirs(PLCT_DIR, exist_ok=True)
+    for name in os.listdir(PLCT_DIR):
+        os.remove(os.path.join(PLCT_DIR, name))
+    rng = np.random.default_rng(0x9C7)
+    cases = {
+        "vol3d": (rng.random((40, 36, 28), dtype=np.float32), (16, 16, 16), Scalar.F32, 1, (0.5, 0.75, 1.0)),
+        "seeds3d": (rng.integers(0, 3, (40, 36, 28)).astype(np.uint8), (16, 16, 16), Scalar.U8, 1, (0.5, 0.75, 1.0)),
+        "img2d": (rng.random((37, 29), dtype=np.float32), (8, 8), Scalar.F32, 1, (1.0, 1.0)),
+        "vec2d_u16x2": (rng.integers(0, 65535, (9, 7, 2)).astype(np.uint16), (4, 4), Scalar.U16, 2, (1.0, 2.0)),
+    }
+    entry = {}
+    for name, (arr, chunk, scalar, lanes, spacing) in cases.items():
+        raw = os.path.join(PLCT_DIR, f"{name}.raw")
+        arr.tofile(raw)
+        size = arr.shape[:-1] if lanes > 1 else arr.shape
+        md = TensorMetaData(size, chunk, ElementType(scalar, lanes))
+        out = os.path.join(PLCT_DIR, f"{name}.plct")
+        tf.import_raw(raw, out, md, EmbeddingData(spacing))
+        os.remove(raw)
+        np.save(os.path.join(PLCT_DIR, f"{name}.npy"), arr)
+        entry[name] = {"shape": list(arr.shape), "chunk": list(chunk), "lanes": lanes,
+                       "spacing": list(spacing), "sha256": sha(arr)}
+    # absent chunks and reverse file order, through the reference's writer
+    arr = cases["img2d"][0]
+    md = TensorMetaData(arr.shape, (8, 8), ElementType(Scalar.F32, 1))
+    positions = list(md.chunk_positions())
+    with tf._ChunkWriter(os.path.join(PLCT_DIR, "sparse2d.plct"), md, (1.0, 1.0)) as w:
+        for k, pos in enumerate(reversed(positions)):
+            if k % 3 == 1:
+                continue  # absent: reads as zeros
+            begin, end = md.chunk_logical_region(pos)
+            buf = np.zeros((8, 8), np.float32)
+            buf[tuple(slice(0, e - b) for b, e in zip(begin, end))] = arr[tuple(slice(b, e) for b, e in zip(begin, end))]
+            w.write_chunk(pos, buf)
+    with Engine(EngineConfig(stores=StoreConfig(ram_capacity=1 << 28))) as eng:
+        tf.build_lod_offline(os.path.join(PLCT_DIR, "vol3d.plct"), os.path.join(PLCT_DIR, "vol3d_pyr.json"), eng)
+        tf.build_lod_offline(os.path.join(PLCT_DIR, "img2d.plct"), os.path.join(PLCT_DIR, "img2d_plain.json"), eng,
+                             smooth=False)
+    manifest["plct"] = {"cases": entry, "files": {n: hashlib.sha256(open(os.path.join(PLCT_DIR, n), "rb").read())
+                                                  .hexdigest() for n in sorted(os.listdir(PLCT_DIR))}}
+
+
 def main():
     manifest = {"lod": {}, "rw": {}}
+    if "--plct-only" in sys.argv:
+        path = os.path.join(HERE, "MANIFEST.json")
+        with open(path) as f:
+            manifest = json.load(f)
+        make_plct(manifest)
+        with open(path, "w") as f:
+            json.dump(manifest, f, indent=1, sort_keys=True)
+        return
     path = os.path.join(HERE, "MANIFEST.json")
     if "--c2-only" in sys.argv or "--c3like-only" in sys.argv:  # heavy fixtures, merged into the manifest
         with open(path) as f:
@@ -159,6 +225,7 @@ def main():
     else:
         make_lod(manifest)
         make_rw(manifest)
+        make_plct(manifest)
         if "--c2" in sys.argv:
             make_c2(manifest)
     with open(path, "w") as f:
