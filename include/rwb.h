@@ -182,6 +182,15 @@ int rwb_chunks_gather(int32_t ndim, const int64_t* size, const int64_t* chunk, i
                       const void* dense, const int64_t* chunk_ids, int64_t first, int64_t n, void* payloads,
                       void* stream);
 
+/* Constant-chunk table of a scalar tensor (build_const_chunk_table, ops.py:777-816): table is
+ * dense over the chunk grid (ceil(size/chunk) per dimension, row-major); each element is the
+ * chunk's value when every element of its clipped region equals the first one (element-type
+ * ==, so NaN never matches), else the sentinel: NaN for floats, the type maximum for integers
+ * (sentinel_for, ops.py:770-774).  scalar_code as in PLCT files / model.py:24-29:
+ * 0 u8, 1 i16, 2 u16, 3 f32, 4 f64.  ndim 1..4. */
+int rwb_const_chunk_table(int32_t ndim, const int64_t* size, const int64_t* chunk, int32_t scalar_code,
+                          const void* src, void* table, void* stream);
+
 /* Bytes of solver workspace for n_bricks bricks of `geom` (n_bricks < 0: all)
  * with the given RWB_SOLVE_* flags (the brick-resident path needs almost none). */
 size_t rwb_solve_workspace_bytes(const rwb_geometry_t* geom, int64_t n_bricks, int32_t flags);

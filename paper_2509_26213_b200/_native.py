@@ -49,6 +49,8 @@ SIGNATURES = {
     "rwb_downsample_mean_f32": (c_int32, [c_int32, ctypes.POINTER(c_int64), c_void_p, c_void_p, c_void_p]),
     "rwb_chunks_scatter": (c_int32, [c_int32, ctypes.POINTER(c_int64), ctypes.POINTER(c_int64), c_int32, c_void_p,
                                      c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
+    "rwb_const_chunk_table": (c_int32, [c_int32, ctypes.POINTER(c_int64), ctypes.POINTER(c_int64), c_int32, c_void_p,
+                                        c_void_p, c_void_p]),
     "rwb_chunks_gather": (c_int32, [c_int32, ctypes.POINTER(c_int64), ctypes.POINTER(c_int64), c_int32, c_void_p,
                                     c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "rwb_solve_workspace_bytes": (c_size_t, [c_void_p, c_int64, c_int32]),

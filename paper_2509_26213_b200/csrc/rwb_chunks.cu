@@ -181,3 +181,78 @@ extern "C" int rwb_downsample_mean_f32(int32_t ndim, const int64_t* size, const 
   rwb::count_launches(1);
   return RWB_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Constant-chunk table (build_const_chunk_table, ops.py:777-816): one element per chunk of a
+// scalar tensor, the chunk's value if every element of its logical (clipped) region equals the
+// first one (element type ==, so NaN never matches), else the sentinel (NaN for floats, the
+// type's maximum for integers, ops.py:770-774).  One CTA per chunk.
+namespace rwb {
+namespace {
+
+template <typename T>
+__device__ __forceinline__ T sentinel_of();
+template <> __device__ __forceinline__ uint8_t sentinel_of<uint8_t>() { return 0xFF; }
+template <> __device__ __forceinline__ int16_t sentinel_of<int16_t>() { return 0x7FFF; }
+template <> __device__ __forceinline__ uint16_t sentinel_of<uint16_t>() { return 0xFFFF; }
+template <> __device__ __forceinline__ float sentinel_of<float>() { return __int_as_float(0x7FC00000); }
+template <> __device__ __forceinline__ double sentinel_of<double>() { return __longlong_as_double(0x7FF8000000000000LL); }
+
+template <typename T>
+__global__ void __launch_bounds__(256) const_table_kernel(ChunkGeo g, const T* __restrict__ src, T* __restrict__ table,
+                                                          long long n) {
+  __shared__ int all_eq;
+  for (long long c = blockIdx.x; c < n; c += gridDim.x) {
+    long long id = c, org[4], ext[4], cnt = 1;
+    for (int d = 3; d >= 0; --d) {
+      org[d] = (id % g.grid[d]) * g.chunk[d];
+      id /= g.grid[d];
+      ext[d] = min(g.chunk[d], g.size[d] - org[d]);
+      cnt *= ext[d];
+    }
+    const long long base = ((org[0] * g.size[1] + org[1]) * g.size[2] + org[2]) * g.size[3] + org[3];
+    const T first = src[base];
+    if (threadIdx.x == 0) all_eq = 1;
+    __syncthreads();
+    bool eq = true;
+    for (long long e = threadIdx.x; e < cnt && eq; e += blockDim.x) {
+      long long r = e, off[4];
+      for (int d = 3; d >= 0; --d) {
+        off[d] = r % ext[d];
+        r /= ext[d];
+      }
+      const long long gi = (((org[0] + off[0]) * g.size[1] + org[1] + off[1]) * g.size[2] + org[2] + off[2]) * g.size[3] +
+                           org[3] + off[3];
+      eq = src[gi] == first;
+    }
+    if (!eq) all_eq = 0;  // benign race: every writer stores 0
+    __syncthreads();
+    if (threadIdx.x == 0) table[c] = all_eq ? first : sentinel_of<T>();
+    __syncthreads();
+  }
+}
+
+}  // namespace
+}  // namespace rwb
+
+extern "C" int rwb_const_chunk_table(int32_t ndim, const int64_t* size, const int64_t* chunk, int32_t scalar_code,
+                                     const void* src, void* table, void* stream) {
+  rwb::ChunkGeo g;
+  int rc = rwb::make_chunk_geo(ndim, size, chunk, &g);
+  if (rc) return rc;
+  if (!src || !table) return rwb::fail(RWB_ERR_INVALID, "const_chunk_table: null pointer");
+  const long long n = g.grid[0] * g.grid[1] * g.grid[2] * g.grid[3];
+  const unsigned blocks = (unsigned)(n < 65535 ? n : 65535);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (scalar_code) {
+    case 0: rwb::const_table_kernel<uint8_t><<<blocks, 256, 0, st>>>(g, (const uint8_t*)src, (uint8_t*)table, n); break;
+    case 1: rwb::const_table_kernel<int16_t><<<blocks, 256, 0, st>>>(g, (const int16_t*)src, (int16_t*)table, n); break;
+    case 2: rwb::const_table_kernel<uint16_t><<<blocks, 256, 0, st>>>(g, (const uint16_t*)src, (uint16_t*)table, n); break;
+    case 3: rwb::const_table_kernel<float><<<blocks, 256, 0, st>>>(g, (const float*)src, (float*)table, n); break;
+    case 4: rwb::const_table_kernel<double><<<blocks, 256, 0, st>>>(g, (const double*)src, (double*)table, n); break;
+    default: return rwb::fail(RWB_ERR_INVALID, "const_chunk_table: scalar code must be 0..4 (u8, i16, u16, f32, f64)");
+  }
+  RWB_LAUNCH_CHECK("const_table_kernel");
+  rwb::count_launches(1);
+  return RWB_OK;
+}

@@ -344,23 +344,49 @@ def load_manifest(path) -> tuple:
     return levels
 
 
+def const_chunk_table(level: torch.Tensor, chunk) -> torch.Tensor:
+    """Per-chunk uniform value or sentinel (NaN / type max) over the chunk grid of a scalar device
+    tensor (`build_const_chunk_table`, ops.py:777-816), on the GPU."""
+    if level.dtype not in _CODE_OF:
+        raise ValueError(f"unsupported dtype {level.dtype}")
+    t = level.contiguous()
+    grid = tuple(-(-int(s) // int(c)) for s, c in zip(t.shape, chunk))
+    out = torch.empty(grid, dtype=t.dtype, device=t.device)
+    _native.check(_native.lib().rwb_const_chunk_table(t.dim(), _native.int64_array(t.shape), _native.int64_array(chunk),
+                                                      _CODE_OF[t.dtype], t.data_ptr(), out.data_ptr(),
+                                                      torch.cuda.current_stream(t.device).cuda_stream))
+    return out
+
+
+def _save_const_table(level, chunk, path):
+    table = const_chunk_table(level, chunk)
+    tchunk = tuple(min(int(c), int(g)) for c, g in zip(chunk, table.shape))  # ops.py:787-788
+    save(table, path, tchunk, None)
+
+
 def build_lod_offline(input_path, manifest_path, *, smooth: bool = True, const_tables: bool = False) -> tuple:
     """Materialise the LOD pyramid of a chunked f32 file (`tensorfile.py:307-341`).
 
     Level 0 is the input file itself; level k+1 = f32(downsample_mean(separable_conv(level k)))
     (or downsample_mean alone when `smooth` is False) computed on the GPU — bit-identical to the
     reference's operators — and saved as `<manifest base>.L<k+1>.plct` with the same chunk size
-    and doubled spacing, until every dimension fits one chunk.  Returns the manifest's levels.
+    and doubled spacing, until every dimension fits one chunk.  `const_tables` also writes each
+    level's constant-chunk table as `<base>.L<k>.ctab.plct`.  Returns the manifest's levels.
     """
-    if const_tables:
-        raise NotImplementedError("const chunk tables are not built by this implementation")
     input_path = os.path.abspath(os.fspath(input_path))
     manifest_path = os.fspath(manifest_path)
     base = os.path.splitext(os.path.abspath(manifest_path))[0]
     level, h = load(input_path)
     if h.code != 3 or h.lanes != 1 or h.ndim > 3:
         raise ValueError("build_lod_offline: the GPU LOD kernels take 1- to 3-D f32 scalar tensors")
-    levels = [PyramidLevel(input_path, h.spacing, None)]
+    def table(lv, k):  # the level's constant-chunk table file, when asked for
+        if not const_tables:
+            return None
+        ct = f"{base}.L{k}.ctab.plct"
+        _save_const_table(lv, h.chunk, ct)
+        return ct
+
+    levels = [PyramidLevel(input_path, h.spacing, table(level, 0))]
     size, spacing, k = h.size, h.spacing, 0
     while not all(s <= c for s, c in zip(size, h.chunk)):
         level = device.lod_down(level) if smooth else device.downsample_mean(level)
@@ -368,8 +394,8 @@ def build_lod_offline(input_path, manifest_path, *, smooth: bool = True, const_t
         size = tuple(level.shape)
         path = f"{base}.L{k + 1}.plct"
         save(level, path, h.chunk, spacing)
-        levels.append(PyramidLevel(path, spacing, None))
         k += 1
+        levels.append(PyramidLevel(path, spacing, table(level, k)))
     save_manifest(levels, manifest_path)
     return tuple(levels)
 

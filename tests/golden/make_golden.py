@@ -196,7 +196,23 @@ def make_plct(manifest):
             buf = np.zeros((8, 8), np.float32)
             buf[tuple(slice(0, e - b) for b, e in zip(begin, end))] = arr[tuple(slice(b, e) for b, e in zip(begin, end))]
             w.write_chunk(pos, buf)
+    # a volume with uniform chunks (and one NaN) for the constant-chunk tables
+    blocky = np.zeros((40, 36, 28), np.float32)
+    blocky[16:, :, :] = 0.25
+    blocky[16:32, 16:32, 16:] = rng.random((16, 16, 12), dtype=np.float32)
+    blocky[5, 5, 5] = np.nan
+    raw = os.path.join(PLCT_DIR, "blocky3d.raw")
+    blocky.tofile(raw)
+    tf.import_raw(raw, os.path.join(PLCT_DIR, "blocky3d.plct"),
+                  TensorMetaData(blocky.shape, (16, 16, 16), ElementType(Scalar.F32, 1)), EmbeddingData((1.0, 1.0, 1.0)))
+    os.remove(raw)
+    np.save(os.path.join(PLCT_DIR, "blocky3d.npy"), blocky)
+    from chunkcast import ops as rops
     with Engine(EngineConfig(stores=StoreConfig(ram_capacity=1 << 28))) as eng:
+        tf.save_tensor(rops.build_const_chunk_table(tf.open_chunked(os.path.join(PLCT_DIR, "seeds3d.plct"))),
+                       os.path.join(PLCT_DIR, "seeds3d.ctab.plct"), eng)
+        tf.build_lod_offline(os.path.join(PLCT_DIR, "blocky3d.plct"), os.path.join(PLCT_DIR, "blocky3d_ct.json"), eng,
+                             const_tables=True)
         tf.build_lod_offline(os.path.join(PLCT_DIR, "vol3d.plct"), os.path.join(PLCT_DIR, "vol3d_pyr.json"), eng)
         tf.build_lod_offline(os.path.join(PLCT_DIR, "img2d.plct"), os.path.join(PLCT_DIR, "img2d_plain.json"), eng,
                              smooth=False)

@@ -54,13 +54,17 @@ def test_sparse_file_header():
     assert np.all(np.diff(present.astype(np.int64)) < 0) or present.size <= 1  # written in reverse chunk order
 
 
-@pytest.mark.parametrize("manifest", ["vol3d_pyr.json", "img2d_plain.json"])
+@pytest.mark.parametrize("manifest", ["vol3d_pyr.json", "img2d_plain.json", "blocky3d_ct.json"])
 def test_manifest_roundtrip(tmp_path, manifest):
     levels = plct.load_manifest(gp(manifest))
-    assert all(os.path.exists(lv.path) for lv in levels) and levels[0].const_table is None
+    assert all(os.path.exists(lv.path) for lv in levels)
     for lv in levels:
-        shutil.copy(lv.path, tmp_path / os.path.basename(lv.path))
-    moved = [plct.PyramidLevel(str(tmp_path / os.path.basename(lv.path)), lv.spacing, None) for lv in levels]
+        for f in (lv.path, lv.const_table):
+            if f:
+                shutil.copy(f, tmp_path / os.path.basename(f))
+    moved = [plct.PyramidLevel(str(tmp_path / os.path.basename(lv.path)), lv.spacing,
+                               str(tmp_path / os.path.basename(lv.const_table)) if lv.const_table else None)
+             for lv in levels]
     plct.save_manifest(moved, tmp_path / manifest)
     assert (tmp_path / manifest).read_text() == open(gp(manifest)).read()
     # spacing doubles per level (downsample_mean's embedding, ops.py:620-627)
@@ -137,6 +141,33 @@ def test_build_lod_offline_matches_reference(tmp_path, src, manifest, smooth):
     for ours, theirs in zip(levels, ref):
         assert filecmp.cmp(ours.path, theirs.path, shallow=False), os.path.basename(theirs.path)
     assert (tmp_path / manifest).read_text() == open(gp(manifest)).read()
+
+
+@pytest.mark.gpu
+def test_const_chunk_table_matches_reference(tmp_path):
+    t, h = plct.load(gp("seeds3d.plct"))
+    table = plct.const_chunk_table(t, h.chunk)
+    plct._save_const_table(t, h.chunk, tmp_path / "c.plct")
+    assert filecmp.cmp(tmp_path / "c.plct", gp("seeds3d.ctab.plct"), shallow=False)
+    ref, _ = plct.load(gp("seeds3d.ctab.plct"))
+    assert torch_equal(table, ref)
+
+
+def torch_equal(a, b):
+    import torch
+    return a.shape == b.shape and bool(torch.equal(a.view(torch.uint8), b.view(torch.uint8)))
+
+
+@pytest.mark.gpu
+def test_build_lod_offline_const_tables(tmp_path):
+    shutil.copy(gp("blocky3d.plct"), tmp_path / "blocky3d.plct")
+    levels = plct.build_lod_offline(tmp_path / "blocky3d.plct", tmp_path / "blocky3d_ct.json", const_tables=True)
+    ref = plct.load_manifest(gp("blocky3d_ct.json"))
+    assert len(levels) == len(ref)
+    for ours, theirs in zip(levels, ref):
+        assert filecmp.cmp(ours.path, theirs.path, shallow=False), os.path.basename(theirs.path)
+        assert filecmp.cmp(ours.const_table, theirs.const_table, shallow=False), os.path.basename(theirs.const_table)
+    assert (tmp_path / "blocky3d_ct.json").read_text() == open(gp("blocky3d_ct.json")).read()
 
 
 @pytest.mark.gpu
