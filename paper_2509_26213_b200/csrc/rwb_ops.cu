@@ -185,9 +185,16 @@ __global__ void __launch_bounds__(256) upsample_kernel(const float* __restrict__
   const int jz = j0.nz + blockIdx.z;
   if (jx >= ps.nx || jy >= ps.ny || jz >= ps.nz) return;
   const long long psxy = (long long)pw.ny * pw.nx;
-  const int xm = max(jx - 1, 0) - po.nx, xc = jx - po.nx, xp = min(jx + 1, ps.nx - 1) - po.nx;
-  const int zz[3] = {max(jz - 1, 0) - po.nz, jz - po.nz, min(jz + 1, ps.nz - 1) - po.nz};
-  const int yy[3] = {max(jy - 1, 0) - po.ny, jy - po.ny, min(jy + 1, ps.ny - 1) - po.ny};
+  // window-relative taps, clamped into the parent window: a tap outside it only feeds fine
+  // voxels outside the fine window (the host checked that the window's taps are covered), and
+  // reading it would run past the window buffer
+  auto in_w = [](int v, int n) { return min(max(v, 0), n - 1); };
+  const int xm = in_w(max(jx - 1, 0) - po.nx, pw.nx), xc = in_w(jx - po.nx, pw.nx);
+  const int xp = in_w(min(jx + 1, ps.nx - 1) - po.nx, pw.nx);
+  const int zz[3] = {in_w(max(jz - 1, 0) - po.nz, pw.nz), in_w(jz - po.nz, pw.nz),
+                     in_w(min(jz + 1, ps.nz - 1) - po.nz, pw.nz)};
+  const int yy[3] = {in_w(max(jy - 1, 0) - po.ny, pw.ny), in_w(jy - po.ny, pw.ny),
+                     in_w(min(jy + 1, ps.ny - 1) - po.ny, pw.ny)};
   // x-interpolated parent rows: lo -> fine 2j (0.25 P[j-1] + 0.75 P[j]), hi -> 2j+1 (0.75 P[j] + 0.25 P[j+1])
   float lo[3][3], hi[3][3];
 #pragma unroll

@@ -7,7 +7,10 @@ A reference `Engine` resolves them unchanged: it calls `dependencies(h)`,
 pins the input chunks in RAM and runs the kernel on a worker thread
 (`engine.py:999-1076`); the kernel stages the chunk neighbourhood to the
 GPU, calls the C ABI and writes the result (including zero padding, as
-`ops.py:517-520` requires) into `out`.
+`ops.py:517-520` requires) into `out`.  The random-walker operator instead carries a
+`task_body` (engine-level batching): the engine hands it a batch of up to
+`max_requests_per_task` chunk requests, and the batch becomes ONE brick-list solve over the
+union window of its footprints (one upload, one launch sequence) instead of one solve per chunk.
 
     import chunkcast
     from paper_2509_26213_b200 import ops as rw
@@ -32,6 +35,8 @@ from __future__ import annotations
 import math
 import os
 import sys
+
+import threading
 
 import numpy as np
 
@@ -104,7 +109,10 @@ def _device():
 
 def _to_dev(a: np.ndarray):
     torch, dev = _device()
-    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    a = np.ascontiguousarray(a)
+    if not a.flags.writeable:  # engine-pinned input payloads are read-only views
+        a = a.copy()
+    return torch.from_numpy(a).to(dev)
 
 
 def _from_dev(t) -> np.ndarray:
@@ -117,6 +125,47 @@ def _from_dev(t) -> np.ndarray:
 def _dilated(md, h, r=1):
     begin, end = md.chunk_logical_region(h)
     return ([max(b - r, 0) for b in begin], [min(e + r, s) for e, s in zip(end, md.size)], begin, end)
+
+
+# Device sections of the batched random-walker tasks run one at a time per process: the engine's
+# worker threads still gather and scatter chunk payloads concurrently on the host, and the GPU
+# work is one stream anyway, so interleaving them only adds allocator churn.
+_DEVICE_LOCK = threading.Lock()
+
+
+def _batched_body(ctx, inputs, dependencies, solve_batch):
+    """Engine task body computing a whole batch of chunk requests in one call.
+
+    The reference engine hands an operator's queued requests to one task in batches of up to
+    `max_requests_per_task` (engine.py:790-816); its generic body then runs the operator's
+    kernel once per chunk (`_generic_compute_body`, engine.py:999-1076).  This body keeps the
+    generic body's input protocol (one deduplicated ChunkRequest per input, input states
+    noted), but runs `solve_batch(positions, arrays)` — one device solve for the batch — as a
+    single worker job, then stores every chunk's payload.
+    """
+    from chunkcast.engine import RAM, ChunkRequest, ChunkState, WorkerJob
+
+    positions = [tuple(int(x) for x in p) for p in ctx.positions]
+    per_input = [[] for _ in inputs]
+    seen = [set() for _ in inputs]
+    for pos in positions:
+        for i, plist in enumerate(dependencies(pos)):
+            for q in plist:
+                q = tuple(q)
+                if q not in seen[i]:
+                    seen[i].add(q)
+                    per_input[i].append(q)
+    wanted = ChunkState.PREVIEW if ctx.wanted_state == ChunkState.PREVIEW else ChunkState.FINAL
+    asked = [i for i, plist in enumerate(per_input) if plist]
+    handle_lists = yield [ChunkRequest(inputs[i], per_input[i], RAM, min_state=wanted) for i in asked]
+    arrays = [{} for _ in inputs]
+    for i, handles in zip(asked, handle_lists):
+        for q, h in zip(per_input[i], handles):
+            arrays[i][q] = h.array
+            ctx.note_input_state(h.state)
+    results = yield WorkerJob(solve_batch, positions, arrays)
+    for pos in positions:
+        yield from ctx.store_chunk(pos, results[pos], ChunkState.FINAL)
 
 
 def _check_f32(node, what):
@@ -325,52 +374,83 @@ def random_walker(volume_node, seeds_node, parent=None, *, beta: float = 100.0, 
         vol = _overlapping(md_in, lo, hi)
         return [vol, vol, _overlapping(parent.md, plo, phi)]
 
-    def kernel(h, input_arrays, out):
-        from . import device
+    payload_shape = md.element_type.payload_shape(md.chunk_size)
+    # whole-level solution of a coarsest-level node, computed by the first batch that needs it
+    # (the operator is a pure function of its inputs, so later batches reuse it)
+    whole, whole_lock = [], threading.Lock()
 
-        deps = dependencies(h)
-        begin, end = md.chunk_logical_region(h)
-        region = [e - b for b, e in zip(begin, end)]
-        if parent is None:
-            lo, hi = [0] * md.num_dims, list(md.size)
-            vol = _gather(md_in, dict(zip(deps[0], input_arrays[0])), lo, hi)
-            sd = _gather(seeds_node.md, dict(zip(deps[1], input_arrays[1])), lo, hi)
-            prob, _ = device.solve_level(_to_dev(vol), _to_dev(sd), tuple(md.size), None, cfg)
-            p = _from_dev(prob)
-            _write_out(out, region, p[tuple(slice(b, e) for b, e in zip(begin, end))])
-            return
-        lo, hi, _, _ = _dilated(md, h)
-        vol = _gather(md_in, dict(zip(deps[0], input_arrays[0])), lo, hi)
-        sd = _gather(seeds_node.md, dict(zip(deps[1], input_arrays[1])), lo, hi)
+    def solve_batch(positions, arrays):
+        """Probability payloads of a batch of chunks from one device solve (engine-level
+        batching): the union window of the chunks' footprints is gathered
+        and uploaded once, and every chunk is one brick of a single brick-list solve."""
+        from . import _native, device
+
+        nd = md.num_dims
+        out = {}
+        if parent is None:  # the coarsest level: one whole-level solve serves every batch
+            with whole_lock:
+                if not whole:
+                    lo, hi = [0] * nd, list(md.size)
+                    vol = _gather(md_in, arrays[0], lo, hi)
+                    sd = _gather(seeds_node.md, arrays[1], lo, hi)
+                    with _DEVICE_LOCK:
+                        prob, _ = device.solve_level(_to_dev(vol), _to_dev(sd), tuple(md.size), None, cfg)
+                        whole.append(_from_dev(prob))
+                p = whole[0]
+            for h in positions:
+                begin, end = md.chunk_logical_region(h)
+                o = np.empty(payload_shape, np.float32)
+                _write_out(o, [e - b for b, e in zip(begin, end)], p[tuple(slice(b, e) for b, e in zip(begin, end))])
+                out[h] = o
+            return out
+        boxes = [_dilated(md, h) for h in positions]
+        lo = [min(b[0][d] for b in boxes) for d in range(nd)]
+        hi = [max(b[1][d] for b in boxes) for d in range(nd)]
+        vol = _gather(md_in, arrays[0], lo, hi)
+        sd = _gather(seeds_node.md, arrays[1], lo, hi)
         plo, phi = _parent_window(lo, hi, parent.md.size)
-        par = _gather(parent.md, dict(zip(deps[2], input_arrays[2])), plo, phi)
-        torch, dev = _device()
-        from . import _native
+        par = _gather(parent.md, arrays[2], plo, phi)
+        with _DEVICE_LOCK:
+            p = _solve_window(vol, sd, par, lo, hi, plo, phi, positions)
+        for h, (_, _, begin, end) in zip(positions, boxes):
+            o = np.empty(payload_shape, np.float32)
+            _write_out(o, [e - b for b, e in zip(begin, end)],
+                       p[tuple(slice(b - a, e - a) for a, b, e in zip(lo, begin, end))])
+            out[h] = o
+        return out
 
+    def _solve_window(vol, sd, par, lo, hi, plo, phi, positions):
+        from . import _native, device
+
+        nd = md.num_dims
+        torch, dev = _device()
         win = [b - a for a, b in zip(lo, hi)]
         bound = torch.empty(win, dtype=torch.float32, device=dev)
         par_d = _to_dev(par)
         a64 = _native.int64_array
         _native.check(_native.lib().rwb_upsample_window_f32(
-            len(win), a64(parent.md.size), a64(plo), a64([b - a for a, b in zip(plo, phi)]),
+            nd, a64(parent.md.size), a64(plo), a64([b - a for a, b in zip(plo, phi)]),
             device._ptr(par_d), a64(md.size), a64(lo), a64(win), device._ptr(bound), device._stream_handle()))
-        # one brick of the window's grid is exactly this chunk: shift the grid origin
+        # the window's brick grid is the chunk grid shifted by the window origin
         brick = tuple(md.chunk_size)
-        origin = tuple((b - a) - c if b > a else 0 for a, b, c in zip(lo, begin, brick))
+        origin = tuple(-(a % c) for a, c in zip(lo, brick))
         grid = device.brick_grid(win, brick, origin)
-        coord = [1 if b > a else 0 for a, b in zip(lo, begin)]
-        index = 0
-        for c, gdim in zip(coord, grid):
-            index = index * gdim + c
-        blist = torch.tensor([index], dtype=torch.int32, device=dev)
-        prob, _ = device.solve_level(_to_dev(vol), _to_dev(sd), brick, bound, cfg, brick_list=blist,
-                                     origin=origin)
-        p = _from_dev(prob)
-        _write_out(out, region, p[tuple(slice(b - a, e - a) for a, b, e in zip(lo, begin, end))])
+        index = []
+        for h in positions:
+            i = 0
+            for hd, a, c, gdim in zip(h, lo, brick, grid):
+                i = i * gdim + (hd - a // c)
+            index.append(i)
+        blist = torch.tensor(index, dtype=torch.int32, device=dev)
+        prob, _ = device.solve_level(_to_dev(vol), _to_dev(sd), brick, bound, cfg, brick_list=blist, origin=origin)
+        return _from_dev(prob)
+
+    def task_body(ctx):
+        return _batched_body(ctx, inputs, dependencies, solve_batch)
 
     return cc.graph.OperatorNode(
         name="rwb.random_walker", params=dict(cfg.params(), hierarchical=parent is not None),
-        inputs=inputs, md=md, embedding=volume_node.embedding, dependencies=dependencies, kernel=kernel)
+        inputs=inputs, md=md, embedding=volume_node.embedding, dependencies=dependencies, task_body=task_body)
 
 
 def hierarchical_random_walker(volume_node, seeds_node, levels: int | None = None, *, beta: float = 100.0,

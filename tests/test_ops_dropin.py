@@ -154,6 +154,37 @@ def test_engine_hierarchy_equals_device_path(shape, chunk, levels):
 
 @pytestmark_cc
 @pytest.mark.gpu
+@pytest.mark.parametrize("per_task", [1, 64])
+def test_engine_batching_is_transparent(per_task):
+    """Engine-level batching: the random-walker operator solves each batch of
+    chunk requests as one brick-list solve over the batch's union window; any batch size gives
+    the bytes of the device path."""
+    import torch
+    from chunkcast.engine import Engine, EngineConfig
+    from chunkcast.store import StoreConfig
+
+    from paper_2509_26213_b200 import _native, device
+    from paper_2509_26213_b200.config import RWConfig
+
+    shape, chunk = (96, 64, 64), (32, 32, 32)
+    vol = synthetic.phantom(shape)
+    sd = synthetic.seeds(shape, "S1")
+    pyr = rwops.hierarchical_random_walker(cc.ops.source_from_array(vol, chunk), cc.ops.source_from_array(sd, chunk),
+                                           levels=2, tol=1e-7)
+    lib = _native.lib()
+    with Engine(EngineConfig(stores=StoreConfig(ram_capacity=1 << 28), worker_pool_size=2,
+                             max_requests_per_task=per_task)) as eng:
+        n0 = lib.rwb_kernel_launches()
+        p_engine = _dense(eng, pyr.node(0))
+        launches = lib.rwb_kernel_launches() - n0
+    res = device.hierarchical_random_walker(torch.from_numpy(vol).cuda(), torch.from_numpy(sd).cuda(), chunk, 2,
+                                            RWConfig(tol=1e-7))
+    np.testing.assert_array_equal(p_engine, res.prob.cpu().numpy())
+    assert launches > 0
+
+
+@pytestmark_cc
+@pytest.mark.gpu
 def test_engine_weights_match_oracle():
     from oracle import rw as orw
 
