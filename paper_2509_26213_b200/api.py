@@ -26,30 +26,35 @@ def _as_host_tensor(a, dtype):
 
 def segment(volume, seeds, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConfig(), *,
             out_prob: torch.Tensor | None = None, out_labels: torch.Tensor | None = None,
-            workspace: device.Workspace | None = None):
+            workspace: device.Workspace | None = None, pyramid_store=None, pyramid_key=None):
     """Hierarchical random-walker segmentation.
 
     volume: float32 intensities (numpy or torch, host or CUDA); seeds: uint8
     labels (0 none, 1 foreground, 2 background) of the same shape.  Returns
     (probabilities f32, labels u8) on the device the inputs came from: host
     inputs get host outputs (written into `out_prob` / `out_labels` when
-    given, e.g. pinned buffers).
+    given, e.g. pinned buffers).  `pyramid_store` (a store.DeviceStore) with `pyramid_key`
+    keeps the volume's LOD pyramid in HBM under a budget, so segmenting the same volume again
+    (new seeds or parameters) skips rebuilding it.
     """
     vol = _as_host_tensor(volume, np.float32)
     sd = _as_host_tensor(seeds, np.uint8)
     if vol.is_cuda:
-        res = device.hierarchical_random_walker(vol, sd, brick, levels, cfg, workspace=workspace)
+        res = device.hierarchical_random_walker(vol, sd, brick, levels, cfg, workspace=workspace,
+                                                pyramid_store=pyramid_store, pyramid_key=pyramid_key)
         return res.prob, res.labels
     if out_prob is None:
         out_prob = torch.empty(tuple(vol.shape), dtype=torch.float32, pin_memory=True)
     if out_labels is None:
         out_labels = torch.empty(tuple(vol.shape), dtype=torch.uint8, pin_memory=True)
     # one volume through the overlapped pipeline: level-0 slabs download while the rest solves
-    return segment_many([(vol, sd)], brick, levels, cfg, outputs=[(out_prob, out_labels)], workspace=workspace)[0]
+    return segment_many([(vol, sd)], brick, levels, cfg, outputs=[(out_prob, out_labels)], workspace=workspace,
+                        pyramid_store=pyramid_store, pyramid_keys=[pyramid_key])[0]
 
 
 def segment_many(inputs, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConfig(), *, outputs=None,
-                 workspace: device.Workspace | None = None, level0_chunks: int = 8):
+                 workspace: device.Workspace | None = None, level0_chunks: int = 8, pyramid_store=None,
+                 pyramid_keys=None):
     """Segment a sequence of host volumes with the transfers overlapped.
 
     `inputs`: list of (volume, seeds) host tensors of one shape (pinned for
@@ -113,7 +118,9 @@ def segment_many(inputs, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConf
                 labels.record_stream(down)
 
         device.hierarchical_random_walker(vol_d[i % 2], sd_d[i % 2], brick, levels, cfg, workspace=workspace,
-                                          level0_chunks=level0_chunks, on_level0_chunk=download)
+                                          level0_chunks=level0_chunks, on_level0_chunk=download,
+                                          pyramid_store=pyramid_store,
+                                          pyramid_key=pyramid_keys[i] if pyramid_keys is not None else None)
         ev = torch.cuda.Event()
         ev.record(comp)
         computed.append(ev)

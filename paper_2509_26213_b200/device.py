@@ -94,6 +94,31 @@ def lod_chain(volume: torch.Tensor, chunk, levels: int | None = None) -> list:
     return out
 
 
+def _cached_lod_chain(volume, chunk, levels, store, key):
+    """`lod_chain` with levels 1.. kept in a DeviceStore (store.py) under (key, k): segmenting the
+    same volume again (new seeds, new parameters) reuses its pyramid from HBM while the store's
+    budget lets it stay; evicted levels are recomputed and re-inserted."""
+    total = num_lod_levels(volume.shape, chunk)
+    n = total if levels is None else int(levels)
+    if not 1 <= n <= total:
+        raise ValueError(f"levels={n} outside 1..{total} for size {tuple(volume.shape)}, chunk {tuple(chunk)}")
+    vols = [volume]
+    held = []
+    for k in range(1, n):
+        shape = coarse_shape(vols[-1].shape)
+        got = store.get((key, k), torch.float32, shape)
+        if got is not None:
+            held.append(got[0])
+            vols.append(got[1])
+            continue
+        lv = lod_down(vols[-1])
+        store.put((key, k), lv)
+        vols.append(lv)
+    for e in held:  # views stay valid: the stream orders any later reuse after this solve's reads
+        store.unpin(e)
+    return vols
+
+
 def project_seeds(seeds: torch.Tensor) -> torch.Tensor:
     _check_tensor(seeds, torch.uint8, "seeds", (1, 2, 3))
     lib = _native.lib()
@@ -421,7 +446,7 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
                                cfg: RWConfig = RWConfig(), *, want_labels: bool = True,
                                workspace: Workspace | None = None, brick_lists=None,
                                exchange=None, upsample_planes=None, level0_chunks: int | None = None,
-                               on_level0_chunk=None) -> HRWResult:
+                               on_level0_chunk=None, pyramid_store=None, pyramid_key=None) -> HRWResult:
     """Coarse-to-fine random walker (oracle/rw.py: hierarchical_random_walker).
 
     The coarsest level is solved whole; each finer level is initialised and
@@ -439,7 +464,10 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
     caller can download finished rows while the rest solves.
     """
     brick = tuple(int(b) for b in brick)
-    vols = lod_chain(volume, brick, levels)
+    if pyramid_store is not None and pyramid_key is not None:
+        vols = _cached_lod_chain(volume, brick, levels, pyramid_store, pyramid_key)
+    else:
+        vols = lod_chain(volume, brick, levels)
     seed_levels = [seeds]
     for _ in range(len(vols) - 1):
         seed_levels.append(project_seeds(seed_levels[-1]))
