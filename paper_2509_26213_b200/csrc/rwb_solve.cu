@@ -1138,32 +1138,48 @@ __global__ void __launch_bounds__(NTHREADS) coop_cg_kernel(Geo g, Work w, float*
     const float beta = (it == 0) ? 0.f : (float)(rr / rr_prev);
     // pass 1: p <- r + beta p ; q = A'p ; p.q
     float acc = 0.f;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      TileCtx c = tile_ctx<kCoopTZ>(g, nullptr, 0, item);
-      if (!c.col) continue;
-      const long long lbase = (long long)c.ly * g.bx + c.lx;
-      const bool hx0 = c.lx > 0, hx1 = c.lx + 1 < g.bx, hy0 = c.ly > 0, hy1 = c.ly + 1 < g.by;
-      auto pn_at = [&](long long i) { return w.r[i] + beta * pin[i]; };
-      long long li = lbase + (long long)c.lz0 * sbz;
-      float pm = (g.is3d && c.lz0 > 0) ? pn_at(li - sbz) : 0.f;
-      float wzm = (g.is3d && c.lz0 > 0) ? __ldg(w.wz + li - sbz) : 0.f;
-      float pc = pn_at(li);
-      for (int lz = c.lz0; lz < c.lz1; ++lz, li += sbz) {
-        const bool up = g.is3d && lz + 1 < g.bz;
-        float pp = up ? pn_at(li + sbz) : 0.f;
-        float wzc = up ? __ldg(w.wz + li) : 0.f;
-        float s = wzc * pp + wzm * pm;
-        if (hx1) s += __ldg(w.wx + li) * pn_at(li + 1);
-        if (hx0) s += __ldg(w.wx + li - 1) * pn_at(li - 1);
-        if (hy1) s += __ldg(w.wy + li) * pn_at(li + g.bx);
-        if (hy0) s += __ldg(w.wy + li - g.bx) * pn_at(li - g.bx);
-        const float q = pc - s;
-        pout[li] = pc;
-        w.q[li] = q;
-        acc += pc * q;
-        pm = pc;
-        pc = pp;
-        wzm = wzc;
+    {
+      const float* __restrict__ R = w.r;
+      const float* __restrict__ PI = pin;
+      float* __restrict__ PO = pout;
+      float* __restrict__ Q = w.q;
+      const float* __restrict__ WX = w.wx;
+      const float* __restrict__ WY = w.wy;
+      const float* __restrict__ WZ = w.wz;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        TileCtx c = tile_ctx<kCoopTZ>(g, nullptr, 0, item);
+        if (!c.col) continue;
+        const long long lbase = (long long)c.ly * g.bx + c.lx;
+        const bool hx0 = c.lx > 0, hx1 = c.lx + 1 < g.bx, hy0 = c.ly > 0, hy1 = c.ly + 1 < g.by;
+        auto pn_at = [&](long long i) { return R[i] + beta * PI[i]; };
+        long long li = lbase + (long long)c.lz0 * sbz;
+        float pm = (g.is3d && c.lz0 > 0) ? pn_at(li - sbz) : 0.f;
+        float wzm = (g.is3d && c.lz0 > 0) ? __ldg(WZ + li - sbz) : 0.f;
+        float pc = pn_at(li);
+        auto plane = [&](int lz) {
+          const bool up = g.is3d && lz + 1 < g.bz;
+          float pp = up ? pn_at(li + sbz) : 0.f;
+          float wzc = up ? __ldg(WZ + li) : 0.f;
+          float s = wzc * pp + wzm * pm;
+          if (hx1) s += __ldg(WX + li) * pn_at(li + 1);
+          if (hx0) s += __ldg(WX + li - 1) * pn_at(li - 1);
+          if (hy1) s += __ldg(WY + li) * pn_at(li + g.bx);
+          if (hy0) s += __ldg(WY + li - g.bx) * pn_at(li - g.bx);
+          const float q = pc - s;
+          PO[li] = pc;
+          Q[li] = q;
+          acc += pc * q;
+          pm = pc;
+          pc = pp;
+          wzm = wzc;
+          li += sbz;
+        };
+        if (c.lz1 - c.lz0 == kCoopTZ) {  // full items: unrolled, so the loads of all planes batch up
+#pragma unroll
+          for (int k = 0; k < kCoopTZ; ++k) plane(c.lz0 + k);
+        } else {
+          for (int lz = c.lz0; lz < c.lz1; ++lz) plane(lz);
+        }
       }
     }
     {
@@ -1175,16 +1191,29 @@ __global__ void __launch_bounds__(NTHREADS) coop_cg_kernel(Geo g, Work w, float*
     const float alpha = pq != 0.0 ? (float)(rr / pq) : 0.f;
     // pass 2: y += alpha p ; r -= alpha q ; r.r
     float acc2 = 0.f;
-    for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-      TileCtx c = tile_ctx<kCoopTZ>(g, nullptr, 0, item);
-      if (!c.col) continue;
-      long long li = (long long)c.ly * g.bx + c.lx + (long long)c.lz0 * sbz;
-      for (int lz = c.lz0; lz < c.lz1; ++lz, li += sbz) {
-        const float y = w.y[li] + alpha * pout[li];
-        const float r = w.r[li] - alpha * w.q[li];
-        w.y[li] = y;
-        w.r[li] = r;
-        acc2 += r * r;
+    {
+      float* __restrict__ Y = w.y;
+      float* __restrict__ R = w.r;
+      const float* __restrict__ PO = pout;
+      const float* __restrict__ Q = w.q;
+      for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+        TileCtx c = tile_ctx<kCoopTZ>(g, nullptr, 0, item);
+        if (!c.col) continue;
+        long long li = (long long)c.ly * g.bx + c.lx + (long long)c.lz0 * sbz;
+        auto plane = [&]() {
+          const float y = Y[li] + alpha * PO[li];
+          const float r = R[li] - alpha * Q[li];
+          Y[li] = y;
+          R[li] = r;
+          acc2 += r * r;
+          li += sbz;
+        };
+        if (c.lz1 - c.lz0 == kCoopTZ) {
+#pragma unroll
+          for (int k = 0; k < kCoopTZ; ++k) plane();
+        } else {
+          for (int lz = c.lz0; lz < c.lz1; ++lz) plane();
+        }
       }
     }
     {
