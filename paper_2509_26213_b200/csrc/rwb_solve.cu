@@ -773,7 +773,7 @@ __global__ void __launch_bounds__(STH, 2) setup_brick_kernel(const __grid_consta
 constexpr int ST2 = 64, SH2 = ST2 + 2;  // tile edge, with halo
 constexpr int SQ2 = 4, SQN2 = ST2 / SQ2, STH2 = SQN2 * SQN2;
 
-__global__ void __launch_bounds__(STH2) setup_tile2d_kernel(Geo g, Work w, const int* __restrict__ list,
+__global__ void __launch_bounds__(STH2, 2) setup_tile2d_kernel(Geo g, Work w, const int* __restrict__ list,
                                                             const float* __restrict__ I,
                                                             const uint8_t* __restrict__ S,
                                                             const float* __restrict__ B, float beta, float wmin,
@@ -792,8 +792,7 @@ __global__ void __launch_bounds__(STH2) setup_tile2d_kernel(Geo g, Work w, const
   const int xq = tid % SQN2, yq = tid / SQN2;
   auto wgt = [&](float a, float b) { return edge_weight(a, b, beta, wmin); };
   // ---- tile + halo into shared memory ----
-  for (int e = tid; e < SH2 * SH2; e += STH2) {
-    const int ty = e / SH2, tx = e % SH2;
+  auto load_px = [&](int ty, int tx) {
     const int gy = gy0 - 1 + ty, gx = gx0 - 1 + tx;
     float iv = 0.f, dv = 0.f;
     unsigned char sv = 0;
@@ -806,6 +805,34 @@ __global__ void __launch_bounds__(STH2) setup_tile2d_kernel(Geo g, Work w, const
     sI[ty][tx] = iv;
     sS[ty][tx] = sv;
     sDv[ty][tx] = dv;
+  };
+  if ((g.nx & 3) == 0 && (gx0 & 3) == 0 && gx0 >= 0 && gx0 + ST2 <= g.nx) {
+    // interior columns as 16 B loads (4 pixels of I and B, 4 seeds per 32-bit word), halo
+    // columns and out-of-level rows element-wise
+    for (int e = tid; e < SH2 * (ST2 / 4); e += STH2) {
+      const int ty = e / (ST2 / 4), q = e % (ST2 / 4);
+      const int gy = gy0 - 1 + ty;
+      float4 iv = make_float4(0.f, 0.f, 0.f, 0.f), bv = iv;
+      uchar4 sv = make_uchar4(0, 0, 0, 0);
+      if (gy >= 0 && gy < g.ny) {
+        const long long gi = (long long)gy * g.nx + gx0 + 4 * q;
+        iv = __ldg(reinterpret_cast<const float4*>(I + gi));
+        sv = __ldg(reinterpret_cast<const uchar4*>(S + gi));
+        if (B) bv = __ldg(reinterpret_cast<const float4*>(B + gi));
+      }
+      const float ivs[4] = {iv.x, iv.y, iv.z, iv.w}, bvs[4] = {bv.x, bv.y, bv.z, bv.w};
+      const unsigned char svs[4] = {sv.x, sv.y, sv.z, sv.w};
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int tx = 1 + 4 * q + k;
+        sI[ty][tx] = ivs[k];
+        sS[ty][tx] = svs[k];
+        sDv[ty][tx] = svs[k] ? seed_value(svs[k]) : bvs[k];
+      }
+    }
+    for (int e = tid; e < 2 * SH2; e += STH2) load_px(e >> 1, (e & 1) ? SH2 - 1 : 0);
+  } else {
+    for (int e = tid; e < SH2 * SH2; e += STH2) load_px(e / SH2, e % SH2);
   }
   __syncthreads();
   // ---- weights and scales of the thread's 4 x 4 pixels ----
