@@ -191,6 +191,16 @@ int rwb_chunks_gather(int32_t ndim, const int64_t* size, const int64_t* chunk, i
 int rwb_const_chunk_table(int32_t ndim, const int64_t* size, const int64_t* chunk, int32_t scalar_code,
                           const void* src, void* table, void* stream);
 
+/* Nearest-neighbour pan/zoom view (the reference's viewer: _resample_nn / slice_view /
+ * image_view, render.py:640-741): frame pixel (p0, p1) of the (frame_size[0], frame_size[1])
+ * frame samples source element floor((p + 0.5) * scale + offset) per axis (float64 math), 0
+ * outside the source.  The source is a 2-D image (src_ndim 2, slice_dim < 0) or the slice
+ * slice_index along slice_dim of a 3-D level (the remaining axes in order, slice_node
+ * semantics).  Elements are opaque elem_bytes-byte items (scalar width x lanes). */
+int rwb_resample_nn(int32_t src_ndim, const int64_t* src_size, int32_t slice_dim, int64_t slice_index,
+                    int32_t elem_bytes, const void* src, const int64_t* frame_size, const double* scale,
+                    const double* offset, void* frame, void* stream);
+
 /* Bytes of solver workspace for n_bricks bricks of `geom` (n_bricks < 0: all)
  * with the given RWB_SOLVE_* flags (the brick-resident path needs almost none). */
 size_t rwb_solve_workspace_bytes(const rwb_geometry_t* geom, int64_t n_bricks, int32_t flags);

@@ -51,6 +51,9 @@ SIGNATURES = {
                                      c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "rwb_const_chunk_table": (c_int32, [c_int32, ctypes.POINTER(c_int64), ctypes.POINTER(c_int64), c_int32, c_void_p,
                                         c_void_p, c_void_p]),
+    "rwb_resample_nn": (c_int32, [c_int32, ctypes.POINTER(c_int64), c_int32, c_int64, c_int32, c_void_p,
+                                  ctypes.POINTER(c_int64), ctypes.POINTER(ctypes.c_double),
+                                  ctypes.POINTER(ctypes.c_double), c_void_p, c_void_p]),
     "rwb_chunks_gather": (c_int32, [c_int32, ctypes.POINTER(c_int64), ctypes.POINTER(c_int64), c_int32, c_void_p,
                                     c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "rwb_solve_workspace_bytes": (c_size_t, [c_void_p, c_int64, c_int32]),

@@ -256,3 +256,61 @@ extern "C" int rwb_const_chunk_table(int32_t ndim, const int64_t* size, const in
   rwb::count_launches(1);
   return RWB_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Nearest-neighbour pan/zoom resampling of a 2-D image or an axis-aligned slice of a 3-D level
+// (the reference's viewer path: _resample_nn, slice_view, image_view, render.py:640-741).  Frame
+// pixel (p0, p1) samples source element floor((p + 0.5) * scale + offset) per axis, computed in
+// float64 like the reference (numpy float64 arange), background 0 outside the source.
+namespace rwb {
+namespace {
+
+__global__ void __launch_bounds__(256) resample_nn_kernel(const unsigned char* __restrict__ src, long long st0,
+                                                          long long st1, long long base, long long n0, long long n1,
+                                                          int eb, unsigned char* __restrict__ frame, long long f0,
+                                                          long long f1, double s0, double s1, double o0, double o1) {
+  const long long n = f0 * f1;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    const long long p0 = e / f1, p1 = e % f1;
+    const long long a0 = (long long)floor(__dadd_rn(__dmul_rn(__dadd_rn((double)p0, 0.5), s0), o0));
+    const long long a1 = (long long)floor(__dadd_rn(__dmul_rn(__dadd_rn((double)p1, 0.5), s1), o1));
+    unsigned char* out = frame + e * eb;
+    if (a0 >= 0 && a0 < n0 && a1 >= 0 && a1 < n1)
+      move_elem(out, src + (base + a0 * st0 + a1 * st1) * eb, eb);
+    else
+      zero_elem(out, eb);
+  }
+}
+
+}  // namespace
+}  // namespace rwb
+
+extern "C" int rwb_resample_nn(int32_t src_ndim, const int64_t* src_size, int32_t slice_dim, int64_t slice_index,
+                               int32_t elem_bytes, const void* src, const int64_t* frame_size, const double* scale,
+                               const double* offset, void* frame, void* stream) {
+  if (!src_size || !frame_size || !scale || !offset || !src || !frame)
+    return rwb::fail(RWB_ERR_INVALID, "resample_nn: null pointer");
+  if (elem_bytes < 1 || elem_bytes > 64) return rwb::fail(RWB_ERR_INVALID, "resample_nn: elem_bytes must be 1..64");
+  long long n0, n1, st0, st1, base = 0;
+  if (src_ndim == 2 && slice_dim < 0) {
+    n0 = src_size[0], n1 = src_size[1], st0 = n1, st1 = 1;
+  } else if (src_ndim == 3 && slice_dim >= 0 && slice_dim < 3) {
+    const long long s[3] = {src_size[0], src_size[1], src_size[2]};
+    const long long stride[3] = {s[1] * s[2], s[2], 1};
+    if (slice_index < 0 || slice_index >= s[slice_dim]) return rwb::fail(RWB_ERR_INVALID, "resample_nn: slice index");
+    base = slice_index * stride[slice_dim];
+    const int d0 = slice_dim == 0 ? 1 : 0, d1 = slice_dim == 2 ? 1 : 2;  // the remaining axes, in order
+    n0 = s[d0], n1 = s[d1], st0 = stride[d0], st1 = stride[d1];
+  } else {
+    return rwb::fail(RWB_ERR_INVALID, "resample_nn: a 2-D image (slice_dim < 0) or a 3-D slice");
+  }
+  const long long f0 = frame_size[0], f1 = frame_size[1];
+  if (f0 < 1 || f1 < 1 || n0 < 1 || n1 < 1) return rwb::fail(RWB_ERR_INVALID, "resample_nn: sizes must be positive");
+  const long long blocks = (f0 * f1 + 255) / 256;
+  rwb::resample_nn_kernel<<<(unsigned)(blocks < 8192 ? blocks : 8192), 256, 0, (cudaStream_t)stream>>>(
+      (const unsigned char*)src, st0, st1, base, n0, n1, elem_bytes, (unsigned char*)frame, f0, f1, scale[0],
+      scale[1], offset[0], offset[1]);
+  RWB_LAUNCH_CHECK("resample_nn_kernel");
+  rwb::count_launches(1);
+  return RWB_OK;
+}
