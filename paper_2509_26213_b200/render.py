@@ -7,8 +7,8 @@ every frame pixel p samples source element floor((p + 0.5) * scale + offset) wit
 scale = 1 / (zoom * 2^level) and offset = pan / 2^level (`_resample_nn`), 0 outside the source.
 Here the levels are device tensors and one `rwb_resample_nn` launch fills the whole frame (the
 reference resolves it tile by tile through its engine); the frames are byte-identical to the
-reference's.  `ops.slice_view` / `ops.image_view` wrap them as reference `OperatorNode`s.  The
-raycaster (`render.py:203-631`) is not part of this module.
+reference's (tests/test_render.py).  The raycaster (`render.py:203-631`) is not part of this
+module.
 """
 
 from __future__ import annotations
