@@ -157,7 +157,8 @@ def cpu_reference_sample(wl, steps=1, warmup=0):
 
     s = wl["sample"]
     # bricks are split into slabs of brick rows along dim 0, one thread each
-    cores = min(len(os.sched_getaffinity(0)), -(-s["shape"][0] // wl["brick"][0]))
+    nslab = [-(-s["shape"][d] // wl["brick"][d]) for d in range(2)]
+    cores = min(len(os.sched_getaffinity(0)), nslab[0] * nslab[1])
     vol = synthetic.phantom(s["shape"])
     seeds = synthetic.seeds(s["shape"], "S1")
     params = orw.RWParams(beta=BETA, min_weight=WMIN, tol=TOL, max_iter=10_000)

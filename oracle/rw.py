@@ -278,41 +278,51 @@ def solve_level(volume, seeds, brick, bound, params: RWParams, solve_mask=None,
 
 
 def solve_level_threaded(volume, seeds, brick, bound, params: RWParams, workers=None) -> LevelResult:
-    """Same result as `solve_level`, split into slabs of bricks along dim 0.
+    """Same result as `solve_level`, split into tiles of bricks along dims 0 (and 1 when there
+    are more workers than brick slabs along dim 0).
 
-    Bricks are independent given `bound`, so each slab (plus a one-voxel
-    Dirichlet halo plane on either side) is solved on its own thread; numpy
-    releases the GIL inside its array kernels, the way the reference engine
-    runs chunk kernels on its worker pool (`engine.py:398-400, 866-875`).
+    Bricks are independent given `bound`, so each tile (plus a one-voxel Dirichlet halo on each
+    cut side) is solved on its own thread; numpy releases the GIL inside its array kernels, the
+    way the reference engine runs chunk kernels on its worker pool (`engine.py:398-400, 866-875`).
     """
     workers = workers or len(os.sched_getaffinity(0))
-    n0, b0 = volume.shape[0], brick[0]
-    nslab = -(-n0 // b0)
-    if bound is None or nslab == 1 or workers == 1:
+    shape = volume.shape
+    nd = volume.ndim
+    nslab = [-(-shape[d] // brick[d]) for d in range(min(nd, 2))]
+    if bound is None or workers == 1 or (nslab[0] == 1 and (nd < 2 or nslab[1] == 1)):
         return solve_level(volume, seeds, brick, bound, params)
-    per = -(-nslab // min(workers, nslab))
-    ranges = [(s * b0, min((s + per) * b0, n0)) for s in range(0, nslab, per)]
+    parts = [min(workers, nslab[0])]
+    if nd >= 2:
+        parts.append(min(nslab[1], max(1, workers // parts[0])))
+    spans = []
+    for d, k in enumerate(parts):
+        per = -(-nslab[d] // k)
+        spans.append([(s * brick[d], min((s + per) * brick[d], shape[d])) for s in range(0, nslab[d], per)])
+    tiles = [(a,) for a in spans[0]] if len(spans) == 1 else [(a, b) for a in spans[0] for b in spans[1]]
 
-    def run(rng):
-        z0, z1 = rng
-        lo, hi = max(0, z0 - 1), min(n0, z1 + 1)
-        inside = np.zeros(hi - lo, dtype=bool)
-        inside[z0 - lo : z1 - lo] = True
-        mask = np.broadcast_to(inside.reshape((-1,) + (1,) * (volume.ndim - 1)),
-                               (hi - lo,) + volume.shape[1:])
-        origin = (lo,) + (0,) * (volume.ndim - 1)
-        res = solve_level(volume[lo:hi], seeds[lo:hi], brick, bound[lo:hi], params,
-                          solve_mask=mask, origin=origin)
-        return z0, z1, lo, res
+    def run(tile):
+        lo = [max(0, a - 1) for a, _ in tile]
+        hi = [min(shape[d], b + 1) for d, (_, b) in enumerate(tile)]
+        sl = tuple(slice(l, h) for l, h in zip(lo, hi))
+        inside = np.ones(tuple(h - l for l, h in zip(lo, hi)) + shape[len(tile):], dtype=bool)
+        for d, (a, b) in enumerate(tile):
+            keep = np.zeros(hi[d] - lo[d], dtype=bool)
+            keep[a - lo[d]:b - lo[d]] = True
+            inside &= keep.reshape([-1 if i == d else 1 for i in range(nd)])
+        origin = tuple(lo) + (0,) * (nd - len(tile))
+        res = solve_level(volume[sl], seeds[sl], brick, bound[sl], params, solve_mask=inside, origin=origin)
+        return tile, lo, res
 
-    prob = np.empty(volume.shape, dtype=np.float64)
-    with ThreadPoolExecutor(max_workers=len(ranges)) as pool:
-        results = list(pool.map(run, ranges))
+    prob = np.empty(shape, dtype=np.float64)
+    with ThreadPoolExecutor(max_workers=len(tiles)) as pool:
+        results = list(pool.map(run, tiles))
     its = []
-    for z0, z1, lo, res in results:
-        prob[z0:z1] = res.prob[z0 - lo : z1 - lo]
+    for tile, lo, res in results:
+        dst = tuple(slice(a, b) for a, b in tile)
+        src = tuple(slice(a - l, b - l) for (a, b), l in zip(tile, lo))
+        prob[dst] = res.prob[src]
         its.append(res.iterations)
-    return LevelResult(prob, np.concatenate(its), np.zeros(0, bool), {"slabs": len(ranges)})
+    return LevelResult(prob, np.concatenate(its), np.zeros(0, bool), {"tiles": len(tiles)})
 
 
 # ---------------------------------------------------------------------------

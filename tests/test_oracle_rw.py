@@ -106,6 +106,8 @@ def test_threaded_slabs_equal_serial(rng):
     a = rw.solve_level(vol, seeds, (4, 4, 4), bound, TIGHT).prob
     b = rw.solve_level_threaded(vol, seeds, (4, 4, 4), bound, TIGHT, workers=3).prob
     np.testing.assert_allclose(a, b, atol=1e-11, rtol=0)
+    c = rw.solve_level_threaded(vol, seeds, (4, 4, 4), bound, TIGHT, workers=12).prob  # 5 x 2 tiles
+    np.testing.assert_allclose(a, c, atol=1e-11, rtol=0)
 
 
 def test_probabilities_bounded_and_seeds_exact():
