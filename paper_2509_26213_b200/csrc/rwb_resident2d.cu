@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(TH2, 1) resident2d_kernel(ResidentArgs a) {
     publish();
     __syncthreads();
 
-    float gamma = 0.f, alpha = 0.f, rgamma = 0.f, ralpha = 0.f;
+    float alpha = 0.f, rgamma = 0.f, ralpha = 0.f;  // 1/gamma, 1/alpha one iteration ahead
     int state = ST_ACTIVE, it = 0;
     for (int pass = 0;; ++pass) {
       // ---- w = A'r, partial dots ----
@@ -161,7 +161,6 @@ __global__ void __launch_bounds__(TH2, 1) resident2d_kernel(ResidentArgs a) {
         const float den = delta - beta * (g_new * ralpha);
         alpha = den != 0.f ? g_new * rcp_ftz2(den) : 0.f;
       }
-      gamma = g_new;
       rgamma = rcp_ftz2(g_new);
       ralpha = rcp_ftz2(alpha);
       // ---- update: p = r + beta p, s = w + beta s, y += alpha p, r -= alpha s ----
@@ -176,7 +175,6 @@ __global__ void __launch_bounds__(TH2, 1) resident2d_kernel(ResidentArgs a) {
       publish();  // the barrier above proved every reader of the previous r has finished
       __syncthreads();
     }
-    (void)gamma;
     // ---- epilogue: probabilities and labels straight into the level ----
     {
       const int brick = a.list ? a.list[slot] : slot;

@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
         st_async_f32(mapa_u32(smem_u32(&sm.jn[parJ]), c), __int_as_float(jd), mapa_u32(smem_u32(&sm.barJ[parJ]), c));
     }
 
-    float gamma = 0.f, alpha = 0.f, rgamma = 0.f, ralpha = 0.f;
+    float alpha = 0.f, rgamma = 0.f, ralpha = 0.f;  // 1/gamma, 1/alpha one iteration ahead
     int state = ST_ACTIVE, it = 0;
     float4 rf_dn = f4(0, 0, 0, 0), rf_up = f4(0, 0, 0, 0);
     float4 sf_dn = f4(0, 0, 0, 0), sf_up = f4(0, 0, 0, 0);
@@ -372,7 +372,6 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
         const float den = delta - beta * (g_new * ralpha);
         alpha = den != 0.f ? g_new * rcp_ftz(den) : 0.f;
       }
-      gamma = g_new;
       rgamma = rcp_ftz(g_new);
       ralpha = rcp_ftz(alpha);
       Q4TRACE(4);
@@ -405,7 +404,6 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
       ++trace_it;
 #endif
     }
-    (void)gamma;
     // epilogue: probabilities and labels straight into the level
     {
       const long long sbase = (long long)slot * (RB * RB * RB) + (long long)rank * SLAB;
