@@ -1142,6 +1142,22 @@ __device__ __forceinline__ double coop_total(const float* part, int n, double* s
   return t;
 }
 
+#ifdef RWB_TRACE
+__device__ long long g_coop_trace[2][64][8];  // [block 0 / last block][iteration][phase] clock64
+extern "C" int rwb_coop_trace_dump(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_coop_trace, sizeof(g_coop_trace));
+}
+#define CTRACE(k)                                                                                       \
+  do {                                                                                                  \
+    if (threadIdx.x == 0 && threadIdx.y == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && it < 64) \
+      g_coop_trace[blockIdx.x == 0 ? 0 : 1][it][k] = clock64();                                        \
+  } while (0)
+#else
+#define CTRACE(k) \
+  do {            \
+  } while (0)
+#endif
+
 __global__ void __launch_bounds__(NTHREADS) coop_cg_kernel(Geo g, Work w, float* part_pq, float* part_rr, int n_items,
                                                            float tol2, int max_iter) {
   cg::grid_group grid = cg::this_grid();
@@ -1159,6 +1175,7 @@ __global__ void __launch_bounds__(NTHREADS) coop_cg_kernel(Geo g, Work w, float*
   int it = 0;
   double rr_prev = 0.0;
   while (state == ST_ACTIVE) {
+    CTRACE(0);
     const int par = it & 1;
     const float* pin = par ? w.p1 : w.p0;
     float* pout = par ? w.p0 : w.p1;
@@ -1213,8 +1230,11 @@ __global__ void __launch_bounds__(NTHREADS) coop_cg_kernel(Geo g, Work w, float*
       const float2 sblk = block_sum2(acc, 0.f);
       if (threadIdx.x == 0 && threadIdx.y == 0) part_pq[blockIdx.x] = sblk.x;
     }
+    CTRACE(1);
     grid.sync();
+    CTRACE(2);
     const double pq = coop_total(part_pq, gridDim.x, sh);
+    CTRACE(3);
     const float alpha = pq != 0.0 ? (float)(rr / pq) : 0.f;
     // pass 2: y += alpha p ; r -= alpha q ; r.r
     float acc2 = 0.f;
@@ -1247,8 +1267,11 @@ __global__ void __launch_bounds__(NTHREADS) coop_cg_kernel(Geo g, Work w, float*
       const float2 sblk = block_sum2(acc2, 0.f);
       if (threadIdx.x == 0 && threadIdx.y == 0) part_rr[blockIdx.x] = sblk.x;
     }
+    CTRACE(4);
     grid.sync();
+    CTRACE(5);
     const double rr_new = coop_total(part_rr, gridDim.x, sh);
+    CTRACE(6);
     ++it;
     if (rr_new <= (double)tol2 * bb)
       state = ST_CONVERGED;
