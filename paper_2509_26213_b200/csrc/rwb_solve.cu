@@ -1124,9 +1124,6 @@ __global__ void __launch_bounds__(NTHREADS) cg_pass2_kernel(Geo g, Work w, int n
 #ifndef RWB_COOP_TZ
 #define RWB_COOP_TZ 4
 #endif
-#ifndef RWB_COOP_MINB
-#define RWB_COOP_MINB 1
-#endif
 constexpr int kCoopTZ = RWB_COOP_TZ;  // z planes per work item of the cooperative sweeps
 constexpr int kCoopMaxBlocks = 4096;  // partial slots of the cooperative whole-level solve
 
@@ -1161,7 +1158,7 @@ extern "C" int rwb_coop_trace_dump(long long* out) {
   } while (0)
 #endif
 
-__global__ void __launch_bounds__(NTHREADS, RWB_COOP_MINB) coop_cg_kernel(Geo g, Work w, float* part_pq, float* part_rr, int n_items,
+__global__ void __launch_bounds__(NTHREADS) coop_cg_kernel(Geo g, Work w, float* part_pq, float* part_rr, int n_items,
                                                            float tol2, int max_iter) {
   cg::grid_group grid = cg::this_grid();
   __shared__ double sh[NTHREADS / 32];
