@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -490,7 +491,12 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
         win = upsample_planes[k] if upsample_planes is not None else None
         if k == 0 and level0_chunks is None:
             level0_chunks = 8 if math.prod(brick_grid(vols[0].shape, brick)) >= 4096 else 1
-        slabbed = k == 0 and level0_chunks > 1 and win is None and brick_lists is None
+        # finer levels with many bricks are solved in slabs too (slab c+1's system is built while
+        # slab c solves); only level 0 reports its slabs to on_level0_chunk
+        nchunks = level0_chunks if k == 0 else (2 if math.prod(brick_grid(vols[k].shape, brick)) >= 4096 else 1)
+        if os.environ.get("RWB_UPPER_CHUNKS") and k > 0:  # diagnostics
+            nchunks = int(os.environ["RWB_UPPER_CHUNKS"])
+        slabbed = nchunks > 1 and win is None and brick_lists is None and _resident_geometry(vols[k].shape, brick)
         if slabbed:
             x = None  # upsampled slab by slab inside the chunked solve
         elif win is None:
@@ -505,7 +511,7 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
         # other bricks already write their results
         if slabbed:
             probs[k], stats[k] = _solve_level_chunked(vols[k], seed_levels[k], brick, probs[k + 1], cfg, lab_k,
-                                                      workspace, level0_chunks, on_level0_chunk)
+                                                      workspace, nchunks, on_level0_chunk if k == 0 else None)
         else:
             probs[k], stats[k] = solve_level(vols[k], seed_levels[k], brick, x, cfg, brick_list=bl,
                                              labels_out=lab_k, workspace=workspace, stats_on_device=True)
