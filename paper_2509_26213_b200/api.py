@@ -53,7 +53,7 @@ def segment(volume, seeds, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWCo
 
 
 def segment_many(inputs, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConfig(), *, outputs=None,
-                 workspace: device.Workspace | None = None, level0_chunks: int = 8, pyramid_store=None,
+                 workspace: device.Workspace | None = None, level0_chunks: int | None = None, pyramid_store=None,
                  pyramid_keys=None):
     """Segment a sequence of host volumes with the transfers overlapped.
 

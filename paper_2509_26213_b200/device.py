@@ -489,8 +489,9 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
         if exchange is not None:
             exchange(k + 1, probs[k + 1])
         win = upsample_planes[k] if upsample_planes is not None else None
-        if k == 0 and level0_chunks is None:
-            level0_chunks = 8 if math.prod(brick_grid(vols[0].shape, brick)) >= 4096 else 1
+        if k == 0 and level0_chunks is None:  # measured: 8 slabs at 32768 bricks, 2 at 4096
+            nb0 = math.prod(brick_grid(vols[0].shape, brick))
+            level0_chunks = 8 if nb0 >= 16384 else (2 if nb0 >= 4096 else 1)
         # finer levels with many bricks are solved in slabs too (slab c+1's system is built while
         # slab c solves); only level 0 reports its slabs to on_level0_chunk
         nchunks = level0_chunks if k == 0 else (2 if math.prod(brick_grid(vols[k].shape, brick)) >= 4096 else 1)
