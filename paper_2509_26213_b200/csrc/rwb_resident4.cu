@@ -258,6 +258,12 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
       const int par = gk & 1;
       const uint32_t ph = (gk >> 1) & 1;
       if (tid == 0) mbar_expect_tx(&sm.barR[par], tx_faces + 2 * NPART * 4);
+      // the previous iteration's y += alpha p, deferred off the update -> publish -> barrier
+      // chain: nothing reads y until the epilogue, so it fills the SpMV's load latencies
+      if (pass > 0) {
+#pragma unroll
+        for (int v = 0; v < RV; v += 2) fma2(y[v], y[v + 1], alpha, alpha, p[v], p[v + 1], y[v], y[v + 1]);
+      }
       // w = A'r with the weights from shared memory
       float gp[2] = {0.f, 0.f}, dp[2] = {0.f, 0.f};
       float4 wzl4;  // w'z of the plane below the slab
@@ -379,7 +385,6 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
       for (int v = 0; v < RV; v += 2) {
         fma2(p[v], p[v + 1], beta, beta, p[v], p[v + 1], r[v], r[v + 1]);
         fma2(sv[v], sv[v + 1], beta, beta, sv[v], sv[v + 1], w[v], w[v + 1]);
-        fma2(y[v], y[v + 1], alpha, alpha, p[v], p[v + 1], y[v], y[v + 1]);
         fma2(r[v], r[v + 1], -alpha, -alpha, sv[v], sv[v + 1], r[v], r[v + 1]);
       }
       ++it;
