@@ -9,15 +9,21 @@
 // and 4-CTA clusters also place better (33 clusters = 132 SMs, against 15 x 8
 // = 120 SMs for 8-CTA clusters).  The register file cannot hold 8192 voxels'
 // vectors AND weights, so the split is:
-//   registers:     y, r, p, s, w of the thread's 4(x) x 8(z) voxels (160 floats)
-//   shared memory: the scaled weights w'x, w'y, w'z of the slab (+ the w'z plane
-//                  below it), read by the SpMV every iteration, and the r planes
-//                  (y neighbours), as in the 8-CTA engine.
+//   registers:      y, r, p, s, w of the thread's 4(x) x 8(z) voxels (160 floats)
+//   tensor memory:  the scaled weights (per plane w'y, w'y of the row below, w'z,
+//                   w'x; plus the left w'x per plane and the w'z plane below),
+//                   written once per brick with tcgen05.st and read every
+//                   iteration with tcgen05.ld — each thread owns one TMEM lane
+//                   (32x32b shape), ~900 B/cycle/SM of read bandwidth against
+//                   128 B/cycle for shared memory, which bound the SpMV when the
+//                   weights lived there (3770 -> 2800 cycles per iteration)
+//   shared memory:  the staged slab of the next brick (bulk copies) and the r
+//                   planes (y neighbours), as in the 8-CTA engine.
 // The iteration, exchange protocol, reduction order and scalar recurrences are
-// those of the 8-CTA engine (see there), with 4 partials per reduction.  Each
-// CTA keeps ONE staging buffer (the weights are live for the whole brick): the
-// next brick's slab is prefetched into L2 (cp.async.bulk.prefetch) when a brick
-// starts and bulk-copied into shared memory when it ends.
+// those of the 8-CTA engine (see there), with 4 partials per reduction; y += alpha p
+// is deferred into the next iteration's SpMV.  Bricks are handed out dynamically
+// (global counter drawn one brick ahead); the staging buffer is refilled with the
+// next brick's slab as soon as the current one is in registers and TMEM.
 #include <cooperative_groups.h>
 #include <cstdlib>
 #include <cuda_runtime.h>
