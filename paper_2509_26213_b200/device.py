@@ -15,7 +15,6 @@ from __future__ import annotations
 
 import ctypes
 import math
-import os
 from dataclasses import dataclass, field
 
 import torch
@@ -495,8 +494,6 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
         # finer levels with many bricks are solved in slabs too (slab c+1's system is built while
         # slab c solves); only level 0 reports its slabs to on_level0_chunk
         nchunks = level0_chunks if k == 0 else (2 if math.prod(brick_grid(vols[k].shape, brick)) >= 4096 else 1)
-        if os.environ.get("RWB_UPPER_CHUNKS") and k > 0:  # diagnostics
-            nchunks = int(os.environ["RWB_UPPER_CHUNKS"])
         slabbed = nchunks > 1 and win is None and brick_lists is None and _resident_geometry(vols[k].shape, brick)
         if slabbed:
             x = None  # upsampled slab by slab inside the chunked solve
