@@ -30,6 +30,7 @@ import json
 import math
 import os
 import struct
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
@@ -145,6 +146,42 @@ def read_header(path) -> Header:
     return h
 
 
+# file I/O of a run is split over a few threads (os.preadv / os.pwrite release the GIL): one
+# thread copying out of the page cache tops out near 6 GB/s, far below PCIe
+_IO_THREADS = max(1, min(8, len(os.sched_getaffinity(0))))
+_io_pool = None
+
+
+def _pool():
+    global _io_pool
+    if _io_pool is None:
+        _io_pool = ThreadPoolExecutor(_IO_THREADS, thread_name_prefix="plct-io")
+    return _io_pool
+
+
+def _parallel_io(fn, fd, view: np.ndarray, offset: int, what: str) -> None:
+    """Read (`os.preadv`) or write (`os.pwrite`) `view` at file `offset` in parallel parts."""
+    n = view.nbytes
+    parts = max(1, min(_IO_THREADS, n >> 22))  # >= 4 MiB per part
+    step = -(-n // parts)
+
+    def one(k):
+        a, b = k * step, min(n, (k + 1) * step)
+        mv = memoryview(view)[a:b]
+        done = 0
+        while done < b - a:
+            got = fn(fd, mv[done:], offset + a + done)
+            if got <= 0:
+                raise PlctError(f"short {what} at byte {offset + a + done}")
+            done += got
+
+    list(_pool().map(one, range(parts)))
+
+
+def _preadv1(fd, mv, off):
+    return os.preadv(fd, [mv], off)
+
+
 class _Staging:
     """Two pinned host buffers and two device buffers of `nbytes` for double-buffered transfers."""
 
@@ -212,9 +249,7 @@ def load(path, device_=None, *, staging_bytes: int = 64 << 20) -> tuple:
             stg.wait(b)
             nbytes = len(run) * P
             view = stg.host[b].numpy()[:nbytes]
-            got = os.preadv(fd, [memoryview(view)], int(h.offsets[run[0]]))
-            if got != nbytes:
-                raise PlctError(f"{path}: short read at chunk {run[0]}")
+            _parallel_io(_preadv1, fd, view, int(h.offsets[run[0]]), f"read of {path}")
             with torch.cuda.stream(side):
                 stg.dev[b][:nbytes].copy_(stg.host[b][:nbytes], non_blocking=True)
                 ids, first = _ids_arg(run, dev, keep)
@@ -268,9 +303,15 @@ def save(tensor: torch.Tensor, path, chunk, spacing=None, *, lanes: int = 1,
     comp = torch.cuda.current_stream(dev)
     side = torch.cuda.Stream(dev)
     side.wait_stream(comp)  # the tensor is complete before the gathers
-    pending = None  # (buffer, nbytes) copied to the host, not yet written
-    with open(path, "wb") as f:
-        f.write(_pack_header(size, chunk, code, lanes, spacing, offsets))
+    pending = None  # (buffer, nbytes, file offset) copied to the host, not yet written
+    fd = os.open(path, os.O_WRONLY | os.O_CREAT | os.O_TRUNC, 0o644)
+    try:
+        try:  # the file's blocks up front: the parallel writes then only fill pages
+            os.posix_fallocate(fd, 0, hb + n * P)
+        except OSError:
+            pass
+        head = _pack_header(size, chunk, code, lanes, spacing, offsets)
+        _parallel_io(os.pwrite, fd, np.frombuffer(head, dtype=np.uint8), 0, f"write of {path}")
         for i, first in enumerate(range(0, n, per)):
             b = i & 1
             cnt = min(per, n - first)
@@ -283,14 +324,16 @@ def save(tensor: torch.Tensor, path, chunk, spacing=None, *, lanes: int = 1,
                 ev.record(side)
                 stg.done[b] = ev
             if pending is not None:
-                pb, pn = pending
+                pb, pn, po = pending
                 stg.wait(pb)
-                f.write(memoryview(stg.host[pb].numpy()[:pn]))
-            pending = (b, cnt * P)
+                _parallel_io(os.pwrite, fd, stg.host[pb].numpy()[:pn], po, f"write of {path}")
+            pending = (b, cnt * P, hb + first * P)
         if pending is not None:
-            pb, pn = pending
+            pb, pn, po = pending
             stg.wait(pb)
-            f.write(memoryview(stg.host[pb].numpy()[:pn]))
+            _parallel_io(os.pwrite, fd, stg.host[pb].numpy()[:pn], po, f"write of {path}")
+    finally:
+        os.close(fd)
     t.record_stream(side)
     return read_header(path)
 
