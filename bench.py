@@ -245,8 +245,9 @@ def run_series(args, wl, rank, world):
     alg_b = ALG_BYTES_PER_UNKNOWN_ITER[3]
     lv = max((s for s in res.stats if s), key=lambda s: s["cg_ms"])
     gbs = alg_b * lv["unknown_iterations"] / (lv["cg_ms"] / 1e3) / 1e9
+    comm = comm_info(world)  # collective: every rank
     cpu = None
-    if not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n, times, cores, sample = cpu_reference_sample(wl, steps=1)
         cpu = {"value": n / times[0], "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
     if rank == 0:
@@ -269,7 +270,7 @@ def run_series(args, wl, rank, world):
                     "h2d_bytes_per_step": nvox * 5, "d2h_bytes_per_step": nvox * 5,
                     "api": "paper_2509_26213_b200.api.segment_series (host series streamed through "
                            "segment_many; the value above is this end-to-end number)"},
-            "clocks": clocks.summary(), "gpu_launches": int(launches),
+            "clocks": clocks.summary(), "gpu_launches": int(launches), "comm": comm,
             "levels": [dict(st, level=k) for k, st in enumerate(res.stats) if st is not None],
         }
         print(json.dumps(line), flush=True)
@@ -388,10 +389,12 @@ def run_ours(args, wl, rank, world):
         lat_ms = e0.elapsed_time(e1)
         # K volumes through the streaming API (throughput): every step still uploads its
         # inputs and downloads its result, overlapped with the neighbouring steps' compute
-        api.segment_many([(vol_h, seeds_h)] * 2, brick, levels, cfg, outputs=outs, workspace=ws)
+        api.segment_many([(vol_h, seeds_h)] * 2, brick, levels, cfg, outputs=outs, workspace=ws,
+                         cyclic_outputs=True)
         torch.cuda.synchronize()
         e0.record(stream)
-        api.segment_many([(vol_h, seeds_h)] * args.steps, brick, levels, cfg, outputs=outs, workspace=ws)
+        api.segment_many([(vol_h, seeds_h)] * args.steps, brick, levels, cfg, outputs=outs, workspace=ws,
+                         cyclic_outputs=True)
         e1.record(stream)
         torch.cuda.synchronize()
         e_ms = e0.elapsed_time(e1) / args.steps
@@ -436,6 +439,7 @@ def run_ours(args, wl, rank, world):
                          "this launch (profiles/)"),
                 "kernels": kernels}
 
+    comm = comm_info(world)  # collective: every rank
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n, times, cores, sample = cpu_reference_sample(wl, steps=1)
@@ -456,9 +460,82 @@ def run_ours(args, wl, rank, world):
             "e2e": e2e,
             "clocks": clocks.summary(),
             "gpu_launches": int(launches),
+            "comm": comm,
             "levels": per_level,
         }
         print(json.dumps(line), flush=True)
+    return 0
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(n: int) -> int:
+    """`--gpus N` (N > 1) without a torchrun environment: relaunch this command as N ranks, one
+    process per GPU, under torch.distributed.run on 127.0.0.1; rank 0 prints the line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.run(cmd, env=env).returncode
+
+
+def init_ranks(world: int):
+    """Process group of the N ranks (NCCL on GPUs; gloo where there is no CUDA device)."""
+    import torch
+    import torch.distributed as dist
+
+    if world <= 1 or dist.is_initialized():
+        return
+    if torch.cuda.is_available():
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
+    else:
+        dist.init_process_group("gloo")
+
+
+def comm_info(world: int) -> dict:
+    """Rank count the communicator actually has, and the GPU each rank drives (all-gathered)."""
+    import torch
+
+    if world <= 1:
+        dev = torch.cuda.current_device() if torch.cuda.is_available() else -1
+        return {"backend": None, "nranks": 1, "devices": [dev]}
+    import torch.distributed as dist
+
+    cuda = torch.cuda.is_available()
+    mine = torch.tensor([torch.cuda.current_device() if cuda else -1], dtype=torch.int64,
+                        device="cuda" if cuda else "cpu")
+    got = [torch.zeros_like(mine) for _ in range(dist.get_world_size())]
+    dist.all_gather(got, mine)
+    return {"backend": dist.get_backend(), "nranks": dist.get_world_size(), "devices": [int(t.item()) for t in got]}
+
+
+def run_launch_probe(args, rank, world):
+    """`--launch-probe`: start the ranks exactly as a measured run does (spawned or torchrun),
+    exchange once over the communicator and print the line's launch fields (no kernels; runs on
+    CPU with gloo, which is how the test suite checks `--gpus N`)."""
+    import torch
+
+    init_ranks(world)
+    info = comm_info(world)
+    if world > 1:
+        import torch.distributed as dist
+
+        one = torch.ones(1, device="cuda" if torch.cuda.is_available() else "cpu")
+        dist.all_reduce(one)
+        info["all_reduce_ok"] = int(one.item()) == world
+    if rank == 0:
+        print(json.dumps({"launch_probe": True, "n_gpus": world, "requested_gpus": args.gpus, "comm": info}),
+              flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
     return 0
 
 
@@ -472,21 +549,24 @@ def main():
     ap.add_argument("--check-every", type=int, default=16)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--launch-probe", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", 1))
     rank = int(os.environ.get("RANK", 0))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
+    if args.launch_probe:
+        return run_launch_probe(args, rank, world)
     wl = WORKLOADS[args.config]
     if args.impl == "reference":
         return run_reference(args, wl, rank)
-    if "timesteps" in wl:
-        return run_series(args, wl, rank, world)
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+    init_ranks(world)
     try:
+        if "timesteps" in wl:
+            return run_series(args, wl, rank, world)
         return run_ours(args, wl, rank, world)
     finally:
         if world > 1:

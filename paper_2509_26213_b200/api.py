@@ -54,12 +54,15 @@ def segment(volume, seeds, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWCo
 
 def segment_many(inputs, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConfig(), *, outputs=None,
                  workspace: device.Workspace | None = None, level0_chunks: int | None = None, pyramid_store=None,
-                 pyramid_keys=None):
+                 pyramid_keys=None, cyclic_outputs: bool = False):
     """Segment a sequence of host volumes with the transfers overlapped.
 
     `inputs`: list of (volume, seeds) host tensors of one shape (pinned for
     asynchronous copies); `outputs`: optional list of (prob, labels) pinned
-    host tensors, reused cyclically when shorter than `inputs`.  Volume k+1 is
+    host tensors, one pair per input (default: allocated here).  A shorter
+    list is an error unless `cyclic_outputs=True`, which reuses the pairs
+    cyclically (later volumes overwrite earlier results: a throughput probe
+    that does not keep them).  Volume k+1 is
     uploaded on its own stream while volume k is segmented, and the results
     of volume k are downloaded on a third stream while volume k+1 is
     segmented (device inputs double-buffered), so in steady state a volume
@@ -82,7 +85,11 @@ def segment_many(inputs, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConf
     sd_d = [torch.empty(shape, dtype=torch.uint8, device=dev) for _ in range(min(n, 2))]
     if outputs is None:
         outputs = [(torch.empty(shape, dtype=torch.float32, pin_memory=True),
-                    torch.empty(shape, dtype=torch.uint8, pin_memory=True)) for _ in range(min(n, 2))]
+                    torch.empty(shape, dtype=torch.uint8, pin_memory=True)) for _ in range(n)]
+    elif len(outputs) < n and not cyclic_outputs:
+        raise ValueError(f"{len(outputs)} output pairs for {n} inputs (pass cyclic_outputs=True to reuse them)")
+    elif len(outputs) == 0:
+        raise ValueError("outputs is empty")
     computed = []
 
     def upload(i):

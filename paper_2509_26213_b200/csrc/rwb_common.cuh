@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 
 #include "rwb.h"
@@ -47,6 +48,14 @@ struct Shape3 {
 };
 
 int shape_from(int32_t ndim, const int64_t* size, Shape3* out);
+
+// Launch configurations (occupancy-derived grids, >48 KB shared-memory opt-ins) are properties of
+// one device, so they are cached per device ordinal: a process that drives several GPUs sets the
+// function attributes on each of them.  Concurrent first uses may compute a value twice (same result).
+constexpr int kMaxDevices = 64;
+using DeviceCache = std::atomic<int>[kMaxDevices];
+// current device ordinal into *dev (RWB_ERR_UNSUPPORTED beyond kMaxDevices)
+int device_slot(int* dev);
 
 // process-wide kernel launch counter (rwb_kernel_launches)
 void count_launches(long long n);

@@ -23,6 +23,12 @@ void count_launches(long long n) { g_launches.fetch_add(n, std::memory_order_rel
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 
+int device_slot(int* dev) {
+  RWB_CUDA(cudaGetDevice(dev));
+  if (*dev < 0 || *dev >= kMaxDevices) return fail(RWB_ERR_UNSUPPORTED, "device ordinal beyond the launch caches");
+  return RWB_OK;
+}
+
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;

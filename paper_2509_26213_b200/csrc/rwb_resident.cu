@@ -565,7 +565,10 @@ int resident3d_supported(const Geo& g) { return g.is3d && g.bz == RB && g.by == 
 template <int RPZ, int TZT>
 static int launch_resident(const ResidentArgs& a, int max_bricks, cudaStream_t st) {
   using C = RCfg<RPZ, TZT>;
-  static thread_local int clusters = 0;
+  static DeviceCache cache;
+  int dev = 0;
+  if (int rc = device_slot(&dev)) return rc;
+  int clusters = cache[dev].load(std::memory_order_relaxed);
   auto kern = resident3d_kernel<RPZ, TZT>;
   const int smem = (int)sizeof(ResidentSmem<RPZ, TZT>);
   cudaLaunchConfig_t cfg = {};
@@ -587,6 +590,7 @@ static int launch_resident(const ResidentArgs& a, int max_bricks, cudaStream_t s
     RWB_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
     if (n <= 0) return fail(RWB_ERR_UNSUPPORTED, "no brick cluster fits on this device");
     clusters = n;
+    cache[dev].store(n, std::memory_order_relaxed);
   }
   const int grid_clusters = clusters < max_bricks ? clusters : max_bricks;
   if (grid_clusters <= 0) return RWB_OK;

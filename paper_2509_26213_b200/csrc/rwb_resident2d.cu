@@ -219,14 +219,17 @@ __global__ void __launch_bounds__(TH2, 1) resident2d_kernel(ResidentArgs a) {
 int resident2d_supported(const Geo& g) { return !g.is3d && g.by == T2 && g.bx == T2; }
 
 int launch_resident2d(const ResidentArgs& a, int max_bricks, cudaStream_t st) {
-  static thread_local int grid = 0;
+  static DeviceCache cache;
+  int dev = 0;
+  if (int rc = device_slot(&dev)) return rc;
+  int grid = cache[dev].load(std::memory_order_relaxed);
   if (!grid) {
-    int dev = 0, sms = 0, per = 0;
-    RWB_CUDA(cudaGetDevice(&dev));
+    int sms = 0, per = 0;
     RWB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, resident2d_kernel, TH2, 0));
     if (per <= 0) return fail(RWB_ERR_UNSUPPORTED, "2-D tile engine does not fit on this device");
     grid = sms * per;
+    cache[dev].store(grid, std::memory_order_relaxed);
   }
   const int g = grid < max_bricks ? grid : max_bricks;
   if (g <= 0) return RWB_OK;

@@ -470,7 +470,10 @@ static int launch_q4(const ResidentArgs& a, int max_bricks, cudaStream_t st) {
   using namespace q4;
   constexpr int RTT = Cfg<TZT>::RTT;
   auto kern = resident3d_q4_kernel<TZT>;
-  static thread_local int clusters = 0;
+  static DeviceCache cache;
+  int dev = 0;
+  if (int rc = device_slot(&dev)) return rc;
+  int clusters = cache[dev].load(std::memory_order_relaxed);
   const int smem = (int)sizeof(Q4Smem);
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr;
@@ -490,6 +493,7 @@ static int launch_q4(const ResidentArgs& a, int max_bricks, cudaStream_t st) {
     RWB_CUDA(cudaOccupancyMaxActiveClusters(&n, kern, &cfg));
     if (n <= 0) return fail(RWB_ERR_UNSUPPORTED, "no 4-CTA brick cluster fits on this device");
     clusters = n;
+    cache[dev].store(n, std::memory_order_relaxed);
   }
   const int grid_clusters = clusters < max_bricks ? clusters : max_bricks;
   if (grid_clusters <= 0) return RWB_OK;

@@ -34,7 +34,6 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
-#include <mutex>
 #include <vector>
 
 #include "rwb_common.cuh"
@@ -1518,7 +1517,7 @@ static thread_local PinnedScratch t_pinned;
 
 static int pinned(int** out, int** dev_alias = nullptr) {
   if (!t_pinned.host) {
-    RWB_CUDA(cudaHostAlloc(&t_pinned.host, 64, cudaHostAllocMapped));  // [0] n_active, [2..9] stats, [10..11] unknowns
+    RWB_CUDA(cudaHostAlloc(&t_pinned.host, 64, cudaHostAllocMapped | cudaHostAllocPortable));  // [0] n_active, [2..9] stats, [10..11] unknowns
     RWB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&t_pinned.dev), t_pinned.host, 0));
   }
   *out = t_pinned.host;
@@ -1542,14 +1541,17 @@ static int readback(cudaStream_t st, const void* src, int at, int n) {
 }
 
 static int persistent_grid(int* grid) {
-  static thread_local int cached = 0;
+  static DeviceCache cache;
+  int dev = 0;
+  if (int rc = device_slot(&dev)) return rc;
+  int cached = cache[dev].load(std::memory_order_relaxed);
   if (!cached) {
-    int dev = 0, sms = 0, per1 = 0, per2 = 0;
-    RWB_CUDA(cudaGetDevice(&dev));
+    int sms = 0, per1 = 0, per2 = 0;
     RWB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, cg_pass1_kernel, NTHREADS, 0));
     RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, cg_pass2_kernel, NTHREADS, 0));
     cached = sms * std::max(1, std::min(per1, per2));
+    cache[dev].store(cached, std::memory_order_relaxed);
   }
   *grid = cached;
   return RWB_OK;
@@ -1642,10 +1644,12 @@ static int read_stats(const Work& w, int nb, cudaStream_t st, cudaEvent_t ev0, c
 }
 
 static int coop_grid(int* grid) {
-  static thread_local int cached = 0;
+  static DeviceCache cache;
+  int dev = 0;
+  if (int rc = device_slot(&dev)) return rc;
+  int cached = cache[dev].load(std::memory_order_relaxed);
   if (!cached) {
-    int dev = 0, sms = 0, per = 0, coop = 0;
-    RWB_CUDA(cudaGetDevice(&dev));
+    int sms = 0, per = 0, coop = 0;
     RWB_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
     if (!coop) return fail(RWB_ERR_UNSUPPORTED, "device does not support cooperative launches");
     RWB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -1653,6 +1657,7 @@ static int coop_grid(int* grid) {
     if (const char* e = std::getenv("RWB_COOP_BLOCKS_PER_SM"))  // diagnostics: fewer, fatter blocks
       per = std::max(1, std::min(per, std::atoi(e)));
     cached = std::min(sms * std::max(per, 1), kCoopMaxBlocks);
+    cache[dev].store(cached, std::memory_order_relaxed);
   }
   *grid = cached;
   return RWB_OK;
@@ -1680,18 +1685,15 @@ static int solve_level_impl(const rwb_geometry_t* geom, const float* intensity, 
                             const rwb_solve_params_t* params, float* prob, uint8_t* labels, void* workspace,
                             size_t workspace_bytes, rwb_solve_stats_t* stats, void* stream);
 
-// Host calls are serialised per process: a solve captures CUDA graphs and
-// synchronises its stream for its polls and stats, and concurrent callers
-// (the reference Engine runs kernels on a thread pool) must not interleave
-// those with another thread's capture.  The device work of different calls is
-// stream-ordered anyway.
-static std::mutex g_solve_mutex;
-
+// Reentrant and stream-ordered: every piece of a call's device state lives in the caller's
+// workspace, host-side scratch (the mapped readback words) is per thread, launch caches are per
+// device (atomics), and the streaming path captures its graph in cudaStreamCaptureModeThreadLocal
+// on a private stream, so concurrent callers on distinct streams and workspaces (the reference
+// Engine's worker pool, engine.py:398-400, 866-875) run without a process-wide lock.
 extern "C" int rwb_solve_level(const rwb_geometry_t* geom, const float* intensity, const uint8_t* seeds,
                                const float* bound, const int32_t* brick_list, int64_t n_bricks,
                                const rwb_solve_params_t* params, float* prob, uint8_t* labels, void* workspace,
                                size_t workspace_bytes, rwb_solve_stats_t* stats, void* stream) {
-  std::lock_guard<std::mutex> lock(g_solve_mutex);
   return solve_level_impl(geom, intensity, seeds, bound, brick_list, n_bricks, params, prob, labels, workspace,
                           workspace_bytes, stats, stream);
 }
@@ -1749,11 +1751,13 @@ static int solve_level_impl(const rwb_geometry_t* geom, const float* intensity, 
                                              tol2, max_iter, resident ? 0 : 1);
     RWB_LAUNCH_CHECK("2-D tile setup kernel");
   } else if (!(params->flags & RWB_SOLVE_SETUP2) && make_setup_maps(g, intensity, seeds, bound, &maps)) {
-    static bool smem_set = false;
-    if (!smem_set) {
+    static DeviceCache smem_set;
+    int dev = 0;
+    if ((rc = device_slot(&dev))) return rc;
+    if (!smem_set[dev].load(std::memory_order_relaxed)) {
       RWB_CUDA(cudaFuncSetAttribute(setup_brick_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)sizeof(SetupSmem)));
-      smem_set = true;
+      smem_set[dev].store(1, std::memory_order_relaxed);
     }
     setup_brick_kernel<<<nb, STH, sizeof(SetupSmem), st>>>(maps, g, w, list, bound != nullptr, params->beta,
                                                                    params->min_weight, tol2, max_iter,

@@ -484,6 +484,8 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
     probs[top], stats[top] = solve_level(vols[top], seed_levels[top], tuple(vols[top].shape), None, cfg,
                                          labels_out=top_labels, workspace=workspace, stats_on_device=True)
     lab = top_labels
+    if top == 0 and on_level0_chunk is not None:  # single-level hierarchy: level 0 is the whole-level solve
+        on_level0_chunk(0, vols[0].shape[0], probs[0], top_labels)
     for k in range(top - 1, -1, -1):
         if exchange is not None:
             exchange(k + 1, probs[k + 1])

@@ -11,6 +11,24 @@ if ROOT not in sys.path:
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 
+def reference_package():
+    """The unmodified reference package `chunkcast` (baseline/_ref, installed by
+    __graft_entry__.build() / ensure_reference()).  Its absence is a FAILURE, not a skip: the
+    operator-mode and view tests are the drop-in evidence and must run wherever the suite runs."""
+    import __graft_entry__ as entry
+
+    try:
+        entry.ensure_reference()
+    except Exception as e:  # noqa: BLE001 - reported through the failure below
+        pytest.fail(f"reference package chunkcast could not be installed into baseline/_ref: {e}")
+    from paper_2509_26213_b200 import ops as rwops
+
+    try:
+        return rwops._chunkcast()
+    except ImportError as e:
+        pytest.fail(f"reference package chunkcast not importable (baseline/_ref missing?): {e}")
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a) and the built librwb.so")
 

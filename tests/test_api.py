@@ -44,7 +44,9 @@ def test_segment_many_matches_single_calls(n_out):
         for k, (v, s) in enumerate(inputs):
             got = api.segment_many([(v, s)], (32, 32, 32), 2, cfg, outputs=outs)
             np.testing.assert_array_equal(got[0][0].numpy(), ref[k][0].numpy())
-        got = api.segment_many(inputs, (32, 32, 32), 2, cfg, outputs=outs)
+        with pytest.raises(ValueError):  # fewer outputs than inputs needs the explicit opt-in
+            api.segment_many(inputs, (32, 32, 32), 2, cfg, outputs=outs)
+        got = api.segment_many(inputs, (32, 32, 32), 2, cfg, outputs=outs, cyclic_outputs=True)
         last = (len(inputs) - 1) % n_out
         np.testing.assert_array_equal(outs[last][0].numpy(), ref[-1][0].numpy())
         np.testing.assert_array_equal(outs[last][1].numpy(), ref[-1][1].numpy())
@@ -88,3 +90,33 @@ def test_segment_series_matches_per_timestep_calls():
         np.testing.assert_array_equal(prob[t].numpy(), p.numpy())
         np.testing.assert_array_equal(labels[t].numpy(), l.numpy())
     assert not np.array_equal(prob[0].numpy(), prob[-1].numpy())  # the blobs move
+
+
+def test_segment_many_default_outputs_are_distinct():
+    """Without `outputs`, every volume gets its own result buffers (no cyclic aliasing)."""
+    shape = (64, 64, 64)
+    inputs = [_case(shape, k) for k in ("S1", "S2", "S1")]
+    inputs[2] = (inputs[2][0] * 0.5, inputs[2][1])
+    cfg = RWConfig(tol=1e-6)
+    got = api.segment_many(inputs, (32, 32, 32), 2, cfg)
+    assert len({p.data_ptr() for p, _ in got}) == 3
+    for (p, l), (v, s) in zip(got, inputs):
+        rp, rl = api.segment(v, s, (32, 32, 32), 2, cfg)
+        np.testing.assert_array_equal(p.numpy(), rp.numpy())
+        np.testing.assert_array_equal(l.numpy(), rl.numpy())
+
+
+@pytest.mark.parametrize("shape,brick,levels", [((64, 64, 64), (64, 64, 64), 1), ((64, 64, 64), (32, 32, 32), 1),
+                                                ((96, 80), (96, 80), 1)])
+def test_single_level_host_path(shape, brick, levels):
+    """A one-level hierarchy through the host API downloads its (whole-level) result."""
+    vol, sd = _case(shape, "S1")
+    cfg = RWConfig(tol=1e-6)
+    out_p = torch.full(shape, float("nan"), dtype=torch.float32).pin_memory()
+    out_l = torch.full(shape, 7, dtype=torch.uint8).pin_memory()
+    p_h, l_h = api.segment(vol, sd, brick, levels, cfg, out_prob=out_p, out_labels=out_l)
+    p_d, l_d = api.segment(vol.cuda(), sd.cuda(), brick, levels, cfg)
+    torch.cuda.synchronize()
+    assert not np.isnan(p_h.numpy()).any()
+    np.testing.assert_array_equal(p_h.numpy(), p_d.cpu().numpy())
+    np.testing.assert_array_equal(l_h.numpy(), l_d.cpu().numpy())

@@ -39,3 +39,23 @@ def test_workloads_cover_the_baseline_configs():
         assert len(s["shape"]) == len(wl["shape"]) and s["levels"] <= wl["levels"]
     assert bench.WORKLOADS["c5"]["timesteps"] == 16
     assert bench.ALG_BYTES_PER_UNKNOWN_ITER == {3: 56, 2: 52}
+
+
+def test_gpus_flag_launches_ranks():
+    """`bench.py --gpus 2` outside torchrun starts two ranks itself (one process per GPU; gloo on CPU)
+    whose communicator really has two members."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launch-probe"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT,
+                         env={k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["comm"]["nranks"] == 2 and d["comm"]["all_reduce_ok"] is True
+
+
+def test_gpus_flag_must_match_world_size():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launch-probe"],
+                         capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
+    assert out.returncode == 2 and "WORLD_SIZE" in out.stderr

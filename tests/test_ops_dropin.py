@@ -9,16 +9,12 @@ and the oracle.  `chunkcast` comes from the environment or baseline/_ref.
 import numpy as np
 import pytest
 
-from conftest import load_golden
+from conftest import load_golden, reference_package
 from paper_2509_26213_b200 import ops as rwops
 from paper_2509_26213_b200 import synthetic
 
-try:
-    cc = rwops._chunkcast()
-except ImportError:  # pragma: no cover - reference package not installed
-    cc = None
+cc = reference_package()  # fails (does not skip) when the reference is missing
 
-pytestmark_cc = pytest.mark.skipif(cc is None, reason="reference package chunkcast not importable")
 
 
 def _engine():
@@ -40,7 +36,6 @@ def _dense(engine, node):
 # -- structure (CPU) -----------------------------------------------------------------
 
 
-@pytestmark_cc
 def test_pyramid_metadata_matches_reference_build_lod():
     src = cc.ops.source_from_array(np.zeros((100, 70, 40), np.float32), (16, 16, 16),
                                    embedding=(0.5, 1.0, 2.0))
@@ -52,7 +47,6 @@ def test_pyramid_metadata_matches_reference_build_lod():
         assert ours.embedding(k) == ref.embedding(k)
 
 
-@pytestmark_cc
 def test_level_cap():
     src = cc.ops.source_from_array(np.zeros((256, 256), np.float32), (32, 32))
     assert rwops.build_lod(src, levels=2).num_levels == 2
@@ -60,7 +54,6 @@ def test_level_cap():
         rwops.build_lod(src, levels=9)
 
 
-@pytestmark_cc
 def test_random_walker_footprint_is_dilated_neighbourhood():
     # like the reference's conv footprint test (test_engine.py:62-81): 3^d chunks, clipped at corners
     shape, chunk = (128, 128, 128), (16, 16, 16)
@@ -78,7 +71,6 @@ def test_random_walker_footprint_is_dilated_neighbourhood():
     assert len(top.dependencies((0, 0, 0))[0]) == 64  # whole coarsest level
 
 
-@pytestmark_cc
 def test_ids_are_deterministic_and_parameter_sensitive():
     data = synthetic.phantom((32, 32))
     vol = cc.ops.source_from_array(data, (16, 16))
@@ -89,7 +81,6 @@ def test_ids_are_deterministic_and_parameter_sensitive():
     assert a.op_id == b.op_id and a.op_id != c.op_id
 
 
-@pytestmark_cc
 def test_type_errors_raise_operator_error():
     f32 = cc.ops.source_from_array(np.zeros((8, 8), np.float32), (4, 4))
     u8 = cc.ops.source_from_array(np.zeros((8, 8), np.uint8), (4, 4))
@@ -106,7 +97,6 @@ def test_type_errors_raise_operator_error():
 # -- through the reference Engine (GPU) ------------------------------------------------
 
 
-@pytestmark_cc
 @pytest.mark.gpu
 @pytest.mark.parametrize("name", ["r3d", "r2d", "phantom3d"])
 def test_engine_resolves_lod_bit_exact(name):
@@ -125,7 +115,6 @@ def test_engine_resolves_lod_bit_exact(name):
             np.testing.assert_array_equal(_dense(eng, pyr.node(k)), g[f"{name}/level{k}"])
 
 
-@pytestmark_cc
 @pytest.mark.gpu
 @pytest.mark.parametrize("shape,chunk,levels", [((64, 64, 64), (32, 32, 32), 2),   # resident path
                                                 ((40, 36, 28), (16, 16, 16), 2),   # streaming, ragged
@@ -152,7 +141,6 @@ def test_engine_hierarchy_equals_device_path(shape, chunk, levels):
     np.testing.assert_array_equal(l_engine, res.labels.cpu().numpy())
 
 
-@pytestmark_cc
 @pytest.mark.gpu
 @pytest.mark.parametrize("per_task", [1, 64])
 def test_engine_batching_is_transparent(per_task):
@@ -183,7 +171,6 @@ def test_engine_batching_is_transparent(per_task):
     assert launches > 0
 
 
-@pytestmark_cc
 @pytest.mark.gpu
 def test_engine_weights_match_oracle():
     from oracle import rw as orw
@@ -197,7 +184,6 @@ def test_engine_weights_match_oracle():
         np.testing.assert_allclose(w[..., k], ref[k], rtol=5e-6, atol=1e-12)
 
 
-@pytestmark_cc
 @pytest.mark.gpu
 def test_engine_pull_is_lazy():
     shape, chunk = (128, 64, 64), (32, 32, 32)

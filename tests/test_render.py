@@ -5,13 +5,12 @@ Engine — byte-identical frames."""
 import numpy as np
 import pytest
 
+from conftest import reference_package
+
 from paper_2509_26213_b200 import ops as rwops
 from paper_2509_26213_b200.render import zoom_level
 
-try:
-    cc = rwops._chunkcast()
-except ImportError:  # pragma: no cover
-    cc = None
+cc = reference_package()  # fails (does not skip) when the reference is missing
 
 
 def test_zoom_level_rule():
@@ -30,7 +29,6 @@ def _frame(eng, node):
     return out
 
 
-@pytest.mark.skipif(cc is None, reason="reference package chunkcast not importable")
 @pytest.mark.gpu
 @pytest.mark.parametrize("dim,index,pan,zoom", [(0, 17, (0.0, 0.0), 1.0), (1, 40, (-3.5, 7.25), 0.6),
                                                 (2, 63, (10.0, -20.0), 2.5), (0, 5, (1.0, 2.0), 0.2)])
@@ -55,7 +53,6 @@ def test_slice_view_matches_reference(dim, index, pan, zoom):
     np.testing.assert_array_equal(ours, ref)
 
 
-@pytest.mark.skipif(cc is None, reason="reference package chunkcast not importable")
 @pytest.mark.gpu
 @pytest.mark.parametrize("pan,zoom", [((0.0, 0.0), 1.0), ((-5.0, 3.0), 0.45), ((20.0, 11.0), 3.0)])
 def test_image_view_matches_reference(pan, zoom):
