@@ -96,3 +96,25 @@ def lod_chain(volume: np.ndarray, chunk, levels: int | None = None) -> list:
     for _ in range(levels - 1):
         out.append(lod_down(out[-1]))
     return out
+
+
+def lod_down_slabbed(level: np.ndarray, slab: int = 32) -> np.ndarray:
+    """`lod_down` computed `slab` coarse planes (dim 0) at a time — bit-identical, with float64
+    temporaries bounded by the slab (1024^3 levels).
+
+    Coarse planes [j0, j1) read fine planes [2 j0 - 1, 2 j1 + 1) through the radius-1 dim-0 taps.
+    Each slab is convolved over that window: interior window edges only change the discarded
+    outermost planes, and where the window meets the level's border the edge padding is the
+    reference's own clamp (`ops.py:509-515`); the per-element float64 operations are unchanged.
+    """
+    level = np.asarray(level, dtype=np.float32)
+    n = level.shape[0]
+    m = -(-n // 2)
+    out = np.empty((m,) + tuple(-(-s // 2) for s in level.shape[1:]), dtype=np.float32)
+    for j0 in range(0, m, slab):
+        j1 = min(j0 + slab, m)
+        f0, f1 = max(2 * j0 - 1, 0), min(2 * j1 + 1, n)
+        conv = separable_conv_clamp(level[f0:f1], [SMOOTHING_KERNEL] * level.ndim).astype(np.float32)
+        keep = conv[2 * j0 - f0:min(2 * j1, n) - f0]
+        out[j0:j1] = pairwise_mean(keep).astype(np.float32)
+    return out

@@ -136,6 +136,55 @@ def upsample_linear(parent: np.ndarray, fine_shape) -> np.ndarray:
     return out
 
 
+def upsample_linear_window(parent: np.ndarray, fine_shape, lo, hi) -> np.ndarray:
+    """Fine voxels [lo, hi) of `upsample_linear(parent, fine_shape)` — the same float64
+    operations per element (the same taps in the same dimension order), so identical to slicing
+    the full prolongation; only the parent planes the window reads are touched."""
+    out = None
+    src = parent
+    for dim, n in enumerate(fine_shape):
+        m = parent.shape[dim]
+        if -(-n // 2) != m:
+            raise ValueError(f"fine size {n} is not a 2x refinement of {m}")
+        g = np.arange(lo[dim], hi[dim], dtype=np.float64)
+        c = g / 2.0 - 0.25
+        fl = np.floor(c)
+        t = c - fl
+        i0 = np.clip(fl.astype(np.int64), 0, m - 1)
+        i1 = np.clip(fl.astype(np.int64) + 1, 0, m - 1)
+        if dim == 0:  # cut the parent to the planes this window reads before anything is float64
+            a, b = int(min(i0.min(), i1.min())), int(max(i0.max(), i1.max())) + 1
+            src = np.asarray(parent[a:b], dtype=np.float64)
+            i0, i1 = i0 - a, i1 - a
+        shape = [1] * parent.ndim
+        shape[dim] = len(g)
+        t = t.reshape(shape)
+        src = np.take(src, i0, axis=dim) * (1.0 - t) + np.take(src, i1, axis=dim) * t
+        out = src
+    return out
+
+
+def solve_brick(volume, seeds, parent_prob, brick, h, params: RWParams) -> tuple:
+    """The oracle's solution of ONE brick `h` (grid position) of a finer level, given the
+    parent level's probabilities (`parent_prob`, e.g. the ones the GPU computed): its box plus
+    a one-voxel Dirichlet halo is cut out of the level, bounded by the windowed prolongation of
+    the parent, and solved exactly as `solve_level` solves it inside the whole level (the brick
+    is an independent Dirichlet problem).  Returns (box slices, probabilities over the box)."""
+    nd = volume.ndim
+    b0 = [int(h[d]) * brick[d] for d in range(nd)]
+    b1 = [min(b0[d] + brick[d], volume.shape[d]) for d in range(nd)]
+    lo = [max(b0[d] - 1, 0) for d in range(nd)]
+    hi = [min(b1[d] + 1, volume.shape[d]) for d in range(nd)]
+    sl = tuple(slice(l, e) for l, e in zip(lo, hi))
+    bound = upsample_linear_window(parent_prob, volume.shape, lo, hi)
+    inside = np.zeros(bound.shape, dtype=bool)
+    inside[tuple(slice(a - l, b - l) for a, b, l in zip(b0, b1, lo))] = True
+    res = solve_level(np.asarray(volume[sl]), np.asarray(seeds[sl]), brick, bound, params, solve_mask=inside,
+                      origin=tuple(lo))
+    box = tuple(slice(a, b) for a, b in zip(b0, b1))
+    return box, res.prob[tuple(slice(a - l, b - l) for a, b, l in zip(b0, b1, lo))], res
+
+
 def seed_values(seeds: np.ndarray) -> np.ndarray:
     return (seeds == SEED_FG).astype(np.float64)
 

@@ -27,6 +27,8 @@ with open(os.path.join(GOLDEN, "MANIFEST.json")) as f:
 PROB_TOL = 1e-4
 BAND = 1e-4
 GPU_CFG = RWConfig(tol=1e-7, max_iter=20000)
+BENCH_CFG = RWConfig()  # the bench's settings (tol 1e-6): every solver path is checked at both
+CFGS = pytest.mark.parametrize("cfg", [GPU_CFG, BENCH_CFG], ids=["tol1e7", "tol1e6"])
 TIGHT = orw.RWParams(tol=1e-10, max_iter=50000)
 
 
@@ -121,12 +123,13 @@ def _random_case(rng, shape, frac=0.05):
     ((70, 90), (32, 32)),
     ((1, 50, 60), (1, 16, 16)),       # degenerate z
 ])
-def test_solve_level_matches_oracle(rng, shape, brick):
+@CFGS
+def test_solve_level_matches_oracle(rng, shape, brick, cfg):
     vol, seeds = _random_case(rng, shape)
     whole = tuple(brick) == tuple(shape)
     bound = None if whole else rng.random(shape).astype(np.float32)
     ref = orw.solve_level(vol, seeds, brick, None if whole else bound.astype(np.float64), TIGHT).prob
-    out, stats = device.solve_level(cuda(vol), cuda(seeds), brick, None if whole else cuda(bound), GPU_CFG)
+    out, stats = device.solve_level(cuda(vol), cuda(seeds), brick, None if whole else cuda(bound), cfg)
     assert stats["not_converged"] == 0
     assert_rw_parity(host(out), ref)
     # seeds are exact Dirichlet values
@@ -196,12 +199,13 @@ def test_input_validation():
 
 
 @pytest.mark.parametrize("name", sorted(MANIFEST["rw"]))
-def test_hierarchical_rw_vs_golden(name):
+@CFGS
+def test_hierarchical_rw_vs_golden(name, cfg):
     meta = MANIFEST["rw"][name]
     shape = tuple(meta["shape"])
     vol = synthetic.phantom(shape)
     seeds = synthetic.seeds(shape, meta["seeds"])
-    res = device.hierarchical_random_walker(cuda(vol), cuda(seeds), tuple(meta["brick"]), meta["levels"], GPU_CFG)
+    res = device.hierarchical_random_walker(cuda(vol), cuda(seeds), tuple(meta["brick"]), meta["levels"], cfg)
     g = load_golden(f"rw_{name}.npz")
     for k, p in enumerate(res.levels):
         assert_rw_parity(host(p), g[f"prob{k}"].astype(np.float64),
@@ -232,11 +236,12 @@ def test_label_swap_symmetry_gpu():
 
 
 @pytest.mark.parametrize("shape", [(64, 64, 64), (70, 40, 33), (32, 96, 45)])
-def test_resident_path_matches_oracle(rng, shape):
+@CFGS
+def test_resident_path_matches_oracle(rng, shape, cfg):
     vol, seeds = _random_case(rng, shape)
     bound = rng.random(shape).astype(np.float32)
     ref = orw.solve_level(vol, seeds, (32, 32, 32), bound.astype(np.float64), TIGHT).prob
-    out, st = device.solve_level(cuda(vol), cuda(seeds), (32, 32, 32), cuda(bound), GPU_CFG)
+    out, st = device.solve_level(cuda(vol), cuda(seeds), (32, 32, 32), cuda(bound), cfg)
     assert st["path"] == 1 and st["not_converged"] == 0
     got = host(out)
     assert_rw_parity(got, ref)
@@ -281,10 +286,11 @@ def test_resident_zero_rhs_and_seeded_bricks():
     assert st["zero_rhs"] == 2
 
 
-def test_resident_hierarchy_vs_golden_c2_like():
+@CFGS
+def test_resident_hierarchy_vs_golden_c2_like(cfg):
     vol = synthetic.phantom((96, 96, 96))
     seeds = synthetic.seeds(vol.shape, "S1")
-    res = device.hierarchical_random_walker(cuda(vol), cuda(seeds), (32, 32, 32), 2, GPU_CFG)
+    res = device.hierarchical_random_walker(cuda(vol), cuda(seeds), (32, 32, 32), 2, cfg)
     ref = orw.hierarchical_random_walker(vol, seeds, (32, 32, 32), 2, TIGHT)
     assert res.stats[0]["path"] == 1
     assert_rw_parity(host(res.prob), ref.prob[0], host(res.labels))
@@ -301,13 +307,14 @@ def test_resident_in_place_output(rng):
     np.testing.assert_array_equal(host(out), ref)
 
 
-def test_cooperative_whole_level_matches_graph_path():
+@CFGS
+def test_cooperative_whole_level_matches_graph_path(cfg):
     vol = synthetic.phantom((48, 40, 36))
     seeds = synthetic.seeds(vol.shape, "S2")
     ref = orw.solve_level(vol, seeds, vol.shape, None, TIGHT).prob
-    a, sa = device.solve_level(cuda(vol), cuda(seeds), vol.shape, None, GPU_CFG)
+    a, sa = device.solve_level(cuda(vol), cuda(seeds), vol.shape, None, cfg)
     b, sb = device.solve_level(cuda(vol), cuda(seeds), vol.shape, None,
-                               RWConfig(tol=GPU_CFG.tol, max_iter=GPU_CFG.max_iter, cooperative=False))
+                               RWConfig(tol=cfg.tol, max_iter=cfg.max_iter, cooperative=False))
     assert sa["path"] == 2 and sb["path"] == 0
     assert_rw_parity(host(a), ref)
     assert_rw_parity(host(b), ref)
@@ -327,7 +334,8 @@ def test_upsample_window_slabs_match_full(rng):
             assert np.isnan(got[:z0]).all() and np.isnan(got[z1:]).all()
 
 
-def test_config2_full_size_vs_oracle():
+@CFGS
+def test_config2_full_size_vs_oracle(cfg):
     """Config 2 at its full size (256^3, 2 levels, 32^3 bricks): the level-0 probabilities and
     labels of the brick-resident hierarchy against the float64 oracle (tol 1e-9), on a strided
     subsample (every 4th voxel per axis; fixture made by tests/golden/make_golden.py --c2-only)."""
@@ -337,14 +345,15 @@ def test_config2_full_size_vs_oracle():
     vol = synthetic.phantom(tuple(meta["shape"]))
     seeds = synthetic.seeds(vol.shape, meta["seeds"])
     assert hashlib.sha256(np.ascontiguousarray(vol).tobytes()).hexdigest() == meta["input_sha256"]
-    res = device.hierarchical_random_walker(cuda(vol), cuda(seeds), tuple(meta["brick"]), meta["levels"], GPU_CFG)
+    res = device.hierarchical_random_walker(cuda(vol), cuda(seeds), tuple(meta["brick"]), meta["levels"], cfg)
     assert res.stats[0]["path"] == 1 and res.stats[1]["path"] == 2
     s = meta["stride"]
     ref = load_golden("rw_c2_sub4.npz")["prob0"].astype(np.float64)
     assert_rw_parity(host(res.prob)[::s, ::s, ::s], ref, host(res.labels)[::s, ::s, ::s])
 
 
-def test_config3_structure_2048_vs_oracle():
+@CFGS
+def test_config3_structure_2048_vs_oracle(cfg):
     """Config 3's structure at 2048^2 (64^2 tiles, all 6 levels: tile-resident levels down to a
     64^2 whole-level solve) against the float64 oracle (tol 1e-9), every 4th pixel per axis."""
     import hashlib
@@ -353,7 +362,7 @@ def test_config3_structure_2048_vs_oracle():
     vol = synthetic.phantom(tuple(meta["shape"]))
     seeds = synthetic.seeds(vol.shape, meta["seeds"])
     assert hashlib.sha256(np.ascontiguousarray(vol).tobytes()).hexdigest() == meta["input_sha256"]
-    res = device.hierarchical_random_walker(cuda(vol), cuda(seeds), tuple(meta["brick"]), meta["levels"], GPU_CFG)
+    res = device.hierarchical_random_walker(cuda(vol), cuda(seeds), tuple(meta["brick"]), meta["levels"], cfg)
     assert res.stats[0]["path"] == 1 and res.stats[-1]["path"] == 2
     s = meta["stride"]
     ref = load_golden("rw_c3like_sub4.npz")["prob0"].astype(np.float64)
@@ -361,36 +370,39 @@ def test_config3_structure_2048_vs_oracle():
 
 
 @pytest.mark.parametrize("shape", [(128, 192), (130, 201), (64, 64 * 3)])
-def test_resident2d_tiles_match_oracle(rng, shape):
+@CFGS
+def test_resident2d_tiles_match_oracle(rng, shape, cfg):
     """2-D levels with 64^2 bricks run on the tile-resident engine (one CTA per tile)."""
     vol, seeds = _random_case(rng, shape)
     bound = rng.random(shape).astype(np.float32)
     ref = orw.solve_level(vol, seeds, (64, 64), bound.astype(np.float64), TIGHT).prob
-    out, st = device.solve_level(cuda(vol), cuda(seeds), (64, 64), cuda(bound), GPU_CFG)
+    out, st = device.solve_level(cuda(vol), cuda(seeds), (64, 64), cuda(bound), cfg)
     assert st["path"] == 1 and st["not_converged"] == 0
     assert_rw_parity(host(out), ref)
     streaming, ss = device.solve_level(cuda(vol), cuda(seeds), (64, 64), cuda(bound),
-                                       RWConfig(tol=GPU_CFG.tol, max_iter=GPU_CFG.max_iter, resident=False))
+                                       RWConfig(tol=cfg.tol, max_iter=cfg.max_iter, resident=False))
     assert ss["path"] == 0
     assert np.abs(host(out) - host(streaming)).max() <= 2e-5
 
 
-def test_resident2d_hierarchy_vs_oracle():
+@CFGS
+def test_resident2d_hierarchy_vs_oracle(cfg):
     vol = synthetic.phantom((256, 320))
     seeds = synthetic.seeds(vol.shape, "S2")
-    res = device.hierarchical_random_walker(cuda(vol), cuda(seeds), (64, 64), 3, GPU_CFG)
+    res = device.hierarchical_random_walker(cuda(vol), cuda(seeds), (64, 64), 3, cfg)
     ref = orw.hierarchical_random_walker(vol, seeds, (64, 64), 3, TIGHT)
     assert res.stats[0]["path"] == 1 and res.stats[1]["path"] == 1
     assert_rw_parity(host(res.prob), ref.prob[0], host(res.labels))
 
 
 @pytest.mark.parametrize("cluster", [4, 8, 16, 512])
-def test_resident_cluster_variants(rng, cluster):
+@CFGS
+def test_resident_cluster_variants(rng, cluster, cfg):
     vol = synthetic.phantom((64, 96, 64))
     seeds = synthetic.seeds(vol.shape, "S1")
     bound = rng.random(vol.shape).astype(np.float32)
     ref = orw.solve_level(vol, seeds, (32, 32, 32), bound.astype(np.float64), TIGHT).prob
-    cfg = RWConfig(tol=GPU_CFG.tol, max_iter=GPU_CFG.max_iter, cluster=cluster)
+    cfg = RWConfig(tol=cfg.tol, max_iter=cfg.max_iter, cluster=cluster)
     out, st = device.solve_level(cuda(vol), cuda(seeds), (32, 32, 32), cuda(bound), cfg)
     assert st["path"] == 1 and st["not_converged"] == 0
     assert_rw_parity(host(out), ref)
