@@ -431,7 +431,7 @@ def run_ours(args, wl, rank, world):
 
     peak, peak_src = load_peak()
     path_name = {0: "streaming cg_pass1/cg_pass2", 1: "resident3d_q4_kernel" if len(wl["shape"]) == 3 else
-                 "resident2d_kernel", 2: "coop_cg_kernel"}
+                 "resident2d_kernel", 2: "coop_cg_kernel", 3: "mgcg_kernel"}
     kernels = {}
     for k, a in sorted(acc.items()):
         if a["ms"] <= 0:

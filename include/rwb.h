@@ -83,13 +83,18 @@ typedef struct {
    by a kernel on `stream` with no host synchronisation (brick-resident / cooperative paths never
    block the host then; cg_ms from %globaltimer around the solve launches). */
 #define RWB_SOLVE_STATS_DEVICE 512
-/* brick-resident solver: 4-CTA clusters (8 planes x 8192 voxels per CTA, weights in shared memory) */
+/* brick-resident solver: 4-CTA clusters (8 planes x 8192 voxels per CTA, scaled weights in tensor memory) */
 #define RWB_SOLVE_CLUSTER4 1024
+
+/* whole-level (single-brick) solves: Jacobi-PCG (the cooperative kernel, or the graph-launched
+   passes with NO_COOP) instead of the default multigrid-preconditioned CG */
+#define RWB_SOLVE_NO_MG 2048
 
 /* Solver paths (rwb_solve_stats_t.path) */
 #define RWB_PATH_STREAMING 0 /* brick-batched CG, state in HBM, 2 launches per iteration */
-#define RWB_PATH_RESIDENT 1  /* CG state on chip: one 32^3 brick per 8-CTA cluster (3-D), one 64^2 tile per CTA (2-D) */
-#define RWB_PATH_COOPERATIVE 2 /* single-brick (whole-level) solve: all iterations in one cooperative kernel */
+#define RWB_PATH_RESIDENT 1  /* CG state on chip: one 32^3 brick per 4-CTA cluster (3-D, default), one 64^2 tile per CTA (2-D) */
+#define RWB_PATH_COOPERATIVE 2 /* single-brick (whole-level) Jacobi-PCG: all iterations in one cooperative kernel */
+#define RWB_PATH_MULTIGRID 3   /* single-brick (whole-level) solve: V-cycle-preconditioned CG, one cooperative kernel */
 
 typedef struct {
   int64_t bricks;          /* bricks solved by this call */
@@ -221,9 +226,9 @@ size_t rwb_solve_workspace_bytes(const rwb_geometry_t* geom, int64_t n_bricks, i
  *  stats     : host pointer or NULL.
  * Path: 3-D levels with 32^3 bricks and more than one brick run the
  * brick-resident solver (unless RWB_SOLVE_STREAMING); whole-level (coarsest,
- * single-brick) solves run the streaming passes inside one cooperative
- * kernel (unless RWB_SOLVE_NO_COOP); everything else runs the streaming
- * solver with graph-launched passes.
+ * single-brick) solves run multigrid-preconditioned CG in one cooperative
+ * kernel (RWB_SOLVE_NO_MG: Jacobi-PCG, cooperative unless RWB_SOLVE_NO_COOP);
+ * everything else runs the streaming solver with graph-launched passes.
  * Blocking on the host: returns when the listed bricks have converged (or hit
  * max_iter); all work is stream-ordered on `stream`. */
 int rwb_solve_level(const rwb_geometry_t* geom, const float* intensity, const uint8_t* seeds,

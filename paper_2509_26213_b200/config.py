@@ -18,8 +18,9 @@ class RWConfig:
     max_iter: int = 10_000     # per-brick iteration cap
     check_every: int = 16      # CG iterations per convergence poll (one CUDA graph)
     use_graph: bool = True     # streaming solver: run each poll interval as one CUDA graph launch
-    resident: bool = True      # 32^3 bricks: solve each brick on chip (8-CTA cluster) instead of streaming
-    cooperative: bool = True   # whole-level solves: one cooperative kernel for all iterations
+    resident: bool = True      # 32^3 bricks: solve each brick on chip (4-CTA cluster by default) instead of streaming
+    cooperative: bool = True   # whole-level Jacobi-PCG (multigrid=False): one cooperative kernel for all iterations
+    multigrid: bool = True     # whole-level solves: V-cycle-preconditioned CG (one cooperative kernel)
     fused_setup: bool = True   # build the brick system with the fused per-brick setup kernel
     cluster: int = 4           # resident solver: CTAs per brick cluster (4: weights in TMEM, default; 8: all in registers;
                                # 16: 2 CTAs/SM; 512: 8-CTA with 512 threads) — 4 is 1.4x faster than 8 on config 4
@@ -30,6 +31,7 @@ class RWConfig:
         d.pop("use_graph")
         d.pop("resident")
         d.pop("cooperative")
+        d.pop("multigrid")
         d.pop("cluster")
         d.pop("fused_setup")
         return {k: (float(v) if isinstance(v, float) else int(v)) for k, v in d.items()}

@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
 #pragma unroll
         for (int v = 0; v < RV; v += 2) fma2(y[v], y[v + 1], alpha, alpha, p[v], p[v + 1], y[v], y[v + 1]);
       }
-      // w = A'r with the weights from shared memory
+      // w = A'r with the scaled weights from tensor memory
       float gp[2] = {0.f, 0.f}, dp[2] = {0.f, 0.f};
       float4 wzl4;  // w'z of the plane below the slab
       {

@@ -1452,7 +1452,7 @@ static int make_geo(const rwb_geometry_t* geom, Geo* g) {
 
 
 enum { L_Y, L_R, L_P0, L_P1, L_Q, L_WX, L_WY, L_WZ, L_SC, L_RR, L_PQ, L_BB, L_STATE, L_ITERS, L_UNK, L_TICKET,
-       L_ALIST, L_PART, L_MISC, L_N };
+       L_ALIST, L_PART, L_MISC, L_MG, L_N };
 
 struct Layout {
   size_t off[L_N];
@@ -1467,7 +1467,9 @@ static Layout layout(const Geo& g, long long nb) {
                              nb * sizeof(int), nb * sizeof(int), nb * sizeof(unsigned), nb * sizeof(unsigned), nb * sizeof(int),
                              std::max((size_t)nb * std::max(g.tiles, setup_tiles(g)) * sizeof(float2),
                                       (size_t)2 * kCoopMaxBlocks * sizeof(float)),
-                             128};
+                             128,
+                             // whole-level geometry: the multigrid solver's vectors and aggregate levels
+                             (g.gz == 1 && g.gy == 1 && g.gx == 1) ? mg_workspace_bytes(g.bz, g.by, g.bx) : 0};
   size_t o = 0;
   for (int i = 0; i < L_N; ++i) {
     L.off[i] = o;
@@ -1781,7 +1783,7 @@ static int solve_level_impl(const rwb_geometry_t* geom, const float* intensity, 
   if (setup_only) return RWB_OK;
 
   if (resident) {
-    // every CG iteration of a brick on chip: one 8-CTA cluster per 32^3 brick
+    // every CG iteration of a brick on chip: one 4-CTA cluster per 32^3 brick (cluster=8/16: 8- or 16-CTA variants)
     ResidentArgs ra;
     ra.wx = w.wx;
     ra.wy = w.wy;
@@ -1826,6 +1828,61 @@ static int solve_level_impl(const rwb_geometry_t* geom, const float* intensity, 
     count_launches(2);
     if (stats) {
       rc = read_stats(w, nb, st, ev0, ev1, 0, RWB_PATH_RESIDENT, stats, -1.f, dev_stats);
+      if (rc) return rc;
+    }
+    cudaEventDestroy(ev0);
+    cudaEventDestroy(ev1);
+    return RWB_OK;
+  }
+
+  if (total == 1 && !(params->flags & RWB_SOLVE_NO_MG)) {
+    // whole-level solve: multigrid-preconditioned CG, all iterations in one cooperative launch
+    MgArgs ma;
+    std::memset(&ma, 0, sizeof(ma));
+    mg_carve(&ma, (char*)workspace + L.off[L_MG], g.bz, g.by, g.bx);
+    ma.nz = g.bz, ma.ny = g.by, ma.nx = g.bx;
+    ma.wx = w.wx;
+    ma.wy = w.wy;
+    ma.wz = w.wz;
+    ma.sc = w.sc;
+    ma.y = w.y;
+    ma.r[0] = w.r;
+    ma.r[1] = w.p1;
+    ma.p = w.p0;
+    ma.q = w.q;
+    ma.bb = w.bb;
+    ma.rr0 = w.rr;
+    ma.state = w.state;
+    ma.iters = w.iters;
+    ma.tol2 = tol2;
+    ma.max_iter = max_iter;
+    ma.omega = 0.8f;
+    ma.bottom_sweeps = 8;  // an exact (dense-inverse) bottom solve was tried: no fewer iterations
+    ma.intensity = intensity;
+    ma.seeds = seeds;
+    ma.beta = params->beta;
+    ma.min_weight = params->min_weight;
+    ma.trace = mg_trace_buffer();
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    RWB_CUDA(cudaEventCreate(&ev0));
+    RWB_CUDA(cudaEventCreate(&ev1));
+    RWB_CUDA(cudaEventRecord(ev0, st));
+    stamp_kernel<<<1, 1, 0, st>>>(w.stamp);
+    rc = launch_mgcg(ma, st);
+    if (rc) {
+      cudaEventDestroy(ev0);
+      cudaEventDestroy(ev1);
+      return rc;
+    }
+    stamp_kernel<<<1, 1, 0, st>>>(w.stamp + 1);
+    count_launches(2);
+    RWB_CUDA(cudaEventRecord(ev1, st));
+    epilogue_kernel<<<sgrid, block, 0, st>>>(g, w, list, prob, labels);
+    stats_kernel<<<1, 1024, 0, st>>>(w, nb);
+    RWB_LAUNCH_CHECK("multigrid solve");
+    count_launches(2);
+    if (stats) {
+      rc = read_stats(w, nb, st, ev0, ev1, 0, RWB_PATH_MULTIGRID, stats, -1.f, dev_stats);
       if (rc) return rc;
     }
     cudaEventDestroy(ev0);
