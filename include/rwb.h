@@ -167,6 +167,10 @@ int rwb_labels_u8(int64_t n, const float* prob, uint8_t* labels, void* stream);
  * rounded to f32.
  * dst has size ceil(size/2); ndim 1..3. */
 int rwb_downsample_mean_f32(int32_t ndim, const int64_t* size, const float* src, float* dst, void* stream);
+/* The same over a subset of the dimensions (downsample_mean(input, dims), ops.py:611-616): bit d of
+ * dims_mask selects dimension d; unselected dimensions keep their size (dst[d] = size[d]). */
+int rwb_downsample_mean_dims_f32(int32_t ndim, const int64_t* size, uint32_t dims_mask, const float* src, float* dst,
+                                 void* stream);
 
 /* Chunk payloads <-> dense tensor, for chunked tensor files (PLCT,
  * tensorfile.py:1-13).  A payload is the full chunk box (chunk[0..ndim)),

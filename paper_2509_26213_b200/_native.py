@@ -48,6 +48,8 @@ SIGNATURES = {
                                        c_void_p, c_void_p]),
     "rwb_labels_u8": (c_int32, [c_int64, c_void_p, c_void_p, c_void_p]),
     "rwb_downsample_mean_f32": (c_int32, [c_int32, ctypes.POINTER(c_int64), c_void_p, c_void_p, c_void_p]),
+    "rwb_downsample_mean_dims_f32": (c_int32, [c_int32, ctypes.POINTER(c_int64), ctypes.c_uint32, c_void_p, c_void_p,
+                                               c_void_p]),
     "rwb_chunks_scatter": (c_int32, [c_int32, ctypes.POINTER(c_int64), ctypes.POINTER(c_int64), c_int32, c_void_p,
                                      c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "rwb_const_chunk_table": (c_int32, [c_int32, ctypes.POINTER(c_int64), ctypes.POINTER(c_int64), c_int32, c_void_p,

@@ -126,18 +126,20 @@ int run_chunks(int32_t ndim, const int64_t* size, const int64_t* chunk, int32_t 
 
 // f32(pairwise means along z, then y, then x) of each 2^d block, a trailing odd
 // element passing through (downsample_mean / _pairwise_mean, ops.py:611-676;
-// float64 arithmetic: assemble_region hands the means float64 blocks, ops.py:426-464)
+// float64 arithmetic: assemble_region hands the means float64 blocks, ops.py:426-464).
+// sel[k] = 0: dimension k is not downsampled (downsample_mean(dims=...), ops.py:614-616).
 __global__ void __launch_bounds__(256) downsample_mean_kernel(const float* __restrict__ src, long long fz, long long fy,
                                                               long long fx, float* __restrict__ dst, long long cz,
-                                                              long long cy, long long cx) {
+                                                              long long cy, long long cx, int sz, int sy, int sx) {
   const long long n = cz * cy * cx;
   for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < n; o += (long long)gridDim.x * blockDim.x) {
     const long long jx = o % cx, jy = (o / cx) % cy, jz = o / (cx * cy);
-    const int nz = (2 * jz + 1 < fz) ? 2 : 1, ny = (2 * jy + 1 < fy) ? 2 : 1, nx = (2 * jx + 1 < fx) ? 2 : 1;
+    const long long bz = sz ? 2 * jz : jz, by = sy ? 2 * jy : jy, bx = sx ? 2 * jx : jx;
+    const int nz = (sz && bz + 1 < fz) ? 2 : 1, ny = (sy && by + 1 < fy) ? 2 : 1, nx = (sx && bx + 1 < fx) ? 2 : 1;
     double v[2][2][2];
     for (int a = 0; a < nz; ++a)
       for (int b = 0; b < ny; ++b)
-        for (int c = 0; c < nx; ++c) v[a][b][c] = src[((2 * jz + a) * fy + (2 * jy + b)) * fx + (2 * jx + c)];
+        for (int c = 0; c < nx; ++c) v[a][b][c] = src[((bz + a) * fy + (by + b)) * fx + (bx + c)];
     double m1[2][2], m2[2];
     for (int b = 0; b < ny; ++b)
       for (int c = 0; c < nx; ++c) m1[b][c] = nz == 2 ? __dmul_rn(__dadd_rn(v[0][b][c], v[1][b][c]), 0.5) : v[0][b][c];
@@ -163,23 +165,31 @@ extern "C" int rwb_chunks_gather(int32_t ndim, const int64_t* size, const int64_
                                const_cast<void*>(dense), stream);
 }
 
-extern "C" int rwb_downsample_mean_f32(int32_t ndim, const int64_t* size, const float* src, float* dst,
-                                       void* stream) {
+extern "C" int rwb_downsample_mean_dims_f32(int32_t ndim, const int64_t* size, uint32_t dims_mask, const float* src,
+                                            float* dst, void* stream) {
   if (ndim < 1 || ndim > 3 || !size || !src || !dst) return rwb::fail(RWB_ERR_INVALID, "downsample_mean: bad arguments");
+  if (dims_mask >> ndim) return rwb::fail(RWB_ERR_INVALID, "downsample_mean: dims outside the tensor");
   long long f[3] = {1, 1, 1};
+  int sel[3] = {0, 0, 0};
   for (int d = 0; d < ndim; ++d) {
     if (size[d] < 1) return rwb::fail(RWB_ERR_INVALID, "downsample_mean: sizes must be positive");
     f[3 - ndim + d] = size[d];
+    sel[3 - ndim + d] = (dims_mask >> d) & 1;
   }
-  // unit leading dims stay 1 (ceil(1/2) = 1), matching a (ndim)-dim downsample_mean
-  const long long c[3] = {(f[0] + 1) / 2, (f[1] + 1) / 2, (f[2] + 1) / 2};
+  // unselected (and unit leading) dims keep their size
+  const long long c[3] = {sel[0] ? (f[0] + 1) / 2 : f[0], sel[1] ? (f[1] + 1) / 2 : f[1], sel[2] ? (f[2] + 1) / 2 : f[2]};
   const long long n = c[0] * c[1] * c[2];
   const long long blocks = (n + 255) / 256;
   rwb::downsample_mean_kernel<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, (cudaStream_t)stream>>>(
-      src, f[0], f[1], f[2], dst, c[0], c[1], c[2]);
+      src, f[0], f[1], f[2], dst, c[0], c[1], c[2], sel[0], sel[1], sel[2]);
   RWB_LAUNCH_CHECK("downsample_mean_kernel");
   rwb::count_launches(1);
   return RWB_OK;
+}
+
+extern "C" int rwb_downsample_mean_f32(int32_t ndim, const int64_t* size, const float* src, float* dst,
+                                       void* stream) {
+  return rwb_downsample_mean_dims_f32(ndim, size, ndim >= 1 && ndim <= 3 ? (1u << ndim) - 1u : 0u, src, dst, stream);
 }
 
 // ---------------------------------------------------------------------------

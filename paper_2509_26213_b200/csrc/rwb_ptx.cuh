@@ -42,6 +42,12 @@ __device__ __forceinline__ void st_async_f32(uint32_t remote, float v, uint32_t 
                : "memory");
 }
 
+__device__ __forceinline__ void st_async_f64(uint32_t remote, double v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(remote),
+               "l"(__double_as_longlong(v)), "r"(remote_bar)
+               : "memory");
+}
+
 __device__ __forceinline__ void st_async_v4(uint32_t remote, float4 v, uint32_t remote_bar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
                    remote),

@@ -62,14 +62,21 @@ def lod_down(level: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def downsample_mean(level: torch.Tensor) -> torch.Tensor:
+def downsample_mean(level: torch.Tensor, dims=None) -> torch.Tensor:
     """Factor-2 mean downsampling alone (the reference's build_lod(smooth=False) step,
-    `downsample_mean`, ops.py:611-676; float64 pairwise means rounded to f32, bit-identical)."""
+    `downsample_mean`, ops.py:611-676; float64 pairwise means rounded to f32, bit-identical).
+    `dims`: the dimensions to halve (default all), as `downsample_mean(input, dims)`."""
     _check_tensor(level, torch.float32, "level", (1, 2, 3))
+    nd = level.dim()
+    sel = tuple(range(nd)) if dims is None else tuple(sorted({int(d) for d in dims}))
+    if any(d < 0 or d >= nd for d in sel):
+        raise ValueError(f"dims {dims} outside a {nd}-d level")
     lib = _native.lib()
-    out = torch.empty(coarse_shape(level.shape), dtype=torch.float32, device=level.device)
-    _native.check(lib.rwb_downsample_mean_f32(level.dim(), _native.int64_array(level.shape), _ptr(level), _ptr(out),
-                                              _stream_handle()))
+    shape = [-(-s // 2) if d in sel else s for d, s in enumerate(level.shape)]
+    out = torch.empty(shape, dtype=torch.float32, device=level.device)
+    mask = sum(1 << d for d in sel)
+    _native.check(lib.rwb_downsample_mean_dims_f32(nd, _native.int64_array(level.shape), mask, _ptr(level),
+                                                   _ptr(out), _stream_handle()))
     return out
 
 

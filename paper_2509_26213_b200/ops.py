@@ -226,15 +226,55 @@ def lod_down(input_node):
         inputs=(input_node,), md=md, embedding=emb, dependencies=dependencies, kernel=kernel)
 
 
+def downsample_mean(input_node, dims=None):
+    """`chunkcast.ops.downsample_mean` on the GPU (`ops.py:611-676`): factor-2 mean over `dims`
+    (default all), ceil sizes, a trailing odd element passing through, spacing x2 on the halved
+    dimensions; float64 pairwise means rounded to f32, bit-identical to the reference."""
+    cc = _chunkcast()
+    _check_f32(input_node, "downsample_mean input")
+    md_in = input_node.md
+    d = md_in.num_dims
+    sel = tuple(range(d)) if dims is None else tuple(sorted(dims))
+    if any(not 0 <= k < d for k in sel):
+        raise _error(f"downsample_mean dims {dims} outside a {d}-d tensor")
+    size = tuple(-(-s // 2) if i in sel else s for i, s in enumerate(md_in.size))
+    md = cc.model.TensorMetaData(size, md_in.chunk_size, md_in.element_type)
+    emb = None
+    if input_node.embedding is not None:
+        emb = cc.model.EmbeddingData(tuple(sp * 2 if i in sel else sp
+                                           for i, sp in enumerate(input_node.embedding.spacing)))
+
+    def src_window(h):
+        begin, end = md.chunk_logical_region(h)
+        lo = [2 * b if i in sel else b for i, b in enumerate(begin)]
+        hi = [min(2 * e, md_in.size[i]) if i in sel else e for i, e in enumerate(end)]
+        return lo, hi, begin, end
+
+    def dependencies(h):
+        lo, hi, _, _ = src_window(h)
+        return [_overlapping(md_in, lo, hi)]
+
+    def kernel(h, input_arrays, out):
+        from . import device
+
+        lo, hi, begin, end = src_window(h)
+        block = _gather(md_in, dict(zip(dependencies(h)[0], input_arrays[0])), lo, hi)
+        coarse = _from_dev(device.downsample_mean(_to_dev(block), sel))
+        _write_out(out, [e - b for b, e in zip(begin, end)], coarse)
+
+    return cc.graph.OperatorNode(
+        name="rwb.downsample_mean", params={"dims": [int(i) for i in sel]},
+        inputs=(input_node,), md=md, embedding=emb, dependencies=dependencies, kernel=kernel)
+
+
 def build_lod(input_node, embedding=None, smooth: bool = True, levels: int | None = None):
     """`chunkcast.ops.build_lod` with the fused GPU level step (`ops.py:714-727`).
 
     Same stop rule (halve until every dim fits one chunk) and the same level
-    values; `levels` optionally truncates the chain.
+    values: smooth=True chains the fused conv+mean `lod_down`, smooth=False the
+    plain 2x mean (`downsample_mean`); `levels` optionally truncates the chain.
     """
     cc = _chunkcast()
-    if not smooth:
-        raise _error("the GPU LOD path implements the smoothed pyramid only (smooth=True)")
     d = input_node.md.num_dims
     emb = embedding if embedding is not None else input_node.embedding
     if emb is None:
@@ -246,7 +286,7 @@ def build_lod(input_node, embedding=None, smooth: bool = True, levels: int | Non
     while any(s > c for s, c in zip(node.md.size, node.md.chunk_size)):
         if levels is not None and len(out) >= levels:
             break
-        node = lod_down(node)
+        node = lod_down(node) if smooth else downsample_mean(node)
         emb = cc.model.EmbeddingData(tuple(sp * 2 for sp in emb.spacing))
         out.append((node, emb))
     if levels is not None and len(out) < levels:
@@ -474,6 +514,49 @@ def hierarchical_random_walker(volume_node, seeds_node, levels: int | None = Non
     for k in range(n - 2, -1, -1):
         probs[k] = random_walker(vol_pyr.node(k), seeds[k], probs[k + 1], **kw)
     return cc.ops.LodPyramid(tuple((probs[k], vol_pyr.embedding(k)) for k in range(n)))
+
+
+def rasterize_seeds(fg_points, bg_points, md, radius: float = 0.0, embedding=None):
+    """U8 seed labels {0, 1, 2} as a source node: voxel g is foreground (1)
+    when ||g - p|| <= radius for a point p of `fg_points`, background (2) for `bg_points`, and
+    unseeded (0) when it is in both or neither (the conflict rule of the seed projection).
+    `md`: a reference `TensorMetaData` or a node whose metadata (size, chunking) the labels share.
+    Points are voxel coordinates (d floats).  Identity is content-addressed like
+    `source_from_array` (`ops.py:282-325`): equal point sets give equal operator ids.  Host-side
+    rasterisation of a handful of balls per chunk; any U8 label node serves as seeds just as well."""
+    cc = _chunkcast()
+    if hasattr(md, "md"):
+        md = md.md
+    d = md.num_dims
+    md = cc.model.TensorMetaData(tuple(md.size), tuple(md.chunk_size), cc.model.U8)
+    pts = []
+    for plist, what in ((fg_points, "fg_points"), (bg_points, "bg_points")):
+        a = np.asarray(plist, dtype=np.float64) if len(plist) else np.zeros((0, d))
+        if a.ndim != 2 or a.shape[1] != d:
+            raise _error(f"{what} must hold {d}-d coordinates")
+        pts.append(a)
+    r = float(radius)
+    if r < 0:
+        raise _error("radius must be non-negative")
+
+    def kernel(h, input_arrays, out):
+        begin, end = md.chunk_logical_region(h)
+        grids = np.meshgrid(*[np.arange(b, e, dtype=np.float64) for b, e in zip(begin, end)], indexing="ij")
+        hit = []
+        for a in pts:
+            m = np.zeros(grids[0].shape, bool)
+            for p in a:
+                if all(pk + r >= b and pk - r <= e - 1 for pk, b, e in zip(p, begin, end)):
+                    m |= sum((g - pk) ** 2 for g, pk in zip(grids, p)) <= r * r
+            hit.append(m)
+        lab = np.where(hit[0] & ~hit[1], 1, np.where(hit[1] & ~hit[0], 2, 0)).astype(np.uint8)
+        _write_out(out, [e - b for b, e in zip(begin, end)], lab)
+
+    return cc.graph.OperatorNode(
+        name="rwb.rasterize_seeds",
+        params={"fg": [[float(x) for x in p] for p in pts[0]], "bg": [[float(x) for x in p] for p in pts[1]],
+                "radius": r, "size": [int(s) for s in md.size], "chunk": [int(c) for c in md.chunk_size]},
+        inputs=(), md=md, embedding=embedding, dependencies=lambda h: [], kernel=kernel)
 
 
 def rw_labels(prob_node):

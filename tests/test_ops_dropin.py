@@ -91,7 +91,22 @@ def test_type_errors_raise_operator_error():
     with pytest.raises(cc.ops.OperatorError):
         rwops.rw_weights(u8)
     with pytest.raises(cc.ops.OperatorError):
-        rwops.build_lod(f32, smooth=False)
+        rwops.downsample_mean(u8)
+    with pytest.raises(cc.ops.OperatorError):
+        rwops.downsample_mean(f32, dims=(2,))
+
+
+def test_unsmoothed_pyramid_and_dims_metadata_match_reference():
+    src = cc.ops.source_from_array(np.zeros((100, 70, 40), np.float32), (16, 16, 16), embedding=(0.5, 1.0, 2.0))
+    ref = cc.ops.build_lod(src, smooth=False)
+    ours = rwops.build_lod(src, smooth=False)
+    assert ours.num_levels == ref.num_levels
+    for k in range(ref.num_levels):
+        assert ours.node(k).md == ref.node(k).md and ours.embedding(k) == ref.embedding(k)
+    for dims in [(0,), (1, 2), None]:
+        r, o = cc.ops.downsample_mean(src, dims), rwops.downsample_mean(src, dims)
+        assert o.md == r.md and o.embedding == r.embedding
+        assert o.dependencies((1, 1, 0)) == r.dependencies((1, 1, 0))
 
 
 # -- through the reference Engine (GPU) ------------------------------------------------
@@ -113,6 +128,23 @@ def test_engine_resolves_lod_bit_exact(name):
     with _engine() as eng:
         for k in range(1, pyr.num_levels):
             np.testing.assert_array_equal(_dense(eng, pyr.node(k)), g[f"{name}/level{k}"])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,chunk", [((37, 50, 23), (16, 16, 16)), ((99, 70), (32, 16))])
+def test_engine_unsmoothed_pyramid_and_dims_bit_exact(shape, chunk):
+    """build_lod(smooth=False) and downsample_mean(dims=...) through the reference Engine equal the
+    reference's own numpy operators resolved by the same Engine, byte for byte (ops.py:611-727)."""
+    x = np.random.default_rng(7).normal(0.3, 0.2, shape).astype(np.float32)
+    src = cc.ops.source_from_array(x, chunk)
+    ref, ours = cc.ops.build_lod(src, smooth=False), rwops.build_lod(src, smooth=False)
+    assert ours.num_levels == ref.num_levels > 1
+    with _engine() as eng:
+        for k in range(1, ref.num_levels):
+            np.testing.assert_array_equal(_dense(eng, ours.node(k)), _dense(eng, ref.node(k)))
+        for dims in [(0,), (len(shape) - 1,)]:
+            np.testing.assert_array_equal(_dense(eng, rwops.downsample_mean(src, dims)),
+                                          _dense(eng, cc.ops.downsample_mean(src, dims)))
 
 
 @pytest.mark.gpu
@@ -195,3 +227,26 @@ def test_engine_pull_is_lazy():
         # only the parent chunks under the dilated footprint of brick (0,0,0)
         assert eng.stats.requested_positions(pyr.node(0), pyr.node(1)) == {(0, 0, 0)}
         assert eng.stats.computed(pyr.node(0)) == 1
+
+
+def test_rasterize_seeds_balls_and_conflicts():
+    src = cc.ops.source_from_array(np.zeros((20, 24, 18), np.float32), (8, 8, 8))
+    node = rwops.rasterize_seeds([(5, 6, 7), (15, 20, 3)], [(5, 8, 7), (0, 0, 0)], src, radius=2.0)
+    assert node.md.element_type == cc.model.U8 and node.md.size == src.md.size
+    with cc.engine.Engine(cc.engine.EngineConfig(stores=cc.store.StoreConfig(ram_capacity=1 << 26))) as eng:
+        got = _dense(eng, node)
+    g = np.stack(np.meshgrid(*[np.arange(n) for n in src.md.size], indexing="ij"), -1).astype(float)
+
+    def ball(p):
+        return ((g - np.array(p)) ** 2).sum(-1) <= 4.0
+
+    fg = ball((5, 6, 7)) | ball((15, 20, 3))
+    bg = ball((5, 8, 7)) | ball((0, 0, 0))
+    want = np.where(fg & ~bg, 1, np.where(bg & ~fg, 2, 0)).astype(np.uint8)
+    np.testing.assert_array_equal(got, want)
+    assert (want == 0)[fg & bg].all() and (fg & bg).any()
+    same = rwops.rasterize_seeds([(5, 6, 7), (15, 20, 3)], [(5, 8, 7), (0, 0, 0)], src, radius=2.0)
+    assert same.op_id == node.op_id
+    assert rwops.rasterize_seeds([(5, 6, 7)], [], src).op_id != node.op_id
+    with pytest.raises(cc.ops.OperatorError):
+        rwops.rasterize_seeds([(1, 2)], [], src)
