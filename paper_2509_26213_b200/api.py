@@ -54,7 +54,7 @@ def segment(volume, seeds, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWCo
 
 def segment_many(inputs, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConfig(), *, outputs=None,
                  workspace: device.Workspace | None = None, level0_chunks: int | None = None, pyramid_store=None,
-                 pyramid_keys=None, cyclic_outputs: bool = False):
+                 pyramid_keys=None, cyclic_outputs: bool = False, store=None, input_ids=None):
     """Segment a sequence of host volumes with the transfers overlapped.
 
     `inputs`: list of (volume, seeds) host tensors of one shape (pinned for
@@ -70,6 +70,12 @@ def segment_many(inputs, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConf
     solved in `level0_chunks` slabs whose rows download while the next slab
     solves, so even the last volume's download mostly overlaps its compute.  Returns the
     list of (prob, labels) host tensors, complete when the call returns.
+
+    `store` (a store.DeviceStore): the device copies of the inputs live in the store's HBM arena
+    under its budget instead of a private double buffer — one entry per input (volume bytes then
+    seed bytes, key `input_ids[i]`), reserved and uploaded one volume ahead, pinned while
+    segmented, then retired on the compute stream, so the LRU / epoch GC recycles them once their
+    work has run.  Inputs already resident (same id) are not uploaded again.
     """
     n = len(inputs)
     if n == 0:
@@ -81,8 +87,17 @@ def segment_many(inputs, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConf
     up.wait_stream(comp)
     down.wait_stream(comp)
     shape = tuple(inputs[0][0].shape)
-    vol_d = [torch.empty(shape, dtype=torch.float32, device=dev) for _ in range(min(n, 2))]
-    sd_d = [torch.empty(shape, dtype=torch.uint8, device=dev) for _ in range(min(n, 2))]
+    nvox = 1
+    for d in shape:
+        nvox *= int(d)
+    if store is None:
+        vol_d = [torch.empty(shape, dtype=torch.float32, device=dev) for _ in range(min(n, 2))]
+        sd_d = [torch.empty(shape, dtype=torch.uint8, device=dev) for _ in range(min(n, 2))]
+    else:
+        vol_d, sd_d = [None] * n, [None] * n
+        held = [None] * n  # pinned store entries
+        if input_ids is None:
+            input_ids = [("segment_many", id(v), id(sd), i) for i, (v, sd) in enumerate(inputs)]
     if outputs is None:
         outputs = [(torch.empty(shape, dtype=torch.float32, pin_memory=True),
                     torch.empty(shape, dtype=torch.uint8, pin_memory=True)) for _ in range(n)]
@@ -93,6 +108,8 @@ def segment_many(inputs, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConf
     computed = []
 
     def upload(i):
+        if store is not None:
+            return upload_to_store(i)
         b = i % 2
         with torch.cuda.stream(up):
             if i >= 2:
@@ -104,13 +121,38 @@ def segment_many(inputs, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConf
             ev.record(up)
         return ev
 
+    def upload_to_store(i):
+        from .store import ChunkState
+
+        got = store.get(input_ids[i], torch.uint8, (5 * nvox,))
+        if got is not None:  # resident: no transfer
+            e, payload = got
+            ev = None
+        else:
+            e = store.reserve(input_ids[i], 5 * nvox)  # may evict retired inputs (their work has run)
+            payload = e.payload
+            with torch.cuda.stream(up):
+                v, s = inputs[i]
+                payload[: 4 * nvox].view(torch.float32).view(shape).copy_(_as_host_tensor(v, np.float32),
+                                                                         non_blocking=True)
+                payload[4 * nvox:].view(shape).copy_(_as_host_tensor(s, np.uint8), non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(up)
+            e.state = ChunkState.FINAL
+        held[i] = e
+        vol_d[i] = payload[: 4 * nvox].view(torch.float32).view(shape)
+        sd_d[i] = payload[4 * nvox:].view(shape)
+        return ev
+
     uploaded = [upload(0)]
     results = []
     for i in range(n):
         if i + 1 < n:
             uploaded.append(upload(i + 1))
-        comp.wait_event(uploaded[i])
+        if uploaded[i] is not None:
+            comp.wait_event(uploaded[i])
         out_p, out_l = outputs[i % len(outputs)]
+        slot = i if store is not None else i % 2
 
         def download(r0, r1, prob, labels, out_p=out_p, out_l=out_l):
             # level-0 rows [r0, r1) are final at this point of the compute stream:
@@ -124,7 +166,7 @@ def segment_many(inputs, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConf
                 prob.record_stream(down)
                 labels.record_stream(down)
 
-        device.hierarchical_random_walker(vol_d[i % 2], sd_d[i % 2], brick, levels, cfg, workspace=workspace,
+        device.hierarchical_random_walker(vol_d[slot], sd_d[slot], brick, levels, cfg, workspace=workspace,
                                           level0_chunks=level0_chunks, on_level0_chunk=download,
                                           pyramid_store=pyramid_store,
                                           pyramid_key=pyramid_keys[i] if pyramid_keys is not None else None)
@@ -132,6 +174,9 @@ def segment_many(inputs, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConf
         ev.record(comp)
         computed.append(ev)
         results.append((out_p, out_l))
+        if store is not None:  # collectable once this volume's work has run
+            store.retire(held[i], comp)
+            held[i] = vol_d[i] = sd_d[i] = None
     comp.wait_stream(down)
     comp.wait_stream(up)
     comp.synchronize()
@@ -139,7 +184,7 @@ def segment_many(inputs, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConf
 
 
 def segment_series(volume, seeds, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConfig(), *,
-                   outputs=None, workspace: device.Workspace | None = None):
+                   outputs=None, workspace: device.Workspace | None = None, store=None, series_id=None):
     """Per-timestep hierarchical random walker of a 4-D (T, Z, Y, X) host series.
 
     The reference's 4-D → 3-D `slice_node` view (`ops.py:555-586`), one
@@ -147,7 +192,11 @@ def segment_series(volume, seeds, brick=(32, 32, 32), levels=None, cfg: RWConfig
     `segment_many` (upload of t+1 and download of t-1 overlapped with t), so
     only two timesteps are ever resident on the device — the series may be far
     larger than HBM.  Returns (prob, labels) host tensors of shape (T, ...);
-    `outputs` = (prob, labels) pinned 4-D buffers to write into.
+    `outputs` = (prob, labels) pinned 4-D buffers to write into.  With `store`
+    (a store.DeviceStore whose budget may be far below the series) the timesteps
+    stream through the store's arena as entries (series_id, t): evicted LRU-first
+    once segmented, still resident — and not uploaded again — on a later call
+    while the budget holds them.
     """
     vol = _as_host_tensor(volume, np.float32)
     sd = _as_host_tensor(seeds, np.uint8)
@@ -158,6 +207,8 @@ def segment_series(volume, seeds, brick=(32, 32, 32), levels=None, cfg: RWConfig
                    torch.empty(tuple(vol.shape), dtype=torch.uint8, pin_memory=True))
     prob, labels = outputs
     n = vol.shape[0]
+    sid = series_id if series_id is not None else ("series", vol.data_ptr(), sd.data_ptr(), tuple(vol.shape))
     segment_many([(vol[t], sd[t]) for t in range(n)], brick, levels, cfg,
-                 outputs=[(prob[t], labels[t]) for t in range(n)], workspace=workspace)
+                 outputs=[(prob[t], labels[t]) for t in range(n)], workspace=workspace, store=store,
+                 input_ids=[(sid, t) for t in range(n)] if store is not None else None)
     return prob, labels
