@@ -149,6 +149,29 @@ def upsample(parent: torch.Tensor, fine_shape, out: torch.Tensor | None = None) 
     return out
 
 
+def upsample_planes(parent: torch.Tensor, parent_z0: int, fine_shape, g0: int, g1: int, out: torch.Tensor,
+                    out_z0: int = 0) -> torch.Tensor:
+    """Fine planes [g0, g1) (dim 0, global indices) of a level of global shape `fine_shape`, from a
+    parent window: `parent` holds the parent level's global planes [parent_z0, parent_z0 +
+    parent.shape[0]) and must cover their prolongation taps (sharding.parent_planes).  `out`
+    holds the fine global planes [out_z0, out_z0 + out.shape[0]).  Same values as `upsample`."""
+    _check_tensor(parent, torch.float32, "parent", (2, 3))
+    _check_tensor(out, torch.float32, "out")
+    fine_shape = tuple(int(s) for s in fine_shape)
+    if g1 <= g0:
+        return out
+    if g0 < out_z0 or g1 > out_z0 + out.shape[0] or tuple(out.shape[1:]) != fine_shape[1:]:
+        raise ValueError("out does not hold the requested planes")
+    nd = parent.dim()
+    psize = coarse_shape(fine_shape)
+    a64 = _native.int64_array
+    view = out[g0 - out_z0:g1 - out_z0]
+    _native.check(_native.lib().rwb_upsample_window_f32(
+        nd, a64(psize), a64([parent_z0] + [0] * (nd - 1)), a64(parent.shape), _ptr(parent), a64(fine_shape),
+        a64([g0] + [0] * (nd - 1)), a64([g1 - g0] + list(fine_shape[1:])), _ptr(view), _stream_handle()))
+    return out
+
+
 def upsample_window(parent: torch.Tensor, fine_shape, z0: int, z1: int, out: torch.Tensor) -> torch.Tensor:
     """Upsample only planes [z0, z1) (dim 0) of the fine level into `out` (full fine shape)."""
     _check_tensor(parent, torch.float32, "parent", (2, 3))
@@ -351,33 +374,48 @@ def _merge_stats(parts):
     return out
 
 
-def _solve_level_chunked(volume, seeds, brick, parent, cfg, labels_out, workspace, chunks, on_chunk):
+def _solve_level_chunked(volume, seeds, brick, parent, cfg, labels_out, workspace, chunks, on_chunk, *,
+                         z0: int = 0, fine_shape=None, parent_z0: int = 0, origin_z: int = 0, n_rows=None):
     """One level solved as `chunks` slabs of whole brick rows along dim 0, in order,
     all into the same output; `on_chunk(r0, r1, prob, labels)` is called after each slab's
     launches are queued (its rows [r0, r1) are final once the stream reaches
     that point), e.g. to queue the slab's download while the next one solves.  The
     bound (the upsampled `parent` level) is produced slab by slab (the slab's planes
-    plus their one-plane halo), just before the slab's setup."""
-    grid = brick_grid(volume.shape, brick)
+    plus their one-plane halo), just before the slab's setup.
+
+    Slab-local use (sharding.py): `volume` / `seeds` hold the global planes [z0, z0 + nz) of a
+    level of global shape `fine_shape`, the solved brick rows start at local plane `origin_z`
+    (the planes before it are Dirichlet halo) and `n_rows` of them are solved; `parent` holds the
+    parent level's global planes from `parent_z0` on.  Defaults: the whole level."""
+    fine_shape = tuple(volume.shape) if fine_shape is None else tuple(int(x) for x in fine_shape)
+    # the ABI's brick grid origin lies in (-brick, 0]: a halo plane before the first solved row is
+    # the tail of a brick row 0 that is not listed
+    if not 0 <= origin_z < brick[0]:
+        raise ValueError("origin_z must lie in [0, brick)")
+    row0 = 1 if origin_z > 0 else 0
+    origin = (origin_z - brick[0] if origin_z > 0 else 0,) + (0,) * (volume.dim() - 1)
+    grid = brick_grid(volume.shape, brick, origin)
     per_row = math.prod(grid[1:])
-    rows = grid[0]
+    rows = grid[0] - row0 if n_rows is None else int(n_rows)
     chunks = max(1, min(chunks, rows))
     out = torch.empty(volume.shape, dtype=torch.float32, device=volume.device)
     parts = []
     bounds = [(rows * c // chunks, rows * (c + 1) // chunks) for c in range(chunks)]
-    lists = [torch.arange(h0 * per_row, h1 * per_row, dtype=torch.int32, device=volume.device) for h0, h1 in bounds]
-    rows_of = [(h0 * brick[0], min(h1 * brick[0], volume.shape[0])) for h0, h1 in bounds]
+    lists = [torch.arange((row0 + h0) * per_row, (row0 + h1) * per_row, dtype=torch.int32, device=volume.device)
+             for h0, h1 in bounds]
+    rows_of = [(origin_z + h0 * brick[0], min(origin_z + h1 * brick[0], volume.shape[0])) for h0, h1 in bounds]
     bound = torch.empty(volume.shape, dtype=torch.float32, device=volume.device)
+    nz = volume.shape[0]
 
     def upsample_slab(c):  # the slab's planes + one-plane halo (identical bytes where slabs overlap)
         r0, r1 = rows_of[c]
-        upsample_window(parent, volume.shape, max(r0 - 1, 0), min(r1 + 1, volume.shape[0]), bound)
+        upsample_planes(parent, parent_z0, fine_shape, z0 + max(r0 - 1, 0), z0 + min(r1 + 1, nz), bound, z0)
 
     if not (cfg.resident and _resident_geometry(volume.shape, brick)):
         for c in range(chunks):
             upsample_slab(c)
             _, st = solve_level(volume, seeds, brick, bound, cfg, brick_list=lists[c], out=out, labels_out=labels_out,
-                                workspace=workspace, stats_on_device=True)
+                                workspace=workspace, origin=origin, stats_on_device=True)
             parts.append(st)
             if on_chunk is not None:
                 on_chunk(*rows_of[c], out, labels_out)
@@ -399,7 +437,7 @@ def _solve_level_chunked(volume, seeds, brick, parent, cfg, labels_out, workspac
             if done[c % 2] is not None:
                 setup.wait_event(done[c % 2])
             solve_level(volume, seeds, brick, bound, cfg, brick_list=lists[c], out=out, labels_out=labels_out,
-                        workspace=spaces[c % 2], phase="setup")
+                        workspace=spaces[c % 2], origin=origin, phase="setup")
             ev = torch.cuda.Event()
             ev.record(setup)
         return ev
@@ -410,7 +448,7 @@ def _solve_level_chunked(volume, seeds, brick, parent, cfg, labels_out, workspac
         with torch.cuda.stream(solver):
             solver.wait_event(built)
             _, st = solve_level(volume, seeds, brick, bound, cfg, brick_list=lists[c], out=out, labels_out=labels_out,
-                                workspace=spaces[c % 2], phase="solve", stats_on_device=True)
+                                workspace=spaces[c % 2], origin=origin, phase="solve", stats_on_device=True)
             ev = torch.cuda.Event()
             ev.record(solver)
             done[c % 2] = ev
@@ -453,18 +491,13 @@ class HRWResult:
 
 def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick, levels: int | None = None,
                                cfg: RWConfig = RWConfig(), *, want_labels: bool = True,
-                               workspace: Workspace | None = None, brick_lists=None,
-                               exchange=None, upsample_planes=None, level0_chunks: int | None = None,
+                               workspace: Workspace | None = None, level0_chunks: int | None = None,
                                on_level0_chunk=None, pyramid_store=None, pyramid_key=None) -> HRWResult:
     """Coarse-to-fine random walker (oracle/rw.py: hierarchical_random_walker).
 
     The coarsest level is solved whole; each finer level is initialised and
     bounded by the upsampled solution of the level above and solved brick
-    by brick.  `brick_lists[k]` (int32 device tensor) restricts level k to a
-    subset of bricks (multi-GPU sharding) and `exchange(k, prob_k)` is called
-    after level k is solved so the caller can complete the halo of the
-    parent level before it is upsampled; `upsample_planes[k]` = (z0, z1)
-    limits the prolongation of level k to those planes (see sharding.py).
+    by brick (multi-GPU: sharding.hierarchical_random_walker_sharded).
     `level0_chunks` > 1 solves level 0 as that many slabs of brick rows (same
     results: bricks are independent; on brick-resident levels slab c+1's system
     is built while slab c solves; default: 8 slabs for levels of >= 4096 bricks,
@@ -496,34 +529,24 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
     if top == 0 and on_level0_chunk is not None:  # single-level hierarchy: level 0 is the whole-level solve
         on_level0_chunk(0, vols[0].shape[0], probs[0], top_labels)
     for k in range(top - 1, -1, -1):
-        if exchange is not None:
-            exchange(k + 1, probs[k + 1])
-        win = upsample_planes[k] if upsample_planes is not None else None
         if k == 0 and level0_chunks is None:  # measured: 8 slabs at 32768 bricks, 2 at 4096
             nb0 = math.prod(brick_grid(vols[0].shape, brick))
             level0_chunks = 8 if nb0 >= 16384 else (2 if nb0 >= 4096 else 1)
         # finer levels with many bricks are solved in slabs too (slab c+1's system is built while
         # slab c solves); only level 0 reports its slabs to on_level0_chunk
         nchunks = level0_chunks if k == 0 else (2 if math.prod(brick_grid(vols[k].shape, brick)) >= 4096 else 1)
-        slabbed = nchunks > 1 and win is None and brick_lists is None and _resident_geometry(vols[k].shape, brick)
-        if slabbed:
-            x = None  # upsampled slab by slab inside the chunked solve
-        elif win is None:
-            x = upsample(probs[k + 1], vols[k].shape)
-        else:  # sharded: only the planes this rank's bricks (+ halo) read
-            x = upsample_window(probs[k + 1], vols[k].shape, win[0], win[1],
-                                torch.empty(vols[k].shape, dtype=torch.float32, device=volume.device))
+        slabbed = nchunks > 1 and _resident_geometry(vols[k].shape, brick)
+        x = None if slabbed else upsample(probs[k + 1], vols[k].shape)  # slabbed: upsampled slab by slab
         lab_k = torch.empty(vols[k].shape, dtype=torch.uint8, device=volume.device) \
             if (want_labels and k == 0) else None
-        bl = brick_lists[k] if brick_lists is not None else None
         # separate output: the brick-resident solver reads neighbour bounds while
         # other bricks already write their results
         if slabbed:
             probs[k], stats[k] = _solve_level_chunked(vols[k], seed_levels[k], brick, probs[k + 1], cfg, lab_k,
                                                       workspace, nchunks, on_level0_chunk if k == 0 else None)
         else:
-            probs[k], stats[k] = solve_level(vols[k], seed_levels[k], brick, x, cfg, brick_list=bl,
-                                             labels_out=lab_k, workspace=workspace, stats_on_device=True)
+            probs[k], stats[k] = solve_level(vols[k], seed_levels[k], brick, x, cfg, labels_out=lab_k,
+                                             workspace=workspace, stats_on_device=True)
             if k == 0 and on_level0_chunk is not None:
                 on_level0_chunk(0, vols[0].shape[0], probs[0], lab_k)
         del x

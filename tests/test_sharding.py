@@ -1,7 +1,11 @@
-"""Host-side multi-GPU logic on CPU: shard plans, halo planes, and the halo
-exchange itself over a world_size-2 gloo process group."""
+"""Host-side multi-GPU logic on CPU: the slab plan, work-balanced splits, plane redistribution
+and the whole sharded hierarchy over world_size-2 / 3 gloo process groups (the level operators
+swapped for the float64 oracle on CPU tensors, so exactly the host logic that runs on GPUs is
+exercised: LOD slabs with halos, the all-gathered coarsest level, the per-level splits, the
+point-to-point redistribution of volumes, seeds and parent planes, the stats reduction)."""
 
 import os
+import random
 import socket
 
 import numpy as np
@@ -45,40 +49,58 @@ def test_parent_planes_agree_with_oracle_upsample():
     np.testing.assert_array_equal(orw.upsample_linear(pert, fine_shape)[z0:z1], base)
 
 
-@pytest.mark.parametrize("world", [1, 2, 3, 8])
-def test_plan_partitions_every_level(world):
-    shape, brick, levels = (256, 96, 80), (32, 32, 32), 3
-    for rank in range(world):
-        plan = sharding.ShardPlan.build(shape, brick, levels, rank, world)
-        assert plan.shards[-1] is None
-        for k, sh in enumerate(plan.shards[:-1]):
-            grid = [-(-a // b) for a, b in zip(sh.shape, brick)]
-            allb = sorted(b for r in range(world) for b in sh.bricks[r])
-            assert allb == list(range(int(np.prod(grid))))
-            planes = [p for r in range(world) for p in range(*sh.planes[r])]
-            assert planes == list(range(sh.shape[0]))
-            # bricks of a rank lie inside its planes
-            bid, _ = orw.brick_ids(sh.shape, brick)
-            z0, z1 = sh.planes[rank]
-            owned = np.isin(bid, sh.bricks[rank])
-            zz = np.nonzero(owned.any(axis=(1, 2)))[0]
-            if len(zz):
-                assert zz.min() >= z0 and zz.max() < z1
+@pytest.mark.parametrize("world", [1, 2, 3, 8, 40])
+def test_lod_slabs_partition_every_level(world):
+    shape, brick, levels = (300, 40, 24), (32, 32, 32), 4
+    plan = sharding.ShardPlan.build(shape, brick, levels, 0, world)
+    for k, planes in enumerate(plan.lod):
+        n = plan.shapes[k][0]
+        cover = [z for a, b in planes for z in range(a, b)]
+        assert cover == list(range(n))  # contiguous, disjoint, complete, in rank order
+        if k > 0:  # coarse plane j lives with fine plane 2j
+            for (a, b), (fa, fb) in zip(planes, plan.lod[k - 1]):
+                assert all(fa <= 2 * j < fb for j in range(a, b))
+    assert all(a % 32 == 0 for a, _ in plan.lod[0])
 
 
-def test_halo_messages_cover_needs():
-    plan = sharding.ShardPlan.build((128, 64, 64), (16, 16, 16), 3, 0, 4)
-    for level in range(1, plan.levels):
-        msgs = sharding.halo_messages(plan, level)
-        for dst in range(plan.world):
-            n0, n1 = plan.needed_planes(level, dst)
-            have = set(range(*plan.owned_planes(level, dst)))
-            for src, d, a, b in msgs:
-                if d == dst:
-                    assert src != dst
-                    have.update(range(a, b))
-            assert set(range(n0, n1)) <= have
-    assert sharding.halo_messages(plan, plan.levels - 1) == []
+def test_split_by_weight_is_contiguous_and_balanced():
+    rnd = random.Random(5)
+    for _ in range(300):
+        n, world = rnd.randint(1, 60), rnd.randint(1, 9)
+        w = [rnd.choice([0.0, 0.1, 1.0, 5.0, 40.0]) * rnd.random() for _ in range(n)]
+        parts = sharding.split_by_weight(w, world)
+        assert len(parts) == world and parts[0][0] == 0 and parts[-1][1] == n
+        assert all(a <= b for a, b in parts) and all(p[1] == q[0] for p, q in zip(parts, parts[1:]))
+        total = sum(w)
+        if total > 0:  # no rank exceeds its share by more than one row's weight
+            assert max(sum(w[a:b]) for a, b in parts) <= total / world + max(w) + 1e-9
+    # heavy rows in the middle pull the cuts towards them
+    w = [1.0] * 16 + [100.0] * 4 + [1.0] * 16
+    parts = sharding.split_by_weight(w, 4)
+    assert [b - a for a, b in parts] != [9, 9, 9, 9] and all(sum(w[a:b]) <= 120 for a, b in parts)
+
+
+def test_messages_cover_needs_once():
+    rnd = random.Random(2)
+    for _ in range(500):
+        n, world = rnd.randint(1, 50), rnd.randint(1, 6)
+        cuts = sorted(rnd.randint(0, n) for _ in range(world - 1))
+        have = list(zip([0] + cuts, cuts + [n]))
+        if rnd.random() < 0.2:  # replicated
+            have = [(0, n)] * world
+        need = []
+        for _ in range(world):
+            a = rnd.randint(0, n)
+            need.append((a, rnd.randint(a, n)))
+        got = {d: [] for d in range(world)}
+        for src, dst, a, b in sharding.messages(have, need):
+            assert src != dst and have[src][0] <= a < b <= have[src][1]
+            got[dst].append((a, b))
+        for d in range(world):
+            planes = [z for a, b in got[d] for z in range(a, b)]
+            own = set(range(*have[d]))
+            assert len(planes) == len(set(planes)) and not (set(planes) & own)  # each plane once
+            assert set(range(*need[d])) <= own | set(planes)
 
 
 def _free_port():
@@ -87,49 +109,54 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _exchange_worker(rank, world, port, q):
+def _spawn(target, world, *args):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=target, args=(r, world, port, q) + args) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(p.exitcode == 0 for p in procs)
+    return got
+
+
+def _redistribute_worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        shape, brick, levels = (64, 8, 8), (8, 8, 8), 3
-        plan = sharding.ShardPlan.build(shape, brick, levels, rank, world)
-        ok = True
-        for level in range(1, levels - 1):
-            n = sharding.level_shapes(shape, levels)[level]
-            truth = torch.arange(int(np.prod(n)), dtype=torch.float32).reshape(n)
-            prob = torch.full(n, float("nan"))
-            o0, o1 = plan.owned_planes(level, rank)
-            prob[o0:o1] = truth[o0:o1]
-            sharding.exchange_halo(plan, level, prob)
-            a, b = plan.needed_planes(level, rank)
-            ok &= bool(torch.equal(prob[a:b], truth[a:b]))
-        q.put((rank, ok))
+        n = 23
+        truth = torch.arange(n * 6, dtype=torch.float64).reshape(n, 2, 3)
+        have = [(0, 9), (9, 9), (9, 23)][:world] if world == 3 else [(0, 12), (12, 23)]
+        need = [(5, 23), (0, 23), (8, 10)][:world] if world == 3 else [(10, 23), (0, 14)]
+        a, b = have[rank]
+        out = sharding.redistribute(truth[a:b].clone(), have, need, rank)
+        c, d = need[rank]
+        q.put((rank, bool(torch.equal(out, truth[c:d]))))
     finally:
         dist.destroy_process_group()
 
 
-def test_halo_exchange_gloo_world2():
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_exchange_worker, args=(r, 2, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    for p in procs:
-        p.join(timeout=120)
-    results = dict(q.get(timeout=5) for _ in procs)
-    assert results == {0: True, 1: True}
-    assert all(p.exitcode == 0 for p in procs)
+@pytest.mark.parametrize("world", [2, 3])
+def test_redistribute_gloo(world):
+    assert all(ok for _, ok in _spawn(_redistribute_worker, world))
 
 
-# -- the sharded hierarchical driver end to end, world_size 2 over gloo -------------------
-# The level operators are swapped for the float64 oracle on CPU tensors, so the
-# test exercises exactly the host logic that runs on GPUs: the shard plan, the
-# per-level brick lists, and the point-to-point halo exchange of parent planes.
+# -- the sharded hierarchical driver end to end over gloo, oracle level operators ----------
+
 
 def _install_oracle_backend():
     from oracle import lod as olod
     from paper_2509_26213_b200 import device
+
+    zero = {k: 0 for k in ("bricks", "converged", "not_converged", "zero_rhs", "iterations_sum", "unknowns",
+                           "unknown_iterations", "iterations_max", "sweeps", "path")}
+    zero["cg_ms"] = 0.0
+
+    def params(cfg):
+        return orw.RWParams(beta=cfg.beta, min_weight=cfg.min_weight, tol=1e-10)
 
     def lod_down(level):
         return torch.from_numpy(olod.lod_down(level.numpy()))
@@ -137,40 +164,45 @@ def _install_oracle_backend():
     def project_seeds(seeds):
         return torch.from_numpy(orw.project_seeds(seeds.numpy()))
 
-    def upsample(parent, fine_shape, out=None):
-        return torch.from_numpy(orw.upsample_linear(parent.numpy(), tuple(fine_shape)).astype(np.float32))
-
-    def solve_level(vol, seeds, brick, bound, cfg, *, brick_list=None, out=None, labels_out=None,
-                    workspace=None, origin=None, **_unused):
-        params = orw.RWParams(beta=cfg.beta, min_weight=cfg.min_weight, tol=1e-10)
-        b = None if bound is None else bound.numpy().astype(np.float64)
-        res = orw.solve_level(vol.numpy(), seeds.numpy(), brick, b, params).prob.astype(np.float32)
-        if out is None:
-            out = torch.full(vol.shape, float("nan"))
-        if brick_list is None:
-            out.copy_(torch.from_numpy(res))
-        else:
-            bid, _ = orw.brick_ids(tuple(vol.shape), brick)
-            sel = torch.from_numpy(np.isin(bid, brick_list.numpy()))
-            out[sel] = torch.from_numpy(res)[sel]
+    def solve_level(vol, seeds, brick, bound, cfg, *, labels_out=None, **_unused):
+        assert bound is None  # the sharded driver solves only the coarsest level whole
+        res = orw.solve_level(vol.numpy(), seeds.numpy(), tuple(vol.shape), None, params(cfg))
+        out = torch.from_numpy(res.prob)
         if labels_out is not None:
             labels_out.copy_(out > 0.5)
-        return out, {"bricks": 0, "cg_ms": 0.0, "iterations_sum": 0}
+        return out, dict(zero, bricks=1)
 
-    def upsample_window(parent, fine_shape, z0, z1, out):
-        full = torch.from_numpy(orw.upsample_linear(parent.numpy(), tuple(fine_shape)).astype(np.float32))
-        out.fill_(float("nan"))  # planes outside the window must never be read
-        out[z0:z1] = full[z0:z1]
-        return out
+    def chunked(vol, seeds, brick, parent, cfg, labels_out, workspace, chunks, on_chunk, *, z0, fine_shape,
+                parent_z0, origin_z, n_rows):
+        nz = vol.shape[0]
+        # the bound from a NaN-padded parent: a tap outside the window the driver shipped
+        # poisons the result
+        pshape = tuple(-(-s // 2) for s in fine_shape)
+        full = np.full(pshape, np.nan)
+        full[parent_z0:parent_z0 + parent.shape[0]] = parent.numpy()
+        lo = (z0,) + (0,) * (len(fine_shape) - 1)
+        hi = (z0 + nz,) + tuple(fine_shape[1:])
+        bound = orw.upsample_linear_window(full, tuple(fine_shape), lo, hi)
+        mask = np.zeros(vol.shape, bool)
+        mask[origin_z:min(origin_z + n_rows * brick[0], nz)] = True
+        res = orw.solve_level(vol.numpy(), seeds.numpy(), brick, bound, params(cfg), solve_mask=mask,
+                              origin=lo)
+        out = torch.from_numpy(res.prob)
+        if labels_out is not None:
+            labels_out.copy_(out > 0.5)
+        return out, [dict(zero, bricks=int(n_rows))]
 
     device.lod_down = lod_down
     device.project_seeds = project_seeds
-    device.upsample = upsample
-    device.upsample_window = upsample_window
     device.solve_level = solve_level
+    device._solve_level_chunked = chunked
 
 
-def _sharded_worker(rank, world, port, q):
+CASES = {"even": ((80, 16, 16), (8, 8, 8), 3), "ragged": ((75, 12, 10), (8, 8, 8), 3),
+         "2d": ((70, 22), (8, 8), 3)}
+
+
+def _sharded_worker(rank, world, port, q, case, balance):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -178,41 +210,38 @@ def _sharded_worker(rank, world, port, q):
         from paper_2509_26213_b200 import synthetic
         from paper_2509_26213_b200.config import RWConfig
 
-        shape, brick, levels = (48, 16, 16), (8, 8, 8), 3
+        shape, brick, levels = CASES[case]
         vol = synthetic.phantom(shape)
-        sd = synthetic.seeds(shape, "S1")
+        sd = synthetic.seeds(shape, "S2")
         plan = sharding.ShardPlan.build(shape, brick, levels, rank, world)
-        for s in plan.shards:
-            if s is not None:
-                s.brick_list = torch.tensor(s.bricks[rank], dtype=torch.int32)
-        res = sharding.hierarchical_random_walker_sharded(torch.from_numpy(vol), torch.from_numpy(sd), plan,
-                                                          RWConfig(), want_labels=False)
-        z0, z1 = plan.owned_planes(0, rank)
-        q.put((rank, z0, z1, res.prob[z0:z1].numpy()))
+        a, b = plan.lod_slab(0)
+        res = sharding.hierarchical_random_walker_sharded(torch.from_numpy(vol[a:b].copy()),
+                                                          torch.from_numpy(sd[a:b].copy()), plan, RWConfig(),
+                                                          balance=balance)
+        q.put((rank, res.z0, res.z1, res.prob.numpy(), res.labels.numpy(), res.stats, res.solve_rows))
     finally:
         dist.destroy_process_group()
 
 
-def test_sharded_hierarchy_matches_single_process_gloo_world2():
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    port = _free_port()
-    procs = [ctx.Process(target=_sharded_worker, args=(r, 2, port, q)) for r in range(2)]
-    for p in procs:
-        p.start()
-    got = [q.get(timeout=300) for _ in procs]
-    for p in procs:
-        p.join(timeout=60)
-    assert all(p.exitcode == 0 for p in procs)
+@pytest.mark.parametrize("case,world,balance", [("even", 2, True), ("ragged", 3, True), ("ragged", 2, False),
+                                                ("2d", 2, True)])
+def test_sharded_hierarchy_matches_single_process(case, world, balance):
     from paper_2509_26213_b200 import synthetic
 
-    shape = (48, 16, 16)
+    got = _spawn(_sharded_worker, world, case, balance)
+    shape, brick, levels = CASES[case]
     vol = synthetic.phantom(shape)
-    sd = synthetic.seeds(shape, "S1")
-    ref = orw.hierarchical_random_walker(vol, sd, (8, 8, 8), 3, orw.RWParams(tol=1e-10)).prob[0].astype(np.float32)
-    covered = np.zeros(shape[0], bool)
-    for rank, z0, z1, part in got:
+    sd = synthetic.seeds(shape, "S2")
+    ref = orw.hierarchical_random_walker(vol, sd, brick, levels, orw.RWParams(tol=1e-10))
+    covered = np.zeros(shape[0], int)
+    for rank, z0, z1, part, lab, stats, rows in got:
         assert not np.isnan(part).any()
-        np.testing.assert_array_equal(part, ref[z0:z1])
-        covered[z0:z1] = True
-    assert covered.all()
+        np.testing.assert_array_equal(part, ref.prob[0][z0:z1])
+        np.testing.assert_array_equal(lab, ref.labels[z0:z1])
+        covered[z0:z1] += 1
+        # every rank holds the same all-reduced stats and the same splits
+        assert stats == got[0][5] and rows == got[0][6]
+        assert stats[-1]["bricks"] == world  # the replicated coarsest solve, counted per rank
+        grid0 = -(-shape[0] // brick[0])
+        assert stats[0]["bricks"] == grid0 and rows[0][-1][1] == grid0
+    assert (covered == 1).all()

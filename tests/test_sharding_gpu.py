@@ -1,6 +1,6 @@
-"""The sharded multi-rank path on real kernels: 2 ranks share cuda:0 (gloo
+"""The sharded multi-rank path on real kernels: 2 or 3 ranks share cuda:0 (gloo
 transport, planes staged through the host; NCCL needs one GPU per rank and the
-GPU box has one).  The ranks' kernels never wait on each other — the halo
+GPU box has one).  Each rank starts from its own level-0 slab only.  The ranks' kernels never wait on each other — the halo
 exchange is host-driven between levels — so sharing a GPU is safe.  Every
 rank's slab must be bit-identical to the single-process solve."""
 
@@ -23,7 +23,8 @@ def _free_port():
         return s.getsockname()[1]
 
 
-CASES = {"resident": ((128, 64, 64), (32, 32, 32), 3), "streaming": ((96, 40, 40), (16, 16, 16), 3)}
+CASES = {"resident": ((128, 64, 64), (32, 32, 32), 3), "streaming": ((96, 40, 40), (16, 16, 16), 3),
+         "resident2d": ((448, 192), (64, 64), 3), "ragged": ((150, 70, 40), (32, 32, 32), 3)}
 
 
 def _worker(rank, world, port, case, q):
@@ -35,26 +36,26 @@ def _worker(rank, world, port, case, q):
 
         shape, brick, levels = CASES[case]
         dev = torch.device("cuda", 0)
-        vol = torch.from_numpy(synthetic.phantom(shape)).to(dev)
-        sd = torch.from_numpy(synthetic.seeds(shape, "S1")).to(dev)
-        plan = sharding.ShardPlan.build(shape, brick, levels, rank, world, device=dev)
+        plan = sharding.ShardPlan.build(shape, brick, levels, rank, world)
+        a, b = plan.lod_slab(0)
+        vol = torch.from_numpy(synthetic.phantom(shape)[a:b].copy()).to(dev)
+        sd = torch.from_numpy(synthetic.seeds(shape, "S1")[a:b].copy()).to(dev)
         res = sharding.hierarchical_random_walker_sharded(vol, sd, plan, RWConfig(tol=1e-7))
         torch.cuda.synchronize()
-        z0, z1 = plan.owned_planes(0, rank)
-        q.put((rank, z0, z1, res.prob[z0:z1].cpu().numpy(), res.labels[z0:z1].cpu().numpy()))
+        q.put((rank, res.z0, res.z1, res.prob.cpu().numpy(), res.labels.cpu().numpy(), res.stats))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", sorted(CASES))
-def test_two_ranks_on_one_gpu_match_single_process(case):
+@pytest.mark.parametrize("case,world", [("resident", 2), ("streaming", 2), ("resident2d", 2), ("ragged", 3)])
+def test_ranks_on_one_gpu_match_single_process(case, world):
     from paper_2509_26213_b200 import device, synthetic
     from paper_2509_26213_b200.config import RWConfig
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, q)) for r in range(world)]
     for p in procs:
         p.start()
     got = [q.get(timeout=300) for _ in procs]
@@ -67,9 +68,12 @@ def test_two_ranks_on_one_gpu_match_single_process(case):
                                             RWConfig(tol=1e-7))
     torch.cuda.synchronize()
     p_ref, l_ref = ref.prob.cpu().numpy(), ref.labels.cpu().numpy()
-    covered = np.zeros(shape[0], bool)
-    for rank, z0, z1, p, lab in got:
+    covered = np.zeros(shape[0], int)
+    for rank, z0, z1, p, lab, stats in got:
         np.testing.assert_array_equal(p, p_ref[z0:z1])
         np.testing.assert_array_equal(lab, l_ref[z0:z1])
-        covered[z0:z1] = True
-    assert covered.all()
+        covered[z0:z1] += 1
+        assert stats == got[0][5]  # all-reduced: identical on every rank
+        assert [s["bricks"] for s in stats[:-1]] == [st["bricks"] for st in ref.stats[:-1]]
+        assert stats[0]["not_converged"] == 0
+    assert (covered == 1).all()
