@@ -149,31 +149,66 @@ class ClockSampler:
 # CPU reference (oracle) on a bounded sample
 
 
-def cpu_reference_sample(wl, steps=1, warmup=0):
+def cpu_reference_sample(wl, steps=1, warmup=0, inputs=None):
+    """The CPU reference (float64 numpy oracle on the host's cores) for a workload, by the
+    BASELINE.md §4 plan: config 1 timed fully; larger configs extrapolated from a per-step sample
+    (oracle/cpu_baseline.py: slab LOD, the whole coarsest solve, brick chains per finer level).
+    `inputs` = (volume, seeds) numpy arrays of the workload (generated here when None).
+    Returns (level-0 voxels, per-step seconds, cores, sample description, per-part seconds)."""
     import numpy as np
 
+    from oracle import cpu_baseline as cbl
     from oracle import rw as orw
     from paper_2509_26213_b200 import synthetic
 
-    s = wl["sample"]
-    # bricks are split into slabs of brick rows along dim 0, one thread each
-    nslab = [-(-s["shape"][d] // wl["brick"][d]) for d in range(2)]
-    cores = min(len(os.sched_getaffinity(0)), nslab[0] * nslab[1])
-    vol = synthetic.phantom(s["shape"])
-    seeds = synthetic.seeds(s["shape"], "S1")
     params = orw.RWParams(beta=BETA, min_weight=WMIN, tol=TOL, max_iter=10_000)
-    times = []
-    for i in range(warmup + steps):
-        t0 = time.perf_counter()
-        orw.hierarchical_random_walker(vol, seeds, wl["brick"], s["levels"], params, threads=cores)
-        dt = time.perf_counter() - t0
-        if i >= warmup:
-            times.append(dt)
-    n = int(np.prod(s["shape"]))
-    sample = (f"full hierarchical RW of the same generator/seeds/beta/tol/bricks at {'x'.join(map(str, s['shape']))} "
-              f"with {s['levels']} levels ({n} voxels) instead of {'x'.join(map(str, wl['shape']))}; "
-              f"float64 numpy oracle, bricks split over {cores} threads")
-    return n, times, cores, sample
+    shape = tuple(wl["shape"])
+    cores = len(os.sched_getaffinity(0))
+    if wl is WORKLOADS["c1"]:
+        vol = synthetic.phantom(shape)
+        seeds = synthetic.seeds(shape, "S1")
+        times = []
+        for i in range(warmup + steps):
+            t0 = time.perf_counter()
+            orw.hierarchical_random_walker(vol, seeds, wl["brick"], wl["levels"], params, threads=1)
+            if i >= warmup:
+                times.append(time.perf_counter() - t0)
+        return (math.prod(shape), times, 1, "the full configuration (64^3, one level), float64 numpy oracle, "
+                "1 thread", None)
+    if inputs is None:
+        slab = max(1, (1 << 24) // math.prod(shape[1:]))
+        vol = np.empty(shape, np.float32)
+        seeds = np.empty(shape, np.uint8)
+        if "timesteps" in wl:
+            synthetic.series_timestep(shape, 0, wl["timesteps"], slab=slab, out=vol)
+            synthetic.seeds_streamed(shape, "S1", t=0, steps=wl["timesteps"], slab=slab, out=seeds)
+        else:
+            synthetic.phantom_streamed(shape, slab=slab, out=vol)
+            synthetic.seeds_streamed(shape, "S1", slab=slab, out=seeds)
+    else:
+        vol, seeds = inputs
+    base = cbl.C4Baseline(vol, seeds, wl["brick"], wl["levels"], params, cores=cores, chains=cores,
+                          slab_planes=min(128, shape[0]))
+    times, parts = [], None
+    try:
+        for i in range(warmup + steps):
+            total, parts = base.step()
+            if i >= warmup:
+                times.append(total)
+    finally:
+        base.close()
+    nd = len(shape)
+    per = 2 ** nd
+    sample = (f"extrapolated (BASELINE.md §4): the real {'x'.join(map(str, shape))} input and its full "
+              f"{wl['levels']}-level pyramid; per step, timed on {cores} threads: the LOD + seed projection of a "
+              f"{min(128, shape[0])}-plane level-0 slab (scaled by planes), {base.top_sample} iterations of the "
+              f"coarsest {'x'.join(map(str, base.shapes[-1]))} Jacobi-PCG scaled to its {base.top_iterations} "
+              f"(the full solve, timed once at setup: {base.top_full_seconds:.1f} s), the prolongation (scaled by "
+              f"voxels), and {cores} brick chains ({per} real bricks per finer level each, true Dirichlet halos) "
+              f"scaled by brick count; float64 numpy oracle")
+    if "timesteps" in wl:
+        sample += f"; one timestep of the {wl['timesteps']}-step series (the same per-voxel rate for all)"
+    return math.prod(shape), times, cores, sample, parts
 
 
 def host_inputs(shape, t=None, steps=1):
@@ -273,8 +308,9 @@ def run_series(args, wl, rank, world):
     comm = comm_info(world)  # collective: every rank
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        n, times, cores, sample = cpu_reference_sample(wl, steps=1)
-        cpu = {"value": n / times[0], "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+        n, times, cores, sample, parts = cpu_reference_sample(wl, steps=1)
+        cpu = {"value": n / times[0], "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+               "seconds": parts}
     if rank == 0:
         line = {
             "metric": METRIC, "value": nvox / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -309,7 +345,7 @@ def run_series(args, wl, rank, world):
 def run_reference(args, wl, rank):
     if rank != 0:
         return 0
-    n, times, cores, sample = cpu_reference_sample(wl, args.steps, args.warmup)
+    n, times, cores, sample, parts = cpu_reference_sample(wl, args.steps, args.warmup)
     total = sum(times)
     value = n * len(times) / total
     line = {
@@ -317,7 +353,8 @@ def run_reference(args, wl, rank):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": wl["desc"], "sample": sample},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                         "seconds_last_step": parts},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -357,6 +394,7 @@ def run_ours(args, wl, rank, world):
         vol_h, seeds_h = vol_h[a:b].clone().pin_memory(), seeds_h[a:b].clone().pin_memory()
     vol = vol_h.to(dev)
     seeds = seeds_h.to(dev)
+    cpu_inputs = (vol_h.numpy(), seeds_h.numpy()) if world == 1 else None
     level_voxels = [math.prod(s) for s in sharding.level_shapes(shape, levels)]
 
     def step():
@@ -470,7 +508,7 @@ def run_ours(args, wl, rank, world):
                       "step k-1's download overlap step k's compute on their own streams)",
                "latency_ms_single_call": lat_ms,
                "latency_api": "paper_2509_26213_b200.api.segment (upload, segment, download in sequence)"}
-        del vol_h, seeds_h, outs
+        del outs
 
     peak, peak_src = load_peak()
     path_name = {0: "streaming cg_pass1/cg_pass2", 1: "resident3d_q4_kernel" if len(wl["shape"]) == 3 else
@@ -507,8 +545,9 @@ def run_ours(args, wl, rank, world):
     comm = comm_info(world)  # collective: every rank
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        n, times, cores, sample = cpu_reference_sample(wl, steps=1)
-        cpu = {"value": n / times[0], "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+        n, times, cores, sample, parts = cpu_reference_sample(wl, steps=1, inputs=cpu_inputs)
+        cpu = {"value": n / times[0], "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+               "seconds": parts}
 
     if rank == 0:
         line = {

@@ -4,8 +4,9 @@
         CG iterations of one level with direct (non-graph) launches, all bricks active,
         so `ncu -k regex:cg_pass` sees ordinary kernel launches of bench shapes.
     python tools/ncu_target.py hierarchy [--config c4] [--levels N]
-        one full hierarchical solve (coarse streaming level, then brick-resident
-        levels): `ncu -k regex:resident3d -c 1` captures level L-2 (C4: 256^3, 512 bricks).
+        one full hierarchical solve of the bench inputs (multigrid coarsest level, then
+        brick-resident levels): at C4 `ncu -k regex:resident3d_q4 -s 3 -c 1` captures the first
+        level-0 slab (launch order: level 2 x1, level 1 x2, level 0 x8).
 """
 
 import argparse
@@ -31,8 +32,15 @@ ap.add_argument("--level", type=int, default=0)
 ap.add_argument("--iters", type=int, default=4)
 args = ap.parse_args()
 wl = WORKLOADS[args.config]
-vol = synthetic.phantom_device(wl["shape"])
-seeds = synthetic.seeds_device(wl["shape"], "S1")
+if args.mode == "hierarchy":  # the bench's inputs (SURVEY.md 8(d) numpy generator)
+    from bench import host_inputs
+
+    vh, sh = host_inputs(wl["shape"])
+    vol, seeds = vh.cuda(), sh.cuda()
+    del vh, sh
+else:
+    vol = synthetic.phantom_device(wl["shape"])
+    seeds = synthetic.seeds_device(wl["shape"], "S1")
 if args.mode == "hierarchy":
     res = device.hierarchical_random_walker(vol, seeds, wl["brick"], wl["levels"], RWConfig())
     torch.cuda.synchronize()
