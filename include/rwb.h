@@ -90,6 +90,10 @@ typedef struct {
    passes with NO_COOP) instead of the default multigrid-preconditioned CG */
 #define RWB_SOLVE_NO_MG 2048
 
+/* brick-resident 4-CTA solver: plain Jacobi-PCG instead of the default coarse-corrected PCG
+   (Jacobi + an additive correction on the brick's 8^3-voxel aggregates) */
+#define RWB_SOLVE_NO_COARSE 4096
+
 /* Solver paths (rwb_solve_stats_t.path) */
 #define RWB_PATH_STREAMING 0 /* brick-batched CG, state in HBM, 2 launches per iteration */
 #define RWB_PATH_RESIDENT 1  /* CG state on chip: one 32^3 brick per 4-CTA cluster (3-D, default), one 64^2 tile per CTA (2-D) */

@@ -21,6 +21,7 @@ class RWConfig:
     resident: bool = True      # 32^3 bricks: solve each brick on chip (4-CTA cluster by default) instead of streaming
     cooperative: bool = True   # whole-level Jacobi-PCG (multigrid=False): one cooperative kernel for all iterations
     multigrid: bool = True     # whole-level solves: V-cycle-preconditioned CG (one cooperative kernel)
+    coarse: bool = True        # 32^3 bricks (4-CTA engine): Jacobi + 8^3-aggregate coarse correction (False: Jacobi-PCG)
     fused_setup: bool = True   # build the brick system with the fused per-brick setup kernel
     cluster: int = 4           # resident solver: CTAs per brick cluster (4: weights in TMEM, default; 8: all in registers;
                                # 16: 2 CTAs/SM; 512: 8-CTA with 512 threads) — 4 is 1.4x faster than 8 on config 4
@@ -32,6 +33,7 @@ class RWConfig:
         d.pop("resident")
         d.pop("cooperative")
         d.pop("multigrid")
+        d.pop("coarse")
         d.pop("cluster")
         d.pop("fused_setup")
         return {k: (float(v) if isinstance(v, float) else int(v)) for k, v in d.items()}

@@ -71,7 +71,8 @@ struct Cfg {
   static constexpr int COLS = 512 / (RW / 4);       // TMEM columns per thread (warps sharing a lane quarter)
   static constexpr int TAIL = 16 * TZT;             // column of the per-plane left w'x values
   static constexpr int WZB = TAIL + 8;              // column of the w'z plane below the thread's first plane
-  static_assert(WZB + 4 <= COLS, "TMEM row");
+  static constexpr int TAU = WZB + 8;               // columns of tau = m - sigma per voxel (coarse correction)
+  static_assert(TAU + 4 * TZT <= COLS, "TMEM row");
 };
 }  // namespace q4
 
@@ -83,13 +84,21 @@ struct Q4Smem {
   float sv[q4::SLAB];                       // staged y0
   float4 rp[q4::RPZ][q4::RB][q4::RQN];      // r planes (y neighbours of the SpMV)
   float4 rface[2][2][q4::RB][q4::RQN];      // received faces [parity][0 = from below, 1 = from above]
-  __align__(16) float red[2][2][q4::NPART]; // pushed partials [parity][gamma, delta][rank]
+  __align__(16) float red[2][2][q4::NPART]; // pushed partials [parity][r.r, delta][rank]
   float2 wpart[q4::MAXW];
+  float cgs[2][2];                          // c . g per iteration parity (two warps' halves): r.u = r.r + c . g
   unsigned long long barR[2];               // faces + partials, per parity
   unsigned long long barL;                  // slab staging
   uint32_t tmem;                            // TMEM base address (512 columns)
   unsigned long long barJ[2];               // next brick index, per parity
   int jn[2];
+  // coarse correction (8^3 aggregates of the brick, index rank*16 + ay*4 + ax; see the header)
+  __align__(16) float aggw[2][64];          // received aggregate sums per parity: P^T w, or P^T r0 at brick start
+  __align__(16) float aggr[2][64];          // received aggregate sums per parity: P^T r of the iteration's r
+  __align__(16) float aggd[64];             // received aggregate diagonals (brick start)
+  float cc[64];                             // c per aggregate
+  float cst[3][64];                         // g = P^T r, P^T s, 1/d (updated by warp 1)
+  float wagg[3][8][4];                      // per warp: 4 aggregate half sums (w, r; or r0 / d at brick start)
 };
 
 // Bulk-copy `slot`'s slab of this CTA into shared memory (one thread; completes on barL).
@@ -109,13 +118,16 @@ __device__ __forceinline__ void q4_stage(const ResidentArgs& a, Q4Smem& sm, int 
   bulk_g2s(sm.sv, a.y + base, slab_bytes, &sm.barL);
 }
 
-__device__ __forceinline__ void q4_prefetch(const ResidentArgs& a, int slot, int rank) {
+__device__ __forceinline__ void q4_prefetch(const ResidentArgs& a, int slot, int rank, bool y0) {
   using namespace q4;
   const long long base = (long long)slot * (RB * RB * RB) + (long long)rank * SLAB;
   prefetch_l2(a.sc + base, SLAB * 4);
+  if (y0) prefetch_l2(a.y + base, SLAB * 4);  // the Dirichlet values the coarse-corrected epilogue writes
 }
 
-template <int TZT>
+constexpr float kCcOmega = 0.8f;  // damping of the coarse correction
+
+template <int TZT, bool CC>
 __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(ResidentArgs a) {
   using namespace q4;
   using C = Cfg<TZT>;
@@ -162,6 +174,30 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
     st_async_f32(dst, g, bar);
     st_async_f32(dst + NPART * 4, d, bar);
   };
+  constexpr uint32_t tx_parts = 2 * NPART * 4;
+  static_assert(!CC || TZT == 8, "the coarse correction maps one 8^3 aggregate layer per CTA (8 planes per thread)");
+  // this thread's aggregate and its neighbours across the aggregate faces it touches
+  const int ax = xq >> 1, ay = ly >> 3;
+  const int agg = rank * 16 + ay * 4 + ax;
+  const int agg_x = (xq & 1) ? (ax < 3 ? agg + 1 : agg) : (ax > 0 ? agg - 1 : agg);
+  const bool ydn = (ly & 7) == 0, yup = (ly & 7) == 7;
+  const int agg_y = ydn ? (ay > 0 ? agg - 4 : agg) : (yup ? (ay < 3 ? agg + 4 : agg) : agg);
+  const uint32_t tx_agg = CC ? RCL * 16 * 4 : 0;  // aggregate sums received per exchange
+  // warp 0 lanes 0..15: the CTA's 16 aggregate sums (halves from the warp pairs covering their 8 rows),
+  // one float4 (4 aggregates of a row band) to each CTA of the cluster
+  auto push_agg = [&](int par, float* dst, const float (*wg)[4]) {
+    const int dest = lane >> 2, by = lane & 3;
+    const float4 v = f4(wg[2 * by][0] + wg[2 * by + 1][0], wg[2 * by][1] + wg[2 * by + 1][1],
+                        wg[2 * by][2] + wg[2 * by + 1][2], wg[2 * by][3] + wg[2 * by + 1][3]);
+    st_async_v4(mapa_u32(smem_u32(dst + rank * 16 + by * 4), dest), v, mapa_u32(smem_u32(&sm.barR[par]), dest));
+  };
+  // sum over the 16 threads of an aggregate inside the warp (quad pairs, the warp's 4 rows): lanes 0, 2, 4, 6
+  auto agg_warp_sum = [&](float v) {
+    v += __shfl_xor_sync(0xffffffffu, v, 1);
+    v += __shfl_xor_sync(0xffffffffu, v, 8);
+    v += __shfl_xor_sync(0xffffffffu, v, 16);
+    return v;
+  };
   if (warp == 0) tmem_alloc(&sm.tmem, 512);
   tmem_fence_before();
   cluster.sync();
@@ -172,7 +208,10 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
 
   // dynamic brick scheduling as in the 8-CTA engine: bricks cid and cid + ncl static, then a
   // global counter drawn one brick ahead by rank 0 and pushed into the cluster's CTAs
-  if (cid < n_act && tid == 0) q4_stage(a, sm, a.alist[cid], rank);
+  if (cid < n_act && tid == 0) {
+    q4_stage(a, sm, a.alist[cid], rank);
+    q4_prefetch(a, a.alist[cid], rank, CC);
+  }
   for (int j = cid, jn = cid + ncl, jnn; j < n_act; j = jn, jn = jnn) {
     const int slot = a.alist[j];
     const bool draw = jn < n_act;
@@ -182,15 +221,25 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
       mbar_expect_tx(&sm.barJ[parJ], 4);
       if (rank == 0) jd = 2 * ncl + atomicAdd(a.next, 1);
     }
-    if (tid == 0) q4_prefetch(a, slot, rank);  // scales of this brick, for the epilogue
+    // the unknowns of this thread's voxels (s > 0), from the scales prefetched into L2 when the
+    // brick was staged; the loads overlap the staging wait
+    float4 s4c[CC ? TZT : 1];
+    if (CC) {
+      const long long sb = (long long)slot * (RB * RB * RB) + (long long)rank * SLAB;
+#pragma unroll
+      for (int z = 0; z < TZT; ++z)
+        s4c[z] = __ldg(reinterpret_cast<const float4*>(a.sc + sb + (pz0 + z) * PLANE + ly * RB + xq * RQ));
+    }
     mbar_wait(&sm.barL, usesL & 1);
     ++usesL;
 
     // the slab's weights into this thread's TMEM row: per plane z, columns 16z.. hold w'y of
     // the quad, w'y of the row below, w'z and w'x of the quad; columns TAIL.. the w'x left of
     // the quad for each plane, WZB.. the w'z plane below the thread's first plane
+    float dpart = 0.f;  // coarse correction: this thread's share of its aggregate's diagonal d_I
     {
       float tt[16];
+      float tau[2][16];  // tau = m - sigma per voxel (m = 1 on unknowns, sigma = sum of the 6 scaled weights)
 #pragma unroll
       for (int z = 0; z < TZT; ++z) {
         const int o = (pz0 + z) * PLANE + ly * RB + xq * RQ;
@@ -202,6 +251,29 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
                              wz4.x, wz4.y, wz4.z, wz4.w, wx4.x, wx4.y, wx4.z, wx4.w};
         tmem_st16(tb + 16 * z, v);
         tt[z] = xq > 0 ? sm.sx[o - 1] : 0.f;
+        if (CC) {
+          // d_I = sum over the aggregate of tau + the weights of the edges leaving it (no cancellation)
+          const float4 wzd4 = *reinterpret_cast<const float4*>(&sm.sz[o]);  // w'z of the plane below
+          const float4 s4 = s4c[CC ? z : 0];
+#pragma unroll
+          for (int i = 0; i < RQ; ++i) {
+            const float wxl = i > 0 ? lane_of(wx4, i - 1) : tt[z];
+            const float sig = ((lane_of(wx4, i) + wxl) + (lane_of(wy4, i) + lane_of(wyb4, i))) +
+                              (lane_of(wz4, i) + lane_of(wzd4, i));
+            const float t = (lane_of(s4, i) > 0.f ? 1.f : 0.f) - sig;
+            tau[(z * RQ + i) >> 4][(z * RQ + i) & 15] = t;
+            dpart += t;
+            if (ydn) dpart += lane_of(wyb4, i);
+            if (yup) dpart += lane_of(wy4, i);
+            if (z == 0) dpart += lane_of(wzd4, i);
+            if (z == TZT - 1) dpart += lane_of(wz4, i);
+          }
+          dpart += (xq & 1) ? lane_of(wx4, 3) : tt[z];
+        }
+      }
+      if (CC) {
+        tmem_st16(tb + C::TAU, tau[0]);
+        tmem_st16(tb + C::TAU + 16, tau[1]);
       }
 #pragma unroll
       for (int z = TZT; z < 8; ++z) tt[z] = 0.f;
@@ -242,19 +314,49 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
     {
       const int par = gk & 1;
       const uint32_t ph = (gk >> 1) & 1;
-      if (tid == 0) mbar_expect_tx(&sm.barR[par], tx_faces + 2 * NPART * 4);
+      if (tid == 0) mbar_expect_tx(&sm.barR[par], tx_faces + tx_parts + 2 * tx_agg);
       if (below && first_zg) push_dn(par, plane4(r, 0));
       if (above && last_zg) push_up(par, plane4(r, TZT - 1));
       if (warp == 0 && lane < RCL) push_parts(par, 0.f, 0.f);
+      if (CC) {  // the aggregates' P^T r0 and d_I, all 64 to every CTA
+        float gpart = 0.f;
+#pragma unroll
+        for (int v = 0; v < RV; ++v) gpart += r[v];
+        const float gv = agg_warp_sum(gpart), dv = agg_warp_sum(dpart);
+        if ((lane & 0x19) == 0) {
+          sm.wagg[0][warp][lane >> 1] = gv;
+          sm.wagg[1][warp][lane >> 1] = dv;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(RTT) : "memory");
+        if (warp == 0 && lane < 16) {
+          push_agg(par, sm.aggw[par], sm.wagg[0]);
+          push_agg(par, sm.aggd, sm.wagg[1]);
+        }
+      }
       mbar_wait(&sm.barR[par], ph);
       ++gk;
       if (below && first_zg) rf_dn = sm.rface[par][0][ly][xq];
       if (above && last_zg) rf_up = sm.rface[par][1][ly][xq];
+      if (CC && (warp == 1 || warp == 2)) {  // coarse state: g = P^T r0, P^T s = 0, c = w g / d
+        const int I = lane + 32 * (warp - 1);
+        const float g = sm.aggw[par][I], d = sm.aggd[I];
+        const float di = d > 1e-6f ? 1.f / d : 0.f;
+        sm.cst[0][I] = g;
+        sm.cst[1][I] = 0.f;
+        sm.cst[2][I] = di;
+        const float c = kCcOmega * g * di;
+        sm.cc[I] = c;
+        const float cg = warp_sum(c * g);
+        if (lane == 0) sm.cgs[0][warp - 1] = cg;
+      }
       tmem_wait_st();
       __syncthreads();  // r planes published; every thread has left the staged slab
     }
     // the staging buffer is free: bring in the next brick's slab while this one iterates
-    if (draw && tid == 0) q4_stage(a, sm, a.alist[jn], rank);
+    if (draw && tid == 0) {
+      q4_stage(a, sm, a.alist[jn], rank);
+      q4_prefetch(a, a.alist[jn], rank, CC);  // its scales (unknown mask, epilogue) and y0
+    }
 
 #ifdef RWB_TRACE
     int trace_it = (int)gk;
@@ -263,7 +365,17 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
       Q4TRACE(0);
       const int par = gk & 1;
       const uint32_t ph = (gk >> 1) & 1;
-      if (tid == 0) mbar_expect_tx(&sm.barR[par], tx_faces + 2 * NPART * 4);
+      if (tid == 0) mbar_expect_tx(&sm.barR[par], tx_faces + tx_parts + 2 * tx_agg);
+      // u = r + c (c of the voxel's aggregate): the SpMV runs on r, and the c part enters as
+      // c_own * tau plus the differences (c_neighbour - c_own) across the aggregate faces
+      float c_own = 0.f, dxc = 0.f, dyc = 0.f, dzd = 0.f, dzu = 0.f, wsa = 0.f, wsb = 0.f, rsa = 0.f, rsb = 0.f;
+      if (CC) {
+        c_own = sm.cc[agg];
+        dxc = sm.cc[agg_x] - c_own;
+        dyc = sm.cc[agg_y] - c_own;
+        dzd = below ? sm.cc[agg - 16] - c_own : 0.f;
+        dzu = above ? sm.cc[agg + 16] - c_own : 0.f;
+      }
       // the previous iteration's y += alpha p, deferred off the update -> publish -> barrier
       // chain: nothing reads y until the epilogue, so it fills the SpMV's load latencies
       if (pass > 0) {
@@ -310,12 +422,17 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
           fma2(acc[i], acc[i + 1], lane_of(wzl4, i), lane_of(wzl4, i + 1), lane_of(rzd, i), lane_of(rzd, i + 1), acc[i],
                acc[i + 1]);
         }
-        float tx[5];  // w'x of the quad and the one left of it, once the y / z terms are done
+        float tx[9];  // w'x of the quad and the one left of it (+ tau), once the y / z terms are done
         uint32_t adx = tb + 16 * z + 12, adl = tb + C::TAIL + z;
         asm volatile("" : "+r"(adx), "+r"(adl) : "f"(acc[0]), "f"(acc[2]));
         tmem_ld4p(adx, tx);
         tmem_ld1(adl, tx[4]);
-        tmem_wait_ld5(tx);
+        if (CC) {
+          tmem_ld4p(tb + C::TAU + RQ * z, tx + 5);
+          tmem_wait_ld9(tx);
+        } else {
+          tmem_wait_ld5(tx);
+        }
         const float4 wx4 = f4(tx[0], tx[1], tx[2], tx[3]);
         const float wxl0 = tx[4];
 #pragma unroll
@@ -327,10 +444,31 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
           acc[i] = fmaf(lane_of(wx4, i), rxr, acc[i]);
           acc[i] = fmaf(wxl, rxl, acc[i]);
         }
+        // coarse part of A'u: c_own tau - sum over the aggregate faces of w' (c_neighbour - c_own)
+        if (CC) {
+          const float4 wye = ydn ? wyb4 : wy4;
+#pragma unroll
+          for (int i = 0; i < RQ; ++i) acc[i] = fmaf(lane_of(wye, i), dyc, acc[i]);
+          if (z == 0) {
+#pragma unroll
+            for (int i = 0; i < RQ; ++i) acc[i] = fmaf(lane_of(wzl4, i), dzd, acc[i]);
+          }
+          if (z == TZT - 1) {
+#pragma unroll
+            for (int i = 0; i < RQ; ++i) acc[i] = fmaf(lane_of(wz4, i), dzu, acc[i]);
+          }
+          acc[0] = fmaf((xq & 1) ? 0.f : wxl0, dxc, acc[0]);
+          acc[RQ - 1] = fmaf((xq & 1) ? lane_of(wx4, RQ - 1) : 0.f, dxc, acc[RQ - 1]);
+        }
 #pragma unroll
         for (int i = 0; i < RQ; i += 2) {
           const int v = z * RQ + i;
           fma2(w[v], w[v + 1], -1.f, -1.f, acc[i], acc[i + 1], r[v], r[v + 1]);
+          if (CC) {
+            fma2(w[v], w[v + 1], c_own, c_own, tx[5 + i], tx[6 + i], w[v], w[v + 1]);
+            fma2(wsa, wsb, 1.f, 1.f, w[v], w[v + 1], wsa, wsb);
+            fma2(rsa, rsb, 1.f, 1.f, r[v], r[v + 1], rsa, rsb);
+          }
           fma2(gp[0], gp[1], r[v], r[v + 1], r[v], r[v + 1], gp[0], gp[1]);
           fma2(dp[0], dp[1], w[v], w[v + 1], r[v], r[v + 1], dp[0], dp[1]);
         }
@@ -341,10 +479,19 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
       if (above && last_zg) push_up(par, plane4(w, TZT - 1));
       {
         const float gs = gp[0] + gp[1];
-        const float ds = dp[0] + dp[1];
+        // u = r + c_own on the unknowns (r = w = 0 off them): delta = w.u = w.r + c_own sum(w),
+        // gamma = r.u = r.r + c_own sum(r)
+        const float ds = CC ? fmaf(c_own, wsa + wsb, dp[0] + dp[1]) : dp[0] + dp[1];
         const float gw = warp_sum(gs);
         const float dw = warp_sum(ds);
         if (lane == 0) sm.wpart[warp] = make_float2(gw, dw);
+        if (CC) {
+          const float wv = agg_warp_sum(wsa + wsb), rv = agg_warp_sum(rsa + rsb);
+          if ((lane & 0x19) == 0) {
+            sm.wagg[0][warp][lane >> 1] = wv;
+            sm.wagg[2][warp][lane >> 1] = rv;
+          }
+        }
         asm volatile("bar.sync 1, %0;" ::"n"(RTT) : "memory");
         if (warp == 0) {
           float gc = 0.f, dc = 0.f;
@@ -355,18 +502,24 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
             dc += v.y;
           }
           if (lane < RCL) push_parts(par, gc, dc);
+          if (CC && lane < 16) {
+            push_agg(par, sm.aggw[par], sm.wagg[0]);
+            push_agg(par, sm.aggr[par], sm.wagg[2]);
+          }
         }
       }
       Q4TRACE(2);
       mbar_wait(&sm.barR[par], ph);
       Q4TRACE(3);
       ++gk;
-      const float g_new = sum_parts<NPART>(sm.red[par][0]);
+      const float g_new = sum_parts<NPART>(sm.red[par][0]);  // r.r (the stop rule)
       const float delta = sum_parts<NPART>(sm.red[par][1]);
+      // r.u = r.r + c . g, g = P^T r (one step from this iteration's exact aggregate sums)
+      const float gam = CC ? g_new + (sm.cgs[pass & 1][0] + sm.cgs[pass & 1][1]) : g_new;
       float beta;
       if (pass == 0) {
         beta = 0.f;
-        alpha = delta != 0.f ? g_new * rcp_ftz(delta) : 0.f;
+        alpha = delta != 0.f ? gam * rcp_ftz(delta) : 0.f;
         if (a.max_iter <= 0) {
           state = ST_MAXITER;
           break;
@@ -380,16 +533,33 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
           state = ST_MAXITER;
           break;
         }
-        beta = g_new * rgamma;
-        const float den = delta - beta * (g_new * ralpha);
-        alpha = den != 0.f ? g_new * rcp_ftz(den) : 0.f;
+        beta = gam * rgamma;
+        const float den = delta - beta * (gam * ralpha);
+        alpha = den != 0.f ? gam * rcp_ftz(den) : 0.f;
       }
-      rgamma = rcp_ftz(g_new);
+      rgamma = rcp_ftz(gam);
       ralpha = rcp_ftz(alpha);
+      if (CC && (warp == 1 || warp == 2)) {  // next c: P^T s = P^T w + beta P^T s, g -= alpha P^T s, c = w g / d
+        const int I = lane + 32 * (warp - 1);
+        // P^T r of the next residual from this iteration's exact P^T r (no drift over iterations)
+        const float ps = fmaf(beta, sm.cst[1][I], sm.aggw[par][I]);
+        const float g = fmaf(-alpha, ps, sm.aggr[par][I]);
+        const float c = kCcOmega * g * sm.cst[2][I];
+        sm.cst[1][I] = ps;
+        sm.cst[0][I] = g;
+        sm.cc[I] = c;
+        const float cg = warp_sum(c * g);
+        if (lane == 0) sm.cgs[(pass + 1) & 1][warp - 1] = cg;
+      }
       Q4TRACE(4);
 #pragma unroll
       for (int v = 0; v < RV; v += 2) {
-        fma2(p[v], p[v + 1], beta, beta, p[v], p[v + 1], r[v], r[v + 1]);
+        // p = u + beta p, u = r + c_own (unmasked: p drifts off the unknowns, where only y reads it,
+        // and the epilogue writes the staged Dirichlet value there instead)
+        if (CC)
+          fma2(p[v], p[v + 1], beta, beta, p[v], p[v + 1], r[v] + c_own, r[v + 1] + c_own);
+        else
+          fma2(p[v], p[v + 1], beta, beta, p[v], p[v + 1], r[v], r[v + 1]);
         fma2(sv[v], sv[v + 1], beta, beta, sv[v], sv[v + 1], w[v], w[v + 1]);
         fma2(r[v], r[v + 1], -alpha, -alpha, sv[v], sv[v + 1], r[v], r[v + 1]);
       }
@@ -428,11 +598,13 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
         const int gz = a.oz + hz * RB + rank * RPZ + pz0 + z;
         if (!row_in || gz < 0 || gz >= a.nz) continue;
         const float4 s4 = __ldg(reinterpret_cast<const float4*>(a.sc + sbase + (pz0 + z) * PLANE + ly * RB + xq * RQ));
+        const float4 y04 = CC ? __ldcg(reinterpret_cast<const float4*>(a.y + sbase + (pz0 + z) * PLANE + ly * RB + xq * RQ))
+                              : f4(0.f, 0.f, 0.f, 0.f);
         float pv[RQ];
 #pragma unroll
         for (int i = 0; i < RQ; ++i) {
           const float s = lane_of(s4, i), yv = y[z * RQ + i];
-          pv[i] = s > 0.f ? s * yv : yv;
+          pv[i] = s > 0.f ? s * yv : (CC ? lane_of(y04, i) : yv);
         }
         const long long gi = ((long long)gz * a.ny + gy) * a.nx + gx0;
         if (quad_in && (gi & 3) == 0) {
@@ -465,11 +637,11 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
   if (warp == 0) tmem_dealloc(sm.tmem, 512);
 }
 
-template <int TZT>
+template <int TZT, bool CC>
 static int launch_q4(const ResidentArgs& a, int max_bricks, cudaStream_t st) {
   using namespace q4;
   constexpr int RTT = Cfg<TZT>::RTT;
-  auto kern = resident3d_q4_kernel<TZT>;
+  auto kern = resident3d_q4_kernel<TZT, CC>;
   static DeviceCache cache;
   int dev = 0;
   if (int rc = device_slot(&dev)) return rc;
@@ -508,7 +680,12 @@ int launch_resident3d_q4(const ResidentArgs& a, int max_bricks, cudaStream_t st)
     const char* e = getenv("RWB_Q4_THREADS");
     return e ? atoi(e) : 256;
   }();
-  return threads == 512 ? launch_q4<4>(a, max_bricks, st) : launch_q4<8>(a, max_bricks, st);
+  static const bool cc_env = [] {  // RWB_Q4_CC=0: plain Jacobi-PCG everywhere (diagnostics)
+    const char* e = getenv("RWB_Q4_CC");
+    return !(e && atoi(e) == 0);
+  }();
+  if (threads == 512) return launch_q4<4, false>(a, max_bricks, st);
+  return (cc_env && a.coarse) ? launch_q4<8, true>(a, max_bricks, st) : launch_q4<8, false>(a, max_bricks, st);
 }
 
 }  // namespace rwb

@@ -1805,6 +1805,7 @@ static int solve_level_impl(const rwb_geometry_t* geom, const float* intensity, 
     ra.nz = g.nz, ra.ny = g.ny, ra.nx = g.nx;
     ra.oz = g.oz, ra.oy = g.oy, ra.ox = g.ox;
     ra.gy = g.gy, ra.gx = g.gx;
+    ra.coarse = !(params->flags & RWB_SOLVE_NO_COARSE);
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     RWB_CUDA(cudaEventCreate(&ev0));
     RWB_CUDA(cudaEventCreate(&ev1));

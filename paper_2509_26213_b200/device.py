@@ -262,6 +262,8 @@ def _flags(cfg: RWConfig) -> int:
         f |= _native.SOLVE_NO_COOP
     if not cfg.multigrid:
         f |= _native.SOLVE_NO_MG
+    if not cfg.coarse:
+        f |= _native.SOLVE_NO_COARSE
     if not cfg.fused_setup:
         f |= _native.SOLVE_SETUP2
     if cfg.cluster == 4:  # 4-CTA clusters, weights in shared memory
