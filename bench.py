@@ -66,13 +66,24 @@ ALG_BYTES_PER_UNKNOWN_ITER = {3: 56, 2: 52}
 
 
 def load_traffic(config, level_key):
-    """ncu DRAM bytes (read + write) of the dominant launch, from the committed profile, if present."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1_traffic.json")
-    try:
-        with open(path) as f:
-            return json.load(f).get(config, {}).get(level_key)
-    except (OSError, ValueError):
-        return None
+    """The ncu capture of the dominant kernel (profiles/rNN_traffic.json, newest round first,
+    written by tools/ncu_traffic.py): per-level DRAM bytes and on-chip utilisation, or None."""
+    import glob
+
+    prof = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles")
+    files = sorted(glob.glob(os.path.join(prof, "r*_traffic.json")),
+                   key=lambda f: int(os.path.basename(f)[1:].split("_")[0]), reverse=True)
+    for path in files:
+        try:
+            with open(path) as f:
+                got = json.load(f).get(config, {}).get(level_key)
+        except (OSError, ValueError):
+            continue
+        if isinstance(got, dict):
+            return dict(got, file=os.path.relpath(path, os.path.dirname(prof)))
+        if got is not None:
+            return {"bytes_per_level": got, "file": os.path.relpath(path, os.path.dirname(prof))}
+    return None
 
 
 def load_peak():
@@ -429,7 +440,8 @@ def run_ours(args, wl, rank, world):
                 if st is None:
                     continue
                 a = acc.setdefault(k, {"ms": 0.0, "alg_bytes": 0.0, "unknown_iterations": 0, "path": st["path"],
-                                       "voxels": level_voxels[k]})
+                                       "voxels": level_voxels[k], "brick_iterations": 0})
+                a["brick_iterations"] += st["iterations_sum"]
                 a["ms"] += st["cg_ms"]
                 a["alg_bytes"] += alg_b * st["unknown_iterations"]
                 a["unknown_iterations"] += st["unknown_iterations"]
@@ -522,15 +534,28 @@ def run_ours(args, wl, rank, world):
             "kernel": path_name.get(a["path"], "?"), "ms_per_step": a["ms"] / args.steps,
             "share_of_step": a["ms"] / ms_max, "achieved_gbs": gbs, "frac": gbs / peak,
             "unknown_iterations_per_step": a["unknown_iterations"] // args.steps,
-            # what actually crosses HBM when the CG state is on chip: intensity, bound, seeds in,
-            # probabilities (+ labels) out, once per solve
-            "hbm_gbs_if_resident": 14 * a["voxels"] / (a["ms"] / args.steps / 1e3) / 1e9 if a["path"] == 1 else None,
+            "brick_iterations_per_step": a["brick_iterations"] // args.steps,
         }
     dom = max(kernels, key=lambda n: kernels[n]["ms_per_step"])
     dk = kernels[dom]
-    traffic = load_traffic(args.config, dom)
+    prof = load_traffic(args.config, dom)
+    traffic = prof["bytes_per_level"] if prof else None
+    clk = clocks.summary()
+    onchip = None
+    if prof and acc.get(int(dom[5:]), {}).get("path") == 1 and clk.get("sm_mhz"):
+        # the resident engine's real limit: cycles per brick iteration of one cluster (live), beside
+        # the ncu issue / FMA-pipe activity of the same kernel and the HBM bytes it actually moves
+        clusters = prof["grid_size"] // max(1, prof["cluster_dim"])
+        per_step_ms = dk["ms_per_step"]
+        cyc = per_step_ms * 1e-3 * clk["sm_mhz"] * 1e6 * clusters / max(1, dk["brick_iterations_per_step"])
+        actual_gbs = traffic / (per_step_ms / 1e3) / 1e9
+        onchip = {"cycles_per_brick_iteration": cyc, "clusters": clusters, "sm_mhz": clk["sm_mhz"],
+                  "issue_active_pct": prof["issue_active_pct"], "fma_pipe_pct": prof["fma_pipe_pct"],
+                  "hbm_bytes_per_voxel": prof["bytes_per_voxel"], "hbm_gbs_actual": actual_gbs,
+                  "hbm_frac_actual": actual_gbs / peak, "profile": prof.get("file"),
+                  "profile_commit": prof.get("commit")}
     roofline = {"bound": "hbm", "achieved": dk["achieved_gbs"], "peak": peak, "unit": "GB/s", "frac": dk["frac"],
-                "traffic": traffic,
+                "traffic": traffic, "onchip": onchip,
                 "kernel": f"{dk['kernel']} ({dom}: the level with the largest solve time; its launches)",
                 "algorithmic_bytes": f"{alg_b} B per unknown voxel per PCG iteration (SURVEY.md 8(d)) x "
                                      f"{dk['unknown_iterations_per_step']} unknown-iterations per launch",
@@ -538,8 +563,10 @@ def run_ours(args, wl, rank, world):
                 "note": ("frac > 1: the brick-resident engine keeps every CG vector of a brick on chip (registers, "
                          "TMEM and SMEM of a 4-CTA cluster), so per-iteration traffic never reaches HBM; the HBM roofline of "
                          "the streaming algorithm (the 8(d) bytes) is beaten, and the kernel is bound by the "
-                         "latency of its per-iteration cluster reduction instead. traffic = ncu DRAM bytes of "
-                         "this launch (profiles/)"),
+                         "latency of its per-iteration cluster reduction instead: onchip = live cycles per brick "
+                         "iteration per cluster, with the ncu issue / FMA-pipe activity and the bytes the kernel "
+                         "really moves (hbm_frac_actual); traffic = ncu DRAM bytes of the level's launches, from "
+                         "the profile named in onchip.profile"),
                 "kernels": kernels}
 
     comm = comm_info(world)  # collective: every rank
@@ -563,7 +590,7 @@ def run_ours(args, wl, rank, world):
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "clocks": clocks.summary(),
+            "clocks": clk,
             "gpu_launches": int(launches),
             "comm": comm,
             "levels": per_level,
