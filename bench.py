@@ -542,7 +542,8 @@ def run_ours(args, wl, rank, world):
     traffic = prof["bytes_per_level"] if prof else None
     clk = clocks.summary()
     onchip = None
-    if prof and acc.get(int(dom[5:]), {}).get("path") == 1 and clk.get("sm_mhz"):
+    need = ("grid_size", "cluster_dim", "issue_active_pct", "fma_pipe_pct", "bytes_per_voxel")
+    if prof and all(k in prof for k in need) and acc.get(int(dom[5:]), {}).get("path") == 1 and clk.get("sm_mhz"):
         # the resident engine's real limit: cycles per brick iteration of one cluster (live), beside
         # the ncu issue / FMA-pipe activity of the same kernel and the HBM bytes it actually moves
         clusters = prof["grid_size"] // max(1, prof["cluster_dim"])
