@@ -94,6 +94,10 @@ typedef struct {
    (Jacobi + an additive correction on the brick's 8^3-voxel aggregates) */
 #define RWB_SOLVE_NO_COARSE 4096
 
+/* whole-level solves: multigrid-PCG at any size (default: levels of at least 2^19 voxels; on
+   smaller ones the V-cycle's per-iteration barriers cost more than the iterations it saves) */
+#define RWB_SOLVE_MG 8192
+
 /* Solver paths (rwb_solve_stats_t.path) */
 #define RWB_PATH_STREAMING 0 /* brick-batched CG, state in HBM, 2 launches per iteration */
 #define RWB_PATH_RESIDENT 1  /* CG state on chip: one 32^3 brick per 4-CTA cluster (3-D, default), one 64^2 tile per CTA (2-D) */
@@ -234,8 +238,9 @@ size_t rwb_solve_workspace_bytes(const rwb_geometry_t* geom, int64_t n_bricks, i
  *  stats     : host pointer or NULL.
  * Path: 3-D levels with 32^3 bricks and more than one brick run the
  * brick-resident solver (unless RWB_SOLVE_STREAMING); whole-level (coarsest,
- * single-brick) solves run multigrid-preconditioned CG in one cooperative
- * kernel (RWB_SOLVE_NO_MG: Jacobi-PCG, cooperative unless RWB_SOLVE_NO_COOP);
+ * single-brick) solves of at least 2^19 voxels (any size with RWB_SOLVE_MG) run
+ * multigrid-preconditioned CG in one cooperative kernel, smaller ones (and
+ * RWB_SOLVE_NO_MG) Jacobi-PCG, cooperative unless RWB_SOLVE_NO_COOP;
  * everything else runs the streaming solver with graph-launched passes.
  * Blocking on the host: returns when the listed bricks have converged (or hit
  * max_iter); all work is stream-ordered on `stream`. */

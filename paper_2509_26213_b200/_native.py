@@ -31,6 +31,7 @@ SOLVE_STATS_DEVICE = 512
 SOLVE_CLUSTER4 = 1024
 SOLVE_NO_MG = 2048
 SOLVE_NO_COARSE = 4096
+SOLVE_MG = 8192
 PATH_STREAMING, PATH_RESIDENT, PATH_COOPERATIVE, PATH_MULTIGRID = 0, 1, 2, 3
 
 # every symbol include/rwb.h declares, with (restype, argtypes)

@@ -20,7 +20,8 @@ class RWConfig:
     use_graph: bool = True     # streaming solver: run each poll interval as one CUDA graph launch
     resident: bool = True      # 32^3 bricks: solve each brick on chip (4-CTA cluster by default) instead of streaming
     cooperative: bool = True   # whole-level Jacobi-PCG (multigrid=False): one cooperative kernel for all iterations
-    multigrid: bool = True     # whole-level solves: V-cycle-preconditioned CG (one cooperative kernel)
+    multigrid: bool | None = None  # whole-level solves: V-cycle-preconditioned CG (one cooperative kernel);
+                               # None: on levels of >= 2^19 voxels, True: always, False: Jacobi-PCG
     coarse: bool = True        # 32^3 bricks (4-CTA engine): Jacobi + 8^3-aggregate coarse correction (False: Jacobi-PCG)
     fused_setup: bool = True   # build the brick system with the fused per-brick setup kernel
     cluster: int = 4           # resident solver: CTAs per brick cluster (4: weights in TMEM, default; 8: all in registers;

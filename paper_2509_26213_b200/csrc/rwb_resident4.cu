@@ -59,9 +59,20 @@ __device__ long long g_q4_trace[4][64][8];  // phase clocks of cluster 0 (diagno
 extern "C" int rwb_q4_trace_dump(long long* out) {
   return (int)cudaMemcpyFromSymbol(out, g_q4_trace, sizeof(g_q4_trace));
 }
+__device__ long long g_q4_pro[4][64][4];  // per brick of cluster 0: loop top, slab staged, loop start, epilogue done
+#define Q4PRO(k)                                                                          \
+  do {                                                                                    \
+    if (tid == 0 && blockIdx.x < 4 && trace_b < 64) g_q4_pro[rank][trace_b][k] = clock64(); \
+  } while (0)
+extern "C" int rwb_q4_pro_dump(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_q4_pro, sizeof(g_q4_pro));
+}
 #else
 #define Q4TRACE(k) \
   do {             \
+  } while (0)
+#define Q4PRO(k) \
+  do {           \
   } while (0)
 #endif
 
@@ -228,7 +239,11 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
     q4_stage(a, sm, a.alist[cid], rank);
     q4_prefetch(a, a.alist[cid], rank, CC);
   }
+#ifdef RWB_TRACE
+  int trace_b = 0;
+#endif
   for (int j = cid, jn = cid + ncl, jnn; j < n_act; j = jn, jn = jnn) {
+    Q4PRO(0);
     const int slot = a.alist[j];
     const bool draw = jn < n_act;
     const int parJ = uJ & 1;
@@ -248,6 +263,7 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
     }
     mbar_wait(&sm.barL, usesL & 1);
     ++usesL;
+    Q4PRO(1);
 
     // the slab's weights into this thread's TMEM row: per plane z, columns 16z.. hold w'y of
     // the quad, w'y of the row below, w'z and w'x of the quad; columns TAIL.. the w'x left of
@@ -377,6 +393,7 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
 #ifdef RWB_TRACE
     int trace_it = (int)gk;
 #endif
+    Q4PRO(2);
     for (int pass = 0;; ++pass) {
       Q4TRACE(0);
       const int par = gk & 1;
@@ -641,6 +658,10 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
       a.state[slot] = state;
       a.iters[slot] = it;
     }
+    Q4PRO(3);
+#ifdef RWB_TRACE
+    ++trace_b;
+#endif
     jnn = n_act;
     if (draw) {
       mbar_wait(&sm.barJ[parJ], (uJ >> 1) & 1);

@@ -1670,7 +1670,11 @@ static int coop_grid(int* grid) {
 using namespace rwb;
 
 static bool use_resident(const Geo& g, long long total, int flags) {
-  return !(flags & RWB_SOLVE_STREAMING) && total > 1 && (resident3d_supported(g) || resident2d_supported(g));
+  if (flags & RWB_SOLVE_STREAMING) return false;
+  // a whole 2-D level of one 64^2 tile (config 3's coarsest) is one tile-resident CTA: CTA-local
+  // reductions instead of the whole-level kernels' grid barriers (1.4 -> ~0.3 ms)
+  if (total == 1) return resident2d_supported(g) && !(flags & RWB_SOLVE_MG);
+  return resident3d_supported(g) || resident2d_supported(g);
 }
 
 extern "C" size_t rwb_solve_workspace_bytes(const rwb_geometry_t* geom, int64_t n_bricks, int32_t flags) {
@@ -1836,7 +1840,11 @@ static int solve_level_impl(const rwb_geometry_t* geom, const float* intensity, 
     return RWB_OK;
   }
 
-  if (total == 1 && !(params->flags & RWB_SOLVE_NO_MG)) {
+  // multigrid for large whole levels (128^3: 6.5 vs 13.3 ms); below ~2^19 voxels Jacobi-PCG is
+  // faster (64^3: 1.6 vs 1.9 ms, 64^2: 0.6 vs 0.8 ms; tools/mg_small_probe.py)
+  constexpr long long kMgMinVoxels = 1LL << 19;
+  const bool use_mg = !(params->flags & RWB_SOLVE_NO_MG) && ((params->flags & RWB_SOLVE_MG) || g.bvol >= kMgMinVoxels);
+  if (total == 1 && use_mg) {
     // whole-level solve: multigrid-preconditioned CG, all iterations in one cooperative launch
     MgArgs ma;
     std::memset(&ma, 0, sizeof(ma));

@@ -260,8 +260,10 @@ def _flags(cfg: RWConfig) -> int:
         f |= _native.SOLVE_STREAMING
     if not cfg.cooperative:
         f |= _native.SOLVE_NO_COOP
-    if not cfg.multigrid:
+    if cfg.multigrid is False:
         f |= _native.SOLVE_NO_MG
+    elif cfg.multigrid is True:
+        f |= _native.SOLVE_MG
     if not cfg.coarse:
         f |= _native.SOLVE_NO_COARSE
     if not cfg.fused_setup:

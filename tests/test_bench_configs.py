@@ -137,7 +137,7 @@ def test_config3_full_size_vs_oracle():
     res = device.hierarchical_random_walker(torch.from_numpy(vol).cuda(), torch.from_numpy(seeds).cuda(), brick,
                                             spec["levels"], BENCH_CFG)
     assert all(s["not_converged"] == 0 for s in res.stats)
-    assert res.stats[0]["path"] == 1 and res.stats[-1]["path"] == 3
+    assert res.stats[0]["path"] == 1 and res.stats[-1]["path"] == 1  # 64^2 top: one tile-resident CTA
     check_pyramid(res, meta)
     check_top(res, fx["top_prob"], spec["stride"])
     check_sampled_bricks(res, brick, seed=3, labels0=host(res.labels))

@@ -345,7 +345,8 @@ def test_multigrid_whole_level_matches_oracle(shape, cfg):
         seeds = np.zeros(shape, np.uint8)
         seeds.flat[0], seeds.flat[-1] = 1, 2
     ref = orw.solve_level(vol, seeds, shape, None, TIGHT)
-    out, st = device.solve_level(cuda(vol), cuda(seeds), shape, None, cfg)
+    out, st = device.solve_level(cuda(vol), cuda(seeds), shape, None,
+                                 RWConfig(tol=cfg.tol, max_iter=cfg.max_iter, multigrid=True))
     assert st["path"] == 3 and st["not_converged"] == 0
     got = host(out)
     assert_rw_parity(got, ref.prob, (got > 0.5).astype(np.uint8))
@@ -363,8 +364,9 @@ def test_multigrid_deterministic_and_random_systems(rng):
     for shape in [(40, 36, 28), (77, 64)]:
         vol, seeds = _random_case(rng, shape)
         ref = orw.solve_level(vol, seeds, shape, None, TIGHT).prob
-        a, sa = device.solve_level(cuda(vol), cuda(seeds), shape, None, BENCH_CFG)
-        b, sb = device.solve_level(cuda(vol), cuda(seeds), shape, None, BENCH_CFG)
+        mg = RWConfig(multigrid=True)
+        a, sa = device.solve_level(cuda(vol), cuda(seeds), shape, None, mg)
+        b, sb = device.solve_level(cuda(vol), cuda(seeds), shape, None, mg)
         np.testing.assert_array_equal(host(a), host(b))
         assert sa["iterations_max"] == sb["iterations_max"] and sa["path"] == 3
         assert_rw_parity(host(a), ref)
@@ -412,7 +414,7 @@ def test_config3_structure_2048_vs_oracle(cfg):
     seeds = synthetic.seeds(vol.shape, meta["seeds"])
     assert hashlib.sha256(np.ascontiguousarray(vol).tobytes()).hexdigest() == meta["input_sha256"]
     res = device.hierarchical_random_walker(cuda(vol), cuda(seeds), tuple(meta["brick"]), meta["levels"], cfg)
-    assert res.stats[0]["path"] == 1 and res.stats[-1]["path"] == 3
+    assert res.stats[0]["path"] == 1 and res.stats[-1]["path"] == 1
     s = meta["stride"]
     ref = load_golden("rw_c3like_sub4.npz")["prob0"].astype(np.float64)
     assert_rw_parity(host(res.prob)[::s, ::s], ref, host(res.labels)[::s, ::s])

@@ -22,3 +22,15 @@ for rank in range(4):
     d = np.diff(t[rank][:, :7], axis=1)[5:40]
     tot = (t[rank, 6:41, 0] - t[rank, 5:40, 0])
     print("rank", rank, "median cycles per phase", dict(zip(names, np.median(d, axis=0).astype(int))), "iter", int(np.median(tot)))
+
+# per brick of cluster 0 (CTA rank 0): staging wait, prologue (TMEM weights, coarse setup, initial
+# exchange), iterations, epilogue — cycles
+pro = (ctypes.c_longlong * (4 * 64 * 4))()
+lib.rwb_q4_pro_dump.argtypes = [ctypes.c_void_p]
+lib.rwb_q4_pro_dump(pro)
+p = np.frombuffer(pro, dtype=np.int64).reshape(4, 64, 4)[0]
+ok = p[:, 0] > 0
+p = p[ok][2:40]
+print("per brick median cycles: staging wait", int(np.median(p[:, 1] - p[:, 0])), "prologue",
+      int(np.median(p[:, 2] - p[:, 1])), "iterations+epilogue", int(np.median(p[:, 3] - p[:, 2])),
+      "next brick gap", int(np.median(p[1:, 0] - p[:-1, 3])))
