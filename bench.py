@@ -250,7 +250,7 @@ def run_series(args, wl, rank, world):
     from paper_2509_26213_b200 import _native, api, device, synthetic
     from paper_2509_26213_b200.config import RWConfig
 
-    local = int(os.environ.get("LOCAL_RANK", 0))
+    local = local_device()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     lib = _native.lib()
@@ -298,7 +298,7 @@ def run_series(args, wl, rank, world):
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
         tm = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        all_reduce_(tm, dist.ReduceOp.MAX)
         ms = float(tm.item())
     nvox = math.prod(full)
     # kernel-level view: one timestep device-resident
@@ -387,7 +387,7 @@ def run_ours(args, wl, rank, world):
     from paper_2509_26213_b200 import _native, api, device, sharding, synthetic
     from paper_2509_26213_b200.config import RWConfig
 
-    local = int(os.environ.get("LOCAL_RANK", 0))
+    local = local_device()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     lib = _native.lib()
@@ -452,7 +452,7 @@ def run_ours(args, wl, rank, world):
     ms = ev0.elapsed_time(ev1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce_(t, dist.ReduceOp.MAX)
     ms_max = float(t.item())
     per_level = [dict(st, level=k, shape=list(sharding.level_shapes(shape, levels)[k]))
                  for k, st in enumerate(res.stats) if st is not None]
@@ -481,10 +481,10 @@ def run_ours(args, wl, rank, world):
         e1.record(stream)
         torch.cuda.synchronize()
         te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        all_reduce_(te, dist.ReduceOp.MAX)
         e_ms = float(te.item()) / args.steps
         hb = torch.tensor([vol_h.numel() * 5, out_p.numel() * 5], dtype=torch.float64, device=dev)
-        dist.all_reduce(hb)
+        all_reduce_(hb)
         e2e = {"value": nvox / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
                "h2d_bytes_per_step": int(hb[0].item()), "d2h_bytes_per_step": int(hb[1].item()),
                "api": "paper_2509_26213_b200.sharding.hierarchical_random_walker_sharded: every rank uploads its "
@@ -619,6 +619,27 @@ def spawn_ranks(n: int) -> int:
     return subprocess.run(cmd, env=env).returncode
 
 
+def all_reduce_(t, op=None):
+    """dist.all_reduce in place; a CUDA tensor goes through host memory when the backend is not
+    NCCL (the RWB_BENCH_SHARE_GPU gloo dry run)."""
+    import torch.distributed as dist
+
+    op = dist.ReduceOp.SUM if op is None else op
+    if t.is_cuda and dist.get_backend() != "nccl":
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op)
+    return t
+
+
+def local_device() -> int:
+    """This rank's GPU: LOCAL_RANK, or 0 for every rank with RWB_BENCH_SHARE_GPU=1 (a multi-rank
+    dry run of the sharded path on a one-GPU box, over gloo; never a measurement)."""
+    return 0 if os.environ.get("RWB_BENCH_SHARE_GPU") == "1" else int(os.environ.get("LOCAL_RANK", 0))
+
+
 def init_ranks(world: int):
     """Process group of the N ranks (NCCL on GPUs; gloo where there is no CUDA device)."""
     import torch
@@ -627,8 +648,11 @@ def init_ranks(world: int):
     if world <= 1 or dist.is_initialized():
         return
     if torch.cuda.is_available():
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
+        torch.cuda.set_device(local_device())
+        if os.environ.get("RWB_BENCH_SHARE_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_device()))
     else:
         dist.init_process_group("gloo")
 
@@ -644,7 +668,7 @@ def comm_info(world: int) -> dict:
 
     cuda = torch.cuda.is_available()
     mine = torch.tensor([torch.cuda.current_device() if cuda else -1], dtype=torch.int64,
-                        device="cuda" if cuda else "cpu")
+                        device="cuda" if cuda and dist.get_backend() == "nccl" else "cpu")
     got = [torch.zeros_like(mine) for _ in range(dist.get_world_size())]
     dist.all_gather(got, mine)
     return {"backend": dist.get_backend(), "nranks": dist.get_world_size(), "devices": [int(t.item()) for t in got]}
@@ -662,7 +686,7 @@ def run_launch_probe(args, rank, world):
         import torch.distributed as dist
 
         one = torch.ones(1, device="cuda" if torch.cuda.is_available() else "cpu")
-        dist.all_reduce(one)
+        all_reduce_(one)
         info["all_reduce_ok"] = int(one.item()) == world
     if rank == 0:
         print(json.dumps({"launch_probe": True, "n_gpus": world, "requested_gpus": args.gpus, "comm": info}),
