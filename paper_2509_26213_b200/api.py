@@ -26,7 +26,7 @@ def _as_host_tensor(a, dtype):
 
 def segment(volume, seeds, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWConfig(), *,
             out_prob: torch.Tensor | None = None, out_labels: torch.Tensor | None = None,
-            workspace: device.Workspace | None = None, pyramid_store=None, pyramid_key=None):
+            workspace: device.Workspace | None = None, pyramid_store=None, pyramid_key=None, roi=None):
     """Hierarchical random-walker segmentation.
 
     volume: float32 intensities (numpy or torch, host or CUDA); seeds: uint8
@@ -35,10 +35,22 @@ def segment(volume, seeds, brick=(32, 32, 32), levels=None, cfg: RWConfig = RWCo
     inputs get host outputs (written into `out_prob` / `out_labels` when
     given, e.g. pinned buffers).  `pyramid_store` (a store.DeviceStore) with `pyramid_key`
     keeps the volume's LOD pyramid in HBM under a budget, so segmenting the same volume again
-    (new seeds or parameters) skips rebuilding it.
+    (new seeds or parameters) skips rebuilding it.  `roi` = (lo, hi) level-0 voxel box: only the
+    bricks that region needs are solved on every level, and (prob, labels) of the box are returned
+    (identical to the same box of a full segmentation).
     """
     vol = _as_host_tensor(volume, np.float32)
     sd = _as_host_tensor(seeds, np.uint8)
+    if roi is not None:
+        dev = vol.device if vol.is_cuda else torch.device("cuda", torch.cuda.current_device())
+        res = device.hierarchical_random_walker(vol.to(dev, non_blocking=True), sd.to(dev, non_blocking=True), brick,
+                                                levels, cfg, workspace=workspace, pyramid_store=pyramid_store,
+                                                pyramid_key=pyramid_key, roi=roi)
+        box = tuple(slice(max(0, int(a)), int(b)) for a, b in zip(roi[0], roi[1]))
+        p, lab = res.prob[box], res.labels[box]
+        if vol.is_cuda:
+            return p, lab
+        return p.cpu(), lab.cpu()
     if vol.is_cuda:
         res = device.hierarchical_random_walker(vol, sd, brick, levels, cfg, workspace=workspace,
                                                 pyramid_store=pyramid_store, pyramid_key=pyramid_key)

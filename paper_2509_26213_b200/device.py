@@ -493,10 +493,47 @@ class HRWResult:
     stats: list = field(default_factory=list)  # per-level solver stats (level 0 first)
 
 
+def roi_brick_boxes(shapes, brick, roi):
+    """Lazy, region-limited hierarchy (the reference computes only the chunks a request needs,
+    `engine.py:423-462`; Palace only the visible bricks, `PAPER.md:424`): per level k < L-1 the
+    box [b0, b1) of brick coordinates to solve so that level 0 is exact inside `roi` = (lo, hi)
+    (level-0 voxel coordinates).  Level k's listed bricks plus their one-voxel Dirichlet halo read
+    the parent through the prolongation taps; the level-(k+1) bricks covering those taps are listed
+    in turn.  The coarsest level is always whole (None)."""
+    nd = len(shapes[0])
+    lo = [max(0, int(a)) for a in roi[0]]
+    hi = [min(int(b), n) for b, n in zip(roi[1], shapes[0])]
+    if any(b <= a for a, b in zip(lo, hi)):
+        raise ValueError(f"empty region of interest {roi}")
+    from .sharding import parent_planes
+
+    boxes = []
+    for k in range(len(shapes) - 1):
+        b0 = [a // b for a, b in zip(lo, brick)]
+        b1 = [-(-h // b) for h, b in zip(hi, brick)]
+        boxes.append((b0, b1))
+        vlo = [max(a * b - 1, 0) for a, b in zip(b0, brick)]
+        vhi = [min(c * b + 1, n) for c, b, n in zip(b1, brick, shapes[k])]
+        taps = [parent_planes(vlo[d], vhi[d], shapes[k + 1][d]) for d in range(nd)]
+        lo, hi = [t[0] for t in taps], [t[1] for t in taps]
+    boxes.append(None)
+    return boxes
+
+
+def _box_list(box, grid, device):
+    b0, b1 = box
+    axes = [torch.arange(a, b, dtype=torch.int64) for a, b in zip(b0, b1)]
+    ids = torch.zeros([len(x) for x in axes], dtype=torch.int64)
+    for d, ax in enumerate(axes):
+        ids = ids * grid[d] + ax.reshape([-1 if i == d else 1 for i in range(len(axes))])
+    return ids.reshape(-1).to(torch.int32).to(device)
+
+
 def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick, levels: int | None = None,
                                cfg: RWConfig = RWConfig(), *, want_labels: bool = True,
                                workspace: Workspace | None = None, level0_chunks: int | None = None,
-                               on_level0_chunk=None, pyramid_store=None, pyramid_key=None) -> HRWResult:
+                               on_level0_chunk=None, pyramid_store=None, pyramid_key=None,
+                               roi=None) -> HRWResult:
     """Coarse-to-fine random walker (oracle/rw.py: hierarchical_random_walker).
 
     The coarsest level is solved whole; each finer level is initialised and
@@ -508,6 +545,9 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
     else 1) and calls `on_level0_chunk(r0, r1)` after
     each with the level's (partially written) prob / labels tensors, so a
     caller can download finished rows while the rest solves.
+    `roi` = (lo, hi) in level-0 voxels: solve only the bricks that region needs on every level
+    (`roi_brick_boxes`); values inside it are those of the full solve, bit for bit, and NaN (labels
+    255) wherever a level was not solved.
     """
     brick = tuple(int(b) for b in brick)
     if pyramid_store is not None and pyramid_key is not None:
@@ -532,7 +572,26 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
     lab = top_labels
     if top == 0 and on_level0_chunk is not None:  # single-level hierarchy: level 0 is the whole-level solve
         on_level0_chunk(0, vols[0].shape[0], probs[0], top_labels)
+    boxes = roi_brick_boxes([tuple(v.shape) for v in vols], brick, roi) if roi is not None else None
     for k in range(top - 1, -1, -1):
+        if boxes is not None:  # region-limited: the listed bricks, bound upsampled over their planes
+            b0, b1 = boxes[k]
+            grid = brick_grid(vols[k].shape, brick)
+            bl = _box_list(boxes[k], grid, volume.device)
+            z0, z1 = max(b0[0] * brick[0] - 1, 0), min(b1[0] * brick[0] + 1, vols[k].shape[0])
+            x = upsample_planes(probs[k + 1], 0, vols[k].shape, z0, z1,
+                                torch.empty(vols[k].shape, dtype=torch.float32, device=volume.device))
+            out = torch.full(vols[k].shape, float("nan"), dtype=torch.float32, device=volume.device)
+            lab_k = torch.full(vols[k].shape, 255, dtype=torch.uint8, device=volume.device) \
+                if (want_labels and k == 0) else None
+            probs[k], stats[k] = solve_level(vols[k], seed_levels[k], brick, x, cfg, brick_list=bl, out=out,
+                                             labels_out=lab_k, workspace=workspace, stats_on_device=True)
+            if k == 0:
+                lab = lab_k
+                if on_level0_chunk is not None:
+                    on_level0_chunk(0, vols[0].shape[0], probs[0], lab_k)
+            del x
+            continue
         if k == 0 and level0_chunks is None:  # measured: 8 slabs at 32768 bricks, 2 at 4096
             nb0 = math.prod(brick_grid(vols[0].shape, brick))
             level0_chunks = 8 if nb0 >= 16384 else (2 if nb0 >= 4096 else 1)

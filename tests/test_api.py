@@ -120,3 +120,30 @@ def test_single_level_host_path(shape, brick, levels):
     assert not np.isnan(p_h.numpy()).any()
     np.testing.assert_array_equal(p_h.numpy(), p_d.cpu().numpy())
     np.testing.assert_array_equal(l_h.numpy(), l_d.cpu().numpy())
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,brick,levels,roi", [
+    ((128, 96, 64), (32, 32, 32), 3, ((40, 10, 5), (75, 50, 30))),
+    ((128, 96, 64), (32, 32, 32), 3, ((0, 0, 0), (1, 1, 1))),
+    ((96, 80, 72), (16, 16, 16), 3, ((30, 17, 40), (64, 80, 72))),   # streaming solver, ragged
+    ((448, 320), (64, 64), 3, ((100, 200), (260, 320))),             # 2-D tile engine
+])
+def test_region_limited_solve_equals_full_solve(shape, brick, levels, roi):
+    """The lazy, region-limited hierarchy (the reference's pull of only the needed chunks): the
+    region's probabilities and labels are the full solve's, bit for bit, with far fewer bricks."""
+    import torch
+
+    from paper_2509_26213_b200 import device
+    from paper_2509_26213_b200.config import RWConfig
+
+    vol = torch.from_numpy(synthetic.phantom(shape)).cuda()
+    sd = torch.from_numpy(synthetic.seeds(shape, "S1")).cuda()
+    full = device.hierarchical_random_walker(vol, sd, brick, levels, RWConfig())
+    part = device.hierarchical_random_walker(vol, sd, brick, levels, RWConfig(), roi=roi)
+    box = tuple(slice(a, b) for a, b in zip(*roi))
+    assert torch.equal(part.prob[box], full.prob[box]) and torch.equal(part.labels[box], full.labels[box])
+    assert part.stats[0]["bricks"] < full.stats[0]["bricks"]
+    assert torch.isnan(part.prob).any() or part.stats[0]["bricks"] == full.stats[0]["bricks"]
+    p, lab = api.segment(vol.cpu().numpy(), sd.cpu().numpy(), brick, levels, RWConfig(), roi=roi)
+    assert torch.equal(p, full.prob[box].cpu()) and torch.equal(lab, full.labels[box].cpu())

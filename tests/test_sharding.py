@@ -245,3 +245,27 @@ def test_sharded_hierarchy_matches_single_process(case, world, balance):
         grid0 = -(-shape[0] // brick[0])
         assert stats[0]["bricks"] == grid0 and rows[0][-1][1] == grid0
     assert (covered == 1).all()
+
+
+def test_roi_brick_boxes_cover_the_prolongation_taps():
+    """Every parent voxel the listed bricks (+1 halo) of level k read is inside level k+1's box."""
+    from paper_2509_26213_b200 import device
+
+    rnd = random.Random(9)
+    for _ in range(200):
+        nd = rnd.choice([2, 3])
+        brick = tuple(rnd.choice([8, 16]) for _ in range(nd))
+        shape0 = tuple(rnd.randint(20, 120) for _ in range(nd))
+        shapes = sharding.level_shapes(shape0, rnd.randint(2, 4))
+        lo = [rnd.randint(0, n - 1) for n in shape0]
+        hi = [rnd.randint(a + 1, n) for a, n in zip(lo, shape0)]
+        boxes = device.roi_brick_boxes(shapes, brick, (lo, hi))
+        assert boxes[-1] is None and len(boxes) == len(shapes)
+        b0, b1 = boxes[0]
+        assert all(x * b <= a and y * b >= h for x, y, a, h, b in zip(b0, b1, lo, hi, brick))
+        for k in range(len(shapes) - 2):
+            (b0, b1), (p0, p1) = boxes[k], boxes[k + 1]
+            for d in range(nd):
+                v0, v1 = max(b0[d] * brick[d] - 1, 0), min(b1[d] * brick[d] + 1, shapes[k][d])
+                t0, t1 = brute_parent_planes(v0, v1, shapes[k + 1][d])
+                assert p0[d] * brick[d] <= t0 and min(p1[d] * brick[d], shapes[k + 1][d]) >= t1
