@@ -387,9 +387,25 @@ class HierarchyResult:
     labels: np.ndarray
 
 
+def decided_bricks(bound, seeds, brick, eps: float) -> np.ndarray:
+    """The optional brick-skip rule of the hierarchical scheme (Drees et al. 2022, `PAPER.md:419`,
+    SURVEY.md §8(a) N5): a brick is skipped — its values are the upsampled parent, seeds exact —
+    when every value its solve would read, the upsampled parent over the brick and its one-voxel
+    halo, is within `eps` of 0 or 1 (seeded voxels count as decided).  Per brick, row-major."""
+    amb = np.minimum(bound, 1.0 - bound)
+    amb = np.where(np.asarray(seeds) != SEED_NONE, 0.0, amb)
+    grid = [-(-n // b) for n, b in zip(amb.shape, brick)]
+    out = np.zeros(grid, dtype=bool)
+    for h in np.ndindex(*grid):
+        sl = tuple(slice(max(i * b - 1, 0), min((i + 1) * b + 1, n)) for i, b, n in zip(h, brick, amb.shape))
+        out[h] = amb[sl].max() < eps
+    return out.reshape(-1)
+
+
 def hierarchical_random_walker(volume, seeds, brick, levels=None, params: RWParams = RWParams(),
-                               threads: int | None = 1) -> HierarchyResult:
-    """Coarsest level whole, then every finer level brick by brick."""
+                               threads: int | None = 1, skip_eps: float | None = None) -> HierarchyResult:
+    """Coarsest level whole, then every finer level brick by brick (with `skip_eps`, bricks whose
+    parent is decided keep the upsampled parent: `decided_bricks`)."""
     vols = lod.lod_chain(volume, brick, levels)
     seed_levels = [np.asarray(seeds, dtype=np.uint8)]
     for _ in range(len(vols) - 1):
@@ -401,7 +417,11 @@ def hierarchical_random_walker(volume, seeds, brick, levels=None, params: RWPara
     probs[-1], iters[-1] = top.prob, top.iterations
     for k in range(nlev - 2, -1, -1):
         bound = upsample_linear(probs[k + 1], vols[k].shape)
-        if threads == 1:
+        if skip_eps is not None:
+            bid, _ = brick_ids(vols[k].shape, brick)
+            keep = ~decided_bricks(bound, seed_levels[k], brick, skip_eps)[bid]
+            res = solve_level(vols[k], seed_levels[k], brick, bound, params, solve_mask=keep)
+        elif threads == 1:
             res = solve_level(vols[k], seed_levels[k], brick, bound, params)
         else:
             res = solve_level_threaded(vols[k], seed_levels[k], brick, bound, params, threads)

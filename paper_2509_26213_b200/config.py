@@ -23,6 +23,8 @@ class RWConfig:
     multigrid: bool | None = None  # whole-level solves: V-cycle-preconditioned CG (one cooperative kernel);
                                # None: on levels of >= 2^19 voxels, True: always, False: Jacobi-PCG
     coarse: bool = True        # 32^3 bricks (4-CTA engine): Jacobi + 8^3-aggregate coarse correction (False: Jacobi-PCG)
+    skip_eps: float | None = None  # optional brick-skip rule (oracle/rw.py decided_bricks): bricks whose
+                               # upsampled parent (+ halo) is within skip_eps of 0 or 1 are not solved
     fused_setup: bool = True   # build the brick system with the fused per-brick setup kernel
     cluster: int = 4           # resident solver: CTAs per brick cluster (4: weights in TMEM, default; 8: all in registers;
                                # 16: 2 CTAs/SM; 512: 8-CTA with 512 threads) — 4 is 1.4x faster than 8 on config 4
@@ -37,4 +39,8 @@ class RWConfig:
         d.pop("coarse")
         d.pop("cluster")
         d.pop("fused_setup")
-        return {k: (float(v) if isinstance(v, float) else int(v)) for k, v in d.items()}
+        skip = d.pop("skip_eps")
+        out = {k: (float(v) if isinstance(v, float) else int(v)) for k, v in d.items()}
+        if skip is not None:  # part of the result's identity only when the rule is on
+            out["skip_eps"] = float(skip)
+        return out

@@ -469,6 +469,41 @@ def _solve_level_chunked(volume, seeds, brick, parent, cfg, labels_out, workspac
     return out, parts
 
 
+def decided_bricks(bound: torch.Tensor, seeds: torch.Tensor, brick, eps: float) -> torch.Tensor:
+    """The brick-skip rule (oracle/rw.py `decided_bricks`): True per brick (row-major) when the
+    upsampled parent over the brick and its one-voxel halo is within `eps` of 0 or 1 everywhere
+    (seeded voxels count as decided).  One max-pool over the level."""
+    import torch.nn.functional as F
+
+    amb = torch.minimum(bound, 1.0 - bound).masked_fill(seeds != 0, 0.0)
+    nd = bound.dim()
+    grid = brick_grid(bound.shape, brick)
+    pool = F.max_pool3d if nd == 3 else F.max_pool2d
+    m = pool(amb[None, None], kernel_size=tuple(b + 2 for b in brick), stride=tuple(brick), padding=1,
+             ceil_mode=True)[0, 0]
+    m = m[tuple(slice(0, g) for g in grid)]
+    if tuple(m.shape) != tuple(grid):
+        raise RuntimeError("brick-skip pooling does not match the brick grid")
+    return (m < eps).reshape(-1)
+
+
+def _solve_level_skipping(volume, seeds, brick, parent, cfg, want_labels, workspace):
+    """One level under the brick-skip rule: the decided bricks keep the upsampled parent (seeds
+    exact), the others are solved as a brick list."""
+    bound = upsample(parent, volume.shape)
+    skip = decided_bricks(bound, seeds, brick, cfg.skip_eps)
+    out = torch.where(seeds == 1, torch.ones_like(bound), torch.where(seeds == 2, torch.zeros_like(bound), bound))
+    todo = torch.nonzero(~skip).reshape(-1).to(torch.int32)
+    nskip = int(skip.numel() - todo.numel())
+    if todo.numel() == 0:
+        return out, {"bricks": 0, "converged": 0, "not_converged": 0, "zero_rhs": 0, "iterations_max": 0,
+                     "iterations_sum": 0, "unknowns": 0, "unknown_iterations": 0, "sweeps": 0, "cg_ms": 0.0,
+                     "path": -1}, nskip
+    _, st = solve_level(volume, seeds, brick, bound, cfg, brick_list=todo, out=out, workspace=workspace,
+                        stats_on_device=True)
+    return out, st, nskip
+
+
 def _resident_geometry(shape, brick) -> bool:
     """Levels the brick-resident engines take (rwb_solve.cu use_resident)."""
     return (len(shape) == 3 and tuple(brick) == (32, 32, 32)) or (len(shape) == 2 and tuple(brick) == (64, 64))
@@ -573,6 +608,7 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
     if top == 0 and on_level0_chunk is not None:  # single-level hierarchy: level 0 is the whole-level solve
         on_level0_chunk(0, vols[0].shape[0], probs[0], top_labels)
     boxes = roi_brick_boxes([tuple(v.shape) for v in vols], brick, roi) if roi is not None else None
+    skipped = [None] * nlev
     for k in range(top - 1, -1, -1):
         if boxes is not None:  # region-limited: the listed bricks, bound upsampled over their planes
             b0, b1 = boxes[k]
@@ -591,6 +627,14 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
                 if on_level0_chunk is not None:
                     on_level0_chunk(0, vols[0].shape[0], probs[0], lab_k)
             del x
+            continue
+        if cfg.skip_eps is not None:  # brick-skip rule: decided bricks keep the upsampled parent
+            probs[k], stats[k], skipped[k] = _solve_level_skipping(vols[k], seed_levels[k], brick, probs[k + 1],
+                                                                   cfg, want_labels and k == 0, workspace)
+            if k == 0:
+                lab = probs[0].gt(0.5).to(torch.uint8) if want_labels else None
+                if on_level0_chunk is not None:
+                    on_level0_chunk(0, vols[0].shape[0], probs[0], lab)
             continue
         if k == 0 and level0_chunks is None:  # measured: 8 slabs at 32768 bricks, 2 at 4096
             nb0 = math.prod(brick_grid(vols[0].shape, brick))
@@ -618,4 +662,7 @@ def hierarchical_random_walker(volume: torch.Tensor, seeds: torch.Tensor, brick,
     if volume.is_cuda:
         torch.cuda.current_stream().synchronize()
     stats = [_merge_stats(s) if isinstance(s, list) else _resolve(s) for s in stats]
+    for k, n in enumerate(skipped):
+        if n is not None:
+            stats[k] = dict(stats[k], skipped=n)
     return HRWResult(probs[0], lab, probs, vols, seed_levels, stats)

@@ -507,3 +507,26 @@ def test_two_phase_rejected_off_the_resident_path(rng):
     bound = cuda(rng.random(vol.shape).astype(np.float32))
     with pytest.raises(ValueError):  # 16^3 bricks: streaming path, no split
         device.solve_level(cuda(vol), cuda(seeds), (16, 16, 16), bound, GPU_CFG, phase="setup")
+
+
+@pytest.mark.parametrize("eps", [1e-3, 5e-2])
+def test_brick_skip_rule_matches_oracle(eps):
+    """The optional brick-skip rule (Drees 2022): decided bricks keep the upsampled parent; the
+    device and the float64 oracle make the same decisions and agree within the parity bar."""
+    shape, brick, levels = (128, 96, 64), (16, 16, 16), 3
+    vol = synthetic.phantom(shape)
+    seeds = synthetic.seeds(shape, "S1")
+    cfg = RWConfig(tol=1e-7, skip_eps=eps)
+    res = device.hierarchical_random_walker(cuda(vol), cuda(seeds), brick, levels, cfg)
+    ref = orw.hierarchical_random_walker(vol, seeds, brick, levels, orw.RWParams(tol=1e-10), skip_eps=eps)
+    assert_rw_parity(host(res.prob), ref.prob[0], host(res.labels))
+    skipped = 0
+    for k in range(levels - 1):
+        nb = int(np.prod([-(-n // b) for n, b in zip(res.volumes[k].shape, brick)]))
+        assert res.stats[k]["skipped"] + res.stats[k]["bricks"] == nb
+        skipped += res.stats[k]["skipped"]
+        bid, _ = orw.brick_ids(res.volumes[k].shape, brick)
+        bound = orw.upsample_linear(ref.prob[k + 1], res.volumes[k].shape)
+        want = orw.decided_bricks(bound, ref.seeds[k], brick, eps).sum()
+        assert abs(res.stats[k]["skipped"] - int(want)) <= max(2, nb // 100)  # the same decisions
+    assert skipped > 0 or eps < 1e-2

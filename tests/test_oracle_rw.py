@@ -188,3 +188,22 @@ def test_oracle_reproduces_frozen_fixture(name):
     g = load_golden(f"rw_{name}.npz")
     np.testing.assert_array_equal(res.prob[0].astype(np.float32), g["prob0"])
     np.testing.assert_array_equal(res.labels, g["labels"])
+
+
+def test_brick_skip_rule_oracle():
+    """decided_bricks: a brick is decided when the parent over it and its one-voxel halo is within
+    eps of 0 or 1 (seeds count as decided); skipped bricks keep the upsampled parent."""
+    bound = np.zeros((16, 16))
+    seeds = np.zeros((16, 16), np.uint8)
+    bound[3, 3] = 0.5           # inside brick (0, 0)
+    bound[8, 2] = 0.01          # row 8 = halo of brick (0, 0) and inside brick (1, 0)
+    seeds[12, 12] = 1
+    bound[12, 12] = 0.5         # seeded: decided anyway
+    d = rw.decided_bricks(bound, seeds, (8, 8), 1e-3)
+    assert d.tolist() == [False, True, False, True]
+    assert rw.decided_bricks(bound, seeds, (8, 8), 0.6).all()
+    vol = syn.phantom((48, 40))
+    sd = syn.seeds(vol.shape, "S1")
+    full = rw.hierarchical_random_walker(vol, sd, (8, 8), 3, rw.RWParams(tol=1e-10))
+    skip = rw.hierarchical_random_walker(vol, sd, (8, 8), 3, rw.RWParams(tol=1e-10), skip_eps=1e-6)
+    assert np.abs(full.prob[0] - skip.prob[0]).max() < 1e-4
