@@ -564,7 +564,10 @@ def run_ours(args, wl, rank, world):
                 "note": ("frac > 1: the brick-resident engine keeps every CG vector of a brick on chip (registers, "
                          "TMEM and SMEM of a 4-CTA cluster), so per-iteration traffic never reaches HBM; the HBM roofline of "
                          "the streaming algorithm (the 8(d) bytes) is beaten, and the kernel is bound by the "
-                         "latency of its per-iteration cluster reduction instead: onchip = live cycles per brick "
+                         "latency of its per-iteration cluster reduction instead (achieved counts 56 B per "
+                         "EXECUTED unknown-iteration: the default coarse-corrected engine runs a third fewer "
+                         "iterations than Jacobi-PCG for the same stop rule, so a faster solve reports a lower "
+                         "work rate); onchip = live cycles per brick "
                          "iteration per cluster, with the ncu issue / FMA-pipe activity and the bytes the kernel "
                          "really moves (hbm_frac_actual); traffic = ncu DRAM bytes of the level's launches, from "
                          "the profile named in onchip.profile"),

@@ -408,7 +408,7 @@ constexpr int LCPT = (LCOLS + LTH - 1) / LTH;             // columns per thread 
 __global__ void __launch_bounds__(LTH) lod_down3_kernel(const float* __restrict__ src, Shape3 fs,
                                                         float* __restrict__ dst, Shape3 cs) {
   __shared__ double A[2][LFY][LFX];
-  __shared__ double B[2][2 * LCY][LFX];
+  __shared__ __align__(16) double B[2][2 * LCY][LFX];
   const int tid = threadIdx.x;
   const int cx0 = blockIdx.x * LCX, cy0 = blockIdx.y * LCY, cz0 = blockIdx.z * LZC;
   const int fx0 = 2 * cx0 - 1, fy0 = 2 * cy0 - 1;
@@ -486,8 +486,10 @@ __global__ void __launch_bounds__(LTH) lod_down3_kernel(const float* __restrict_
       for (int cz = 0; cz < 2; ++cz)
 #pragma unroll
         for (int cy = 0; cy < 2; ++cy) {
-          const double* b = &B[cz][2 * oy + cy][2 * ox];
-          const double b0 = b[0], b1 = b[1], b2 = b[2], b3 = b[3];
+          // two 16-byte loads (2 ox doubles apart: 16-byte aligned) instead of four 8-byte ones
+          const double2* b = reinterpret_cast<const double2*>(&B[cz][2 * oy + cy][2 * ox]);
+          const double2 bl = b[0], bh = b[1];
+          const double b0 = bl.x, b1 = bl.y, b2 = bh.x, b3 = bh.y;
           C[cz][cy][0] = (float)conv3(b0, b1, b2);
           C[cz][cy][1] = (float)conv3(b1, b2, b3);
         }
