@@ -208,6 +208,17 @@ int rwb_chunks_gather(int32_t ndim, const int64_t* size, const int64_t* chunk, i
 int rwb_const_chunk_table(int32_t ndim, const int64_t* size, const int64_t* chunk, int32_t scalar_code,
                           const void* src, void* table, void* stream);
 
+/* Volume raycaster (the reference's `raycast` / `render_frame` final frame, render.py:101-631):
+ * marches n_px rays over an LOD pyramid of n_levels 3-D float32 levels (levels[k] device
+ * pointers, sizes 3 per level, spacing 3 per level, finest spacing ascending).  rays: per pixel 10
+ * doubles — origin (3), unit direction (3) from the reference's _pixel_rays, then its entry-exit
+ * record (t_entry, t_exit, fp0, fps) as float32 values (t_entry = +inf: miss).  compositing 0 =
+ * DVR (opacity-corrected front to back, early termination at 0.99), 1 = MOP; grey-ramp transfer
+ * function [tf_lo, tf_hi].  out: n_px premultiplied RGBA, uchar4 (out_u8) or float4. */
+int rwb_raycast(int32_t n_levels, const float* const* levels, const int64_t* sizes, const double* spacing,
+                int64_t n_px, const double* rays, int32_t compositing, double sample_distance_factor,
+                double lod_bias, double tf_lo, double tf_hi, int32_t out_u8, void* out, void* stream);
+
 /* Nearest-neighbour pan/zoom view (the reference's viewer: _resample_nn / slice_view /
  * image_view, render.py:640-741): frame pixel (p0, p1) of the (frame_size[0], frame_size[1])
  * frame samples source element floor((p + 0.5) * scale + offset) per axis (float64 math), 0

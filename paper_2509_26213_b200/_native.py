@@ -56,6 +56,9 @@ SIGNATURES = {
                                      c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "rwb_const_chunk_table": (c_int32, [c_int32, ctypes.POINTER(c_int64), ctypes.POINTER(c_int64), c_int32, c_void_p,
                                         c_void_p, c_void_p]),
+    "rwb_raycast": (c_int32, [c_int32, c_void_p, ctypes.POINTER(c_int64), ctypes.POINTER(ctypes.c_double), c_int64,
+                              c_void_p, c_int32, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                              c_int32, c_void_p, c_void_p]),
     "rwb_resample_nn": (c_int32, [c_int32, ctypes.POINTER(c_int64), c_int32, c_int64, c_int32, c_void_p,
                                   ctypes.POINTER(c_int64), ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(ctypes.c_double), c_void_p, c_void_p]),
