@@ -37,7 +37,7 @@ struct ResidentArgs {
   int* state;             // per slot
   int* iters;             // per slot
   int* next;              // dynamic brick counter (zero at launch)
-  int coarse;             // 4-CTA engine: coarse-corrected PCG (8^3 aggregates) instead of Jacobi-PCG
+  int coarse;             // coarse-corrected PCG (4-CTA engine: 8^3 aggregates, 2-D engine: 8^2) instead of Jacobi-PCG
   float tol2;
   int max_iter;
   // results straight into the level: prob = s y (unknowns) or y, labels = prob > 0.5
