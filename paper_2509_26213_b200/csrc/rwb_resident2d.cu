@@ -35,14 +35,10 @@ constexpr int NW2 = TH2 / 32;     // warps
 constexpr int PV2 = Q2 * Q2;      // pixels per thread
 
 struct Resident2dSmem {
-  float4 rp[T2][QN2];   // the tile's r (y neighbours of the SpMV)
-  float4 wpart[2][NW2];  // per-warp (r.r, delta, r.u), double-buffered by iteration parity
-  // coarse correction: 8 x 8 aggregates of 8 x 8 pixels (2 x 2 thread quads), index ay * 8 + ax
-  float aggw[64], aggr[64];  // this iteration's P^T w, P^T r (P^T r0, d at the tile's start)
-  float cc[64];              // c per aggregate
-  float cps[64], cdi[64];    // P^T s, 1 / d
+  float4 rp[T2][QN2];    // the tile's r (Jacobi) or u = M r (CC): the y neighbours of the SpMV
+  float4 wpart[2][NW2];  // per-warp (r.r, w.u, r.u), double-buffered by iteration parity
 };
-constexpr int NA2 = 8;           // aggregates per tile row / column
+constexpr int NA2 = 8;  // aggregates per tile row / column
 // omega 0.5 (the 3-D engine uses 0.8): tools/tile_cc_model.py, float64, stop at tol 1e-6 — on the
 // random tiles of test_resident2d_tiles_match_oracle the max error vs the exact solution is 1.2e-4
 // at 0.8 and 7.2e-5 at 0.5 (Jacobi-PCG: 7.9e-5), iterations x0.83 at both; on phantom tiles x0.53
@@ -59,9 +55,13 @@ __device__ __forceinline__ float rcp_ftz2(float x) {
   return y;
 }
 
-// CC: Jacobi + additive coarse correction M = I + w P D_c^-1 P^T on the tile's 8 x 8 aggregates
-// (the 3-D engine's, csrc/rwb_resident4.cu header, CTA-local here: each aggregate's 4 threads share
-// a warp, so its sums are two shuffles and one shared-memory store)
+// CC: PCG with M = I + w P D_c^-1 P^T on the tile's 8 x 8 aggregates of 8 x 8 pixels (one damped
+// Jacobi sweep of the Galerkin coarse system, the 3-D engine's correction, csrc/rwb_resident4.cu).
+// An aggregate is 2 x 2 thread quads inside one warp, so P^T r is a 2-shuffle warp sum and every
+// thread forms its own aggregate's c = w (P^T r) / d: u = M r is explicit (u = r + c on the
+// unknowns, 0 elsewhere), the SpMV runs on u (w = A'u) and publishes u instead of r, and the
+// iteration is plain Chronopoulos-Gear PCG (gamma = r.u, delta = w.u; r.r drives the stop rule) —
+// no coarse state in shared memory, no extra barrier.
 template <bool CC>
 __global__ void __launch_bounds__(TH2, 1) resident2d_kernel(ResidentArgs a) {
   __shared__ Resident2dSmem sm;
@@ -71,22 +71,19 @@ __global__ void __launch_bounds__(TH2, 1) resident2d_kernel(ResidentArgs a) {
   const int n_act = *a.n_active;
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
   const int tile_vox = T2 * T2;
-  const int ax = xq >> 1, ay = yq >> 1, agg = ay * NA2 + ax;
-  const int agg_x = (xq & 1) ? (ax < NA2 - 1 ? agg + 1 : agg) : (ax > 0 ? agg - 1 : agg);
-  const int agg_y = (yq & 1) ? (ay < NA2 - 1 ? agg + NA2 : agg) : (ay > 0 ? agg - NA2 : agg);
-  // the 4 threads of an aggregate: lanes xq, xq^1 of both quad rows of the warp
+  // the 4 threads of an aggregate: lanes xq, xq^1 of the warp's two quad rows (fixed order)
   auto agg_sum = [&](float v) {
     v += __shfl_xor_sync(0xffffffffu, v, 1);
     v += __shfl_xor_sync(0xffffffffu, v, 16);
     return v;
   };
-  const bool agg_lead = (lane & 17) == 0;
 
   for (int j = blockIdx.x; j < n_act; j += gridDim.x) {
     const int slot = a.alist[j];
     const long long base = (long long)slot * tile_vox;
     // ---- registers from the brick-local system (coalesced 16 B loads) ----
     float y[PV2], r[PV2], p[PV2], sv[PV2], w[PV2], wxf[PV2], wyf[PV2], wxb[Q2], wyb[Q2];
+    float u[CC ? PV2 : 1];
 #pragma unroll
     for (int i = 0; i < Q2; ++i) {
       const long long o = base + (long long)(Q2 * yq + i) * T2 + Q2 * xq;
@@ -113,10 +110,20 @@ __global__ void __launch_bounds__(TH2, 1) resident2d_kernel(ResidentArgs a) {
       for (int k = 0; k < Q2; ++k) wyb[k] = q4l(fyb, k);
     }
     const float thresh = (float)((double)a.tol2 * a.bb[slot]);
-    // coarse correction: tau = m - sigma per pixel, the aggregate diagonals and P^T r0
-    float tau[CC ? PV2 : 1];
+    // coarse correction: the unknown mask, the aggregate's Galerkin diagonal d = sum over its
+    // pixels of (m - sigma) + the weights leaving it, and u0
+    unsigned mbits = 0;
+    float cw = 0.f;  // w / d of the thread's aggregate
+    auto form_u = [&]() {
+      float rs4[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) rs4[k] = (r[k] + r[k + 4]) + (r[k + 8] + r[k + 12]);
+      const float c = cw * agg_sum((rs4[0] + rs4[1]) + (rs4[2] + rs4[3]));
+#pragma unroll
+      for (int v = 0; v < PV2; ++v) u[v] = (mbits >> v) & 1u ? r[v] + c : 0.f;
+    };
     if (CC) {
-      float dpart = 0.f, gpart = 0.f;
+      float dpart = 0.f;
 #pragma unroll
       for (int i = 0; i < Q2; ++i) {
         const float4 s4 = __ldg(reinterpret_cast<const float4*>(a.sc + base + (long long)(Q2 * yq + i) * T2 + Q2 * xq));
@@ -125,29 +132,24 @@ __global__ void __launch_bounds__(TH2, 1) resident2d_kernel(ResidentArgs a) {
           const int v = i * Q2 + k;
           const float wxl = k > 0 ? wxf[v - 1] : wxb[i];
           const float wyl = i > 0 ? wyf[v - Q2] : wyb[k];
-          const float t = (q4l(s4, k) > 0.f ? 1.f : 0.f) - ((wxf[v] + wxl) + (wyf[v] + wyl));
-          tau[v] = t;
-          dpart += t;
-          gpart += r[v];
-          if (i == 0 && !(yq & 1)) dpart += wyl;            // edges leaving the aggregate
+          const bool m = q4l(s4, k) > 0.f;
+          mbits |= (m ? 1u : 0u) << v;
+          dpart += (m ? 1.f : 0.f) - ((wxf[v] + wxl) + (wyf[v] + wyl));
+          if (i == 0 && !(yq & 1)) dpart += wyl;  // edges leaving the aggregate
           if (i == Q2 - 1 && (yq & 1)) dpart += wyf[v];
           if (k == 0 && !(xq & 1)) dpart += wxl;
           if (k == Q2 - 1 && (xq & 1)) dpart += wxf[v];
         }
       }
-      const float dv = agg_sum(dpart), gv = agg_sum(gpart);
-      if (agg_lead) {
-        sm.cdi[agg] = dv > 1e-6f ? 1.f / dv : 0.f;
-        sm.aggr[agg] = gv;
-        sm.cps[agg] = 0.f;
-      }
-      __syncthreads();
-      if (tid < 64) sm.cc[tid] = kCc2Omega * sm.aggr[tid] * sm.cdi[tid];
+      const float d = agg_sum(dpart);
+      cw = d > 1e-6f ? kCc2Omega / d : 0.f;
+      form_u();
     }
     auto publish = [&]() {
+      const float* q = CC ? u : r;
 #pragma unroll
       for (int i = 0; i < Q2; ++i)
-        sm.rp[Q2 * yq + i][xq] = make_float4(r[i * Q2], r[i * Q2 + 1], r[i * Q2 + 2], r[i * Q2 + 3]);
+        sm.rp[Q2 * yq + i][xq] = make_float4(q[i * Q2], q[i * Q2 + 1], q[i * Q2 + 2], q[i * Q2 + 3]);
     };
     publish();
     __syncthreads();
@@ -155,79 +157,57 @@ __global__ void __launch_bounds__(TH2, 1) resident2d_kernel(ResidentArgs a) {
     float alpha = 0.f, rgamma = 0.f, ralpha = 0.f;  // 1/gamma, 1/alpha one iteration ahead
     int state = ST_ACTIVE, it = 0;
     for (int pass = 0;; ++pass) {
-      // ---- w = A'u (u = r + c of the pixel's aggregate), partial dots ----
-      const float4 rd = yq > 0 ? sm.rp[Q2 * yq - 1][xq] : z4;
-      const float4 ru = yq + 1 < QN2 ? sm.rp[Q2 * yq + Q2][xq] : z4;
-      float gs = 0.f, ds = 0.f, rs = 0.f, ws = 0.f;
-      float c_own = 0.f, dxc = 0.f, dyc = 0.f;
-      if (CC) {
-        c_own = sm.cc[agg];
-        dxc = sm.cc[agg_x] - c_own;
-        dyc = sm.cc[agg_y] - c_own;
-      }
+      // ---- w = A'q (q = u with CC, else r), partial dots ----
+      const float* q = CC ? u : r;
+      const float4 qd = yq > 0 ? sm.rp[Q2 * yq - 1][xq] : z4;
+      const float4 qu = yq + 1 < QN2 ? sm.rp[Q2 * yq + Q2][xq] : z4;
+      float rs2[2] = {0.f, 0.f}, ds2[2] = {0.f, 0.f}, us2[2] = {0.f, 0.f};  // two chains each (latency)
 #pragma unroll
       for (int i = 0; i < Q2; ++i) {
-        const float rl = __shfl_up_sync(0xffffffffu, r[i * Q2 + Q2 - 1], 1);
-        const float rr_ = __shfl_down_sync(0xffffffffu, r[i * Q2], 1);
+        const float ql = __shfl_up_sync(0xffffffffu, q[i * Q2 + Q2 - 1], 1);
+        const float qr = __shfl_down_sync(0xffffffffu, q[i * Q2], 1);
 #pragma unroll
         for (int k = 0; k < Q2; ++k) {
           const int v = i * Q2 + k;
-          const float rxl = k > 0 ? r[v - 1] : rl;
-          const float rxr = k < Q2 - 1 ? r[v + 1] : rr_;
+          const float qxl = k > 0 ? q[v - 1] : ql;
+          const float qxr = k < Q2 - 1 ? q[v + 1] : qr;
           const float wxl = k > 0 ? wxf[v - 1] : wxb[i];
-          const float ryd = i > 0 ? r[v - Q2] : q4l(rd, k);
-          const float ryu = i < Q2 - 1 ? r[v + Q2] : q4l(ru, k);
+          const float qyd = i > 0 ? q[v - Q2] : q4l(qd, k);
+          const float qyu = i < Q2 - 1 ? q[v + Q2] : q4l(qu, k);
           const float wyl = i > 0 ? wyf[v - Q2] : wyb[k];
-          float acc = wyf[v] * ryu;
-          acc = fmaf(wyl, ryd, acc);
-          acc = fmaf(wxf[v], rxr, acc);
-          acc = fmaf(wxl, rxl, acc);
-          w[v] = r[v] - acc;
-          if (CC) {  // + c_own tau - the aggregate-face differences
-            float kk = c_own * tau[v];
-            if (i == 0 && !(yq & 1)) kk = fmaf(-wyl, dyc, kk);
-            if (i == Q2 - 1 && (yq & 1)) kk = fmaf(-wyf[v], dyc, kk);
-            if (k == 0 && !(xq & 1)) kk = fmaf(-wxl, dxc, kk);
-            if (k == Q2 - 1 && (xq & 1)) kk = fmaf(-wxf[v], dxc, kk);
-            w[v] += kk;
-          }
-          gs = fmaf(r[v], r[v], gs);
-          ds = fmaf(w[v], r[v], ds);
-          if (CC) {
-            rs += r[v];
-            ws += w[v];
-          }
+          float acc = wyf[v] * qyu;
+          acc = fmaf(wyl, qyd, acc);
+          acc = fmaf(wxf[v], qxr, acc);
+          acc = fmaf(wxl, qxl, acc);
+          w[v] = q[v] - acc;
+          rs2[k & 1] = fmaf(r[v], r[v], rs2[k & 1]);
+          ds2[k & 1] = fmaf(w[v], q[v], ds2[k & 1]);
+          if (CC) us2[k & 1] = fmaf(r[v], q[v], us2[k & 1]);
         }
       }
-      // ---- CTA reduction (fixed order); CC: gamma = r.u = r.r + c P^T r, delta = w.u = w.r + c P^T w ----
-      float us = gs;
-      if (CC) {
-        const float pr = agg_sum(rs), pw = agg_sum(ws);
-        if (agg_lead) {
-          sm.aggr[agg] = pr;
-          sm.aggw[agg] = pw;
-        }
-        us = fmaf(c_own, rs, gs);
-        ds = fmaf(c_own, ws, ds);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        gs += __shfl_xor_sync(0xffffffffu, gs, o);
-        ds += __shfl_xor_sync(0xffffffffu, ds, o);
-        if (CC) us += __shfl_xor_sync(0xffffffffu, us, o);
-      }
+      // ---- CTA reduction (fixed order): transpose-reduce the three warp sums (6 shuffles, not
+      // 15; lanes 0-7 end with r.r, 8-15 with w.q, 16-23 with r.u), then a depth-3 tree over warps
       const int par = pass & 1;
-      if (lane == 0) sm.wpart[par][warp] = make_float4(gs, ds, us, 0.f);
-      __syncthreads();  // partials visible; every thread has read rp and cc (its SpMV is done)
-      float rr = 0.f, delta = 0.f, g_new = 0.f;
-#pragma unroll
-      for (int wv = 0; wv < NW2; ++wv) {
-        const float4 v = sm.wpart[par][wv];
-        rr += v.x;
-        delta += v.y;
-        g_new += v.z;
+      {
+        const float rs = rs2[0] + rs2[1], ds = ds2[0] + ds2[1], us = CC ? us2[0] + us2[1] : 0.f;
+        const bool hi = lane & 16, b3 = lane & 8;
+        const float x0 = (hi ? us : rs) + __shfl_xor_sync(0xffffffffu, hi ? rs : us, 16);
+        const float x1 = (hi ? 0.f : ds) + __shfl_xor_sync(0xffffffffu, hi ? ds : 0.f, 16);
+        float t = (b3 ? x1 : x0) + __shfl_xor_sync(0xffffffffu, b3 ? x0 : x1, 8);
+        t += __shfl_xor_sync(0xffffffffu, t, 4);
+        t += __shfl_xor_sync(0xffffffffu, t, 2);
+        t += __shfl_xor_sync(0xffffffffu, t, 1);
+        if ((lane & 7) == 0 && lane < 24) reinterpret_cast<float*>(&sm.wpart[par][warp])[lane >> 3] = t;
       }
-      if (!CC) g_new = rr;
+      __syncthreads();  // partials visible; every thread has read rp (its SpMV is done)
+      float4 wp[NW2];
+#pragma unroll
+      for (int wv = 0; wv < NW2; ++wv) wp[wv] = sm.wpart[par][wv];
+      static_assert(NW2 == 8, "warp-sum tree");
+      const float rr = ((wp[0].x + wp[1].x) + (wp[2].x + wp[3].x)) + ((wp[4].x + wp[5].x) + (wp[6].x + wp[7].x));
+      const float delta = ((wp[0].y + wp[1].y) + (wp[2].y + wp[3].y)) + ((wp[4].y + wp[5].y) + (wp[6].y + wp[7].y));
+      const float g_new =
+          CC ? ((wp[0].z + wp[1].z) + (wp[2].z + wp[3].z)) + ((wp[4].z + wp[5].z) + (wp[6].z + wp[7].z)) : rr;
       float beta;
       if (pass == 0) {
         beta = 0.f;
@@ -251,22 +231,17 @@ __global__ void __launch_bounds__(TH2, 1) resident2d_kernel(ResidentArgs a) {
       }
       rgamma = rcp_ftz2(g_new);
       ralpha = rcp_ftz2(alpha);
-      // ---- update: p = u + beta p, s = w + beta s, y += alpha p, r -= alpha s ----
-      if (CC && tid < 64) {  // the next c from P^T r' = P^T r - alpha (P^T w + beta P^T s)
-        const float ps = fmaf(beta, sm.cps[tid], sm.aggw[tid]);
-        sm.cps[tid] = ps;
-        sm.cc[tid] = kCc2Omega * fmaf(-alpha, ps, sm.aggr[tid]) * sm.cdi[tid];
-      }
+      // ---- update: p = q + beta p, s = w + beta s, y += alpha p, r -= alpha s ----
 #pragma unroll
       for (int v = 0; v < PV2; ++v) {
-        p[v] = fmaf(beta, p[v], CC ? r[v] + c_own : r[v]);  // u off the unknowns is harmless: y0 is
-                                                            // restored there in the epilogue
+        p[v] = fmaf(beta, p[v], q[v]);
         sv[v] = fmaf(beta, sv[v], w[v]);
         y[v] = fmaf(alpha, p[v], y[v]);
         r[v] = fmaf(-alpha, sv[v], r[v]);
       }
       ++it;
-      publish();  // the barrier above proved every reader of the previous r has finished
+      if (CC) form_u();
+      publish();  // the barrier above proved every reader of the previous q has finished
       __syncthreads();
     }
     // ---- epilogue: probabilities and labels straight into the level ----
@@ -279,13 +254,11 @@ __global__ void __launch_bounds__(TH2, 1) resident2d_kernel(ResidentArgs a) {
       for (int i = 0; i < Q2; ++i) {
         const int gy = a.oy + hy * T2 + Q2 * yq + i;
         if (gy < 0 || gy >= a.ny) continue;
-        const long long o = base + (long long)(Q2 * yq + i) * T2 + Q2 * xq;
-        const float4 s4 = __ldg(reinterpret_cast<const float4*>(a.sc + o));
-        const float4 y0 = CC ? __ldg(reinterpret_cast<const float4*>(a.y + o)) : z4;
+        const float4 s4 = __ldg(reinterpret_cast<const float4*>(a.sc + base + (long long)(Q2 * yq + i) * T2 + Q2 * xq));
         float pv[Q2];
 #pragma unroll
         for (int k = 0; k < Q2; ++k) {
-          const float s = q4l(s4, k), yv = CC && !(s > 0.f) ? q4l(y0, k) : y[i * Q2 + k];
+          const float s = q4l(s4, k), yv = y[i * Q2 + k];
           pv[k] = s > 0.f ? s * yv : yv;
         }
         const long long gi = (long long)gy * a.nx + gx0;

@@ -27,8 +27,10 @@ P = orw.RWParams(tol=1e-10)
 bid, nb = orw.brick_ids(shape, (B, B))
 S = orw.assemble(vol, seeds, bid, nb, bound, P)
 x_ref, _, _ = orw.pcg(S, bound, orw.RWParams(tol=1e-10))
-worst = {"jacobi": 0.0, "cc": 0.0}
-its = {"jacobi": 0, "cc": 0}
+EXTRA = "extra" in sys.argv
+OM2 = float(sys.argv[sys.argv.index("extra") + 1]) if EXTRA and len(sys.argv) > sys.argv.index("extra") + 1 else 0.8
+worst = {k: 0.0 for k in ["jacobi", "cc", "exact", "j2", "j3"]}
+its = {k: 0 for k in worst}
 for b in range(nb):
     by, bx = np.unravel_index(b, (shape[0] // B, shape[1] // B))
     sl = (slice(by * B, by * B + B), slice(bx * B, bx * B + B))
@@ -55,6 +57,17 @@ for b in range(nb):
         e = np.zeros(nc); e[j] = 1; Ac[:, j] = agg(A(Pm(e.reshape(na, na)))).ravel()
     dg = np.diag(Ac); dci = np.where(dg > 1e-6, 1 / np.where(dg > 1e-6, dg, 1), 0)
     precs = {"jacobi": lambda r: r, "cc": lambda r: r + Pm((OM * dci * agg(r).ravel()).reshape(na, na))}
+    if EXTRA:
+        live = dg > 1e-6
+        Acl = Ac.copy(); Acl[~live, :] = 0; Acl[:, ~live] = 0; Acl[~live, ~live] = 1
+        Aci = np.linalg.inv(Acl)
+        def cj(r, k):
+            g = agg(r).ravel(); c = OM2 * dci * g
+            for _ in range(k - 1): c = c + OM2 * dci * (g - Ac @ c)
+            return Pm(c.reshape(na, na))
+        precs["exact"] = lambda r: r + Pm((Aci @ agg(r).ravel()).reshape(na, na))
+        precs["j2"] = lambda r: r + cj(r, 2)
+        precs["j3"] = lambda r: r + cj(r, 3)
     out = [b]
     bb2 = (rhs ** 2).sum()
     for nm, pr in precs.items():
@@ -64,5 +77,5 @@ for b in range(nb):
         err = np.abs(np.where(unk, y * s, 0) - np.where(unk, x_ref[sl], 0)).max()
         worst[nm] = max(worst[nm], err); its[nm] += it
         out += [nm, it, f"{err:.1e}"]
-    if len(sys.argv) > 4: print(*out, flush=True)
+    if "v" in sys.argv[4:]: print(*out, flush=True)
 print("worst", {k: f"{v:.2e}" for k, v in worst.items()}, "iterations", its)
