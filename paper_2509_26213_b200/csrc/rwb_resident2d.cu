@@ -23,6 +23,7 @@
 #include <cstdlib>
 
 #include "rwb_common.cuh"
+#include "rwb_ptx.cuh"
 #include "rwb_resident.cuh"
 
 namespace rwb {
@@ -167,22 +168,23 @@ __global__ void __launch_bounds__(TH2, 1) resident2d_kernel(ResidentArgs a) {
         const float ql = __shfl_up_sync(0xffffffffu, q[i * Q2 + Q2 - 1], 1);
         const float qr = __shfl_down_sync(0xffffffffu, q[i * Q2], 1);
 #pragma unroll
-        for (int k = 0; k < Q2; ++k) {
+        for (int k = 0; k < Q2; k += 2) {  // pixel pairs (k, k+1) on the packed f32x2 FMA
           const int v = i * Q2 + k;
-          const float qxl = k > 0 ? q[v - 1] : ql;
-          const float qxr = k < Q2 - 1 ? q[v + 1] : qr;
-          const float wxl = k > 0 ? wxf[v - 1] : wxb[i];
-          const float qyd = i > 0 ? q[v - Q2] : q4l(qd, k);
-          const float qyu = i < Q2 - 1 ? q[v + Q2] : q4l(qu, k);
-          const float wyl = i > 0 ? wyf[v - Q2] : wyb[k];
-          float acc = wyf[v] * qyu;
-          acc = fmaf(wyl, qyd, acc);
-          acc = fmaf(wxf[v], qxr, acc);
-          acc = fmaf(wxl, qxl, acc);
-          w[v] = q[v] - acc;
-          rs2[k & 1] = fmaf(r[v], r[v], rs2[k & 1]);
-          ds2[k & 1] = fmaf(w[v], q[v], ds2[k & 1]);
-          if (CC) us2[k & 1] = fmaf(r[v], q[v], us2[k & 1]);
+          float acc0, acc1;
+          const float qyd0 = i > 0 ? q[v - Q2] : q4l(qd, k), qyd1 = i > 0 ? q[v + 1 - Q2] : q4l(qd, k + 1);
+          const float qyu0 = i < Q2 - 1 ? q[v + Q2] : q4l(qu, k), qyu1 = i < Q2 - 1 ? q[v + 1 + Q2] : q4l(qu, k + 1);
+          const float wyl0 = i > 0 ? wyf[v - Q2] : wyb[k], wyl1 = i > 0 ? wyf[v + 1 - Q2] : wyb[k + 1];
+          fma2(acc0, acc1, wyf[v], wyf[v + 1], qyu0, qyu1, 0.f, 0.f);
+          fma2(acc0, acc1, wyl0, wyl1, qyd0, qyd1, acc0, acc1);
+          // x neighbours straddle the pairs: scalar
+          acc0 = fmaf(wxf[v], q[v + 1], acc0);
+          acc0 = fmaf(k > 0 ? wxf[v - 1] : wxb[i], k > 0 ? q[v - 1] : ql, acc0);
+          acc1 = fmaf(wxf[v + 1], k + 1 < Q2 - 1 ? q[v + 2] : qr, acc1);
+          acc1 = fmaf(wxf[v], q[v], acc1);
+          fma2(w[v], w[v + 1], -1.f, -1.f, acc0, acc1, q[v], q[v + 1]);
+          fma2(rs2[0], rs2[1], r[v], r[v + 1], r[v], r[v + 1], rs2[0], rs2[1]);
+          fma2(ds2[0], ds2[1], w[v], w[v + 1], q[v], q[v + 1], ds2[0], ds2[1]);
+          if (CC) fma2(us2[0], us2[1], r[v], r[v + 1], q[v], q[v + 1], us2[0], us2[1]);
         }
       }
       // ---- CTA reduction (fixed order): transpose-reduce the three warp sums (6 shuffles, not
@@ -233,11 +235,11 @@ __global__ void __launch_bounds__(TH2, 1) resident2d_kernel(ResidentArgs a) {
       ralpha = rcp_ftz2(alpha);
       // ---- update: p = q + beta p, s = w + beta s, y += alpha p, r -= alpha s ----
 #pragma unroll
-      for (int v = 0; v < PV2; ++v) {
-        p[v] = fmaf(beta, p[v], q[v]);
-        sv[v] = fmaf(beta, sv[v], w[v]);
-        y[v] = fmaf(alpha, p[v], y[v]);
-        r[v] = fmaf(-alpha, sv[v], r[v]);
+      for (int v = 0; v < PV2; v += 2) {
+        fma2(p[v], p[v + 1], beta, beta, p[v], p[v + 1], q[v], q[v + 1]);
+        fma2(sv[v], sv[v + 1], beta, beta, sv[v], sv[v + 1], w[v], w[v + 1]);
+        fma2(y[v], y[v + 1], alpha, alpha, p[v], p[v + 1], y[v], y[v + 1]);
+        fma2(r[v], r[v + 1], -alpha, -alpha, sv[v], sv[v + 1], r[v], r[v + 1]);
       }
       ++it;
       if (CC) form_u();

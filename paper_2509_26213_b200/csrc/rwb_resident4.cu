@@ -432,9 +432,14 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
         float ta[12];
         uint32_t ad = tb + 16 * z;
         if (z > 0) asm volatile("" : "+r"(ad) : "f"(w[z * RQ - 1]));
+#ifdef RWB_EXP_NOTMEM  // diagnostics only: the SpMV without its TMEM latency (wrong weights)
+#pragma unroll
+        for (int k = 0; k < 12; ++k) ta[k] = 0.01f * (float)(k + 1) + 1e-9f * (float)ad;
+#else
         tmem_ld8(ad, ta);
         tmem_ld4p(ad + 8, ta + 8);
         tmem_wait_ld12(ta);
+#endif
         const float4 wy4 = f4(ta[0], ta[1], ta[2], ta[3]);
         const float4 wyb4 = f4(ta[4], ta[5], ta[6], ta[7]);
         const float4 wz4 = f4(ta[8], ta[9], ta[10], ta[11]);
@@ -458,6 +463,10 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
         float tx[9];  // w'x of the quad and the one left of it (+ tau), once the y / z terms are done
         uint32_t adx = tb + 16 * z + 12, adl = tb + C::TAIL + z;
         asm volatile("" : "+r"(adx), "+r"(adl) : "f"(acc[0]), "f"(acc[2]));
+#ifdef RWB_EXP_NOTMEM
+#pragma unroll
+        for (int k = 0; k < 9; ++k) tx[k] = 0.01f * (float)(k + 1) + 1e-9f * (float)(adx + adl);
+#else
         tmem_ld4p(adx, tx);
         tmem_ld1(adl, tx[4]);
         if (CC) {
@@ -466,6 +475,7 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
         } else {
           tmem_wait_ld5(tx);
         }
+#endif
         const float4 wx4 = f4(tx[0], tx[1], tx[2], tx[3]);
         const float wxl0 = tx[4];
 #pragma unroll

@@ -4,7 +4,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import numpy as np, torch
 from paper_2509_26213_b200 import _native
-_native.load_library(os.path.join(_native.LIB_DIR, "librwb_trace.so"))
+_native.load_library(os.path.join(_native.LIB_DIR, os.environ.get("RWB_TRACE_LIB", "librwb_trace.so")))
 from paper_2509_26213_b200 import device, synthetic
 from paper_2509_26213_b200.config import RWConfig
 shape = (256, 256, 256)
