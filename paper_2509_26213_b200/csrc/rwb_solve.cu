@@ -1108,6 +1108,346 @@ __global__ void __launch_bounds__(NTHREADS) cg_pass2_kernel(Geo g, Work w, int n
 }
 
 // ---------------------------------------------------------------------------
+// Column-marching CG passes (the default streaming passes).  A work item is a
+// column tile of a brick: TX x TY threads, each marching the brick's whole
+// extent along the march axis (3-D: z, planes of by*bx; 2-D: y, rows of bx,
+// thread row ty taking a segment of ceil(by / TY) rows), so an item carries
+// 4x (3-D 32^3) to 8x (2-D 64^2) the voxels of a cg_pass1/2 tile and its
+// start-up (slot, state, scalars) and brick reduction are amortised over
+// them.  Pass 1 keeps a two-plane-deep register pipeline (the loads of plane
+// m+2 are issued before plane m is computed) and takes the x neighbours of
+// p = r + beta p from the neighbouring lanes (a warp is one 32-voxel row
+// segment); pass 2 streams four planes per step.  Same arithmetic, same
+// per-brick fixed-order float64 reductions (over the brick's column items).
+struct ColCtx {
+  int slot, col, lx, ly, m0, m1;  // ly: 3-D row (2-D: 0); [m0, m1): march range of this thread
+  bool in;                        // column inside the brick box
+};
+
+__device__ __host__ __forceinline__ int col_items(const Geo& g) {
+  return g.is3d ? ((g.bx + TX - 1) / TX) * ((g.by + TY - 1) / TY) : (g.bx + TX - 1) / TX;
+}
+
+__device__ __forceinline__ ColCtx col_ctx(const Geo& g, int slot, int col) {
+  ColCtx c;
+  c.slot = slot;
+  c.col = col;
+  const int ntx = (g.bx + TX - 1) / TX;
+  c.lx = (col % ntx) * TX + threadIdx.x;
+  if (g.is3d) {
+    c.ly = (col / ntx) * TY + threadIdx.y;
+    c.m0 = 0;
+    c.m1 = g.bz;
+    c.in = c.lx < g.bx && c.ly < g.by;
+  } else {
+    const int my = (g.by + TY - 1) / TY;
+    c.ly = 0;
+    c.m0 = min(threadIdx.y * my, g.by);
+    c.m1 = min(c.m0 + my, g.by);
+    c.in = c.lx < g.bx && c.m0 < c.m1;
+  }
+  return c;
+}
+
+__global__ void __launch_bounds__(NTHREADS) cg_pass1_col_kernel(Geo g, Work w, int nb, int j) {
+  const int ncol = col_items(g);
+  const int n_items = *w.n_active * ncol;
+  const int par = j & 1;
+  const int it = *w.base_it + j;
+  const float* __restrict__ pin = par ? w.p1 : w.p0;
+  float* __restrict__ pout = par ? w.p0 : w.p1;
+  float* __restrict__ Q = w.q;
+  const float* __restrict__ R = w.r;
+  const float* __restrict__ WM = g.is3d ? w.wz : w.wy;  // weight along the march axis
+  const long long sm_ = g.is3d ? (long long)g.by * g.bx : (long long)g.bx;
+  const int nm = g.is3d ? g.bz : g.by;
+  const int lane = threadIdx.x;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int slot = w.alist[item / ncol];
+    if (w.state[slot] != ST_ACTIVE) continue;  // uniform per CTA
+    const ColCtx c = col_ctx(g, slot, item % ncol);
+    const double rr = w.rr[(long long)par * nb + slot];
+    const double rr_prev = w.rr[(long long)(par ^ 1) * nb + slot];
+    const float beta = (it == 0 || rr_prev <= 0.0) ? 0.f : (float)(rr / rr_prev);
+    float acc = 0.f;
+    // every lane of a row segment runs the march (shuffles need the whole warp); lanes outside
+    // the brick box load nothing and store nothing
+    const bool in = c.in;
+    const bool hx0 = in && c.lx > 0, hx1 = in && c.lx + 1 < g.bx;
+    const bool hy0 = g.is3d && in && c.ly > 0, hy1 = g.is3d && in && c.ly + 1 < g.by;
+    const bool ex0 = hx0 && lane == 0, ex1 = hx1 && lane == TX - 1;  // x neighbours outside the warp
+    const long long base = (long long)slot * g.bvol + (long long)c.ly * g.bx + c.lx;
+    auto ld = [&](const float* a, long long i, bool ok) { return ok ? __ldg(a + i) : 0.f; };
+    int m = c.m0;
+    long long li = base + (long long)m * sm_;
+    const bool any = in && m < c.m1;
+    // pipeline: (r, p) of planes m+1 and m+2 in flight; pm = pn(m - 1), pc = pn(m)
+    float pm = 0.f, wmm = 0.f;
+    if (any && m > 0) {
+      pm = ld(R, li - sm_, true) + beta * ld(pin, li - sm_, true);
+      wmm = ld(WM, li - sm_, true);
+    }
+    float pc = any ? ld(R, li, true) + beta * ld(pin, li, true) : 0.f;
+    bool ok1 = any && m + 1 < nm, ok2 = any && m + 2 < nm;
+    float r1 = ld(R, li + sm_, ok1), p1 = ld(pin, li + sm_, ok1);
+    float r2 = ld(R, li + 2 * sm_, ok2), p2 = ld(pin, li + 2 * sm_, ok2);
+    const int mend = __reduce_max_sync(0xffffffffu, any ? c.m1 : -1);  // warp-uniform trip count
+    for (; m < mend; ++m, li += sm_) {
+      const bool act = any && m < c.m1;
+      const bool ok3 = act && m + 3 < nm;
+      const float r3 = ld(R, li + 3 * sm_, ok3), p3 = ld(pin, li + 3 * sm_, ok3);
+      const bool up = act && m + 1 < nm;
+      const float pp = up ? r1 + beta * p1 : 0.f;
+      const float wmc = ld(WM, li, up);
+      float s = wmc * pp + wmm * pm;
+      const float wxr = ld(w.wx, li, act && hx1), wxl = ld(w.wx, li - 1, act && hx0);
+      float xr = __shfl_down_sync(0xffffffffu, pc, 1), xl = __shfl_up_sync(0xffffffffu, pc, 1);
+      if (act && ex1) xr = __ldg(R + li + 1) + beta * __ldg(pin + li + 1);
+      if (act && ex0) xl = __ldg(R + li - 1) + beta * __ldg(pin + li - 1);
+      if (act && hx1) s += wxr * xr;
+      if (act && hx0) s += wxl * xl;
+      if (g.is3d) {
+        if (act && hy1) s += __ldg(w.wy + li) * (__ldg(R + li + g.bx) + beta * __ldg(pin + li + g.bx));
+        if (act && hy0) s += __ldg(w.wy + li - g.bx) * (__ldg(R + li - g.bx) + beta * __ldg(pin + li - g.bx));
+      }
+      if (act) {
+        const float q = pc - s;
+        pout[li] = pc;
+        Q[li] = q;
+        acc += pc * q;
+      }
+      pm = pc;
+      pc = pp;
+      wmm = wmc;
+      r1 = r2, p1 = p2, r2 = r3, p2 = p3;
+    }
+    double pq, unused;
+    if (brick_reduce(g, w, slot, c.col, acc, 0.f, &pq, &unused, ncol)) w.pq[slot] = pq;
+  }
+}
+
+// 3-D pass 1 with the operands staged through shared memory: per plane, r and p of the tile's 8
+// rows plus one halo row each side, w'x, w'y (with the row below), w'z — 45 rows of 32 floats —
+// copied by cp.async (4 B per lane, zero-filled outside the brick) KS planes ahead of the march,
+// so every thread has KS - 1 planes of loads in flight without holding them in registers.  The
+// arithmetic (operand values and order) is cg_pass1_col_kernel's.
+constexpr int KS = 8;           // stages (a plane of compute is ~0.1 us: 6 planes in flight cover the DRAM latency)
+struct StgPlane {
+  float r[TY + 2][TX], p[TY + 2][TX], wx[TY][TX], wy[TY + 1][TX], wz[TY][TX];
+};
+
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, bool ok) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(d), "l"(ok ? src : dst), "r"(ok ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const float* src, bool ok) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+
+// VEC: 16-byte copies (brick rows a multiple of 4 floats), 360 per plane over the CTA's 256 threads
+template <bool VEC>
+__global__ void __launch_bounds__(NTHREADS, 3) cg_pass1_stg_kernel(Geo g, Work w, int nb, int j) {
+  __shared__ __align__(16) StgPlane st[KS];
+  const int ncol = col_items(g);
+  const int n_items = *w.n_active * ncol;
+  const int par = j & 1;
+  const int it = *w.base_it + j;
+  const float* __restrict__ pin = par ? w.p1 : w.p0;
+  float* __restrict__ pout = par ? w.p0 : w.p1;
+  float* __restrict__ Q = w.q;
+  const float* __restrict__ R = w.r;
+  const long long sbz = (long long)g.by * g.bx;
+  const int lane = threadIdx.x, warp = threadIdx.y;
+  const int ntx = (g.bx + TX - 1) / TX;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int slot = w.alist[item / ncol];
+    if (w.state[slot] != ST_ACTIVE) continue;  // uniform per CTA
+    const int col = item % ncol;
+    const int x0 = (col % ntx) * TX, y0 = (col / ntx) * TY;
+    const int lx = x0 + lane, ly = y0 + warp;
+    const double rr = w.rr[(long long)par * nb + slot];
+    const double rr_prev = w.rr[(long long)(par ^ 1) * nb + slot];
+    const float beta = (it == 0 || rr_prev <= 0.0) ? 0.f : (float)(rr / rr_prev);
+    const long long sbase = (long long)slot * g.bvol;
+    const bool xin = lx < g.bx;
+    // this warp's copy rows (fixed per item): r, p and w'y of brick row y0 - 1 + warp (stage rows
+    // warp), w'x and w'z of row y0 + warp; warps 0-1 also r, p of rows y0 + 7 + warp (stage rows
+    // 8 + warp), warp 0 also w'y of row y0 + 7 (stage row 8)
+    // VEC: chunk q of this thread = plane row k = c / 8 (StgPlane order), 4 floats at x0 + 4 (c % 8)
+    const float* vsrc[2];
+    uint32_t vdst[2];
+    bool vok[2];
+    if (VEC) {
+      const int tid = warp * TX + lane;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int c = tid + NTHREADS * q, k = c >> 3, xs = x0 + 4 * (c & 7);
+        const float* arr;
+        int row;
+        if (k < TY + 2) {
+          arr = R, row = y0 - 1 + k;
+        } else if (k < 2 * (TY + 2)) {
+          arr = pin, row = y0 - 1 + k - (TY + 2);
+        } else if (k < 2 * (TY + 2) + TY) {
+          arr = w.wx, row = y0 + k - 2 * (TY + 2);
+        } else if (k < 2 * (TY + 2) + 2 * TY + 1) {
+          arr = w.wy, row = y0 - 1 + k - 2 * (TY + 2) - TY;
+        } else {
+          arr = w.wz, row = y0 + k - 2 * (TY + 2) - 2 * TY - 1;
+        }
+        vok[q] = k < 45 && row >= 0 && row < g.by && xs < g.bx;
+        vsrc[q] = arr + sbase + (long long)(vok[q] ? row : 0) * g.bx + (vok[q] ? xs : 0);
+        vdst[q] = (uint32_t)__cvta_generic_to_shared(&st[0].r[0][0]) + 4u * (uint32_t)(k * TX + 4 * (c & 7));
+        if (k >= 45) vdst[q] = 0xffffffffu;  // no such chunk
+      }
+    }
+    const int ra = y0 - 1 + warp, rb = y0 + 7 + warp;
+    const bool oka = xin && ra >= 0 && ra < g.by, okb = xin && warp < 2 && rb < g.by;
+    const bool okc = xin && y0 + warp < g.by, okd = xin && warp == 0 && y0 + 7 < g.by;
+    const long long ga = sbase + (long long)ra * g.bx + lx;
+    const long long gb = ga + 8LL * g.bx;
+    auto issue = [&](int m) {
+      const bool inm = m < g.bz;
+      if (VEC) {
+        const uint32_t so = (uint32_t)((m % KS) * sizeof(StgPlane));
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          if (vdst[q] != 0xffffffffu) cp_async16(vdst[q] + so, vsrc[q] + (inm ? (long long)m * sbz : 0), inm && vok[q]);
+        return;
+      }
+      StgPlane& sp = st[m % KS];
+      const long long o = ga + (long long)m * sbz;
+      cp_async4(&sp.r[warp][lane], R + o, inm && oka);
+      cp_async4(&sp.p[warp][lane], pin + o, inm && oka);
+      cp_async4(&sp.wy[warp][lane], w.wy + o, inm && oka);
+      cp_async4(&sp.wx[warp][lane], w.wx + o + g.bx, inm && okc);
+      cp_async4(&sp.wz[warp][lane], w.wz + o + g.bx, inm && okc);
+      if (warp < 2) {
+        const long long ob = gb + (long long)m * sbz;
+        cp_async4(&sp.r[TY + warp][lane], R + ob, inm && okb);
+        cp_async4(&sp.p[TY + warp][lane], pin + ob, inm && okb);
+        if (warp == 0) cp_async4(&sp.wy[TY][lane], w.wy + ob, inm && okd);
+      }
+    };
+#pragma unroll
+    for (int m = 0; m < KS - 1; ++m) {
+      issue(m);
+      cp_async_commit();
+    }
+    const bool in = xin && ly < g.by;
+    const bool hx0 = in && lx > 0, hx1 = in && lx + 1 < g.bx;
+    const bool hy0 = in && ly > 0, hy1 = in && ly + 1 < g.by;
+    const bool ex0 = hx0 && lane == 0, ex1 = hx1 && lane == TX - 1;
+    long long li = sbase + (long long)ly * g.bx + lx;
+    float acc = 0.f, pm = 0.f, wzm = 0.f, pc = 0.f;
+    for (int m = 0; m < g.bz; ++m, li += sbz) {
+      cp_async_wait<KS - 3>();  // planes m and m + 1 have landed (this thread's copies)
+      __syncthreads();          // ... everyone's; and everyone is done with plane m - 1's stage
+      issue(m + KS - 1);        // refills plane m - 1's stage (zero-filled past the brick)
+      cp_async_commit();
+      const StgPlane& sc = st[m % KS];
+      const StgPlane& sn = st[(m + 1) % KS];
+      if (m == 0) pc = sc.r[warp + 1][lane] + beta * sc.p[warp + 1][lane];
+      const bool up = m + 1 < g.bz;
+      const float pp = up ? sn.r[warp + 1][lane] + beta * sn.p[warp + 1][lane] : 0.f;
+      const float wzc = up ? sc.wz[warp][lane] : 0.f;
+      float s = wzc * pp + wzm * pm;
+      const float wxo = sc.wx[warp][lane];
+      float xr = __shfl_down_sync(0xffffffffu, pc, 1), xl = __shfl_up_sync(0xffffffffu, pc, 1);
+      float wxl = __shfl_up_sync(0xffffffffu, wxo, 1);
+      if (ex1) xr = __ldg(R + li + 1) + beta * __ldg(pin + li + 1);
+      if (ex0) {
+        xl = __ldg(R + li - 1) + beta * __ldg(pin + li - 1);
+        wxl = __ldg(w.wx + li - 1);
+      }
+      if (hx1) s += wxo * xr;
+      if (hx0) s += wxl * xl;
+      if (hy1) s += sc.wy[warp + 1][lane] * (sc.r[warp + 2][lane] + beta * sc.p[warp + 2][lane]);
+      if (hy0) s += sc.wy[warp][lane] * (sc.r[warp][lane] + beta * sc.p[warp][lane]);
+      if (in) {
+        const float q = pc - s;
+        pout[li] = pc;
+        Q[li] = q;
+        acc += pc * q;
+      }
+      pm = pc;
+      pc = pp;
+      wzm = wzc;
+    }
+    cp_async_wait<0>();
+    double pq, unused;
+    if (brick_reduce(g, w, slot, col, acc, 0.f, &pq, &unused, ncol)) w.pq[slot] = pq;
+  }
+}
+
+__global__ void __launch_bounds__(NTHREADS) cg_pass2_col_kernel(Geo g, Work w, int nb, int j, float tol2,
+                                                                int max_iter) {
+  const int ncol = col_items(g);
+  const int n_items = *w.n_active * ncol;
+  const int par = j & 1;
+  const int it = *w.base_it + j;
+  const float* __restrict__ P = par ? w.p0 : w.p1;  // pass-1 output
+  const float* __restrict__ Q = w.q;
+  float* __restrict__ Y = w.y;
+  float* __restrict__ Rw = w.r;
+  const long long sm_ = g.is3d ? (long long)g.by * g.bx : (long long)g.bx;
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int slot = w.alist[item / ncol];
+    if (w.state[slot] != ST_ACTIVE) continue;
+    const ColCtx c = col_ctx(g, slot, item % ncol);
+    const double rr = w.rr[(long long)par * nb + slot];
+    const double pq = w.pq[slot];
+    const float alpha = pq != 0.0 ? (float)(rr / pq) : 0.f;
+    float acc = 0.f;
+    if (c.in) {
+      long long li = (long long)slot * g.bvol + (long long)c.ly * g.bx + c.lx + (long long)c.m0 * sm_;
+      int m = c.m0;
+      for (; m + 4 <= c.m1; m += 4, li += 4 * sm_) {
+        float y[4], r[4], pv[4], qv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          y[k] = Y[li + k * sm_];
+          r[k] = Rw[li + k * sm_];
+          pv[k] = __ldg(P + li + k * sm_);
+          qv[k] = __ldg(Q + li + k * sm_);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          y[k] += alpha * pv[k];
+          r[k] -= alpha * qv[k];
+          Y[li + k * sm_] = y[k];
+          Rw[li + k * sm_] = r[k];
+          acc += r[k] * r[k];
+        }
+      }
+      for (; m < c.m1; ++m, li += sm_) {
+        const float y = Y[li] + alpha * __ldg(P + li);
+        const float r = Rw[li] - alpha * __ldg(Q + li);
+        Y[li] = y;
+        Rw[li] = r;
+        acc += r * r;
+      }
+    }
+    double rr_new, unused;
+    if (brick_reduce(g, w, slot, c.col, acc, 0.f, &rr_new, &unused, ncol)) {
+      w.rr[(long long)(par ^ 1) * nb + slot] = rr_new;
+      if (rr_new <= (double)tol2 * w.bb[slot]) {
+        w.iters[slot] = it + 1;
+        w.state[slot] = ST_CONVERGED;
+      } else if (it + 1 >= max_iter) {
+        w.iters[slot] = it + 1;
+        w.state[slot] = ST_MAXITER;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Whole-level (single-brick) solve as ONE cooperative persistent kernel: every
 // iteration's two passes are separated by grid-wide barriers instead of kernel
 // launches, and the level's working set (~36 B/voxel, 75 MB at 128^3) stays in
@@ -1542,20 +1882,35 @@ static int readback(cudaStream_t st, const void* src, int at, int n) {
   return RWB_OK;
 }
 
-static int persistent_grid(int* grid) {
-  static DeviceCache cache;
+// persistent grids of the CG passes: [0] the plane-tile passes (and the default for other users),
+// [1] the staged 3-D pass 1, [2] the column-marching passes
+static int persistent_grid(int* grid, int* grids3 = nullptr) {
+  static DeviceCache cache[3];
   int dev = 0;
   if (int rc = device_slot(&dev)) return rc;
-  int cached = cache[dev].load(std::memory_order_relaxed);
+  int cached = cache[0][dev].load(std::memory_order_relaxed);
   if (!cached) {
-    int sms = 0, per1 = 0, per2 = 0;
+    int sms = 0, per[5] = {0, 0, 0, 0, 0};
     RWB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per1, cg_pass1_kernel, NTHREADS, 0));
-    RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, cg_pass2_kernel, NTHREADS, 0));
-    cached = sms * std::max(1, std::min(per1, per2));
-    cache[dev].store(cached, std::memory_order_relaxed);
+    RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per[0], cg_pass1_kernel, NTHREADS, 0));
+    RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per[1], cg_pass2_kernel, NTHREADS, 0));
+    int per_b = 0;
+    RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per[2], cg_pass1_stg_kernel<false>, NTHREADS, 0));
+    RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_b, cg_pass1_stg_kernel<true>, NTHREADS, 0));
+    per[2] = std::min(per[2], per_b);
+    RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per[3], cg_pass1_col_kernel, NTHREADS, 0));
+    RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per[4], cg_pass2_col_kernel, NTHREADS, 0));
+    cache[1][dev].store(sms * std::max(1, per[2]), std::memory_order_relaxed);
+    cache[2][dev].store(sms * std::max(1, std::min(per[3], per[4])), std::memory_order_relaxed);
+    cached = sms * std::max(1, std::min(per[0], per[1]));
+    cache[0][dev].store(cached, std::memory_order_relaxed);
   }
   *grid = cached;
+  if (grids3) {
+    grids3[0] = cached;
+    grids3[1] = cache[1][dev].load(std::memory_order_relaxed);
+    grids3[2] = cache[2][dev].load(std::memory_order_relaxed);
+  }
   return RWB_OK;
 }
 
@@ -1563,9 +1918,25 @@ static int launch_chunk(const Geo& g, const Work& w, int nb, const int* list, in
                         int grid, cudaStream_t st) {
   // counted by the caller (graph replays count 2k+1 kernels each)
   dim3 block(TX, TY);
+  static const bool tiles_env = [] {  // RWB_CG_TILES=1: the plane-tile passes (diagnostics)
+    const char* e = std::getenv("RWB_CG_TILES");
+    return e && e[0] == '1';
+  }();
+  int grids[3];
+  if (int rc = persistent_grid(&grid, grids)) return rc;
   for (int j = 0; j < k; ++j) {
-    cg_pass1_kernel<<<grid, block, 0, st>>>(g, w, nb, list, j);
-    cg_pass2_kernel<<<grid, block, 0, st>>>(g, w, nb, list, j, tol2, max_iter);
+    if (tiles_env) {
+      cg_pass1_kernel<<<grids[0], block, 0, st>>>(g, w, nb, list, j);
+      cg_pass2_kernel<<<grids[0], block, 0, st>>>(g, w, nb, list, j, tol2, max_iter);
+    } else {
+      if (g.is3d && g.bx % 4 == 0)
+        cg_pass1_stg_kernel<true><<<grids[1], block, 0, st>>>(g, w, nb, j);
+      else if (g.is3d)
+        cg_pass1_stg_kernel<false><<<grids[1], block, 0, st>>>(g, w, nb, j);
+      else
+        cg_pass1_col_kernel<<<grids[2], block, 0, st>>>(g, w, nb, j);
+      cg_pass2_col_kernel<<<grids[2], block, 0, st>>>(g, w, nb, j, tol2, max_iter);
+    }
   }
   advance_kernel<<<1, 1024, 0, st>>>(w, nb, k);
   RWB_LAUNCH_CHECK_CAPTURE("cg iteration kernels");
