@@ -1385,6 +1385,69 @@ __global__ void __launch_bounds__(NTHREADS, 3) cg_pass1_stg_kernel(Geo g, Work w
   }
 }
 
+// 2-D pass 1 for bricks of up to 64 x 64 with rows a multiple of 4 floats (config 3's 64^2):
+// one brick per item, its r, p, w'x, w'y staged whole into shared memory by 16-byte cp.async
+// (64 KB; three CTAs per SM overlap one brick's loads with the others' compute), p = r + beta p
+// formed once in place, then the 5-point product from shared memory.  Arithmetic order as
+// cg_pass1_col_kernel's (march-axis y terms first, then x).
+constexpr int B2 = 64;
+struct Brick2Smem {
+  float r[B2 * B2], p[B2 * B2], wx[B2 * B2], wy[B2 * B2];
+};
+
+__global__ void __launch_bounds__(NTHREADS, 3) cg_pass1_brick2d_kernel(Geo g, Work w, int nb, int j) {
+  extern __shared__ __align__(16) unsigned char smem2[];
+  Brick2Smem& sm = *reinterpret_cast<Brick2Smem*>(smem2);
+  const int n_items = *w.n_active;
+  const int par = j & 1;
+  const int it = *w.base_it + j;
+  const float* __restrict__ pin = par ? w.p1 : w.p0;
+  float* __restrict__ pout = par ? w.p0 : w.p1;
+  const int tid = threadIdx.y * TX + threadIdx.x;
+  const int bx = g.bx, by = g.by, n = bx * by, nq = n >> 2;  // bx % 4 == 0
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int slot = w.alist[item];
+    if (w.state[slot] != ST_ACTIVE) continue;  // uniform per CTA
+    const long long sbase = (long long)slot * g.bvol;
+    const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(smem2);
+    for (int c = tid; c < 4 * nq; c += NTHREADS) {  // brick-local arrays are contiguous: bx*by floats
+      const int a = c / nq, o = 4 * (c - a * nq);
+      const float* src = (a == 0 ? w.r : a == 1 ? pin : a == 2 ? w.wx : w.wy) + sbase + o;
+      cp_async16(s0 + 4u * (uint32_t)(a * B2 * B2 + o), src, true);
+    }
+    cp_async_commit();
+    const double rr = w.rr[(long long)par * nb + slot];
+    const double rr_prev = w.rr[(long long)(par ^ 1) * nb + slot];
+    const float beta = (it == 0 || rr_prev <= 0.0) ? 0.f : (float)(rr / rr_prev);
+    cp_async_wait<0>();
+    __syncthreads();
+    for (int i = tid; i < n; i += NTHREADS) {  // p = r + beta p, in place of r
+      const float pc = sm.r[i] + beta * sm.p[i];
+      sm.r[i] = pc;
+      pout[sbase + i] = pc;
+    }
+    __syncthreads();
+    float acc = 0.f;
+    for (int i = tid; i < n; i += NTHREADS) {
+      const int y = i / bx, x = i - y * bx;
+      const float pc = sm.r[i];
+      const float pp = y + 1 < by ? sm.r[i + bx] : 0.f;
+      const float wmc = y + 1 < by ? sm.wy[i] : 0.f;
+      const float pm = y > 0 ? sm.r[i - bx] : 0.f;
+      const float wmm = y > 0 ? sm.wy[i - bx] : 0.f;
+      float s = wmc * pp + wmm * pm;
+      if (x + 1 < bx) s += sm.wx[i] * sm.r[i + 1];
+      if (x > 0) s += sm.wx[i - 1] * sm.r[i - 1];
+      const float q = pc - s;
+      w.q[sbase + i] = q;
+      acc += pc * q;
+    }
+    double pq, unused;
+    if (brick_reduce(g, w, slot, 0, acc, 0.f, &pq, &unused, 1)) w.pq[slot] = pq;
+    __syncthreads();  // the staging buffer is refilled by the next item
+  }
+}
+
 __global__ void __launch_bounds__(NTHREADS) cg_pass2_col_kernel(Geo g, Work w, int nb, int j, float tol2,
                                                                 int max_iter) {
   const int ncol = col_items(g);
@@ -1883,9 +1946,9 @@ static int readback(cudaStream_t st, const void* src, int at, int n) {
 }
 
 // persistent grids of the CG passes: [0] the plane-tile passes (and the default for other users),
-// [1] the staged 3-D pass 1, [2] the column-marching passes
+// [1] the staged 3-D pass 1, [2] the column-marching passes, [3] the whole-brick 2-D pass 1
 static int persistent_grid(int* grid, int* grids3 = nullptr) {
-  static DeviceCache cache[3];
+  static DeviceCache cache[4];
   int dev = 0;
   if (int rc = device_slot(&dev)) return rc;
   int cached = cache[0][dev].load(std::memory_order_relaxed);
@@ -1901,6 +1964,12 @@ static int persistent_grid(int* grid, int* grids3 = nullptr) {
     RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per[3], cg_pass1_col_kernel, NTHREADS, 0));
     RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per[4], cg_pass2_col_kernel, NTHREADS, 0));
     cache[1][dev].store(sms * std::max(1, per[2]), std::memory_order_relaxed);
+    int per2d = 0;
+    RWB_CUDA(cudaFuncSetAttribute(cg_pass1_brick2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sizeof(Brick2Smem)));
+    RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2d, cg_pass1_brick2d_kernel, NTHREADS,
+                                                           sizeof(Brick2Smem)));
+    cache[3][dev].store(sms * std::max(1, per2d), std::memory_order_relaxed);
     cache[2][dev].store(sms * std::max(1, std::min(per[3], per[4])), std::memory_order_relaxed);
     cached = sms * std::max(1, std::min(per[0], per[1]));
     cache[0][dev].store(cached, std::memory_order_relaxed);
@@ -1910,6 +1979,7 @@ static int persistent_grid(int* grid, int* grids3 = nullptr) {
     grids3[0] = cached;
     grids3[1] = cache[1][dev].load(std::memory_order_relaxed);
     grids3[2] = cache[2][dev].load(std::memory_order_relaxed);
+    grids3[3] = cache[3][dev].load(std::memory_order_relaxed);
   }
   return RWB_OK;
 }
@@ -1922,7 +1992,7 @@ static int launch_chunk(const Geo& g, const Work& w, int nb, const int* list, in
     const char* e = std::getenv("RWB_CG_TILES");
     return e && e[0] == '1';
   }();
-  int grids[3];
+  int grids[4];
   if (int rc = persistent_grid(&grid, grids)) return rc;
   for (int j = 0; j < k; ++j) {
     if (tiles_env) {
@@ -1933,6 +2003,8 @@ static int launch_chunk(const Geo& g, const Work& w, int nb, const int* list, in
         cg_pass1_stg_kernel<true><<<grids[1], block, 0, st>>>(g, w, nb, j);
       else if (g.is3d)
         cg_pass1_stg_kernel<false><<<grids[1], block, 0, st>>>(g, w, nb, j);
+      else if (g.bx % 4 == 0 && g.bx <= B2 && g.by <= B2)
+        cg_pass1_brick2d_kernel<<<grids[3], block, sizeof(Brick2Smem), st>>>(g, w, nb, j);
       else
         cg_pass1_col_kernel<<<grids[2], block, 0, st>>>(g, w, nb, j);
       cg_pass2_col_kernel<<<grids[2], block, 0, st>>>(g, w, nb, j, tol2, max_iter);
