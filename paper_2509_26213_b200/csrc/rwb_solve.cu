@@ -1510,6 +1510,76 @@ __global__ void __launch_bounds__(NTHREADS) cg_pass2_col_kernel(Geo g, Work w, i
   }
 }
 
+// Pass 2 over whole bricks as float4 streams (brick volume a multiple of 4): one brick per item,
+// the CTA's 256 threads each keep four float4 of y, r, p, q in flight per step.
+__global__ void __launch_bounds__(NTHREADS) cg_pass2_vec_kernel(Geo g, Work w, int nb, int j, float tol2, int max_iter) {
+  const int n_items = *w.n_active;
+  const int par = j & 1;
+  const int it = *w.base_it + j;
+  const float4* __restrict__ P = reinterpret_cast<const float4*>(par ? w.p0 : w.p1);  // pass-1 output
+  const float4* __restrict__ Q = reinterpret_cast<const float4*>(w.q);
+  float4* __restrict__ Y = reinterpret_cast<float4*>(w.y);
+  float4* __restrict__ Rw = reinterpret_cast<float4*>(w.r);
+  const int tid = threadIdx.y * TX + threadIdx.x;
+  const int n4 = (int)(g.bvol >> 2);
+  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
+    const int slot = w.alist[item];
+    if (w.state[slot] != ST_ACTIVE) continue;
+    const double rr = w.rr[(long long)par * nb + slot];
+    const double pq = w.pq[slot];
+    const float alpha = pq != 0.0 ? (float)(rr / pq) : 0.f;
+    const long long b4 = (long long)slot * n4;
+    float acc = 0.f;
+    int i = tid;
+    for (; i + 3 * NTHREADS < n4; i += 4 * NTHREADS) {
+      float4 y[4], r[4], pv[4], qv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        y[k] = Y[b4 + i + k * NTHREADS];
+        r[k] = Rw[b4 + i + k * NTHREADS];
+        pv[k] = __ldg(P + b4 + i + k * NTHREADS);
+        qv[k] = __ldg(Q + b4 + i + k * NTHREADS);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        y[k] = make_float4(y[k].x + alpha * pv[k].x, y[k].y + alpha * pv[k].y, y[k].z + alpha * pv[k].z,
+                           y[k].w + alpha * pv[k].w);
+        r[k] = make_float4(r[k].x - alpha * qv[k].x, r[k].y - alpha * qv[k].y, r[k].z - alpha * qv[k].z,
+                           r[k].w - alpha * qv[k].w);
+        Y[b4 + i + k * NTHREADS] = y[k];
+        Rw[b4 + i + k * NTHREADS] = r[k];
+        acc += r[k].x * r[k].x;
+        acc += r[k].y * r[k].y;
+        acc += r[k].z * r[k].z;
+        acc += r[k].w * r[k].w;
+      }
+    }
+    for (; i < n4; i += NTHREADS) {
+      float4 y = Y[b4 + i], r = Rw[b4 + i];
+      const float4 pv = __ldg(P + b4 + i), qv = __ldg(Q + b4 + i);
+      y = make_float4(y.x + alpha * pv.x, y.y + alpha * pv.y, y.z + alpha * pv.z, y.w + alpha * pv.w);
+      r = make_float4(r.x - alpha * qv.x, r.y - alpha * qv.y, r.z - alpha * qv.z, r.w - alpha * qv.w);
+      Y[b4 + i] = y;
+      Rw[b4 + i] = r;
+      acc += r.x * r.x;
+      acc += r.y * r.y;
+      acc += r.z * r.z;
+      acc += r.w * r.w;
+    }
+    double rr_new, unused;
+    if (brick_reduce(g, w, slot, 0, acc, 0.f, &rr_new, &unused, 1)) {
+      w.rr[(long long)(par ^ 1) * nb + slot] = rr_new;
+      if (rr_new <= (double)tol2 * w.bb[slot]) {
+        w.iters[slot] = it + 1;
+        w.state[slot] = ST_CONVERGED;
+      } else if (it + 1 >= max_iter) {
+        w.iters[slot] = it + 1;
+        w.state[slot] = ST_MAXITER;
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Whole-level (single-brick) solve as ONE cooperative persistent kernel: every
 // iteration's two passes are separated by grid-wide barriers instead of kernel
@@ -1946,9 +2016,10 @@ static int readback(cudaStream_t st, const void* src, int at, int n) {
 }
 
 // persistent grids of the CG passes: [0] the plane-tile passes (and the default for other users),
-// [1] the staged 3-D pass 1, [2] the column-marching passes, [3] the whole-brick 2-D pass 1
+// [1] the staged 3-D pass 1, [2] the column-marching passes, [3] the whole-brick 2-D pass 1,
+// [4] the whole-brick float4 pass 2
 static int persistent_grid(int* grid, int* grids3 = nullptr) {
-  static DeviceCache cache[4];
+  static DeviceCache cache[5];
   int dev = 0;
   if (int rc = device_slot(&dev)) return rc;
   int cached = cache[0][dev].load(std::memory_order_relaxed);
@@ -1970,6 +2041,9 @@ static int persistent_grid(int* grid, int* grids3 = nullptr) {
     RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2d, cg_pass1_brick2d_kernel, NTHREADS,
                                                            sizeof(Brick2Smem)));
     cache[3][dev].store(sms * std::max(1, per2d), std::memory_order_relaxed);
+    int perv = 0;
+    RWB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perv, cg_pass2_vec_kernel, NTHREADS, 0));
+    cache[4][dev].store(sms * std::max(1, perv), std::memory_order_relaxed);
     cache[2][dev].store(sms * std::max(1, std::min(per[3], per[4])), std::memory_order_relaxed);
     cached = sms * std::max(1, std::min(per[0], per[1]));
     cache[0][dev].store(cached, std::memory_order_relaxed);
@@ -1980,6 +2054,7 @@ static int persistent_grid(int* grid, int* grids3 = nullptr) {
     grids3[1] = cache[1][dev].load(std::memory_order_relaxed);
     grids3[2] = cache[2][dev].load(std::memory_order_relaxed);
     grids3[3] = cache[3][dev].load(std::memory_order_relaxed);
+    grids3[4] = cache[4][dev].load(std::memory_order_relaxed);
   }
   return RWB_OK;
 }
@@ -1992,7 +2067,11 @@ static int launch_chunk(const Geo& g, const Work& w, int nb, const int* list, in
     const char* e = std::getenv("RWB_CG_TILES");
     return e && e[0] == '1';
   }();
-  int grids[4];
+  static const bool vec2_off = [] {  // RWB_CG_VEC2=0: the column-marching pass 2 (diagnostics)
+    const char* e = std::getenv("RWB_CG_VEC2");
+    return e && e[0] == '0';
+  }();
+  int grids[5];
   if (int rc = persistent_grid(&grid, grids)) return rc;
   for (int j = 0; j < k; ++j) {
     if (tiles_env) {
@@ -2007,7 +2086,10 @@ static int launch_chunk(const Geo& g, const Work& w, int nb, const int* list, in
         cg_pass1_brick2d_kernel<<<grids[3], block, sizeof(Brick2Smem), st>>>(g, w, nb, j);
       else
         cg_pass1_col_kernel<<<grids[2], block, 0, st>>>(g, w, nb, j);
-      cg_pass2_col_kernel<<<grids[2], block, 0, st>>>(g, w, nb, j, tol2, max_iter);
+      if (g.bvol % 4 == 0 && !vec2_off)
+        cg_pass2_vec_kernel<<<grids[4], block, 0, st>>>(g, w, nb, j, tol2, max_iter);
+      else
+        cg_pass2_col_kernel<<<grids[2], block, 0, st>>>(g, w, nb, j, tol2, max_iter);
     }
   }
   advance_kernel<<<1, 1024, 0, st>>>(w, nb, k);
