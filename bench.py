@@ -65,6 +65,52 @@ BETA, WMIN, TOL = 100.0, 1e-6, 1e-6
 ALG_BYTES_PER_UNKNOWN_ITER = {3: 56, 2: 52}
 
 
+STREAM_BYTES_PER_UNKNOWN_ITER = {3: 52, 2: 48}  # what the streaming CG passes move (csrc/rwb_solve.cu header)
+
+
+def streaming_roofline(vol, seeds, brick, levels, cfg, peak, k1=2, k2=6):
+    """The streaming CG passes (the solver of any brick shape the on-chip engines do not take) on the
+    workload's level 0 with every brick active: device ms per iteration from k2 - k1 iterations,
+    HBM rate from the passes' own algorithmic bytes.  Untimed with respect to the bench line."""
+    import torch
+
+    from paper_2509_26213_b200 import device
+    from paper_2509_26213_b200.config import RWConfig
+
+    vols = device.lod_chain(vol, brick, levels)
+    if len(vols) < 2:  # one whole level: the cooperative / multigrid solvers, not the streaming passes
+        return None
+    k, brick_k = 0, brick
+    bound = device.upsample(torch.full(vols[1].shape, 0.5, device=vol.device), vols[0].shape)
+    ws = device.Workspace(vol.device)
+    times = []
+    st = None
+    for iters in (k1, k2):
+        c = RWConfig(beta=cfg.beta, min_weight=cfg.min_weight, tol=1e-30, max_iter=iters, check_every=iters,
+                     resident=False)
+        device.solve_level(vols[k], seeds, brick_k, bound, c, workspace=ws)  # graph capture
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _, st = device.solve_level(vols[k], seeds, brick_k, bound, c, workspace=ws)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    per = (times[1] - times[0]) / (k2 - k1)
+    nd = len(vol.shape)
+    b = STREAM_BYTES_PER_UNKNOWN_ITER[nd]
+    gbs = b * st["unknowns"] / (per / 1e3) / 1e9
+    del ws
+    return {"level": k, "shape": list(vols[k].shape), "brick": list(brick_k), "path": st["path"],
+            "kernels": "cg_pass1_stg_kernel + cg_pass2_vec_kernel" if nd == 3 else
+                       "cg_pass1_brick2d_kernel + cg_pass2_vec_kernel",
+            "ms_per_iteration": per, "unknowns": st["unknowns"], "bytes_per_unknown_iteration": b,
+            "achieved": gbs, "peak": peak, "frac": gbs / peak,
+            "note": f"every brick active (tol 1e-30), {k2}-{k1} iterations differenced; bytes = what the two "
+                    "passes read and write per unknown (r, p, w'x, w'y, w'z in / p, q out; y, r, p, q in / y, r "
+                    "out), the north star's fused-CG HBM figure"}
+
+
 def load_traffic(config, level_key):
     """The ncu capture of the dominant kernel (profiles/rNN_traffic.json, newest round first,
     written by tools/ncu_traffic.py): per-level DRAM bytes and on-chip utilisation, or None."""
@@ -572,6 +618,8 @@ def run_ours(args, wl, rank, world):
                          "really moves (hbm_frac_actual); traffic = ncu DRAM bytes of the level's launches, from "
                          "the profile named in onchip.profile"),
                 "kernels": kernels}
+    if rank == 0 and world == 1 and os.environ.get("RWB_BENCH_NO_STREAMING") != "1":
+        roofline["streaming_cg"] = streaming_roofline(vol, seeds, brick, levels, cfg, peak)
 
     comm = comm_info(world)  # collective: every rank
     cpu = None
