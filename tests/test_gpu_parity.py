@@ -137,6 +137,26 @@ def test_solve_level_matches_oracle(rng, shape, brick, cfg):
     assert np.all(got[seeds == 1] == 1.0) and np.all(got[seeds == 2] == 0.0)
 
 
+@pytest.mark.parametrize("shape,brick,kernel", [
+    ((24, 30, 21), (9, 10, 7), "3-D pass 1, 4-byte staging (rows of 7 floats)"),
+    ((40, 40, 40), (16, 16, 16), "3-D pass 1, 16-byte staging"),
+    ((17, 20, 88), (8, 8, 40), "3-D pass 1, two x tiles, the second partial"),
+    ((130, 140), (64, 64), "2-D whole-brick pass 1"),
+    ((90, 100), (20, 44), "2-D whole-brick pass 1, small bricks"),
+    ((80, 95), (30, 30), "2-D column-marching pass 1 (rows of 30 floats)"),
+    ((80, 200), (70, 96), "2-D column-marching pass 1 (bricks wider than 64)"),
+])
+def test_streaming_pass_variants_match_oracle(rng, shape, brick, kernel):
+    """Every streaming CG pass-1 / pass-2 variant (rwb_solve.cu launch_chunk) against the oracle."""
+    vol, seeds = _random_case(rng, shape)
+    bound = rng.random(shape).astype(np.float32)
+    ref = orw.solve_level(vol, seeds, brick, bound.astype(np.float64), TIGHT).prob
+    out, stats = device.solve_level(cuda(vol), cuda(seeds), brick, cuda(bound),
+                                    RWConfig(tol=GPU_CFG.tol, max_iter=GPU_CFG.max_iter, resident=False))
+    assert stats["path"] == 0 and stats["not_converged"] == 0, kernel
+    assert_rw_parity(host(out), ref)
+
+
 def test_graph_and_direct_launch_identical(rng):
     vol, seeds = _random_case(rng, (48, 40, 36))
     bound = cuda(rng.random(vol.shape).astype(np.float32))
