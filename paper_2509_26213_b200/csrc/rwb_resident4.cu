@@ -59,7 +59,8 @@ __device__ long long g_q4_trace[4][64][8];  // phase clocks of cluster 0 (diagno
 extern "C" int rwb_q4_trace_dump(long long* out) {
   return (int)cudaMemcpyFromSymbol(out, g_q4_trace, sizeof(g_q4_trace));
 }
-__device__ long long g_q4_pro[4][64][4];  // per brick of cluster 0: loop top, slab staged, loop start, epilogue done
+__device__ long long g_q4_pro[4][64][8];  // per brick of cluster 0: loop top, slab staged, loop start, epilogue done,
+                                          // TMEM / registers loaded, exchange pushed, exchange received
 #define Q4PRO(k)                                                                          \
   do {                                                                                    \
     if (tid == 0 && blockIdx.x < 4 && trace_b < 64) g_q4_pro[rank][trace_b][k] = clock64(); \
@@ -341,6 +342,7 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
     float4 sf_dn = f4(0, 0, 0, 0), sf_up = f4(0, 0, 0, 0);
     const float4 z4 = f4(0, 0, 0, 0);
     auto plane4 = [&](const float* v, int z) { return f4(v[z * RQ], v[z * RQ + 1], v[z * RQ + 2], v[z * RQ + 3]); };
+    Q4PRO(4);
 #pragma unroll
     for (int z = 0; z < TZT; ++z) sm.rp[pz0 + z][ly][xq] = plane4(r, z);
     {
@@ -365,7 +367,9 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
           push_agg(par, sm.aggd, sm.wagg[1]);
         }
       }
+      Q4PRO(5);
       mbar_wait(&sm.barR[par], ph);
+      Q4PRO(6);
       ++gk;
       if (below && first_zg) rf_dn = sm.rface[par][0][ly][xq];
       if (above && last_zg) rf_up = sm.rface[par][1][ly][xq];

@@ -25,12 +25,15 @@ for rank in range(4):
 
 # per brick of cluster 0 (CTA rank 0): staging wait, prologue (TMEM weights, coarse setup, initial
 # exchange), iterations, epilogue — cycles
-pro = (ctypes.c_longlong * (4 * 64 * 4))()
+pro = (ctypes.c_longlong * (4 * 64 * 8))()
 lib.rwb_q4_pro_dump.argtypes = [ctypes.c_void_p]
 lib.rwb_q4_pro_dump(pro)
-p = np.frombuffer(pro, dtype=np.int64).reshape(4, 64, 4)[0]
+p = np.frombuffer(pro, dtype=np.int64).reshape(4, 64, 8)[0]
 ok = p[:, 0] > 0
 p = p[ok][2:40]
 print("per brick median cycles: staging wait", int(np.median(p[:, 1] - p[:, 0])), "prologue",
       int(np.median(p[:, 2] - p[:, 1])), "iterations+epilogue", int(np.median(p[:, 3] - p[:, 2])),
       "next brick gap", int(np.median(p[1:, 0] - p[:-1, 3])))
+print("prologue split: TMEM / registers loaded", int(np.median(p[:, 4] - p[:, 1])), "exchange pushed",
+      int(np.median(p[:, 5] - p[:, 4])), "exchange wait", int(np.median(p[:, 6] - p[:, 5])),
+      "coarse init + barrier", int(np.median(p[:, 2] - p[:, 6])))
