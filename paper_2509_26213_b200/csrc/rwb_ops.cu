@@ -542,28 +542,36 @@ __global__ void __launch_bounds__(256) project_seeds8_kernel(const uint8_t* __re
   const int jy = blockIdx.y * BY + threadIdx.y;
   const int jz = blockIdx.z;
   if (jx0 >= cs.nx || jy >= cs.ny) return;
-  unsigned fg = 0, bg = 0;  // bit i: coarse voxel jx0 + i has a fg / bg child
-  for (int z = 2 * jz; z < min(2 * jz + 2, fs.nz); ++z)
-    for (int y = 2 * jy; y < min(2 * jy + 2, fs.ny); ++y) {
-      const uint4 q = *reinterpret_cast<const uint4*>(fine + ((long long)z * fs.ny + y) * fs.nx + 2 * jx0);
-      const unsigned w[4] = {q.x, q.y, q.z, q.w};
+  // byte-parallel: per 32-bit word (4 fine x), OR over the 2 x 2 (z, y) rows of "byte == 1" / "== 2"
+  // masks (0xff per byte), then fold the x pairs; all four rows' loads are issued first
+  uint4 q[4];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const unsigned s = (w[k >> 2] >> (8 * (k & 3))) & 0xffu;
-        fg |= (unsigned)(s == 1) << (k >> 1);
-        bg |= (unsigned)(s == 2) << (k >> 1);
-      }
-    }
-  unsigned lo = 0, hi = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const bool f = (fg >> i) & 1, b = (bg >> i) & 1;
-    const unsigned v = (f && !b) ? 1u : ((b && !f) ? 2u : 0u);
-    if (i < 4)
-      lo |= v << (8 * i);
-    else
-      hi |= v << (8 * (i - 4));
+  for (int k = 0; k < 4; ++k) {
+    const int z = 2 * jz + (k >> 1), y = 2 * jy + (k & 1);
+    q[k] = (z < fs.nz && y < fs.ny)
+               ? *reinterpret_cast<const uint4*>(fine + ((long long)z * fs.ny + y) * fs.nx + 2 * jx0)
+               : make_uint4(0u, 0u, 0u, 0u);
   }
+  unsigned F[4] = {0u, 0u, 0u, 0u}, B[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const unsigned w[4] = {q[k].x, q[k].y, q[k].z, q[k].w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      F[i] |= __vcmpeq4(w[i], 0x01010101u);
+      B[i] |= __vcmpeq4(w[i], 0x02020202u);
+    }
+  }
+  // word i holds coarse voxels 2i (fine bytes 0, 1) and 2i + 1 (bytes 2, 3): fold the pairs into
+  // bytes 0 and 2, value 1 (fg only), 2 (bg only) or 0
+  unsigned v[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const unsigned f = (F[i] | (F[i] >> 8)) & 0x00010001u, g = (B[i] | (B[i] >> 8)) & 0x00010001u;
+    v[i] = (f & ~g) | ((g & ~f) << 1);
+  }
+  const unsigned lo = (v[0] & 0xffu) | ((v[0] >> 16) << 8) | ((v[1] & 0xffu) << 16) | ((v[1] >> 16) << 24);
+  const unsigned hi = (v[2] & 0xffu) | ((v[2] >> 16) << 8) | ((v[3] & 0xffu) << 16) | ((v[3] >> 16) << 24);
   *reinterpret_cast<uint2*>(coarse + ((long long)jz * cs.ny + jy) * cs.nx + jx0) = make_uint2(lo, hi);
 }
 
