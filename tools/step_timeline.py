@@ -1,14 +1,15 @@
-"""Where a config-4 step goes outside the solve kernels (diagnostics): %globaltimer-free host
-events around the phases of device.hierarchical_random_walker, replayed phase by phase."""
+"""Where a step goes outside the solve kernels (diagnostics): CUDA events around the phases of
+device.hierarchical_random_walker, replayed phase by phase.   python tools/step_timeline.py [c4|c3|c2]"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import math
 import torch
-from bench import host_inputs
+from bench import WORKLOADS, host_inputs
 from paper_2509_26213_b200 import device
 from paper_2509_26213_b200.config import RWConfig
 
-shape, brick, L = (1024,) * 3, (32, 32, 32), 4
+wl = WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "c4"]
+shape, brick, L = tuple(wl["shape"]), tuple(wl["brick"]), wl["levels"]
 vh, sh = host_inputs(shape)
 vol, sd = vh.cuda(), sh.cuda()
 del vh, sh
