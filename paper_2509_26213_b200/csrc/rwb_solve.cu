@@ -1345,39 +1345,67 @@ __global__ void __launch_bounds__(NTHREADS, 3) cg_pass1_stg_kernel(Geo g, Work w
     const bool ex0 = hx0 && lane == 0, ex1 = hx1 && lane == TX - 1;
     long long li = sbase + (long long)ly * g.bx + lx;
     float acc = 0.f, pm = 0.f, wzm = 0.f, pc = 0.f;
-    for (int m = 0; m < g.bz; ++m, li += sbz) {
-      cp_async_wait<KS - 3>();  // planes m and m + 1 have landed (this thread's copies)
-      __syncthreads();          // ... everyone's; and everyone is done with plane m - 1's stage
-      issue(m + KS - 1);        // refills plane m - 1's stage (zero-filled past the brick)
-      cp_async_commit();
-      const StgPlane& sc = st[m % KS];
-      const StgPlane& sn = st[(m + 1) % KS];
-      if (m == 0) pc = sc.r[warp + 1][lane] + beta * sc.p[warp + 1][lane];
-      const bool up = m + 1 < g.bz;
-      const float pp = up ? sn.r[warp + 1][lane] + beta * sn.p[warp + 1][lane] : 0.f;
-      const float wzc = up ? sc.wz[warp][lane] : 0.f;
-      float s = wzc * pp + wzm * pm;
-      const float wxo = sc.wx[warp][lane];
-      float xr = __shfl_down_sync(0xffffffffu, pc, 1), xl = __shfl_up_sync(0xffffffffu, pc, 1);
-      float wxl = __shfl_up_sync(0xffffffffu, wxo, 1);
-      if (ex1) xr = __ldg(R + li + 1) + beta * __ldg(pin + li + 1);
-      if (ex0) {
-        xl = __ldg(R + li - 1) + beta * __ldg(pin + li - 1);
-        wxl = __ldg(w.wx + li - 1);
+    // the march, unrolled by the ring size so every stage index (and shared-memory offset) is a
+    // constant; pointers advance by one plane per step
+    const float* vnext[2] = {nullptr, nullptr};  // VEC: the sources of plane m + KS - 1, advanced per plane
+    if (VEC) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) vnext[q] = vsrc[q] + (long long)(KS - 1) * sbz;
+    }
+    const float* pR = R + li;
+    const float* ppin = pin + li;
+    const float* pwx = w.wx + li;
+    float* ppo = pout + li;
+    float* pq_ = Q + li;
+    for (int m0 = 0; m0 < g.bz; m0 += KS) {
+#pragma unroll
+      for (int k = 0; k < KS; ++k) {
+        const int m = m0 + k;
+        if (m >= g.bz) break;
+        cp_async_wait<KS - 3>();  // planes m and m + 1 have landed (this thread's copies)
+        __syncthreads();          // ... everyone's; and everyone is done with plane m - 1's stage
+        if (VEC) {                // refills plane m - 1's stage (zero-filled past the brick)
+          const uint32_t so = (uint32_t)(((k + KS - 1) % KS) * sizeof(StgPlane));
+          const bool inm = m + KS - 1 < g.bz;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            if (vdst[q] != 0xffffffffu) cp_async16(vdst[q] + so, inm ? vnext[q] : vsrc[q], inm && vok[q]);
+            vnext[q] += sbz;
+          }
+        } else {
+          issue(m + KS - 1);
+        }
+        cp_async_commit();
+        const StgPlane& sc = st[k];
+        const StgPlane& sn = st[(k + 1) % KS];
+        if (m == 0) pc = sc.r[warp + 1][lane] + beta * sc.p[warp + 1][lane];
+        const bool up = m + 1 < g.bz;
+        const float pp = up ? sn.r[warp + 1][lane] + beta * sn.p[warp + 1][lane] : 0.f;
+        const float wzc = up ? sc.wz[warp][lane] : 0.f;
+        float s = wzc * pp + wzm * pm;
+        const float wxo = sc.wx[warp][lane];
+        float xr = __shfl_down_sync(0xffffffffu, pc, 1), xl = __shfl_up_sync(0xffffffffu, pc, 1);
+        float wxl = __shfl_up_sync(0xffffffffu, wxo, 1);
+        if (ex1) xr = __ldg(pR + 1) + beta * __ldg(ppin + 1);
+        if (ex0) {
+          xl = __ldg(pR - 1) + beta * __ldg(ppin - 1);
+          wxl = __ldg(pwx - 1);
+        }
+        if (hx1) s += wxo * xr;
+        if (hx0) s += wxl * xl;
+        if (hy1) s += sc.wy[warp + 1][lane] * (sc.r[warp + 2][lane] + beta * sc.p[warp + 2][lane]);
+        if (hy0) s += sc.wy[warp][lane] * (sc.r[warp][lane] + beta * sc.p[warp][lane]);
+        if (in) {
+          const float q = pc - s;
+          *ppo = pc;
+          *pq_ = q;
+          acc += pc * q;
+        }
+        pm = pc;
+        pc = pp;
+        wzm = wzc;
+        pR += sbz, ppin += sbz, pwx += sbz, ppo += sbz, pq_ += sbz;
       }
-      if (hx1) s += wxo * xr;
-      if (hx0) s += wxl * xl;
-      if (hy1) s += sc.wy[warp + 1][lane] * (sc.r[warp + 2][lane] + beta * sc.p[warp + 2][lane]);
-      if (hy0) s += sc.wy[warp][lane] * (sc.r[warp][lane] + beta * sc.p[warp][lane]);
-      if (in) {
-        const float q = pc - s;
-        pout[li] = pc;
-        Q[li] = q;
-        acc += pc * q;
-      }
-      pm = pc;
-      pc = pp;
-      wzm = wzc;
     }
     cp_async_wait<0>();
     double pq, unused;
