@@ -3,7 +3,10 @@ random-walker properties (Grady 2006) and reproduction of the frozen fixtures.
 
 The reference has no random walker, so the RW oracle's parity is
 unpinned against the reference; scipy's SuperLU on an explicitly assembled
-per-brick Laplacian is the independent check of the restated maths.
+per-brick Laplacian is the independent check of the restated maths, and the
+whole hierarchy (seed projection, prolongation taps, per-brick Dirichlet
+halos, level order) is checked against a chain composed from independently
+restated pieces (test_hierarchy_matches_independent_composition).
 """
 
 import json
@@ -207,3 +210,57 @@ def test_brick_skip_rule_oracle():
     full = rw.hierarchical_random_walker(vol, sd, (8, 8), 3, rw.RWParams(tol=1e-10))
     skip = rw.hierarchical_random_walker(vol, sd, (8, 8), 3, rw.RWParams(tol=1e-10), skip_eps=1e-6)
     assert np.abs(full.prob[0] - skip.prob[0]).max() < 1e-4
+
+
+def _independent_projection(s):
+    """Seed projection restated: a coarse voxel is fg (bg) when some child is fg
+    (bg) and none is bg (fg); otherwise unseeded.  Ragged tails pad with unseeded children."""
+    s = np.asarray(s)
+    pad = [(0, n % 2) for n in s.shape]
+    p = np.pad(s, pad)
+    shape = []
+    for n in p.shape:
+        shape += [n // 2, 2]
+    blocks = p.reshape(shape)
+    axes = tuple(range(1, 2 * s.ndim, 2))
+    fg, bg = (blocks == 1).any(axis=axes), (blocks == 2).any(axis=axes)
+    return np.where(fg & ~bg, 1, np.where(bg & ~fg, 2, 0)).astype(np.uint8)
+
+
+def _independent_upsample(parent, fine_shape):
+    """Cell-centred linear prolongation restated with np.interp, one axis at a time: fine voxel g
+    sits at parent coordinate g / 2 - 1/4, clamped to the parent's end values."""
+    out = np.asarray(parent, np.float64)
+    for dim, n in enumerate(fine_shape):
+        c = np.arange(n) / 2.0 - 0.25
+        out = np.apply_along_axis(lambda v: np.interp(c, np.arange(v.size), v), dim, out)
+    return out
+
+
+@pytest.mark.parametrize("shape,brick,levels", [((24, 20), (8, 8), 2), ((12, 10, 9), (4, 4, 4), 2),
+                                                ((30, 26), (8, 8), 3)])
+def test_hierarchy_matches_independent_composition(rng, shape, brick, levels):
+    """The hierarchical driver (coarsest level whole; finer levels brick by brick from the upsampled
+    parent) against the same chain assembled from independent pieces: the LOD pyramid pinned to the
+    reference, restated seed projection and prolongation, and SuperLU per brick."""
+    from oracle import lod
+
+    vol = (rng.random(shape) * 0.3).astype(np.float32)
+    vol[tuple(slice(0, n // 2) for n in shape)] += 0.5  # a blob, so levels differ
+    seeds = np.zeros(shape, np.uint8)
+    u = rng.random(shape)
+    seeds[u < 0.04] = 1
+    seeds[(u >= 0.04) & (u < 0.08)] = 2
+    res = rw.hierarchical_random_walker(vol, seeds, brick, levels, TIGHT)
+    vols = lod.lod_chain(vol, brick, levels)
+    sl = [seeds]
+    for _ in range(levels - 1):
+        sl.append(_independent_projection(sl[-1]))
+    for k in range(levels):
+        np.testing.assert_array_equal(res.seeds[k], sl[k])
+    prob = direct_brick_solve(vols[-1], sl[-1], vols[-1].shape, None)
+    np.testing.assert_allclose(res.prob[-1], prob, atol=1e-8, rtol=0)
+    for k in range(levels - 2, -1, -1):
+        bound = _independent_upsample(prob, vols[k].shape)
+        prob = direct_brick_solve(vols[k], sl[k], brick, bound)
+        np.testing.assert_allclose(res.prob[k], prob, atol=1e-8, rtol=0)
