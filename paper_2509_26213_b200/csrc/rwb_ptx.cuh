@@ -206,6 +206,13 @@ __device__ __forceinline__ void tmem_wait_ld12(float* v) {
 __device__ __forceinline__ void tmem_wait_ld5(float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]) : : "memory");
 }
+__device__ __forceinline__ void tmem_wait_ld13(float* v) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7]),
+                 "+f"(v[8]), "+f"(v[9]), "+f"(v[10]), "+f"(v[11]), "+f"(v[12])
+               :
+               : "memory");
+}
 __device__ __forceinline__ void tmem_wait_ld9(float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;"
                : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]), "+f"(v[7]),

@@ -100,7 +100,8 @@ struct Cfg {
   static constexpr int TAIL = 16 * TZT;             // column of the per-plane left w'x values
   static constexpr int WZB = TAIL + 8;              // column of the w'z plane below the thread's first plane
   static constexpr int TAU = WZB + 8;               // columns of tau = m - sigma per voxel (coarse correction)
-  static_assert(TAU + 4 * TZT <= COLS, "TMEM row");
+  static constexpr int WYE = TAU + 4 * TZT;         // columns of the w'y across the thread's aggregate y face
+  static_assert(WYE + 4 * TZT <= COLS, "TMEM row");
 };
 }  // namespace q4
 
@@ -273,6 +274,7 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
     {
       float tt[16];
       float tau[2][16];  // tau = m - sigma per voxel (m = 1 on unknowns, sigma = sum of the 6 scaled weights)
+      float wye[2][16];  // w'y across the aggregate's y face the thread's row touches (row below / above)
 #pragma unroll
       for (int z = 0; z < TZT; ++z) {
         const int o = (pz0 + z) * PLANE + ly * RB + xq * RQ;
@@ -295,6 +297,7 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
                               (lane_of(wz4, i) + lane_of(wzd4, i));
             const float t = (lane_of(s4, i) > 0.f ? 1.f : 0.f) - sig;
             tau[(z * RQ + i) >> 4][(z * RQ + i) & 15] = t;
+            wye[(z * RQ + i) >> 4][(z * RQ + i) & 15] = ydn ? lane_of(wyb4, i) : lane_of(wy4, i);
             dpart += t;
             if (ydn) dpart += lane_of(wyb4, i);
             if (yup) dpart += lane_of(wy4, i);
@@ -307,6 +310,8 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
       if (CC) {
         tmem_st16(tb + C::TAU, tau[0]);
         tmem_st16(tb + C::TAU + 16, tau[1]);
+        tmem_st16(tb + C::WYE, wye[0]);
+        tmem_st16(tb + C::WYE + 16, wye[1]);
       }
 #pragma unroll
       for (int z = TZT; z < 8; ++z) tt[z] = 0.f;
@@ -413,6 +418,8 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
         dzd = below ? sm.cc[agg - 16] - c_own : 0.f;
         dzu = above ? sm.cc[agg + 16] - c_own : 0.f;
       }
+      // the x-face difference on the side the thread's quad touches (the other side's term is 0)
+      const float dxl = (xq & 1) ? 0.f : dxc, dxr = (xq & 1) ? dxc : 0.f;
       // the previous iteration's y += alpha p, deferred off the update -> publish -> barrier
       // chain: nothing reads y until the epilogue, so it fills the SpMV's load latencies
       if (pass > 0) {
@@ -464,7 +471,7 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
           fma2(acc[i], acc[i + 1], lane_of(wzl4, i), lane_of(wzl4, i + 1), lane_of(rzd, i), lane_of(rzd, i + 1), acc[i],
                acc[i + 1]);
         }
-        float tx[9];  // w'x of the quad and the one left of it (+ tau), once the y / z terms are done
+        float tx[13];  // w'x of the quad and the one left of it (+ tau, + the y-face w'y), once the y / z terms are done
         uint32_t adx = tb + 16 * z + 12, adl = tb + C::TAIL + z;
         asm volatile("" : "+r"(adx), "+r"(adl) : "f"(acc[0]), "f"(acc[2]));
 #ifdef RWB_EXP_NOTMEM
@@ -475,7 +482,8 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
         tmem_ld1(adl, tx[4]);
         if (CC) {
           tmem_ld4p(tb + C::TAU + RQ * z, tx + 5);
-          tmem_wait_ld9(tx);
+          tmem_ld4p(tb + C::WYE + RQ * z, tx + 9);
+          tmem_wait_ld13(tx);
         } else {
           tmem_wait_ld5(tx);
         }
@@ -493,9 +501,8 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
         }
         // coarse part of A'u: c_own tau - sum over the aggregate faces of w' (c_neighbour - c_own)
         if (CC) {
-          const float4 wye = ydn ? wyb4 : wy4;
 #pragma unroll
-          for (int i = 0; i < RQ; ++i) acc[i] = fmaf(lane_of(wye, i), dyc, acc[i]);
+          for (int i = 0; i < RQ; ++i) acc[i] = fmaf(tx[9 + i], dyc, acc[i]);
           if (z == 0) {
 #pragma unroll
             for (int i = 0; i < RQ; ++i) acc[i] = fmaf(lane_of(wzl4, i), dzd, acc[i]);
@@ -504,8 +511,8 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
 #pragma unroll
             for (int i = 0; i < RQ; ++i) acc[i] = fmaf(lane_of(wz4, i), dzu, acc[i]);
           }
-          acc[0] = fmaf((xq & 1) ? 0.f : wxl0, dxc, acc[0]);
-          acc[RQ - 1] = fmaf((xq & 1) ? lane_of(wx4, RQ - 1) : 0.f, dxc, acc[RQ - 1]);
+          acc[0] = fmaf(wxl0, dxl, acc[0]);
+          acc[RQ - 1] = fmaf(lane_of(wx4, RQ - 1), dxr, acc[RQ - 1]);
         }
 #pragma unroll
         for (int i = 0; i < RQ; i += 2) {
