@@ -111,7 +111,8 @@ struct Q4Smem {
   float sz[q4::PLANE + q4::SLAB];           // w'z incl. the plane below the slab
   float sr[q4::SLAB];                       // staged r0; then the Jacobi scales for the epilogue
   float sv[q4::SLAB];                       // staged y0
-  float4 rp[q4::RPZ][q4::RB][q4::RQN];      // r planes (y neighbours of the SpMV)
+  float4 rp[q4::RPZ][q4::RB + 2][q4::RQN];  // r planes (y neighbours of the SpMV), row y at y + 1; rows 0 and
+                                            // RB + 1 stay zero (no neighbour past the brick's y faces)
   float4 rface[2][2][q4::RB][q4::RQN];      // received faces [parity][0 = from below, 1 = from above]
   __align__(16) float red[2][2][q4::NPART]; // pushed partials [parity][r.r, delta][rank]
   float2 wpart[q4::MAXW];
@@ -189,6 +190,10 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
   }
   if (rank == 0)  // the CTA holding plane 0 has no plane below
     for (int i = tid; i < PLANE; i += RTT) sm.sz[i] = 0.f;
+  for (int i = tid; i < RPZ * 2 * RQN; i += RTT) {  // the zero rows past the y faces
+    const int pz = i / (2 * RQN), e = (i / RQN) & 1, x = i % RQN;
+    sm.rp[pz][e ? RB + 1 : 0][x] = f4(0.f, 0.f, 0.f, 0.f);
+  }
   // pushes (remote addresses formed where used: registers are the scarce resource here):
   // plane 0 goes to the CTA below as its "from above" face, plane 7 to the CTA above as its
   // "from below" face, lane t of warp 0 delivers the CTA's partials to CTA t
@@ -349,7 +354,7 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
     auto plane4 = [&](const float* v, int z) { return f4(v[z * RQ], v[z * RQ + 1], v[z * RQ + 2], v[z * RQ + 3]); };
     Q4PRO(4);
 #pragma unroll
-    for (int z = 0; z < TZT; ++z) sm.rp[pz0 + z][ly][xq] = plane4(r, z);
+    for (int z = 0; z < TZT; ++z) sm.rp[pz0 + z][ly + 1][xq] = plane4(r, z);
     {
       const int par = gk & 1;
       const uint32_t ph = (gk >> 1) & 1;
@@ -454,10 +459,10 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
         const float4 wy4 = f4(ta[0], ta[1], ta[2], ta[3]);
         const float4 wyb4 = f4(ta[4], ta[5], ta[6], ta[7]);
         const float4 wz4 = f4(ta[8], ta[9], ta[10], ta[11]);
-        const float4 ru = ly + 1 < RB ? sm.rp[pz][ly + 1][xq] : z4;
-        const float4 rd = ly > 0 ? sm.rp[pz][ly - 1][xq] : z4;
-        const float4 rzu = z + 1 < TZT ? plane4(r, z + 1) : (pz + 1 < RPZ ? sm.rp[pz + 1][ly][xq] : rf_up);
-        const float4 rzd = z > 0 ? plane4(r, z - 1) : (pz > 0 ? sm.rp[pz - 1][ly][xq] : rf_dn);
+        const float4 ru = sm.rp[pz][ly + 2][xq];
+        const float4 rd = sm.rp[pz][ly][xq];
+        const float4 rzu = z + 1 < TZT ? plane4(r, z + 1) : (pz + 1 < RPZ ? sm.rp[pz + 1][ly + 1][xq] : rf_up);
+        const float4 rzd = z > 0 ? plane4(r, z - 1) : (pz > 0 ? sm.rp[pz - 1][ly + 1][xq] : rf_dn);
         const float rl = __shfl_up_sync(0xffffffffu, r[z * RQ + RQ - 1], 1);
         const float rr_ = __shfl_down_sync(0xffffffffu, r[z * RQ], 1);
         float acc[RQ];
@@ -631,7 +636,7 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
                    fmaf(-alpha, sf_up.w, rf_up.w));
       }
 #pragma unroll
-      for (int z = 0; z < TZT; ++z) sm.rp[pz0 + z][ly][xq] = plane4(r, z);
+      for (int z = 0; z < TZT; ++z) sm.rp[pz0 + z][ly + 1][xq] = plane4(r, z);
       Q4TRACE(5);
       __syncthreads();
       Q4TRACE(6);
