@@ -561,10 +561,9 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
             dc += v.y;
           }
           if (lane < RCL) push_parts(par, gc, dc);
-          if (CC && lane < 16) {
-            push_agg(par, sm.aggw[par], sm.wagg[0]);
-            push_agg(par, sm.aggr[par], sm.wagg[2]);
-          }
+        } else if (CC && warp == 1 && lane < 16) {  // the aggregate sums in parallel with warp 0's partials
+          push_agg(par, sm.aggw[par], sm.wagg[0]);
+          push_agg(par, sm.aggr[par], sm.wagg[2]);
         }
       }
       Q4TRACE(2);
