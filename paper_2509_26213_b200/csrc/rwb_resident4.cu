@@ -425,12 +425,6 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
       }
       // the x-face difference on the side the thread's quad touches (the other side's term is 0)
       const float dxl = (xq & 1) ? 0.f : dxc, dxr = (xq & 1) ? dxc : 0.f;
-      // the previous iteration's y += alpha p, deferred off the update -> publish -> barrier
-      // chain: nothing reads y until the epilogue, so it fills the SpMV's load latencies
-      if (pass > 0) {
-#pragma unroll
-        for (int v = 0; v < RV; v += 2) fma2(y[v], y[v + 1], alpha, alpha, p[v], p[v + 1], y[v], y[v + 1]);
-      }
       // w = A'r with the scaled weights from tensor memory
       float gp[2] = {0.f, 0.f}, dp[2] = {0.f, 0.f};
       float4 wzl4;  // w'z of the plane below the slab
@@ -565,6 +559,12 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
           push_agg(par, sm.aggw[par], sm.wagg[0]);
           push_agg(par, sm.aggr[par], sm.wagg[2]);
         }
+      }
+      // the previous iteration's y += alpha p, deferred off the update -> publish -> barrier chain
+      // into the exchange wait (nothing reads y until the epilogue; the SpMV is issue-bound)
+      if (pass > 0) {
+#pragma unroll
+        for (int v = 0; v < RV; v += 2) fma2(y[v], y[v + 1], alpha, alpha, p[v], p[v + 1], y[v], y[v + 1]);
       }
       Q4TRACE(2);
       mbar_wait(&sm.barR[par], ph);
