@@ -643,6 +643,7 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
       ++trace_it;
 #endif
     }
+    Q4PRO(7);
     // epilogue: probabilities and labels straight into the level
     {
       const long long sbase = (long long)slot * (RB * RB * RB) + (long long)rank * SLAB;
@@ -651,13 +652,21 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
       const int gy = a.oy + hy * RB + ly, gx0 = a.ox + hx * RB + xq * RQ;
       const bool row_in = gy >= 0 && gy < a.ny;
       const bool quad_in = gx0 >= 0 && gx0 + RQ <= a.nx;
+      // all planes' scales (and Dirichlet values) first: one load latency for the brick, not one
+      // per plane (the stores below would otherwise keep each plane's loads behind the last store)
+      float4 s4v[TZT], y0v[CC ? TZT : 1];
+#pragma unroll
+      for (int z = 0; z < TZT; ++z) {
+        const long long o = sbase + (pz0 + z) * PLANE + ly * RB + xq * RQ;
+        s4v[z] = __ldg(reinterpret_cast<const float4*>(a.sc + o));
+        if (CC) y0v[CC ? z : 0] = __ldcg(reinterpret_cast<const float4*>(a.y + o));
+      }
 #pragma unroll
       for (int z = 0; z < TZT; ++z) {
         const int gz = a.oz + hz * RB + rank * RPZ + pz0 + z;
         if (!row_in || gz < 0 || gz >= a.nz) continue;
-        const float4 s4 = __ldg(reinterpret_cast<const float4*>(a.sc + sbase + (pz0 + z) * PLANE + ly * RB + xq * RQ));
-        const float4 y04 = CC ? __ldcg(reinterpret_cast<const float4*>(a.y + sbase + (pz0 + z) * PLANE + ly * RB + xq * RQ))
-                              : f4(0.f, 0.f, 0.f, 0.f);
+        const float4 s4 = s4v[z];
+        const float4 y04 = CC ? y0v[CC ? z : 0] : f4(0.f, 0.f, 0.f, 0.f);
         float pv[RQ];
 #pragma unroll
         for (int i = 0; i < RQ; ++i) {

@@ -37,3 +37,4 @@ print("per brick median cycles: staging wait", int(np.median(p[:, 1] - p[:, 0]))
 print("prologue split: TMEM / registers loaded", int(np.median(p[:, 4] - p[:, 1])), "exchange pushed",
       int(np.median(p[:, 5] - p[:, 4])), "exchange wait", int(np.median(p[:, 6] - p[:, 5])),
       "coarse init + barrier", int(np.median(p[:, 2] - p[:, 6])))
+print("epilogue", int(np.median(p[:, 3] - p[:, 7])))
