@@ -252,11 +252,16 @@ __global__ void __launch_bounds__(TH2, 1) resident2d_kernel(ResidentArgs a) {
       const int hx = brick % a.gx, hy = brick / a.gx;
       const int gx0 = a.ox + hx * T2 + Q2 * xq;
       const bool quad_in = gx0 >= 0 && gx0 + Q2 <= a.nx;
+      // all rows' scales first: one load latency per tile, not one per row
+      float4 s4v[Q2];
+#pragma unroll
+      for (int i = 0; i < Q2; ++i)
+        s4v[i] = __ldg(reinterpret_cast<const float4*>(a.sc + base + (long long)(Q2 * yq + i) * T2 + Q2 * xq));
 #pragma unroll
       for (int i = 0; i < Q2; ++i) {
         const int gy = a.oy + hy * T2 + Q2 * yq + i;
         if (gy < 0 || gy >= a.ny) continue;
-        const float4 s4 = __ldg(reinterpret_cast<const float4*>(a.sc + base + (long long)(Q2 * yq + i) * T2 + Q2 * xq));
+        const float4 s4 = s4v[i];
         float pv[Q2];
 #pragma unroll
         for (int k = 0; k < Q2; ++k) {
