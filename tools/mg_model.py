@@ -3,7 +3,7 @@ variants, float64, on the coarsest level of a phantom hierarchy (the bench's §8
 
     python tools/mg_model.py [N] [levels] [variant ...]
       N^3 phantom, seeds S1; the coarsest level is N / 2^(levels-1) per side.
-      variants: base | om=<w> | nu=<pre/post sweeps> | cs=<coarse scale> | bot=<bottom sweeps>
+      variants: base | om=<w> | nu=<pre/post sweeps> | cs=<coarse scale> | bot=<bottom sweeps> | x0=<initial p>
                 | minc=<cells of the bottom level>, combined with commas, e.g. cs=1.6,nu=2
 """
 import sys
@@ -152,8 +152,10 @@ def run(opts):
         return x
 
     b = np.where(unk, S.rhs * s, 0); bb = float((b ** 2).sum())
-    y = np.zeros(v.shape); r = b.copy(); z = vcycle(0, r); p = z.copy(); rz = float((r * z).sum()); it = 0
     dg0 = unk.astype(float)
+    x0 = float(opts.get("x0", 0.0))  # initial probability of the unknowns
+    y = np.where(unk, x0 / np.where(unk, s, 1.0), 0.0)
+    r = b - Aop(W, dg0, y); z = vcycle(0, r); p = z.copy(); rz = float((r * z).sum()); it = 0
     while float((r ** 2).sum()) > 1e-12 * bb and it < 500:
         q = Aop(W, dg0, p); al = rz / float((p * q).sum()); y += al * p; r -= al * q
         z = vcycle(0, r); rzn = float((r * z).sum()); p = z + rzn / rz * p; rz = rzn; it += 1
