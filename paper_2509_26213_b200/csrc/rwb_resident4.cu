@@ -372,10 +372,10 @@ __global__ void __launch_bounds__(q4::Cfg<TZT>::RTT, 1) resident3d_q4_kernel(Res
           sm.wagg[1][warp][lane >> 1] = dv;
         }
         asm volatile("bar.sync 1, %0;" ::"n"(RTT) : "memory");
-        if (warp == 0 && lane < 16) {
+        if (warp == 0 && lane < 16)  // the two arrays from two warps, in parallel
           push_agg(par, sm.aggw[par], sm.wagg[0]);
+        else if (warp == 1 && lane < 16)
           push_agg(par, sm.aggd, sm.wagg[1]);
-        }
       }
       Q4PRO(5);
       mbar_wait(&sm.barR[par], ph);
